@@ -1,0 +1,382 @@
+"""bench.py -- HSDE-ADMM iterations/s on the B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 4] [--no-extras]
+
+A "step" is one ADMM iteration (solver.py:375-395) of the headline workload,
+BASELINE config 4 (block-arrow, n=16040, 400 cliques of order 80, m=1000,
+nnz(A)=38.4M): the largest configuration, and the one whose per-iteration
+working set (A in CSR+CSC: 0.92 GB) exceeds the 126 MB L2, so consecutive
+timed iterations stream from HBM (no L2 flush needed; stated in `config`).
+
+`value`  -- iterations/s with the problem resident in HBM: K iterations replayed
+            as CUDA graphs, timed with CUDA events on the library's stream.
+`e2e`    -- the same metric through the public API `solve_decomposed` on host
+            data (problem H2D + device setup + the default to-tolerance solve +
+            report D2H), i.e. iterations / wall time of the user's call.
+`roofline` -- dominant kernel of the iteration, measured live with CUDA events
+            around each kernel (hsde_profile_iterations); algorithmic bytes or
+            flops per launch are defined in DESIGN.md.
+`cpu_baseline` -- the CPU oracle port (oracle/hsde_oracle.py, numpy/scipy)
+            timed on this host on a bounded sample of the same workload.
+
+--impl reference times that CPU port alone (the reference is pure Python and
+cannot travel to the GPU box; the oracle restates it, pinned by tests/golden).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "HSDE-ADMM iterations/sec and time-to-1e-4 residual per SDP; % of fp64/HBM roofline"
+
+
+def _rank_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.th:
+            self.th.join(timeout=1)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic units per launch
+
+
+def kernel_units(cp, name: str):
+    """(kind, amount) of one launch: kind 'bytes' or 'flops'."""
+    Nc, nd, m, nnz = cp.N_c, cp.n_d, cp.m, int(cp.A.nnz)
+    big = cp.sizes[cp.sizes > 32]
+    small = cp.sizes[(cp.sizes <= 32) & (cp.sizes > 1)]
+    if name == "k_rhs":
+        return "bytes", 52 * Nc + 36 * nd + 12 * nnz + 8 * m
+    if name == "k_spmv_seg":
+        return "bytes", 12 * nnz + 8 * Nc
+    if name == "k_ua":
+        return "bytes", 40 * Nc + 12 * nnz
+    if name == "k_xupd":
+        return "bytes", 48 * Nc
+    if name == "k_schur":
+        return "bytes", 8 * (m * m if not cp_schur_diag(cp) else m)
+    if name == "k_cone_block":
+        return "flops", float((11 * big.astype(np.float64) ** 3).sum())
+    if name == "k_cone_warp":
+        return "flops", float((11 * small.astype(np.float64) ** 3).sum())
+    return None, 0.0
+
+
+def cp_schur_diag(cp) -> bool:
+    counts = np.bincount(cp.A.indices, minlength=cp.N_c)
+    return bool(counts.max(initial=0) <= 1)
+
+
+def load_peaks() -> dict:
+    peaks = {}
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        peaks.update(json.loads(p.read_text()))
+    f = ROOT / "profiles" / "fp64_peaks.json"
+    if f.exists():
+        peaks.update(json.loads(f.read_text()))
+    return peaks
+
+
+def load_traffic(name: str):
+    """dram bytes per launch of `name` from the committed ncu --set full summary."""
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    if not f.exists():
+        return None
+    data = json.loads(f.read_text())
+    return data.get(name)
+
+
+def roofline_for(cp, prof_ms: dict, launches_per_kernel: int, peaks: dict):
+    items = [(ms, name) for name, ms in prof_ms.items() if ms > 0 and kernel_units(cp, name)[0]]
+    if not items:
+        return None, None
+    out = {}
+    for ms, name in sorted(items, reverse=True):
+        kind, amount = kernel_units(cp, name)
+        t = ms / 1e3 / launches_per_kernel
+        if kind == "bytes":
+            peak = peaks.get("hbm_gbs", 6650.0)
+            ach = amount / t / 1e9
+            out[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "traffic": load_traffic(name),
+                         "algorithmic_per_launch": amount, "avg_launch_ms": t * 1e3}
+        else:
+            peak = peaks.get("fp64_tflops")
+            ach = amount / t / 1e12
+            out[name] = {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (ach / peak) if peak else None, "traffic": load_traffic(name),
+                         "algorithmic_per_launch": amount, "avg_launch_ms": t * 1e3}
+    dominant = max(items)[1]
+    return dominant, out
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle sample
+
+
+def cpu_sample(cp, budget_s: float, max_iters: int | None = None):
+    """Time the oracle port on this host: setup + as many iterations as fit."""
+    from oracle import hsde_oracle as O
+
+    try:
+        from threadpoolctl import threadpool_info
+
+        threads = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    st = O.OracleSettings(tol=1e-300, max_iters=max_iters or 10 ** 9)
+    sc, sb = O.normalization_scales(cp, st.normalize)
+    cpi = cp.with_data(c=sc * cp.c, b=sb * cp.b)
+    cache = O.setup_cache(cpi)
+    setup_s = time.perf_counter() - t0
+    u, w = O.initial_state(cpi)
+    t1 = time.perf_counter()
+    k = 0
+    while True:
+        u, w = O.iterate(cpi, cache, u, w, st.alpha)
+        k += 1
+        el = time.perf_counter() - t1
+        if el >= budget_s or (max_iters and k >= max_iters):
+            break
+    return {"iterations": k, "loop_s": el, "setup_s": setup_s, "threads": threads,
+            "rate": k / el}
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args):
+    rank, world, _ = _rank_env()
+    if rank != 0:
+        return 0
+    from paper_1611_01828_b200.synthetic import make_config, config_stats, CONFIG_NAMES
+
+    cp = make_config(args.config)
+    budget = float(os.environ.get("HSDE_REF_BUDGET_S", "45"))
+    # warm-up iterations are part of the sample's setup; the timed sample is
+    # the bounded loop (each "step" = one iteration of the same workload)
+    s = cpu_sample(cp, budget)
+    line = {
+        "metric": METRIC, "impl": "reference", "value": s["rate"], "unit": "iterations/s",
+        "n_gpus": args.gpus, "steps": s["iterations"], "warmup": 0,
+        "ms_per_step": 1e3 * s["loop_s"] / s["iterations"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[args.config], **config_stats(cp),
+                   "l2": "working set > L2 (A alone 0.92 GB in CSR+CSC)"},
+        "cpu_baseline": {"value": s["rate"], "unit": "iterations/s", "cores": s["threads"],
+                         "kind": "port",
+                         "sample": f"{s['iterations']} iterations of config {args.config} "
+                                   f"from the zero start after a {s['setup_s']:.1f}s setup, "
+                                   f"{s['loop_s']:.1f}s loop (oracle/hsde_oracle.py, numpy+scipy)"},
+        "e2e": {"value": s["iterations"] / (s["loop_s"] + s["setup_s"]), "unit": "iterations/s",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    rank, world, local = _rank_env()
+    import torch
+
+    import paper_1611_01828_b200 as H
+    from paper_1611_01828_b200 import _lib
+    from paper_1611_01828_b200.synthetic import make_config, config_stats, CONFIG_NAMES
+
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    cp = make_config(args.config)
+    # --- value: device-resident iterations (CUDA-graph replay) -------------------
+    h = _lib.Handle(cp, device=dev)
+    h.iterate(args.warmup)
+    h.sync()
+    sampler = ClockSampler(dev)
+    sampler.start()
+    time.sleep(0.15)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = h.time_iterations(args.steps)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    t_local = ms / 1e3
+    if dist:
+        t = torch.tensor([t_local], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_local = float(t.item())
+    value = world * args.steps / t_local
+    # --- roofline: per-kernel CUDA events over a few eager iterations ------------
+    prof_iters = 5
+    prof, launches = h.profile_iterations(prof_iters)
+    gpu_launches_per_iter = (launches - 1) / prof_iters
+    peaks = load_peaks()
+    dominant, roofs = roofline_for(cp, prof, prof_iters, peaks)
+    h.close()
+    line = None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_local / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator of BASELINE config; SURVEY 8d RNG order)",
+            "config": {"workload": CONFIG_NAMES[args.config], **config_stats(cp),
+                       "parallelism": "single GPU" if world == 1 else f"replicas x{world}",
+                       "l2": "no flush: per-iteration working set (A CSR+CSC 0.92 GB) > 126 MB L2"},
+            "clocks": clocks,
+            "gpu_launches": int(round(gpu_launches_per_iter * args.steps)) + 1,
+            "kernel_ms_per_iteration": {k: v / prof_iters for k, v in prof.items() if v > 0},
+        }
+        if roofs:
+            line["roofline"] = dict(roofs[dominant], kernel=dominant)
+            line["roofline_all"] = roofs
+    # --- e2e: public API on host data, default to-tolerance solve ------------------
+    if rank == 0 and not args.no_e2e:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = H.solve_decomposed(cp, H.SolverSettings(device=dev))
+        wall = time.perf_counter() - t0
+        nbytes = (cp.A.data.nbytes + cp.A.indices.nbytes // 2 + 8 * (cp.m + 1) + 8 * cp.N_c
+                  + 8 * cp.m + 8 * (cp.p + 1) + 4 * cp.p + 4 * cp.n_d)
+        checks = (rep.iterations + 19) // 20
+        d2h = checks * 8 * 16 + 8 * 2 * (cp.total)
+        line["e2e"] = {"value": rep.iterations / wall, "unit": "iterations/s",
+                       "h2d_bytes_per_step": int(nbytes / max(rep.iterations, 1)),
+                       "d2h_bytes_per_step": int(d2h / max(rep.iterations, 1)),
+                       "what": "solve_decomposed(CompressedProblem on host, default settings) "
+                               "wall clock: H2D + device setup + solve to 1e-4 + report"}
+        line["time_to_tol"] = {"status": rep.status, "iterations": rep.iterations,
+                               "iterations_s": rep.timing.iterations_s,
+                               "setup_s": rep.timing.setup_s, "wall_s": wall,
+                               "objective_primal": rep.objective_primal,
+                               "objective_dual": rep.objective_dual}
+    # --- other configs (small, latency-bound): iterations/s ----------------------------
+    if rank == 0 and not args.no_extras:
+        extra = {}
+        for c in (0, 1, 2, 3):
+            if c == args.config:
+                continue
+            cpc = make_config(c)
+            hc = _lib.Handle(cpc, device=dev)
+            hc.iterate(20)
+            hc.sync()
+            n_it = 500
+            msc = hc.time_iterations(n_it)
+            hc.close()
+            t0 = time.perf_counter()
+            rep = H.solve_decomposed(cpc, H.SolverSettings(device=dev))
+            wall = time.perf_counter() - t0
+            extra[CONFIG_NAMES[c]] = {
+                "iterations_per_s": n_it / (msc / 1e3), "to_tol_status": rep.status,
+                "to_tol_iterations": rep.iterations, "to_tol_wall_s": wall,
+                "to_tol_iterations_s": rep.timing.iterations_s}
+        line["other_configs"] = extra
+    # --- CPU baseline (rank 0, N=1 only) ----------------------------------------------
+    if rank == 0 and world == 1 and not args.no_cpu:
+        s = cpu_sample(cp, float(os.environ.get("HSDE_CPU_BUDGET_S", "20")))
+        line["cpu_baseline"] = {
+            "value": s["rate"], "unit": "iterations/s", "cores": s["threads"], "kind": "port",
+            "sample": f"{s['iterations']} iterations of config {args.config} from the zero start "
+                      f"({s['loop_s']:.1f}s loop after {s['setup_s']:.1f}s setup), "
+                      "oracle/hsde_oracle.py numpy+scipy"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

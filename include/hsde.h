@@ -1,0 +1,145 @@
+/*
+ * hsde.h -- C ABI of libhsde.so, the B200 (sm_100a, fp64) implementation of
+ * the per-iteration HSDE-ADMM hot path for chordally decomposed SDPs
+ * (arXiv:1611.01828; reference package `chordalsdp`).
+ *
+ * The reference is pure Python; it has no FFI.  Each entry point below
+ * replaces one reference function on the hot path (cited file:line, paths
+ * relative to /root/reference/pkg/src/chordalsdp/).  The Python shim
+ * `paper_1611_01828_b200` keeps the reference's Python signatures and calls
+ * these through ctypes.
+ *
+ * Vectors crossing this boundary use the COMPRESSED stacked layout
+ *     [ x : n_c | s : n_d | y : m | v : n_d | tau ]            (length T_c)
+ * i.e. the reference layout of solver.py:119-137 with x restricted to the
+ * n_c covered coordinates (clique-selected, A- or c-supported), ascending in
+ * the reference's column-stacked flat order.  All pointers are HOST pointers
+ * unless stated; the library copies what it needs to the device.
+ *
+ * Return codes: 0 OK, 1 CUDA error, 2 EigenFailure (non-finite eigenvalue,
+ * symmat.py:158-163), 3 FactorizationFailure (solver.py:254-259,270-273),
+ * 4 bad argument (ValueError), 5 TauZero (solver.py:410-412).
+ * A handle is single-threaded; it owns one CUDA stream on one device.
+ */
+#ifndef HSDE_H
+#define HSDE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HSDE_OK 0
+#define HSDE_ERR_CUDA 1
+#define HSDE_ERR_EIGEN 2
+#define HSDE_ERR_FACTOR 3
+#define HSDE_ERR_ARG 4
+#define HSDE_ERR_TAUZERO 5
+
+/* settings flags */
+#define HSDE_FLAG_EXACT_UY 1   /* uy = wy - A ua by an explicit CSR pass (solver.py:241)
+                                  instead of the identity A ua = S^{-1} A t        */
+#define HSDE_FLAG_NO_FACTOR 2  /* skip the Schur factorisation (residual-only handle) */
+
+typedef struct hsde_problem_desc {
+  int64_t n;                 /* ambient matrix order (informational)              */
+  int32_t m;                 /* constraints                                         */
+  int32_t n_c;               /* covered coordinates                                 */
+  int32_t p;                 /* cliques                                             */
+  int64_t n_d;               /* sum over cliques of d_k^2                           */
+  int64_t nnz;               /* nonzeros of A                                       */
+  const int64_t *a_row_ptr;  /* [m+1]  CSR of A over covered columns (decompose.py:148-165) */
+  const int32_t *a_col;      /* [nnz]  ascending within a row                       */
+  const double *a_val;       /* [nnz]                                               */
+  const double *c;           /* [n_c]  objective, ORIGINAL units                    */
+  const double *b;           /* [m]    right-hand side, ORIGINAL units              */
+  const int64_t *clique_offsets; /* [p+1] offsets of clique blocks in s (graphs.py:225-226) */
+  const int32_t *clique_sizes;   /* [p]                                             */
+  const int32_t *slot_cov;       /* [n_d] covered position of each clique slot
+                                     (graphs.py:184-187 gather_index, compressed)  */
+} hsde_problem_desc;
+
+typedef struct hsde_settings {
+  double alpha;              /* over-relaxation in [1,2)        (solver.py:84)     */
+  double tol;                /* termination tolerance           (solver.py:82)     */
+  double infeas_tau_tol;     /*                                  (solver.py:85)    */
+  double infeas_kappa_tol;   /*                                  (solver.py:86)    */
+  int32_t check_interval;    /*                                  (solver.py:87)    */
+  int32_t normalize;         /* scale c, b to unit norm          (solver.py:88,659-665) */
+  int32_t device;            /* CUDA device ordinal                                 */
+  int32_t flags;             /* HSDE_FLAG_*                                         */
+} hsde_settings;
+
+/* layout / scalar info returned by hsde_info */
+typedef struct hsde_info_t {
+  int64_t total;             /* T_c = n_c + 2 n_d + m + 1                           */
+  int32_t n_c, m, p;
+  int64_t n_d, nnz;
+  double sigma_c, sigma_b;   /* normalisation scales (solver.py:659-665)            */
+  double zeta_scale;         /* 1 + zeta . M^{-1} zeta           (solver.py:269)    */
+  int32_t schur_diagonal;    /* S = I + A P^{-1} A' is diagonal                     */
+  int32_t max_clique;
+} hsde_info_t;
+
+typedef struct hsde_handle hsde_t;
+
+/* Replaces setup_cache (solver.py:248-283) + _normalization_scales
+ * (:659-665) + initial_state (:366-372).  Copies the problem to the device,
+ * factors S = I + A P^{-1} A' (cuSOLVER, fp64) and stores S^{-1}, solves
+ * M zeta on the device.  The caller may free the desc buffers on return. */
+int hsde_create(const hsde_problem_desc *desc, const hsde_settings *settings, hsde_t **out);
+void hsde_destroy(hsde_t *h);
+const char *hsde_last_error(const hsde_t *h);  /* h may be NULL: last create error */
+int hsde_info(const hsde_t *h, hsde_info_t *out);
+
+/* State of the ADMM loop in the normalised problem (solver.py:358-363). */
+int hsde_set_state(hsde_t *h, const double *u, const double *w);
+int hsde_get_state(hsde_t *h, double *u, double *w);
+int hsde_reset_state(hsde_t *h);               /* initial_state (solver.py:366-372) */
+/* Change the over-relaxation alpha of subsequent iterations (iterate takes the
+ * settings per call, solver.py:375-380); rebuilds the iteration graphs. */
+int hsde_set_alpha(hsde_t *h, double alpha);
+
+/* Enqueue k iterations of `iterate` (solver.py:375-395) on the handle's stream
+ * (CUDA-graph replay, no host sync).  The state before the last of the k
+ * iterations is kept for the merit of hsde_check. */
+int hsde_iterate(hsde_t *h, int32_t k);
+
+/* Residual check of solve_decomposed (solver.py:721-742) on the device; one
+ * host sync.  out[0..7] = pres, dres, gap, tau, kappa, merit, |b|, |c|
+ * (pres/dres/gap = +inf when tau <= infeas_tau_tol, as solver.py:744-757).
+ * Returns HSDE_ERR_EIGEN if any PSD projection since the last check saw a
+ * non-finite eigenvalue. */
+#define HSDE_CHECK_LEN 8
+int hsde_check(hsde_t *h, double *out);
+
+/* Infeasibility-certificate quantities of _try_certificates (solver.py:455-505)
+ * on the unscaled iterate with the original data (solver.py:758-760).
+ * out: [0] b.y  [1] c.x  [2] |A'y/by + H'v/by|  [3] min clique eig of v/by
+ *      [4] |A x/(-cx)|  [5] |H x/(-cx) - s/(-cx)|  [6] min clique eig of H x/(-cx)
+ * Entries of a ray whose sign test fails (b.y <= 0, resp. c.x >= 0) are NaN. */
+#define HSDE_CERT_LEN 7
+int hsde_certificate(hsde_t *h, double *out);
+
+/* Unit-level entry points (compressed layout, host buffers), so the
+ * reference's operator oracles can be re-pointed at the device: */
+int hsde_affine_project(hsde_t *h, const double *w, double *u);        /* solver.py:296-318 */
+int hsde_solve_inner(hsde_t *h, const double *w12, double *u12);       /* solver.py:286-293 */
+int hsde_project_cone(hsde_t *h, const double *in, double *out);       /* solver.py:321-355 */
+int hsde_residuals(hsde_t *h, const double *u, double *out3);          /* solver.py:398-429 */
+int hsde_get_minv_zeta(hsde_t *h, double *out);                        /* KktCache.minv_zeta */
+
+/* Measurement hooks (bench.py): CUDA-event timing on the handle's stream. */
+int hsde_time_iterations(hsde_t *h, int32_t k, float *ms);             /* graph replay      */
+/* Per-kernel profile of k iterations launched eagerly with events around every
+ * kernel; names/ms arrays of length HSDE_PROFILE_SLOTS (ms summed over k). */
+#define HSDE_PROFILE_SLOTS 16
+int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches);
+const char *hsde_profile_name(int32_t slot);
+int hsde_sync(hsde_t *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSDE_H */

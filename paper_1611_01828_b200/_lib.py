@@ -1,0 +1,294 @@
+"""ctypes binding of libhsde.so (include/hsde.h).
+
+The shared library is built in-tree (``make -C paper_1611_01828_b200/csrc``
+or ``__graft_entry__.build()``).  There is no CPU fallback: if the library or
+a CUDA device is missing, every product entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+from .errors import EigenFailure, FactorizationFailure, TauZero
+
+LIB_PATH = Path(__file__).resolve().parent / "libhsde.so"
+
+HSDE_OK, HSDE_ERR_CUDA, HSDE_ERR_EIGEN, HSDE_ERR_FACTOR, HSDE_ERR_ARG, HSDE_ERR_TAUZERO = range(6)
+HSDE_FLAG_EXACT_UY = 1
+HSDE_FLAG_NO_FACTOR = 2
+HSDE_CHECK_LEN = 8
+HSDE_CERT_LEN = 7
+HSDE_PROFILE_SLOTS = 16
+
+EXPORTED = (
+    "hsde_create", "hsde_destroy", "hsde_last_error", "hsde_info", "hsde_set_state",
+    "hsde_get_state", "hsde_reset_state", "hsde_iterate", "hsde_check", "hsde_certificate",
+    "hsde_affine_project", "hsde_solve_inner", "hsde_project_cone", "hsde_residuals",
+    "hsde_get_minv_zeta", "hsde_time_iterations", "hsde_profile_iterations",
+    "hsde_profile_name", "hsde_sync", "hsde_set_alpha",
+)
+
+_dp = C.POINTER(C.c_double)
+_i64p = C.POINTER(C.c_int64)
+_i32p = C.POINTER(C.c_int32)
+
+
+class ProblemDesc(C.Structure):
+    _fields_ = [
+        ("n", C.c_int64), ("m", C.c_int32), ("n_c", C.c_int32), ("p", C.c_int32),
+        ("n_d", C.c_int64), ("nnz", C.c_int64),
+        ("a_row_ptr", _i64p), ("a_col", _i32p), ("a_val", _dp),
+        ("c", _dp), ("b", _dp),
+        ("clique_offsets", _i64p), ("clique_sizes", _i32p), ("slot_cov", _i32p),
+    ]
+
+
+class Settings(C.Structure):
+    _fields_ = [
+        ("alpha", C.c_double), ("tol", C.c_double), ("infeas_tau_tol", C.c_double),
+        ("infeas_kappa_tol", C.c_double), ("check_interval", C.c_int32),
+        ("normalize", C.c_int32), ("device", C.c_int32), ("flags", C.c_int32),
+    ]
+
+
+class Info(C.Structure):
+    _fields_ = [
+        ("total", C.c_int64), ("n_c", C.c_int32), ("m", C.c_int32), ("p", C.c_int32),
+        ("n_d", C.c_int64), ("nnz", C.c_int64), ("sigma_c", C.c_double),
+        ("sigma_b", C.c_double), ("zeta_scale", C.c_double), ("schur_diagonal", C.c_int32),
+        ("max_clique", C.c_int32),
+    ]
+
+
+_LIB = None
+
+
+def load() -> C.CDLL:
+    """Load libhsde.so (fail loudly: there is no fallback path)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not LIB_PATH.exists():
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `make -C paper_1611_01828_b200/csrc` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(str(LIB_PATH))
+    vp = C.c_void_p
+    sig = {
+        "hsde_create": (C.c_int, [C.POINTER(ProblemDesc), C.POINTER(Settings), C.POINTER(vp)]),
+        "hsde_destroy": (None, [vp]),
+        "hsde_last_error": (C.c_char_p, [vp]),
+        "hsde_info": (C.c_int, [vp, C.POINTER(Info)]),
+        "hsde_set_state": (C.c_int, [vp, _dp, _dp]),
+        "hsde_get_state": (C.c_int, [vp, _dp, _dp]),
+        "hsde_reset_state": (C.c_int, [vp]),
+        "hsde_iterate": (C.c_int, [vp, C.c_int32]),
+        "hsde_check": (C.c_int, [vp, _dp]),
+        "hsde_certificate": (C.c_int, [vp, _dp]),
+        "hsde_affine_project": (C.c_int, [vp, _dp, _dp]),
+        "hsde_solve_inner": (C.c_int, [vp, _dp, _dp]),
+        "hsde_project_cone": (C.c_int, [vp, _dp, _dp]),
+        "hsde_residuals": (C.c_int, [vp, _dp, _dp]),
+        "hsde_get_minv_zeta": (C.c_int, [vp, _dp]),
+        "hsde_time_iterations": (C.c_int, [vp, C.c_int32, C.POINTER(C.c_float)]),
+        "hsde_profile_iterations": (C.c_int, [vp, C.c_int32, C.POINTER(C.c_float), _i32p]),
+        "hsde_profile_name": (C.c_char_p, [C.c_int32]),
+        "hsde_sync": (C.c_int, [vp]),
+        "hsde_set_alpha": (C.c_int, [vp, C.c_double]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = lib
+    return lib
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def raise_for(rc: int, msg: str):
+    if rc == HSDE_OK:
+        return
+    if rc == HSDE_ERR_EIGEN:
+        raise EigenFailure(msg)
+    if rc == HSDE_ERR_FACTOR:
+        raise FactorizationFailure(msg)
+    if rc == HSDE_ERR_TAUZERO:
+        raise TauZero(msg)
+    if rc == HSDE_ERR_ARG:
+        raise ValueError(msg)
+    raise RuntimeError(f"libhsde CUDA error: {msg}")
+
+
+class Handle:
+    """Owns one device-resident problem + ADMM state (one hsde_t)."""
+
+    def __init__(self, cp, *, alpha=1.6, tol=1e-4, infeas_tau_tol=1e-9, infeas_kappa_tol=1e-6,
+                 check_interval=20, normalize=True, device=0, flags=0):
+        lib = load()
+        self._lib = lib
+        self.cp = cp
+        A = cp.A
+        self._keep = keep = {
+            "rp": np.ascontiguousarray(A.indptr, dtype=np.int64),
+            "col": np.ascontiguousarray(A.indices, dtype=np.int32),
+            "val": np.ascontiguousarray(A.data, dtype=np.float64),
+            "c": np.ascontiguousarray(cp.c, dtype=np.float64),
+            "b": np.ascontiguousarray(cp.b, dtype=np.float64),
+            "off": np.ascontiguousarray(cp.offsets, dtype=np.int64),
+            "sz": np.ascontiguousarray(cp.sizes, dtype=np.int32),
+            "sc": np.ascontiguousarray(cp.slot_cov, dtype=np.int32),
+        }
+        desc = ProblemDesc(
+            n=cp.n, m=cp.m, n_c=cp.N_c, p=cp.p, n_d=cp.n_d, nnz=int(A.nnz),
+            a_row_ptr=_ptr(keep["rp"], C.c_int64), a_col=_ptr(keep["col"], C.c_int32),
+            a_val=_ptr(keep["val"], C.c_double), c=_ptr(keep["c"], C.c_double),
+            b=_ptr(keep["b"], C.c_double), clique_offsets=_ptr(keep["off"], C.c_int64),
+            clique_sizes=_ptr(keep["sz"], C.c_int32), slot_cov=_ptr(keep["sc"], C.c_int32))
+        st = Settings(alpha=alpha, tol=tol, infeas_tau_tol=infeas_tau_tol,
+                      infeas_kappa_tol=infeas_kappa_tol, check_interval=check_interval,
+                      normalize=1 if normalize else 0, device=device, flags=flags)
+        h = C.c_void_p()
+        rc = lib.hsde_create(C.byref(desc), C.byref(st), C.byref(h))
+        if rc != HSDE_OK:
+            raise_for(rc, lib.hsde_last_error(None).decode())
+        self._h = h
+        self._keep = None  # library copied everything
+        inf = Info()
+        lib.hsde_info(h, C.byref(inf))
+        self.total = int(inf.total)
+        self.sigma_c = float(inf.sigma_c)
+        self.sigma_b = float(inf.sigma_b)
+        self.zeta_scale = float(inf.zeta_scale)
+        self.schur_diagonal = bool(inf.schur_diagonal)
+        self.max_clique = int(inf.max_clique)
+        self.alpha = alpha
+
+    # -- plumbing -------------------------------------------------------------
+    def _rc(self, rc):
+        if rc != HSDE_OK:
+            raise_for(rc, self._lib.hsde_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.hsde_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _vec(self, a, n=None):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        if n is not None and a.shape != (n,):
+            raise ValueError(f"expected length {n}, got {a.shape}")
+        return a
+
+    # -- state -----------------------------------------------------------------
+    def set_alpha(self, alpha: float):
+        if alpha != self.alpha:
+            self._rc(self._lib.hsde_set_alpha(self._h, float(alpha)))
+            self.alpha = alpha
+
+    def set_state(self, u, w):
+        u = self._vec(u, self.total)
+        w = self._vec(w, self.total)
+        self._rc(self._lib.hsde_set_state(self._h, _ptr(u, C.c_double), _ptr(w, C.c_double)))
+
+    def get_state(self):
+        u = np.empty(self.total)
+        w = np.empty(self.total)
+        self._rc(self._lib.hsde_get_state(self._h, _ptr(u, C.c_double), _ptr(w, C.c_double)))
+        return u, w
+
+    def reset_state(self):
+        self._rc(self._lib.hsde_reset_state(self._h))
+
+    def iterate(self, k: int):
+        self._rc(self._lib.hsde_iterate(self._h, int(k)))
+
+    def sync(self):
+        self._rc(self._lib.hsde_sync(self._h))
+
+    def check(self) -> np.ndarray:
+        out = np.empty(HSDE_CHECK_LEN)
+        self._rc(self._lib.hsde_check(self._h, _ptr(out, C.c_double)))
+        return out
+
+    def certificate(self) -> np.ndarray:
+        out = np.empty(HSDE_CERT_LEN)
+        self._rc(self._lib.hsde_certificate(self._h, _ptr(out, C.c_double)))
+        return out
+
+    # -- unit-level -----------------------------------------------------------------
+    def affine_project(self, w):
+        w = self._vec(w, self.total)
+        u = np.empty(self.total)
+        self._rc(self._lib.hsde_affine_project(self._h, _ptr(w, C.c_double), _ptr(u, C.c_double)))
+        return u
+
+    def solve_inner(self, w12):
+        w12 = self._vec(w12, self.total - 1)
+        u = np.empty(self.total - 1)
+        self._rc(self._lib.hsde_solve_inner(self._h, _ptr(w12, C.c_double), _ptr(u, C.c_double)))
+        return u
+
+    def project_cone(self, v):
+        v = self._vec(v, self.total)
+        out = np.empty(self.total)
+        self._rc(self._lib.hsde_project_cone(self._h, _ptr(v, C.c_double), _ptr(out, C.c_double)))
+        return out
+
+    def residuals(self, u):
+        u = self._vec(u, self.total)
+        out = np.empty(3)
+        self._rc(self._lib.hsde_residuals(self._h, _ptr(u, C.c_double), _ptr(out, C.c_double)))
+        return out
+
+    def minv_zeta(self):
+        out = np.empty(self.total - 1)
+        self._rc(self._lib.hsde_get_minv_zeta(self._h, _ptr(out, C.c_double)))
+        return out
+
+    # -- measurement ---------------------------------------------------------------------
+    def time_iterations(self, k: int) -> float:
+        ms = C.c_float()
+        self._rc(self._lib.hsde_time_iterations(self._h, int(k), C.byref(ms)))
+        return float(ms.value)
+
+    def profile_iterations(self, k: int):
+        ms = (C.c_float * HSDE_PROFILE_SLOTS)()
+        nl = C.c_int32()
+        self._rc(self._lib.hsde_profile_iterations(self._h, int(k), ms, C.byref(nl)))
+        out = {}
+        for i in range(HSDE_PROFILE_SLOTS):
+            name = self._lib.hsde_profile_name(i).decode()
+            if name:
+                out[name] = float(ms[i])
+        return out, int(nl.value)
+
+
+def exported_symbols() -> list[str]:
+    """Symbols include/hsde.h declares (checked by the CPU tests)."""
+    return list(EXPORTED)
+
+
+def device_count() -> int:
+    try:
+        import torch
+
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def default_device() -> int:
+    return int(os.environ.get("HSDE_DEVICE", os.environ.get("LOCAL_RANK", "0")))

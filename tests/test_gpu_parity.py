@@ -1,0 +1,268 @@
+"""GPU parity tests: the CUDA path (through libhsde.so's C ABI) vs the
+reference's golden outputs, the dense oracles, and the CPU oracle.
+
+Tolerances (written per test) follow BASELINE.json's north_star: iterates
+after a fixed iteration count within 1e-8 relative; at termination the same
+status / certificate type, iteration count +-2 and objective within 1e-6
+relative.  Unit-level operators match the reference's own oracle
+tolerances (test_solver_oracles.py: 1e-10 dense solve, 1e-12 cone, 1e-14
+golden first iteration).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1611_01828_b200 as H
+from helpers import dense_embedding, dense_inner, rel, toy_problem
+from oracle import hsde_oracle as O
+from paper_1611_01828_b200.problem import compress
+from paper_1611_01828_b200.synthetic import make_config
+
+pytestmark = pytest.mark.gpu
+
+
+def test_golden_first_iteration(golden_dir):
+    z = np.load(golden_dir / "first_iteration.npz")
+    dp = toy_problem(z)
+    cache = H.setup_cache(dp)
+    _, layout = H.build_hsde(dp)
+    st = H.iterate(H.initial_state(layout), cache, layout, H.SolverSettings(alpha=1.0, normalize=False))
+    assert np.allclose(st.u, z["u"], atol=1e-14, rtol=0)
+    assert np.allclose(st.w_dual, z["w"], atol=1e-14, rtol=0)
+
+
+def _toys(golden_dir):
+    z = np.load(golden_dir / "toys.npz")
+    for t in range(int(z["count"])):
+        yield t, z, f"t{t}_"
+
+
+def test_affine_and_inner_match_dense_and_reference(golden_dir):
+    """test_solver_oracles.py:201-219 and acceptance criterion 6 (<= 1e-9)."""
+    worst = [0.0] * 4
+    for t, z, pre in _toys(golden_dir):
+        dp = toy_problem(z, pre)
+        cache = H.setup_cache(dp)
+        assert cache.factored_dims == (dp.m,)
+        w = z[pre + "aff_in"]
+        got = H.affine_project(cache, w)
+        ref = np.linalg.solve(np.eye(w.size) + dense_embedding(dp), w)
+        worst[0] = max(worst[0], rel(got, ref))
+        worst[1] = max(worst[1], rel(got, z[pre + "aff_out"]))
+        n12a = dp.n * dp.n + dp.n_d
+        w2 = z[pre + "inner_in"]
+        u1, u2 = H.solve_inner(cache, w2[:n12a], w2[n12a:])
+        got2 = np.concatenate([u1, u2])
+        worst[2] = max(worst[2], rel(got2, np.linalg.solve(dense_inner(dp), w2)))
+        worst[3] = max(worst[3], rel(got2, z[pre + "inner_out"]))
+    assert worst[0] <= 1e-10 and worst[2] <= 1e-9, worst
+    assert worst[1] <= 1e-11 and worst[3] <= 1e-11, worst
+
+
+def test_affine_inner_product_identity(golden_dir):
+    """(I + Q) u = w with skew Q forces u'w = |u|^2 (test_solver_oracles.py:221-231)."""
+    z = np.load(golden_dir / "toys.npz")
+    dp = toy_problem(z, "t3_")
+    cache = H.setup_cache(dp)
+    rng = np.random.default_rng(11)
+    _, layout = H.build_hsde(dp)
+    for _ in range(20):
+        w = rng.normal(size=layout.total)
+        u = H.affine_project(cache, w)
+        assert u @ w >= 0
+        assert np.isclose(u @ w, u @ u, rtol=1e-9)
+
+
+def test_project_cone_matches_reference(golden_dir):
+    worst = 0.0
+    for t, z, pre in _toys(golden_dir):
+        dp = toy_problem(z, pre)
+        _, layout = H.build_hsde(dp)
+        got = H.project_cone(z[pre + "cone_in"], layout)
+        worst = max(worst, rel(got, z[pre + "cone_out"]))
+        # free blocks pass through bit for bit (test_solver_oracles.py:270-273)
+        assert np.array_equal(got[layout.sl_x], z[pre + "cone_in"][layout.sl_x])
+        assert np.array_equal(got[layout.sl_v], z[pre + "cone_in"][layout.sl_v])
+    assert worst <= 1e-12
+
+
+def test_project_cone_fixed_point_and_tau_clamp(golden_dir):
+    z = np.load(golden_dir / "toys.npz")
+    dp = toy_problem(z, "t5_")
+    _, layout = H.build_hsde(dp)
+    rng = np.random.default_rng(13)
+    u = rng.normal(size=layout.total)
+    for k in range(dp.p):
+        d = int(dp.dec.sizes[k])
+        g = rng.normal(size=(d, d))
+        u[layout.sl_s][dp.dec.offsets[k]: dp.dec.offsets[k + 1]] = (g @ g.T).ravel()
+    u[layout.idx_tau] = -1.0
+    got = H.project_cone(u, layout)
+    assert got[layout.idx_tau] == 0.0
+    assert np.allclose(got[layout.sl_s], u[layout.sl_s], atol=1e-12)
+
+
+def test_iterate_matches_reference_from_random_starts(golden_dir):
+    worst = 0.0
+    for t, z, pre in _toys(golden_dir):
+        dp = toy_problem(z, pre)
+        cache = H.setup_cache(dp)
+        _, layout = H.build_hsde(dp)
+        st = H.iterate(H.HsdeState(z[pre + "it_u0"], z[pre + "it_w0"]), cache, layout, H.SolverSettings())
+        worst = max(worst, rel(st.u, z[pre + "it_u1"]), rel(st.w_dual, z[pre + "it_w1"]))
+        # dual-side zero blocks exactly zero (test_solver_oracles.py:396-399)
+        assert not st.w_dual[layout.sl_x].any()
+        assert not st.w_dual[layout.sl_y].any()
+        assert not st.w_dual[layout.sl_v].any()
+        # Moreau: complementarity, tau/kappa >= 0
+        scale = max(np.linalg.norm(st.u) * np.linalg.norm(st.w_dual), 1e-30)
+        assert abs(st.u @ st.w_dual) <= 1e-9 * scale
+        assert st.u[-1] >= 0 and st.w_dual[-1] >= 0
+    assert worst <= 1e-10
+
+
+def test_toy_solves_match_reference(golden_dir):
+    for t, z, pre in _toys(golden_dir):
+        dp = toy_problem(z, pre)
+        rep = H.solve_decomposed(dp, H.SolverSettings(max_iters=400, check_interval=20))
+        assert rep.status == str(z[pre + "solve_status"]), t
+        assert abs(rep.iterations - int(z[pre + "solve_iters"])) <= 2, t
+        ref = z[pre + "solve_obj"]
+        if rep.objective_primal is not None and not math.isnan(ref[0]):
+            assert abs(rep.objective_primal - ref[0]) <= 1e-6 * (1 + abs(ref[0])), t
+
+
+def test_residuals_and_tauzero(golden_dir):
+    z = np.load(golden_dir / "toys.npz")
+    dp = toy_problem(z, "t2_")
+    _, layout = H.build_hsde(dp)
+    rng = np.random.default_rng(22)
+    u = rng.normal(size=layout.total)
+    u[-1] = 1.3
+    cp = compress(dp, full=True)
+    want = O.residuals(cp, cp.compress_vector(u))
+    got = H.residuals(H.HsdeState(u, np.zeros_like(u)), dp)
+    assert np.allclose([got.primal, got.dual, got.gap], want, rtol=1e-12)
+    u[-1] = 0.0
+    with pytest.raises(H.TauZero):
+        H.residuals(H.HsdeState(u, np.zeros_like(u)), dp)
+
+
+def test_factorization_failure_on_bad_data():
+    from paper_1611_01828_b200.problem import CliqueDecomposition, DecomposedProblem
+    import scipy.sparse as sp
+
+    dec = CliqueDecomposition.build(2, [[0, 1]])
+    dp = DecomposedProblem(n=2, m=1, c=np.zeros(4), A=sp.csr_matrix(np.array([[np.inf, 0, 0, 1.0]])),
+                           b=np.array([1.0]), dec=dec, block_dims=(2,))
+    with pytest.raises(H.FactorizationFailure):
+        H.setup_cache(dp)
+
+
+def test_eigen_failure_on_nan():
+    from paper_1611_01828_b200.problem import CliqueDecomposition, DecomposedProblem
+    import scipy.sparse as sp
+
+    dec = CliqueDecomposition.build(3, [[0, 1, 2]])
+    dp = DecomposedProblem(n=3, m=1, c=np.zeros(9), A=sp.csr_matrix(np.eye(3).reshape(1, 9)),
+                           b=np.array([1.0]), dec=dec, block_dims=(3,))
+    _, layout = H.build_hsde(dp)
+    u = np.ones(layout.total)
+    u[layout.sl_s][4] = np.nan
+    with pytest.raises(H.EigenFailure):
+        H.project_cone(u, layout)
+
+
+# --------------------------------------------------------------------------
+# BASELINE configs vs the live-reference fixtures
+
+
+def _fixed_run(cfg, iters):
+    cp = make_config(cfg)
+    states = {}
+    logs = []
+
+    def cb(info):
+        logs.append((info.iteration, info.pres, info.dres, info.gap, info.tau, info.kappa))
+        if info.iteration == iters:
+            states["u"], states["w"] = info.state.u.copy(), info.state.w_dual.copy()
+
+    H.solve_decomposed(cp, H.SolverSettings(max_iters=iters, tol=1e-300), iteration_callback=cb)
+    return cp, states, np.array(logs)
+
+
+def _compare_state(z, cp, u, w, tol):
+    if "fixed_u" in z.files:
+        assert rel(u, z["fixed_u"]) <= tol
+        assert rel(w, z["fixed_w"]) <= tol
+    else:
+        for name, vec in (("u", u), ("w", w)):
+            idx, val = z[f"fixed_{name}_idx"], z[f"fixed_{name}_val"]
+            scale = max(np.linalg.norm(z[f"fixed_{name}_norms"][:4]), 1e-300)
+            assert np.linalg.norm(vec[idx] - val) <= tol * scale * math.sqrt(idx.size / vec.size) + 1e-300
+            norms = np.array([np.linalg.norm(vec[sl]) for sl in (cp.sl_x, cp.sl_s, cp.sl_y, cp.sl_v)]
+                             + [vec[-1]])
+            ref = z[f"fixed_{name}_norms"]
+            assert np.allclose(norms, ref, rtol=tol, atol=tol * scale)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_config_fixed_iterations(golden_dir, cfg):
+    """Iterates after 500 iterations within 1e-8 relative of the reference."""
+    z = np.load(golden_dir / f"cfg{cfg}_reference.npz")
+    iters = int(z["fixed_iters"])
+    cp, st, logs = _fixed_run(cfg, iters)
+    _compare_state(z, cp, st["u"], st["w"], 1e-8)
+    ref = z["fixed_log"]
+    assert np.array_equal(logs[:, 0], ref[:, 0])
+    finite = np.isfinite(ref[:, 1])
+    assert np.array_equal(np.isfinite(logs[:, 1]), finite)
+    assert np.allclose(logs[finite, 1:4], ref[finite, 1:4], rtol=1e-6)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_config_to_tolerance(golden_dir, cfg):
+    z = np.load(golden_dir / f"cfg{cfg}_reference.npz")
+    rep = H.solve_decomposed(make_config(cfg), H.SolverSettings())
+    assert rep.status == str(z["tol_status"])
+    assert abs(rep.iterations - int(z["tol_iters"])) <= 2
+    if rep.certificate is not None:
+        assert rep.certificate["ray"] == str(z["cert_ray"])
+        assert rep.certificate["b_dot_y"] == 1.0
+        assert np.allclose(rep.certificate["y"], z["cert_y"], rtol=1e-6, atol=1e-9)
+        assert rep.certificate["residual"] <= 1e-4
+        assert rep.certificate["min_block_eigenvalue"] >= -1e-4
+    else:
+        ref = z["tol_obj"]
+        assert abs(rep.objective_primal - ref[0]) <= 1e-6 * abs(ref[0])
+        assert abs(rep.objective_dual - ref[1]) <= 1e-6 * abs(ref[1])
+
+
+def test_runs_are_bitwise_reproducible():
+    cp = make_config(0)
+    out = []
+    for _ in range(2):
+        got = {}
+
+        def cb(info):
+            if info.iteration == 100:
+                got["u"] = info.state.u.copy()
+
+        H.solve_decomposed(cp, H.SolverSettings(max_iters=100, tol=1e-300), iteration_callback=cb)
+        out.append(got["u"])
+    assert np.array_equal(out[0], out[1])
+
+
+def test_exact_uy_flag_matches_identity_path():
+    """uy by an explicit A ua pass (solver.py:241) vs the identity A ua = S^-1 A t."""
+    from paper_1611_01828_b200 import _lib
+
+    cp = make_config(0)
+    res = []
+    for flags in (0, _lib.HSDE_FLAG_EXACT_UY):
+        h = _lib.Handle(cp, flags=flags)
+        h.iterate(200)
+        res.append(h.get_state()[0])
+        h.close()
+    assert rel(res[1], res[0]) <= 1e-10
