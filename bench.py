@@ -282,6 +282,7 @@ def run_ours(args):
     # --- roofline: per-kernel CUDA events over a few eager iterations ------------
     prof_iters = 5
     prof, launches = h.profile_iterations(prof_iters)
+    eig_stats = h.stats()
     gpu_launches_per_iter = (launches - 1) / prof_iters
     peaks = load_peaks()
     dominant, roofs = roofline_for(cp, prof, prof_iters, peaks)
@@ -299,6 +300,7 @@ def run_ours(args):
             "clocks": clocks,
             "gpu_launches": int(round(gpu_launches_per_iter * args.steps)) + 1,
             "kernel_ms_per_iteration": {k: v / prof_iters for k, v in prof.items() if v > 0},
+            "eig_stats": eig_stats,
         }
         if roofs:
             line["roofline"] = dict(roofs[dominant], kernel=dominant)

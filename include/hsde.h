@@ -41,6 +41,7 @@ extern "C" {
 #define HSDE_FLAG_EXACT_UY 1   /* uy = wy - A ua by an explicit CSR pass (solver.py:241)
                                   instead of the identity A ua = S^{-1} A t        */
 #define HSDE_FLAG_NO_FACTOR 2  /* skip the Schur factorisation (residual-only handle) */
+#define HSDE_FLAG_COLD_EIG 4   /* no warm start of the clique eigensolves             */
 
 typedef struct hsde_problem_desc {
   int64_t n;                 /* ambient matrix order (informational)              */
@@ -138,6 +139,11 @@ int hsde_time_iterations(hsde_t *h, int32_t k, float *ms);             /* graph 
 int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches);
 const char *hsde_profile_name(int32_t slot);
 int hsde_sync(hsde_t *h);
+/* Eigensolver statistics of the last hot projection:
+ * out[0] mean Jacobi sweeps per clique, out[1] max, out[2] mean over d > 32,
+ * out[3] 1 if warm starts are enabled. */
+#define HSDE_STATS_LEN 4
+int hsde_stats(hsde_t *h, double *out);
 
 #ifdef __cplusplus
 }

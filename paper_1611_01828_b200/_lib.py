@@ -20,6 +20,8 @@ LIB_PATH = Path(__file__).resolve().parent / "libhsde.so"
 HSDE_OK, HSDE_ERR_CUDA, HSDE_ERR_EIGEN, HSDE_ERR_FACTOR, HSDE_ERR_ARG, HSDE_ERR_TAUZERO = range(6)
 HSDE_FLAG_EXACT_UY = 1
 HSDE_FLAG_NO_FACTOR = 2
+HSDE_FLAG_COLD_EIG = 4
+HSDE_STATS_LEN = 4
 HSDE_CHECK_LEN = 8
 HSDE_CERT_LEN = 7
 HSDE_PROFILE_SLOTS = 16
@@ -29,7 +31,7 @@ EXPORTED = (
     "hsde_get_state", "hsde_reset_state", "hsde_iterate", "hsde_check", "hsde_certificate",
     "hsde_affine_project", "hsde_solve_inner", "hsde_project_cone", "hsde_residuals",
     "hsde_get_minv_zeta", "hsde_time_iterations", "hsde_profile_iterations",
-    "hsde_profile_name", "hsde_sync", "hsde_set_alpha",
+    "hsde_profile_name", "hsde_sync", "hsde_set_alpha", "hsde_stats",
 )
 
 _dp = C.POINTER(C.c_double)
@@ -99,6 +101,7 @@ def load() -> C.CDLL:
         "hsde_profile_name": (C.c_char_p, [C.c_int32]),
         "hsde_sync": (C.c_int, [vp]),
         "hsde_set_alpha": (C.c_int, [vp, C.c_double]),
+        "hsde_stats": (C.c_int, [vp, _dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -257,6 +260,12 @@ class Handle:
         out = np.empty(self.total - 1)
         self._rc(self._lib.hsde_get_minv_zeta(self._h, _ptr(out, C.c_double)))
         return out
+
+    def stats(self) -> dict:
+        out = np.empty(HSDE_STATS_LEN)
+        self._rc(self._lib.hsde_stats(self._h, _ptr(out, C.c_double)))
+        return {"mean_sweeps": float(out[0]), "max_sweeps": float(out[1]),
+                "mean_sweeps_large": float(out[2]), "warm_start": bool(out[3])}
 
     # -- measurement ---------------------------------------------------------------------
     def time_iterations(self, k: int) -> float:

@@ -75,6 +75,7 @@ struct hsde_handle {
   cudaGraphExec_t g1 = nullptr, gci = nullptr;
   int gci_len = 0;
   bool factor = true;
+  bool warm = true;               // warm-started eigensolves (HSDE_FLAG_COLD_EIG clears)
 };
 
 #define CK(call)                                                                      \
@@ -174,7 +175,7 @@ __global__ void k_finite_check(const double *x, int64_t n, int *flag) {
 int launch_cone(hsde_handle *h, int mode, const ConePlan &pl, bool block, const double *in,
                 double *out, double in_scale, cudaStream_t st) {
   if (pl.count == 0) return 0;
-  ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale};
+  ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0};
   if (!block) {
     const int grid = (pl.count + pl.per_block - 1) / pl.per_block;
     const int thr = pl.per_block * 32;
@@ -182,9 +183,9 @@ int launch_cone(hsde_handle *h, int mode, const ConePlan &pl, bool block, const 
     else if (mode == CONE_PLAIN) k_cone_warp<CONE_PLAIN><<<grid, thr, pl.smem, st>>>(h->P, h->S, h->W, ca);
     else k_cone_warp<CONE_MINEIG><<<grid, thr, pl.smem, st>>>(h->P, h->S, h->W, ca);
   } else {
-    if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kBlock, pl.smem, st>>>(h->P, h->S, h->W, ca);
-    else if (mode == CONE_PLAIN) k_cone_block<CONE_PLAIN><<<pl.count, kBlock, pl.smem, st>>>(h->P, h->S, h->W, ca);
-    else k_cone_block<CONE_MINEIG><<<pl.count, kBlock, pl.smem, st>>>(h->P, h->S, h->W, ca);
+    if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(h->P, h->S, h->W, ca);
+    else if (mode == CONE_PLAIN) k_cone_block<CONE_PLAIN><<<pl.count, kConeBlock, pl.smem, st>>>(h->P, h->S, h->W, ca);
+    else k_cone_block<CONE_MINEIG><<<pl.count, kConeBlock, pl.smem, st>>>(h->P, h->S, h->W, ca);
   }
   CKL();
   return 0;
@@ -478,6 +479,7 @@ int init_state(hsde_handle *h) {
   CK(cudaMemcpyAsync(h->S.w + T - 1, &one, sizeof(double), cudaMemcpyHostToDevice, h->st));
   CK(cudaMemcpyAsync(h->d_prev_u, h->S.u, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
   CK(cudaMemcpyAsync(h->d_prev_w, h->S.w, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaMemsetAsync(h->W.vvalid, 0, sizeof(int) * std::max(h->P.p, 1), h->st));
   CK(cudaStreamSynchronize(h->st));
   return 0;
 }
@@ -507,6 +509,7 @@ int hsde_create(const hsde_problem_desc *d, const hsde_settings *s, hsde_t **out
   h->set = *s;
   h->dev = s->device;
   h->factor = !(s->flags & HSDE_FLAG_NO_FACTOR);
+  h->warm = !(s->flags & HSDE_FLAG_COLD_EIG);
   auto fail = [&](int rc) {
     g_create_error = h->err;
     hsde_destroy(h);
@@ -685,8 +688,12 @@ int hsde_create(const hsde_problem_desc *d, const hsde_settings *s, hsde_t **out
       (rc = dalloc(h, &h->W.qp, m)) || (rc = dalloc(h, &h->W.uy, m)) ||
       (rc = dalloc(h, &h->W.part, kMaxParts)) || (rc = dalloc(h, &h->W.scal, S_COUNT)) ||
       (rc = dalloc(h, &h->W.err, 1)) || (rc = dalloc(h, &h->d_chk, 64)) ||
-      (rc = dalloc(h, &h->d_mineig, std::max(p, 1))))
+      (rc = dalloc(h, &h->d_mineig, std::max(p, 1))) || (rc = dalloc(h, &h->W.vstore, n_d)) ||
+      (rc = dalloc(h, &h->W.vvalid, std::max(p, 1))) || (rc = dalloc(h, &h->W.sweeps, std::max(p, 1))))
     return fail(rc);
+  if (cudaMemset(h->W.vvalid, 0, sizeof(int) * std::max(p, 1)) != cudaSuccess ||
+      cudaMemset(h->W.sweeps, 0, sizeof(int) * std::max(p, 1)) != cudaSuccess)
+    return fail(HSDE_ERR_CUDA);
   if (cudaMemset(h->W.err, 0, sizeof(int)) != cudaSuccess) return fail(HSDE_ERR_CUDA);
   if (cudaMallocHost(&h->h_chk, 64 * sizeof(double)) != cudaSuccess) {
     h->err = "cudaMallocHost failed";
@@ -786,6 +793,7 @@ int hsde_set_state(hsde_t *h, const double *u, const double *w) {
   CK(cudaMemcpyAsync(h->S.w, w, sizeof(double) * T, cudaMemcpyHostToDevice, h->st));
   CK(cudaMemcpyAsync(h->d_prev_u, h->S.u, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
   CK(cudaMemcpyAsync(h->d_prev_w, h->S.w, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaMemsetAsync(h->W.vvalid, 0, sizeof(int) * std::max(h->P.p, 1), h->st));
   CK(cudaStreamSynchronize(h->st));
   return HSDE_OK;
 }
@@ -1132,6 +1140,30 @@ int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches) 
   for (auto &e : ev) cudaEventDestroy(e);
   if (launches) *launches = nl;
   return check_err_flag(h);
+}
+
+int hsde_stats(hsde_t *h, double *out) {
+  if (!h || !out) return HSDE_ERR_ARG;
+  cudaSetDevice(h->dev);
+  std::vector<int> sw(std::max(h->P.p, 1));
+  CK(cudaMemcpyAsync(sw.data(), h->W.sweeps, sizeof(int) * sw.size(), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  double sum = 0, mx = 0, sum_big = 0, n_big = 0;
+  std::vector<int> sizes(h->P.p);
+  if (h->P.p) CK(cudaMemcpy(sizes.data(), h->P.cl_size, sizeof(int) * h->P.p, cudaMemcpyDeviceToHost));
+  for (int k = 0; k < h->P.p; ++k) {
+    sum += sw[k];
+    mx = std::max(mx, (double)sw[k]);
+    if (sizes[k] > 32) {
+      sum_big += sw[k];
+      n_big += 1;
+    }
+  }
+  out[0] = h->P.p ? sum / h->P.p : 0.0;
+  out[1] = mx;
+  out[2] = n_big ? sum_big / n_big : 0.0;
+  out[3] = h->warm ? 1.0 : 0.0;
+  return HSDE_OK;
 }
 
 const char *hsde_profile_name(int32_t slot) {

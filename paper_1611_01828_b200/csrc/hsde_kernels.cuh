@@ -83,6 +83,9 @@ struct DevWork {
   double *part;        // [kMaxParts]
   double *scal;        // [S_COUNT]
   int *err;            // [1] bit 0: non-finite eigenvalue
+  double *vstore;      // [n_d] eigenvectors of the last projection (warm start)
+  int *vvalid;         // [p]   vstore holds a valid basis for clique k
+  int *sweeps;         // [p]   Jacobi sweeps of the last projection (stats)
 };
 
 // ---------------------------------------------------------------------------
@@ -296,337 +299,7 @@ __global__ void __launch_bounds__(kBlock) k_xupd(DevProblem P, DevState S, DevWo
   }
 }
 
-// ---------------------------------------------------------------------------
-// Team-parallel cyclic Jacobi for the PSD projection (symmat.py:153-165).
-//
-// The symmetric matrix lives in shared memory with an even leading dimension
-// dp (a zero row/column pads odd d).  One round of the round-robin tournament
-// rotates dp/2 disjoint pairs at once: rotation parameters first (one thread
-// per pair), then every 2x2 block (pair k rows) x (pair l cols) is transformed
-// independently, A <- J' A J, and the eigenvector rows Vt[p], Vt[q] are
-// rotated.  Two team barriers per round; sweeps until no pair exceeds the
-// absolute threshold 2^-60 |A|_F (projection error is absolute).
-
-struct WarpTeam {
-  int rank;
-  __device__ static constexpr int size() { return 32; }
-  __device__ void sync() const { __syncwarp(); }
-};
-struct BlockTeam {
-  int rank, n;
-  __device__ int size() const { return n; }
-  __device__ void sync() const { __syncthreads(); }
-};
-
-template <class Team>
-__device__ double team_sum(const Team &tm, double v, double *red) {
-  v = warp_sum(v);
-  v = __shfl_sync(0xffffffffu, v, 0);
-  if (tm.size() <= 32) return v;
-  const int lane = tm.rank & 31, wid = tm.rank >> 5;
-  tm.sync();
-  if (lane == 0) red[wid] = v;
-  tm.sync();
-  double r = 0.0;
-  const int nw = (tm.size() + 31) >> 5;
-  for (int i = 0; i < nw; ++i) r += red[i];
-  tm.sync();
-  return r;
-}
-
-__device__ __forceinline__ int tour_player(int pos, int r, int dp) {
-  return pos == 0 ? 0 : 1 + ((pos - 1 + r) % (dp - 1));
-}
-
-// Scratch layout for one team (doubles): A[dp*dp] Vt[dp*dp] cs[dp] (c,s interleaved)
-// tt[dp/2] ; ints: pq[dp/2] ; flags[2] ; red[32]
-struct JacobiScratch {
-  double *A, *Vt, *cs, *tt, *red;
-  int *pq, *flag, *pos;
-};
-
-__host__ __device__ inline int64_t jacobi_scratch_doubles(int dp) {
-  return 2LL * dp * dp + dp + dp / 2 + 32 + (dp / 2 + 2 + dp + 1) / 2 + 2;
-}
-
-__device__ inline JacobiScratch jacobi_carve(double *base, int dp) {
-  JacobiScratch s;
-  s.A = base;
-  s.Vt = s.A + dp * dp;
-  s.cs = s.Vt + dp * dp;
-  s.tt = s.cs + dp;
-  s.red = s.tt + dp / 2;
-  s.pq = reinterpret_cast<int *>(s.red + 32);
-  s.flag = s.pq + dp / 2;
-  s.pos = s.flag + 2;
-  return s;
-}
-
-// Returns number of sweeps; eigenvalues on diag(A) (positions < d), vectors in Vt rows.
-template <class Team>
-__device__ int jacobi_eigh(const Team &tm, JacobiScratch &js, int d, int dp) {
-  double *A = js.A, *Vt = js.Vt;
-  const int half = dp / 2;
-  // Vt = I
-  for (int e = tm.rank; e < dp * dp; e += tm.size()) Vt[e] = (e / dp == e % dp) ? 1.0 : 0.0;
-  double loc = 0.0;
-  for (int e = tm.rank; e < dp * dp; e += tm.size()) loc += A[e] * A[e];
-  const double nrm2 = team_sum(tm, loc, js.red);
-  const double thr = sqrt(nrm2) * 8.673617379884035e-19;  // 2^-60 |A|_F
-  int sweep = 0;
-  const int noff = half * (half - 1) / 2;
-  for (; sweep < kMaxSweeps; ++sweep) {
-    if (tm.rank == 0) js.flag[0] = 0;
-    tm.sync();
-    for (int r = 0; r < dp - 1; ++r) {
-      // step 1: rotation parameters of the dp/2 disjoint pairs
-      for (int k = tm.rank; k < half; k += tm.size()) {
-        const int p = tour_player(k, r, dp), q = tour_player(dp - 1 - k, r, dp);
-        const double apq = A[p * dp + q];
-        double c = 1.0, s = 0.0, t = 0.0;
-        if (fabs(apq) > thr) {
-          const double app = A[p * dp + p], aqq = A[q * dp + q];
-          const double th = (aqq - app) / (2.0 * apq);
-          const double ath = fabs(th);
-          t = ath > 1e150 ? 0.5 / th : (th >= 0.0 ? 1.0 : -1.0) / (ath + sqrt(1.0 + th * th));
-          c = 1.0 / sqrt(1.0 + t * t);
-          s = t * c;
-          js.flag[0] = 1;
-        }
-        js.cs[2 * k] = c;
-        js.cs[2 * k + 1] = s;
-        js.tt[k] = t;
-        js.pq[k] = p | (q << 16);
-      }
-      tm.sync();
-      // step 2: all 2x2 blocks, diagonal blocks, eigenvector rows
-      const int nv = half * dp;
-      const int items = noff + half + nv;
-      for (int it = tm.rank; it < items; it += tm.size()) {
-        if (it < noff) {
-          // unrank (k, l), k < l
-          int k = 0, rem = it;
-          while (rem >= half - 1 - k) { rem -= half - 1 - k; ++k; }
-          const int l = k + 1 + rem;
-          const double ck = js.cs[2 * k], sk = js.cs[2 * k + 1];
-          const double cl = js.cs[2 * l], sl = js.cs[2 * l + 1];
-          if (sk == 0.0 && sl == 0.0) continue;
-          const int pk = js.pq[k] & 0xffff, qk = js.pq[k] >> 16;
-          const int pl = js.pq[l] & 0xffff, ql = js.pq[l] >> 16;
-          const double a = A[pk * dp + pl], bb = A[pk * dp + ql];
-          const double cc = A[qk * dp + pl], ee = A[qk * dp + ql];
-          const double r_pp = ck * a - sk * cc, r_pq = ck * bb - sk * ee;
-          const double r_qp = sk * a + ck * cc, r_qq = sk * bb + ck * ee;
-          const double n_pp = cl * r_pp - sl * r_pq, n_pq = sl * r_pp + cl * r_pq;
-          const double n_qp = cl * r_qp - sl * r_qq, n_qq = sl * r_qp + cl * r_qq;
-          A[pk * dp + pl] = n_pp; A[pl * dp + pk] = n_pp;
-          A[pk * dp + ql] = n_pq; A[ql * dp + pk] = n_pq;
-          A[qk * dp + pl] = n_qp; A[pl * dp + qk] = n_qp;
-          A[qk * dp + ql] = n_qq; A[ql * dp + qk] = n_qq;
-        } else if (it < noff + half) {
-          const int k = it - noff;
-          const double t = js.tt[k];
-          if (t == 0.0 && js.cs[2 * k + 1] == 0.0) continue;
-          const int p = js.pq[k] & 0xffff, q = js.pq[k] >> 16;
-          const double apq = A[p * dp + q];
-          A[p * dp + p] -= t * apq;
-          A[q * dp + q] += t * apq;
-          A[p * dp + q] = 0.0;
-          A[q * dp + p] = 0.0;
-        } else {
-          const int v = it - noff - half;
-          const int k = v / dp, i = v - k * dp;
-          const double c = js.cs[2 * k], s = js.cs[2 * k + 1];
-          if (s == 0.0) continue;
-          const int p = js.pq[k] & 0xffff, q = js.pq[k] >> 16;
-          const double vp = Vt[p * dp + i], vq = Vt[q * dp + i];
-          Vt[p * dp + i] = c * vp - s * vq;
-          Vt[q * dp + i] = s * vp + c * vq;
-        }
-      }
-      tm.sync();
-    }
-    const int rotated = js.flag[0];
-    tm.sync();
-    if (!rotated) break;
-  }
-  return sweep;
-}
-
-// P = sum_{lambda_i > 0} lambda_i v_i v_i'  written through `emit(a, b, value)`
-// for a <= b (caller mirrors).  Uses A's off-diagonal storage as scratch for the
-// scaled vectors; js.pos holds the compacted positive positions.
-template <class Team, class Emit>
-__device__ void psd_rebuild(const Team &tm, JacobiScratch &js, int d, int dp, Emit emit) {
-  double *A = js.A, *Vt = js.Vt;
-  // compact positive eigenvalues (warp 0 ballot, ascending position order)
-  if (tm.rank < 32) {
-    int base = 0;
-    for (int i0 = 0; i0 < d; i0 += 32) {
-      const int i = i0 + tm.rank;
-      const bool pos = i < d && A[i * dp + i] > 0.0;
-      const unsigned mask = __ballot_sync(0xffffffffu, pos);
-      if (pos) js.pos[base + __popc(mask & ((1u << tm.rank) - 1u))] = i;
-      base += __popc(mask);
-    }
-    if (tm.rank == 0) js.pos[dp] = base;
-  }
-  tm.sync();
-  const int r = js.pos[dp];
-  const int nout = d * (d + 1) / 2;
-  for (int o = tm.rank; o < nout; o += tm.size()) {
-    int a = 0, rem = o;
-    while (rem >= d - a) { rem -= d - a; ++a; }
-    const int b = a + rem;
-    double acc = 0.0;
-    for (int k = 0; k < r; ++k) {
-      const int pi = js.pos[k];
-      const double lam = A[pi * dp + pi];
-      acc += (Vt[pi * dp + a] * lam) * Vt[pi * dp + b];
-    }
-    emit(a, b, acc);
-  }
-}
-
-// Cone kernel modes
-enum ConeMode { CONE_HOT = 0, CONE_PLAIN = 1, CONE_MINEIG = 2 };
-
-struct ConeArgs {
-  const int *ids;     // clique ids of this launch
-  int count;
-  int dpmax;          // scratch leading dimension bound
-  const double *in;   // PLAIN/MINEIG: stacked s-segment input [n_d]
-  double *out;        // PLAIN: stacked s-segment output; MINEIG: per-clique min eig [p]
-  double in_scale;    // MINEIG: multiply input by this
-};
-
-// Load phase of the hot path for one slot j of a clique: builds arg_s and
-// performs the v / w_v update and the first half of the w_s update in place.
-__device__ __forceinline__ double hot_slot_load(const DevProblem &P, const DevState &S,
-                                                const DevWork &W, int64_t j, double shift) {
-  const int64_t so = P.n_c, vo = P.n_c + P.n_d + P.m;
-  const double us = S.u[so + j], ws = S.w[so + j];
-  const double uv0 = S.u[vo + j], wv = S.w[vo + j];
-  const double as = us + ws, av = uv0 + wv;                  // a = u + w
-  const double gb = as - av;                                 // solver.py:222
-  const double hua = W.ua[P.slot_cov[j]];                    // :236
-  const double ub = (gb + hua) * 0.5;                        // :237-239
-  const double uv = (ub - hua) + av;                         // :242-244
-  const double mzs = P.mz[P.n_c + j], mzv = P.mz[P.n_c + P.n_d + P.m + j];
-  const double us_h = relax(ub - shift * mzs, us, P.alpha);  // :316, :388-390
-  const double uv_h = relax(uv - shift * mzv, uv0, P.alpha);
-  const double arg_s = us_h - ws;                            // :391
-  const double vn = uv_h - wv;                               // free block: projection = identity
-  S.u[vo + j] = vn;
-  S.w[vo + j] = (wv - uv_h) + vn;                            // :393-394
-  S.w[so + j] = ws - us_h;                                   // completed after projection
-  return arg_s;
-}
-
-template <int MODE, class Team>
-__device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S, const DevWork &W,
-                         const ConeArgs &ca, int k, double *scratch) {
-  const int d = P.cl_size[k];
-  const int64_t off = P.cl_off[k];
-  const int64_t so = P.n_c;
-  const double shift = (MODE == CONE_HOT) ? W.scal[S_SHIFT] : 0.0;
-  if (d == 1) {
-    if (tm.rank == 0) {
-      double a;
-      if (MODE == CONE_HOT) a = hot_slot_load(P, S, W, off, shift);
-      else a = ca.in[off] * (MODE == CONE_MINEIG ? ca.in_scale : 1.0);
-      const double pr = (a != a) ? a : (a > 0.0 ? a : 0.0);  // np.maximum(b, 0.0)
-      if (MODE == CONE_HOT) {
-        S.u[so + off] = pr;
-        S.w[so + off] += pr;
-      } else if (MODE == CONE_PLAIN) {
-        ca.out[off] = pr;
-      } else {
-        ca.out[k] = a;
-      }
-    }
-    return;
-  }
-  const int dp = d + (d & 1);
-  JacobiScratch js = jacobi_carve(scratch, dp);
-  double *A = js.A;
-  // load (raw), then symmetrise sym = 0.5 (B + B')  (symmat.py:157)
-  for (int e = tm.rank; e < d * d; e += tm.size()) {
-    const int a = e / d, bcol = e - a * d;
-    double v;
-    if (MODE == CONE_HOT) v = hot_slot_load(P, S, W, off + e, shift);
-    else v = ca.in[off + e] * (MODE == CONE_MINEIG ? ca.in_scale : 1.0);
-    A[a * dp + bcol] = v;
-  }
-  if (d & 1) {
-    for (int e = tm.rank; e < dp; e += tm.size()) {
-      A[d * dp + e] = 0.0;
-      A[e * dp + d] = 0.0;
-    }
-  }
-  tm.sync();
-  for (int e = tm.rank; e < d * d; e += tm.size()) {
-    const int a = e / d, bcol = e - a * d;
-    if (a < bcol) {
-      const double s = 0.5 * (A[a * dp + bcol] + A[bcol * dp + a]);
-      A[a * dp + bcol] = s;
-      A[bcol * dp + a] = s;
-    } else if (a == bcol) {
-      A[a * dp + a] = 0.5 * (A[a * dp + a] + A[a * dp + a]);
-    }
-  }
-  tm.sync();
-  jacobi_eigh(tm, js, d, dp);
-  // non-finite eigenvalue -> EigenFailure (symmat.py:162-163)
-  bool bad = false;
-  for (int i = tm.rank; i < d; i += tm.size()) bad |= !isfinite(A[i * dp + i]);
-  if (bad) atomicOr(W.err, 1);
-  if (MODE == CONE_MINEIG) {
-    double mn = CUDART_INF;
-    for (int i = 0; i < d; ++i) mn = fmin(mn, A[i * dp + i]);
-    if (tm.rank == 0) ca.out[k] = mn;
-    tm.sync();
-    return;
-  }
-  if (MODE == CONE_HOT) {
-    psd_rebuild(tm, js, d, dp, [&](int a, int bcol, double v) {
-      const int64_t j1 = so + off + (int64_t)a * d + bcol, j2 = so + off + (int64_t)bcol * d + a;
-      S.u[j1] = v;
-      S.w[j1] += v;
-      if (j2 != j1) {
-        S.u[j2] = v;
-        S.w[j2] += v;
-      }
-    });
-  } else {
-    psd_rebuild(tm, js, d, dp, [&](int a, int bcol, double v) {
-      ca.out[off + (int64_t)a * d + bcol] = v;
-      ca.out[off + (int64_t)bcol * d + a] = v;
-    });
-  }
-  tm.sync();
-}
-
-// one warp per clique (d <= 32); dynamic smem = warps * scratch(dpmax)
-template <int MODE>
-__global__ void __launch_bounds__(kBlock) k_cone_warp(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
-  extern __shared__ double smem[];
-  const int wid = threadIdx.x >> 5;
-  const int gw = blockIdx.x * (blockDim.x >> 5) + wid;
-  if (gw >= ca.count) return;
-  double *scratch = smem + (int64_t)wid * jacobi_scratch_doubles(ca.dpmax);
-  WarpTeam tm{(int)(threadIdx.x & 31)};
-  cone_one<MODE>(tm, P, S, W, ca, ca.ids[gw], scratch);
-}
-
-// one CTA per clique (d > 32)
-template <int MODE>
-__global__ void __launch_bounds__(kBlock) k_cone_block(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
-  extern __shared__ double smem[];
-  if ((int)blockIdx.x >= ca.count) return;
-  BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
-  cone_one<MODE>(tm, P, S, W, ca, ca.ids[blockIdx.x], smem);
-}
+#include "hsde_eig.cuh"
 
 // ---------------------------------------------------------------------------
 // generic small kernels for the unit-level API path
