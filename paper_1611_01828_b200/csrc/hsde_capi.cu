@@ -68,6 +68,7 @@ struct hsde_handle {
   double *d_chk = nullptr;        // [64] check sums
   double *d_mineig = nullptr;     // [p]
   double *h_chk = nullptr;        // pinned [64]
+  int grid_heavy = 0;
   int grid_nc = 1, grid_nd = 1, grid_m = 1, grid_T = 1, grid_seg = 1, grid_schur = 1;
   size_t schur_smem = 0;
   double norm_b = 0, norm_c = 0;  // of the iterated (normalised) data
@@ -197,7 +198,7 @@ int inner_explicit(hsde_handle *h, const double *rho, double *u12, cudaStream_t 
   const DevProblem &P = h->P;
   const double *rx = rho, *rs = rho + P.n_c, *ry = rho + P.n_c + P.n_d,
                *rv = rho + P.n_c + P.n_d + P.m;
-  k_rhs<false><<<h->grid_nc, kBlock, 0, st>>>(P, h->S, h->W, rx, rs, ry, rv);
+  k_rhs<false><<<h->grid_nc + h->grid_heavy, kBlock, 0, st>>>(P, h->S, h->W, rx, rs, ry, rv, h->grid_nc);
   CKL();
   k_spmv_seg<<<h->grid_seg, kBlock, 0, st>>>(P, h->W.t, h->W.qseg);
   CKL();
@@ -237,7 +238,8 @@ int launch_iteration(hsde_handle *h, cudaStream_t st, cudaEvent_t *ev = nullptr,
   };
   (void)slot;
   if (ev) cudaEventRecord(ev[PS_COUNT], st);
-  k_rhs<true><<<h->grid_nc, kBlock, 0, st>>>(P, h->S, h->W, nullptr, nullptr, nullptr, nullptr);
+  k_rhs<true><<<h->grid_nc + h->grid_heavy, kBlock, 0, st>>>(P, h->S, h->W, nullptr, nullptr, nullptr,
+                                                             nullptr, h->grid_nc);
   CKL();
   mark(PS_RHS);
   k_spmv_seg<<<h->grid_seg, kBlock, 0, st>>>(P, h->W.t, h->W.qseg);
@@ -599,6 +601,9 @@ int hsde_create(const hsde_problem_desc *d, const hsde_settings *s, hsde_t **out
     std::vector<int> pos(cov_ptr.begin(), cov_ptr.end() - 1);
     for (int64_t j = 0; j < n_d; ++j) cov_slot[pos[d->slot_cov[j]]++] = (int)j;
   }
+  std::vector<int> heavy;
+  for (int c = 0; c < n_c; ++c)
+    if (cov_ptr[c + 1] - cov_ptr[c] > kHeavy) heavy.push_back(c);
   std::vector<double> p_inv(n_c);
   for (int c = 0; c < n_c; ++c)
     p_inv[c] = 1.0 / (1.0 + 0.5 * (double)(cov_ptr[c + 1] - cov_ptr[c]));  // solver.py:250
@@ -651,6 +656,11 @@ int hsde_create(const hsde_problem_desc *d, const hsde_settings *s, hsde_t **out
       (rc = dupload(h, &b_d, bint.data(), m)) || (rc = dupload(h, &pinv_d, p_inv.data(), n_c)) ||
       (rc = dupload(h, &h->d_c_orig, d->c, n_c)) || (rc = dupload(h, &h->d_b_orig, d->b, m)))
     return fail(rc);
+  int *heavy_d = nullptr;
+  if ((rc = dupload(h, &heavy_d, heavy.data(), heavy.size()))) return fail(rc);
+  P.heavy = heavy_d;
+  P.n_heavy = (int)heavy.size();
+  h->grid_heavy = (P.n_heavy + (kBlock / 32) - 1) / (kBlock / 32);
   P.a_rp = a_rp;
   P.a_col = a_col;
   P.a_val = a_val;

@@ -58,6 +58,8 @@ struct DevProblem {
   const int *cov_ptr;  // [n_c+1]
   const int *cov_slot; // [n_d]
   const int *slot_cov; // [n_d]
+  int n_heavy;         // covered coordinates with > kHeavy slots
+  const int *heavy;    // [n_heavy]
   const int64_t *cl_off;
   const int *cl_size;
   // data of the iterated (normalised) problem
@@ -123,40 +125,67 @@ __device__ __forceinline__ double relax(double uhat, double uold, double alpha) 
 // (solver.py:222-231).  FROM_STATE: rho comes from the state u + w and a_tau
 // (affine_project :300-301 fused); otherwise from explicit vectors.
 
+// Covered coordinates with more than kHeavy covering slots (e.g. the arrow
+// head of a block-arrow pattern: 400 cliques share it) get a warp each;
+// the rest a thread each.  Grid = [light blocks | heavy blocks].
+constexpr int kHeavy = 32;
+
+template <bool FROM_STATE>
+__device__ __forceinline__ void rhs_slot(const DevProblem &P, const DevState &S, const double *rs,
+                                         const double *rv, int j, double &sg, double &sv) {
+  const int64_t so = P.n_c, vo = P.n_c + P.n_d + P.m;
+  double as, av;
+  if (FROM_STATE) {
+    as = S.u[so + j] + S.w[so + j];
+    av = S.u[vo + j] + S.w[vo + j];
+  } else {
+    as = rs[j];
+    av = rv[j];
+  }
+  sg += as - av;
+  sv += av;
+}
+
 template <bool FROM_STATE>
 __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWork W,
                                                 const double *rx, const double *rs,
-                                                const double *ry, const double *rv) {
-  const int64_t xo = 0, so = P.n_c, vo = P.n_c + P.n_d + P.m;
+                                                const double *ry, const double *rv, int nb_light) {
   double atau = 0.0;
   if (FROM_STATE) {
     atau = S.u[P.total - 1] + S.w[P.total - 1];
     ry = W.ry;
   }
-  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < P.n_c; l += gridDim.x * blockDim.x) {
-    double sg = 0.0, sv = 0.0;
-    const int jb = P.cov_ptr[l], je = P.cov_ptr[l + 1];
-    for (int e = jb; e < je; ++e) {
-      const int j = P.cov_slot[e];
-      double as, av;
-      if (FROM_STATE) {
-        as = S.u[so + j] + S.w[so + j];
-        av = S.u[vo + j] + S.w[vo + j];
-      } else {
-        as = rs[j];
-        av = rv[j];
-      }
-      sg += as - av;
-      sv += av;
+  if ((int)blockIdx.x < nb_light) {
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < P.n_c; l += nb_light * blockDim.x) {
+      const int jb = P.cov_ptr[l], je = P.cov_ptr[l + 1];
+      if (je - jb > kHeavy) continue;
+      double sg = 0.0, sv = 0.0;
+      for (int e = jb; e < je; ++e) rhs_slot<FROM_STATE>(P, S, rs, rv, P.cov_slot[e], sg, sv);
+      double aty = 0.0;
+      const int64_t cb = P.at_cp[l], ce = P.at_cp[l + 1];
+#pragma unroll 4
+      for (int64_t e = cb; e < ce; ++e) aty += P.at_val[e] * __ldg(ry + P.at_row[e]);
+      const double rx_l = FROM_STATE ? (S.u[l] + S.w[l]) - atau * P.c[l] : rx[l];
+      const double r = ((sg * 0.5 + sv) + aty) + rx_l;
+      W.t[l] = r * P.p_inv[l];
     }
-    double aty = 0.0;
-    const int64_t cb = P.at_cp[l], ce = P.at_cp[l + 1];
-    for (int64_t e = cb; e < ce; ++e) aty += P.at_val[e] * __ldg(ry + P.at_row[e]);
-    double rx_l;
-    if (FROM_STATE)
-      rx_l = (S.u[xo + l] + S.w[xo + l]) - atau * P.c[l];
-    else
-      rx_l = rx[l];
+    return;
+  }
+  // heavy coordinates: one warp each, lanes stride the slot list and the column
+  const int lane = threadIdx.x & 31;
+  const int hw = ((int)blockIdx.x - nb_light) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (hw >= P.n_heavy) return;
+  const int l = P.heavy[hw];
+  double sg = 0.0, sv = 0.0, aty = 0.0;
+  for (int e = P.cov_ptr[l] + lane; e < P.cov_ptr[l + 1]; e += 32)
+    rhs_slot<FROM_STATE>(P, S, rs, rv, P.cov_slot[e], sg, sv);
+  for (int64_t e = P.at_cp[l] + lane; e < P.at_cp[l + 1]; e += 32)
+    aty += P.at_val[e] * __ldg(ry + P.at_row[e]);
+  sg = warp_sum(sg);
+  sv = warp_sum(sv);
+  aty = warp_sum(aty);
+  if (lane == 0) {
+    const double rx_l = FROM_STATE ? (S.u[l] + S.w[l]) - atau * P.c[l] : rx[l];
     const double r = ((sg * 0.5 + sv) + aty) + rx_l;
     W.t[l] = r * P.p_inv[l];
   }

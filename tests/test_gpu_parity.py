@@ -266,3 +266,29 @@ def test_exact_uy_flag_matches_identity_path():
         res.append(h.get_state()[0])
         h.close()
     assert rel(res[1], res[0]) <= 1e-10
+
+
+def test_warm_started_eigensolves_match_cold_and_oracle():
+    """CTA-team cliques (d = 40 > 32) with and without the warm start, vs the
+    CPU oracle after 200 iterations (1e-8 relative)."""
+    from paper_1611_01828_b200 import _lib
+    from paper_1611_01828_b200.synthetic import block_arrow
+
+    cp = block_arrow(12, 24, 16, 50, 0.05, 7, "ctapath")
+    res = []
+    for flags in (0, _lib.HSDE_FLAG_COLD_EIG):
+        h = _lib.Handle(cp, flags=flags)
+        h.iterate(200)
+        res.append(h.get_state())
+        st = h.stats()
+        assert st["warm_start"] == (flags == 0)
+        h.close()
+    assert rel(res[0][0], res[1][0]) <= 1e-9
+    ref = {}
+
+    def cb(k, p, d, g, tau, kap, u, w):
+        if k == 200:
+            ref["u"] = u.copy()
+
+    O.solve(cp, O.OracleSettings(max_iters=200, tol=1e-300), callback=cb)
+    assert rel(res[0][0], ref["u"]) <= 1e-8
