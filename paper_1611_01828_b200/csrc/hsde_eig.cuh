@@ -17,8 +17,9 @@
 // every 2x2 block (pair k rows) x (pair l columns) transforms independently,
 // A <- J' A J, and the eigenvector rows Vt[p], Vt[q] rotate.  Two team
 // barriers per round.  Rotations below 2^-60 |A|_F are skipped; sweeps stop
-// when the off-diagonal mass falls below 2^-57 |A|_F (absolute accuracy is
-// what the projection needs: |P - P_exact| <= |off|).
+// when the off-diagonal mass falls below 2^-56 |A|_F or a sweep rotates
+// nothing (absolute accuracy is what the projection needs: |P - P_exact| is
+// bounded by the remaining off-diagonal mass).
 //
 // Warm start (CTA teams, hot path): ADMM iterates move slowly, so the
 // previous iteration's eigenvectors V nearly diagonalise the new block.  The
@@ -127,12 +128,14 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp) {
   double norm2, off2;
   jacobi_norms(tm, js, dp, norm2, off2);
   const double thr = sqrt(norm2) * 8.673617379884035e-19;   // 2^-60 |A|_F
-  const double stop2 = norm2 * 4.8148248609680896e-35;      // (2^-57 |A|_F)^2
+  const double stop2 = norm2 * 1.925929944387236e-34;       // (2^-56 |A|_F)^2
   const int T = tm.size();
   const int vdk = T / d, vdi = T - (T / d) * d;
   int sweep = 0;
   for (; sweep < kMaxSweeps; ++sweep) {
     if (!(off2 > stop2)) break;  // also stops on NaN
+    if (tm.rank == 0) js.flag[0] = 0;
+    tm.sync();
     for (int r = 0; r < dp - 1; ++r) {
       for (int k = tm.rank; k < half; k += T) {
         const int p = tour_player(k, r, dp), q = tour_player(dp - 1 - k, r, dp);
@@ -145,6 +148,7 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp) {
           if (diff < 0.0) t = -t;
           c = rsqrt(1.0 + t * t);
           s = t * c;
+          js.flag[0] = 1;
         }
         js.cs[2 * k] = c;
         js.cs[2 * k + 1] = s;
@@ -205,8 +209,13 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp) {
       }
       tm.sync();
     }
+    const int rotated = js.flag[0];
     double n2;
-    jacobi_norms(tm, js, dp, n2, off2);
+    jacobi_norms(tm, js, dp, n2, off2);  // (team barriers inside)
+    if (!rotated) {
+      ++sweep;
+      break;  // every pair below the rotation threshold
+    }
   }
   return sweep;
 }
