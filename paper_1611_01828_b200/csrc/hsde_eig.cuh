@@ -7,26 +7,33 @@
 //   P = Q diag(lambda+) Q'
 //
 // One *team* per clique: a warp for d <= 32 (several cliques per CTA), a CTA
-// for d > 32.  The symmetric block and its eigenvector rows live in shared
-// memory with an odd leading dimension ld = dp + 1 (dp = d rounded up to even;
-// a zero row/column pads odd d), which keeps row-strided accesses free of
-// bank conflicts.
+// for d > 32.  The symmetric block lives in shared memory with an odd leading
+// dimension (lda = dp + 1, dp = d rounded up to even; a zero row/column pads
+// odd d) so that row- and column-strided accesses are conflict free; the
+// eigenvector rows Vt use a leading dimension that is a multiple of 4 so they
+// are updated with 16-byte vector accesses.
 //
 // Cyclic Jacobi, round-robin (tournament) ordering: each round rotates the
-// dp/2 disjoint pairs at once -- parameters first (one thread per pair), then
-// every 2x2 block (pair k rows) x (pair l columns) transforms independently,
-// A <- J' A J, and the eigenvector rows Vt[p], Vt[q] rotate.  Two team
-// barriers per round.  Rotations below 2^-60 |A|_F are skipped; sweeps stop
-// when the off-diagonal mass falls below 2^-56 |A|_F or a sweep rotates
-// nothing (absolute accuracy is what the projection needs: |P - P_exact| is
-// bounded by the remaining off-diagonal mass).
+// dp/2 disjoint pairs at once.  Per round:
+//   phase P  -- rotation parameters of round r (one thread per pair, into a
+//               double-buffered table) while the other threads apply round
+//               r-1's rotations to the eigenvector rows;
+//   phase A  -- every 2x2 block (pair k rows) x (pair l columns) transforms
+//               independently, A <- J' A J, plus the closed-form diagonal.
+// Two team barriers per round.  Rotations below 2^-60 |A|_F are skipped;
+// sweeps stop when the off-diagonal mass falls below 2^-56 |A|_F or a sweep
+// rotates nothing (absolute accuracy is what the projection needs: the
+// error of P is bounded by the remaining off-diagonal mass).
 //
 // Warm start (CTA teams, hot path): ADMM iterates move slowly, so the
 // previous iteration's eigenvectors V nearly diagonalise the new block.  The
 // kernel forms B = V X V' with two register-tiled shared-memory GEMMs and runs
-// Jacobi on B starting from V: typically a few sweeps instead of ~10.
+// Jacobi on B starting from V: ~3 sweeps instead of ~10.  V is refreshed by
+// a cold solve every kWarmMaxAge iterations to bound its orthogonality drift.
 #pragma once
 // (included inside namespace hsde by hsde_kernels.cuh)
+
+constexpr int kWarmMaxAge = 64;
 
 struct WarpTeam {
   int rank;
@@ -56,52 +63,63 @@ __device__ double team_sum(const Team &tm, double v, double *red) {
   return r;
 }
 
+// player at tournament position `pos` in round r (0 <= r < dp - 1): position 0
+// is fixed, the others rotate (no integer division: pos - 1 + r < 2 (dp - 1))
 __device__ __forceinline__ int tour_player(int pos, int r, int dp) {
-  return pos == 0 ? 0 : 1 + ((pos - 1 + r) % (dp - 1));
+  int x = pos - 1 + r;
+  if (x >= dp - 1) x -= dp - 1;
+  return pos == 0 ? 0 : 1 + x;
 }
 
+__host__ __device__ inline int jacobi_ldv(int dp) { return (dp + 3) & ~3; }
+
 struct JacobiScratch {
-  double *A, *Vt, *cs, *tt, *lam, *red;
-  int *pq, *offtab, *pos, *flag;
-  int ld;
+  double *A, *Vt;
+  double2 *rot;   // [2][half] (c, s)
+  int4 *idx;      // [2][half] (p, q, p*lda, q*lda)
+  double *tt, *lam, *red;
+  int *offtab, *pos, *flag;
+  int lda, ldv;
 };
 
 __host__ __device__ inline int64_t jacobi_scratch_doubles(int dp) {
-  const int64_t ld = dp + 1, half = dp / 2;
+  const int64_t lda = dp + 1, ldv = jacobi_ldv(dp), half = dp / 2;
   const int64_t noff = half * (half - 1) / 2;
-  const int64_t ints = half + noff + dp + 1 + 2;
-  return 2 * dp * ld + dp + half + dp + 32 + (ints + 1) / 2 + 1;
+  const int64_t ints = noff + dp + 1 + 2;
+  const int64_t n = dp * lda + dp * ldv + 4 * half + 4 * half + half + dp + 32 + (ints + 1) / 2 + 2;
+  return (n + 1) & ~int64_t(1);  // keep per-warp slices 16-byte aligned
 }
 
 __device__ inline JacobiScratch jacobi_carve(double *base, int dp) {
   JacobiScratch s;
   const int half = dp / 2;
-  s.ld = dp + 1;
+  s.lda = dp + 1;
+  s.ldv = jacobi_ldv(dp);
   s.A = base;
-  s.Vt = s.A + dp * s.ld;
-  s.cs = s.Vt + dp * s.ld;
-  s.tt = s.cs + dp;
+  s.Vt = s.A + dp * s.lda;  // dp even -> 16-byte aligned
+  s.rot = reinterpret_cast<double2 *>(s.Vt + dp * s.ldv);
+  s.idx = reinterpret_cast<int4 *>(s.rot + 2 * half);
+  s.tt = reinterpret_cast<double *>(s.idx + 2 * half);
   s.lam = s.tt + half;
   s.red = s.lam + dp;
-  s.pq = reinterpret_cast<int *>(s.red + 32);
-  s.offtab = s.pq + half;
+  s.offtab = reinterpret_cast<int *>(s.red + 32);
   s.pos = s.offtab + half * (half - 1) / 2;
   s.flag = s.pos + dp + 1;
   return s;
 }
 
-// off-block table (k, l), k < l, and Vt = I (unless warm)
+// off-block table (k, l), k < l; Vt = I (cold) with zero padding columns
 template <class Team>
 __device__ void jacobi_prepare(const Team &tm, JacobiScratch &js, int dp, bool init_identity) {
-  const int half = dp / 2, ld = js.ld;
+  const int half = dp / 2;
   for (int k = tm.rank; k < half; k += tm.size()) {
     const int base = k * (half - 1) - k * (k - 1) / 2;
     for (int l = k + 1; l < half; ++l) js.offtab[base + (l - k - 1)] = k | (l << 16);
   }
   if (init_identity)
-    for (int e = tm.rank; e < dp * dp; e += tm.size()) {
-      const int i = e / dp, j = e - i * dp;
-      js.Vt[i * ld + j] = (i == j) ? 1.0 : 0.0;
+    for (int e = tm.rank; e < dp * js.ldv; e += tm.size()) {
+      const int i = e / js.ldv, j = e - i * js.ldv;
+      js.Vt[e] = (i == j) ? 1.0 : 0.0;
     }
 }
 
@@ -111,7 +129,7 @@ __device__ void jacobi_norms(const Team &tm, const JacobiScratch &js, int dp, do
   double a2 = 0.0, o2 = 0.0;
   for (int e = tm.rank; e < dp * dp; e += tm.size()) {
     const int i = e / dp, j = e - i * dp;
-    const double a = js.A[i * js.ld + j];
+    const double a = js.A[i * js.lda + j];
     a2 += a * a;
     if (i != j) o2 += a * a;
   }
@@ -119,30 +137,67 @@ __device__ void jacobi_norms(const Team &tm, const JacobiScratch &js, int dp, do
   off2 = team_sum(tm, o2, js.red);
 }
 
+// apply the rotations of parameter buffer `b` to the eigenvector rows, in
+// 4-column chunks; participating threads [first, team size)
+template <class Team>
+__device__ __forceinline__ void jacobi_vupdate(const Team &tm, JacobiScratch &js, int half, int nch,
+                                               int b, int first) {
+  const int T = tm.size() - first;
+  const int me = tm.rank - first;
+  if (me < 0) return;
+  const int total = half * nch;
+  const double2 *rot = js.rot + b * half;
+  const int4 *idx = js.idx + b * half;
+  // (k, ch) of item `it` advanced incrementally (no division in the loop)
+  const int dk = T / nch, dc = T - (T / nch) * nch;
+  int k = me / nch, ch = me - (me / nch) * nch;
+  for (int it = me; it < total; it += T, k += dk, ch += dc) {
+    if (ch >= nch) {
+      ch -= nch;
+      ++k;
+    }
+    const double2 cs = rot[k];
+    if (cs.y == 0.0) continue;
+    const int4 pq = idx[k];
+    double2 *vp = reinterpret_cast<double2 *>(js.Vt + pq.x * js.ldv + 4 * ch);
+    double2 *vq = reinterpret_cast<double2 *>(js.Vt + pq.y * js.ldv + 4 * ch);
+    const double2 p0 = vp[0], p1 = vp[1], q0 = vq[0], q1 = vq[1];
+    vp[0] = make_double2(cs.x * p0.x - cs.y * q0.x, cs.x * p0.y - cs.y * q0.y);
+    vp[1] = make_double2(cs.x * p1.x - cs.y * q1.x, cs.x * p1.y - cs.y * q1.y);
+    vq[0] = make_double2(cs.y * p0.x + cs.x * q0.x, cs.y * p0.y + cs.x * q0.y);
+    vq[1] = make_double2(cs.y * p1.x + cs.x * q1.x, cs.y * p1.y + cs.x * q1.y);
+  }
+}
+
 // Cyclic Jacobi on the symmetric A (dp x dp, padded); rotations accumulate
 // into the rows of Vt.  Returns the number of sweeps performed.
 template <class Team>
 __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp) {
-  double *A = js.A, *Vt = js.Vt;
-  const int ld = js.ld, half = dp / 2, noff = half * (half - 1) / 2;
+  double *A = js.A;
+  const int lda = js.lda, half = dp / 2, noff = half * (half - 1) / 2;
+  const int nch = (d + 3) >> 2;
+  const int T = tm.size();
+  // threads that only update eigenvectors during phase P (block teams)
+  const int vfirst = (T > 32 && T - ((half + 31) & ~31) >= 64) ? ((half + 31) & ~31) : 0;
   double norm2, off2;
   jacobi_norms(tm, js, dp, norm2, off2);
-  const double thr = sqrt(norm2) * 8.673617379884035e-19;   // 2^-60 |A|_F
-  const double stop2 = norm2 * 1.925929944387236e-34;       // (2^-56 |A|_F)^2
-  const int T = tm.size();
-  const int vdk = T / d, vdi = T - (T / d) * d;
-  int sweep = 0;
+  const double thr = sqrt(norm2) * 8.673617379884035e-19;  // 2^-60 |A|_F
+  const double stop2 = norm2 * 1.925929944387236e-34;      // (2^-56 |A|_F)^2
+  int sweep = 0, round = 0;
+  bool pending = false;
   for (; sweep < kMaxSweeps; ++sweep) {
     if (!(off2 > stop2)) break;  // also stops on NaN
     if (tm.rank == 0) js.flag[0] = 0;
     tm.sync();
-    for (int r = 0; r < dp - 1; ++r) {
+    for (int r = 0; r < dp - 1; ++r, ++round) {
+      const int b = round & 1;
+      // ---- phase P: parameters of round r | eigenvector update of round r-1
       for (int k = tm.rank; k < half; k += T) {
         const int p = tour_player(k, r, dp), q = tour_player(dp - 1 - k, r, dp);
-        const double apq = A[p * ld + q];
+        const double apq = A[p * lda + q];
         double c = 1.0, s = 0.0, t = 0.0;
         if (fabs(apq) > thr) {
-          const double diff = A[q * ld + q] - A[p * ld + p];
+          const double diff = A[q * lda + q] - A[p * lda + p];
           const double rr = sqrt(diff * diff + 4.0 * apq * apq);
           t = (2.0 * apq) / (fabs(diff) + rr);
           if (diff < 0.0) t = -t;
@@ -150,63 +205,43 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp) {
           s = t * c;
           js.flag[0] = 1;
         }
-        js.cs[2 * k] = c;
-        js.cs[2 * k + 1] = s;
+        js.rot[b * half + k] = make_double2(c, s);
+        js.idx[b * half + k] = make_int4(p, q, p * lda, q * lda);
         js.tt[k] = t;
-        js.pq[k] = p | (q << 16);
       }
+      if (pending) jacobi_vupdate(tm, js, half, nch, b ^ 1, vfirst);
       tm.sync();
-      // off-diagonal 2x2 blocks
+      // ---- phase A: off-diagonal 2x2 blocks and the diagonal blocks
+      const double2 *rot = js.rot + b * half;
+      const int4 *idx = js.idx + b * half;
       for (int it = tm.rank; it < noff; it += T) {
         const int kl = js.offtab[it];
         const int k = kl & 0xffff, l = kl >> 16;
-        const double sk = js.cs[2 * k + 1], sl = js.cs[2 * l + 1];
-        if (sk == 0.0 && sl == 0.0) continue;
-        const double ck = js.cs[2 * k], cl = js.cs[2 * l];
-        const int pk = js.pq[k] & 0xffff, qk = js.pq[k] >> 16;
-        const int pl = js.pq[l] & 0xffff, ql = js.pq[l] >> 16;
-        const double a = A[pk * ld + pl], bb = A[pk * ld + ql];
-        const double cc = A[qk * ld + pl], ee = A[qk * ld + ql];
-        const double r_pp = ck * a - sk * cc, r_pq = ck * bb - sk * ee;
-        const double r_qp = sk * a + ck * cc, r_qq = sk * bb + ck * ee;
-        const double n_pp = cl * r_pp - sl * r_pq, n_pq = sl * r_pp + cl * r_pq;
-        const double n_qp = cl * r_qp - sl * r_qq, n_qq = sl * r_qp + cl * r_qq;
-        A[pk * ld + pl] = n_pp; A[pl * ld + pk] = n_pp;
-        A[pk * ld + ql] = n_pq; A[ql * ld + pk] = n_pq;
-        A[qk * ld + pl] = n_qp; A[pl * ld + qk] = n_qp;
-        A[qk * ld + ql] = n_qq; A[ql * ld + qk] = n_qq;
+        const double2 rk = rot[k], rl = rot[l];
+        if (rk.y == 0.0 && rl.y == 0.0) continue;
+        const int4 ik = idx[k], il = idx[l];
+        const double a = A[ik.z + il.x], bb = A[ik.z + il.y];
+        const double cc = A[ik.w + il.x], ee = A[ik.w + il.y];
+        const double r_pp = rk.x * a - rk.y * cc, r_pq = rk.x * bb - rk.y * ee;
+        const double r_qp = rk.y * a + rk.x * cc, r_qq = rk.y * bb + rk.x * ee;
+        const double n_pp = rl.x * r_pp - rl.y * r_pq, n_pq = rl.y * r_pp + rl.x * r_pq;
+        const double n_qp = rl.x * r_qp - rl.y * r_qq, n_qq = rl.y * r_qp + rl.x * r_qq;
+        A[ik.z + il.x] = n_pp; A[il.z + ik.x] = n_pp;
+        A[ik.z + il.y] = n_pq; A[il.w + ik.x] = n_pq;
+        A[ik.w + il.x] = n_qp; A[il.z + ik.y] = n_qp;
+        A[ik.w + il.y] = n_qq; A[il.w + ik.y] = n_qq;
       }
-      // diagonal 2x2 blocks: closed form
       for (int k = tm.rank; k < half; k += T) {
         const double t = js.tt[k];
         if (t == 0.0) continue;
-        const int p = js.pq[k] & 0xffff, q = js.pq[k] >> 16;
-        const double apq = A[p * ld + q];
-        A[p * ld + p] -= t * apq;
-        A[q * ld + q] += t * apq;
-        A[p * ld + q] = 0.0;
-        A[q * ld + p] = 0.0;
+        const int4 ik = idx[k];
+        const double apq = A[ik.z + ik.y];
+        A[ik.z + ik.x] -= t * apq;
+        A[ik.w + ik.y] += t * apq;
+        A[ik.z + ik.y] = 0.0;
+        A[ik.w + ik.x] = 0.0;
       }
-      // eigenvector rows (columns < d only; the pad column stays zero)
-      {
-        int k = tm.rank / d, i = tm.rank - (tm.rank / d) * d;
-        while (k < half) {
-          const double s = js.cs[2 * k + 1];
-          if (s != 0.0) {
-            const double c = js.cs[2 * k];
-            const int p = js.pq[k] & 0xffff, q = js.pq[k] >> 16;
-            const double vp = Vt[p * ld + i], vq = Vt[q * ld + i];
-            Vt[p * ld + i] = c * vp - s * vq;
-            Vt[q * ld + i] = s * vp + c * vq;
-          }
-          k += vdk;
-          i += vdi;
-          if (i >= d) {
-            i -= d;
-            ++k;
-          }
-        }
-      }
+      pending = true;
       tm.sync();
     }
     const int rotated = js.flag[0];
@@ -217,20 +252,24 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp) {
       break;  // every pair below the rotation threshold
     }
   }
+  if (pending) {
+    jacobi_vupdate(tm, js, half, nch, (round - 1) & 1, 0);
+    tm.sync();
+  }
   return sweep;
 }
 
 // ---------------------------------------------------------------------------
-// register-tiled team GEMMs on d x d shared-memory operands (ld-strided).
+// register-tiled team GEMMs on d x d shared-memory operands.
 // Thread t owns the interleaved 4x4 tile rows {u + nt a}, cols {v + nt b},
 // u = t / nt, v = t % nt, nt = ceil(d / 4): consecutive threads read
-// consecutive rows / columns, so the odd ld keeps them conflict free.
+// consecutive rows of R, so R must use an odd leading dimension.
 // Requires nt * nt <= team size.
 
 // out = L * R'   (out[i][j] = sum_k L[i][k] R[j][k]); out may alias L or R.
 template <class Team>
-__device__ void team_gemm_nt(const Team &tm, const double *L, const double *R, double *out,
-                             int d, int ld) {
+__device__ void team_gemm_nt(const Team &tm, const double *L, int ldl, const double *R, int ldr,
+                             double *out, int ldo, int d) {
   const int nt = (d + 3) >> 2;
   const int t = tm.rank;
   const bool active = t < nt * nt;
@@ -244,8 +283,8 @@ __device__ void team_gemm_nt(const Team &tm, const double *L, const double *R, d
     int ri[4], rj[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      ri[a] = min(u + nt * a, d - 1) * ld;
-      rj[a] = min(v + nt * a, d - 1) * ld;
+      ri[a] = min(u + nt * a, d - 1) * ldl;
+      rj[a] = min(v + nt * a, d - 1) * ldr;
     }
     for (int k = 0; k < d; ++k) {
       double l[4], r[4];
@@ -267,17 +306,18 @@ __device__ void team_gemm_nt(const Team &tm, const double *L, const double *R, d
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
         const int i = u + nt * a, j = v + nt * b;
-        if (i < d && j < d) out[i * ld + j] = acc[a][b];
+        if (i < d && j < d) out[i * ldo + j] = acc[a][b];
       }
   }
   tm.sync();
 }
 
-// P = W' V over the first r rows (P[i][j] = sum_k W[k][i] V[k][j]), symmetric
-// output: tiles with u <= v compute, each value emitted for (i, j) and (j, i).
+// P = W' V over the first r rows (P[i][j] = sum_k W[k][i] V[vrow[k]][j]),
+// symmetric output: tiles with u <= v compute; every unordered pair {i, j}
+// is emitted exactly once (caller mirrors).
 template <class Team, class Emit>
-__device__ void team_gemm_tn_sym(const Team &tm, const double *W, const double *V, const int *vrow,
-                                 int r, int d, int ld, Emit emit) {
+__device__ void team_gemm_tn_sym(const Team &tm, const double *W, int ldw, const double *V,
+                                 int ldv, const int *vrow, int r, int d, Emit emit) {
   const int nt = (d + 3) >> 2;
   const int t = tm.rank;
   if (t >= nt * nt) return;
@@ -296,11 +336,10 @@ __device__ void team_gemm_tn_sym(const Team &tm, const double *W, const double *
   }
   for (int k = 0; k < r; ++k) {
     double w[4], x[4];
-#pragma unroll
-    const int vk = vrow[k] * ld;
+    const int vk = vrow[k] * ldv;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      w[a] = W[k * ld + ci[a]];
+      w[a] = W[k * ldw + ci[a]];
       x[a] = V[vk + cj[a]];
     }
 #pragma unroll
@@ -320,12 +359,11 @@ __device__ void team_gemm_tn_sym(const Team &tm, const double *W, const double *
 // compacted positive eigenvalues (warp 0 ballot, ascending position order)
 template <class Team>
 __device__ int compact_positive(const Team &tm, JacobiScratch &js, int d) {
-  const int ld = js.ld;
   if (tm.rank < 32) {
     int base = 0;
     for (int i0 = 0; i0 < d; i0 += 32) {
       const int i = i0 + tm.rank;
-      const double lam = i < d ? js.A[i * ld + i] : 0.0;
+      const double lam = i < d ? js.A[i * js.lda + i] : 0.0;
       const bool pos = i < d && lam > 0.0;
       const unsigned mask = __ballot_sync(0xffffffffu, pos);
       if (pos) {
@@ -344,11 +382,11 @@ __device__ int compact_positive(const Team &tm, JacobiScratch &js, int d) {
 // P = sum_{lambda > 0} lambda v v' -> emit(a, b, value) for all a, b (both triangles)
 template <class Team, class Emit>
 __device__ void psd_rebuild(const Team &tm, JacobiScratch &js, int d, Emit emit) {
-  const int ld = js.ld;
+  const int ldv = js.ldv;
   const int r = compact_positive(tm, js, d);
   const int nt = (d + 3) >> 2;
   if (tm.size() <= 32 || nt * nt > tm.size()) {
-    // small (warp teams) or too large for one tile per thread: direct sums
+    // warp teams (d <= 32) or too large for one tile per thread: direct sums
     const int nout = d * (d + 1) / 2;
     for (int o = tm.rank; o < nout; o += tm.size()) {
       int a = 0, rem = o;
@@ -360,7 +398,7 @@ __device__ void psd_rebuild(const Team &tm, JacobiScratch &js, int d, Emit emit)
       double acc = 0.0;
       for (int k = 0; k < r; ++k) {
         const int pi = js.pos[k];
-        acc += (js.lam[k] * js.Vt[pi * ld + a]) * js.Vt[pi * ld + b];
+        acc += (js.lam[k] * js.Vt[pi * ldv + a]) * js.Vt[pi * ldv + b];
       }
       emit(a, b, acc);
       if (a != b) emit(b, a, acc);
@@ -372,10 +410,10 @@ __device__ void psd_rebuild(const Team &tm, JacobiScratch &js, int d, Emit emit)
   double *W = js.A;
   for (int e = tm.rank; e < r * d; e += tm.size()) {
     const int k = e / d, i = e - k * d;
-    W[k * ld + i] = js.lam[k] * js.Vt[js.pos[k] * ld + i];
+    W[k * js.lda + i] = js.lam[k] * js.Vt[js.pos[k] * ldv + i];
   }
   tm.sync();
-  team_gemm_tn_sym(tm, W, js.Vt, js.pos, r, d, ld, [&](int i, int j, double v) {
+  team_gemm_tn_sym(tm, W, js.lda, js.Vt, ldv, js.pos, r, d, [&](int i, int j, double v) {
     emit(i, j, v);
     if (i != j) emit(j, i, v);
   });
@@ -448,48 +486,55 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   }
   const int dp = d + (d & 1);
   JacobiScratch js = jacobi_carve(scratch, dp);
-  const int ld = js.ld;
+  const int lda = js.lda, ldv = js.ldv;
   double *A = js.A;
-  const bool warm = (MODE == CONE_HOT) && ca.warm && W.vvalid[k] &&
-                    ((d + 3) >> 2) * ((d + 3) >> 2) <= tm.size();
-  // load (raw), then symmetrise sym = 0.5 (B + B')  (symmat.py:157)
+  const int age = (MODE == CONE_HOT && ca.warm) ? W.vvalid[k] : 0;
+  const bool warm = age > 0 && age < kWarmMaxAge && ((d + 3) >> 2) * ((d + 3) >> 2) <= tm.size();
+  jacobi_prepare(tm, js, dp, !warm);
+  // load (raw) and the previous eigenvectors (warm)
   for (int e = tm.rank; e < d * d; e += tm.size()) {
     const int a = e / d, bcol = e - a * d;
     double v;
     if (MODE == CONE_HOT) v = hot_slot_load(P, S, W, off + e, shift);
     else v = ca.in[off + e] * ca.in_scale;
-    A[a * ld + bcol] = v;
-    if (warm) js.Vt[a * ld + bcol] = W.vstore[off + e];
+    A[a * lda + bcol] = v;
+    if (warm) js.Vt[a * ldv + bcol] = W.vstore[off + e];
   }
   if (d & 1) {
     for (int e = tm.rank; e < dp; e += tm.size()) {
-      A[d * ld + e] = 0.0;
-      A[e * ld + d] = 0.0;
-      js.Vt[d * ld + e] = (e == d) ? 1.0 : 0.0;
-      js.Vt[e * ld + d] = (e == d) ? 1.0 : 0.0;
+      A[d * lda + e] = 0.0;
+      A[e * lda + d] = 0.0;
     }
   }
-  jacobi_prepare(tm, js, dp, !warm);
+  if (warm) {
+    // zero padding columns / dummy row of Vt (identity on the dummy)
+    for (int e = tm.rank; e < dp * ldv; e += tm.size()) {
+      const int i = e / ldv, j = e - i * ldv;
+      if (i >= d || j >= d) js.Vt[e] = (i == j) ? 1.0 : 0.0;
+    }
+  }
   tm.sync();
+  // sym = 0.5 (B + B')  (symmat.py:157)
   for (int e = tm.rank; e < d * d; e += tm.size()) {
     const int a = e / d, bcol = e - a * d;
     if (a < bcol) {
-      const double s = 0.5 * (A[a * ld + bcol] + A[bcol * ld + a]);
-      A[a * ld + bcol] = s;
-      A[bcol * ld + a] = s;
+      const double s = 0.5 * (A[a * lda + bcol] + A[bcol * lda + a]);
+      A[a * lda + bcol] = s;
+      A[bcol * lda + a] = s;
     }
   }
   tm.sync();
   if (warm) {
-    // B = V X V' (rows of Vt are the previous eigenvectors)
-    team_gemm_nt(tm, js.Vt, A, A, d, ld);   // T1 = Vt X   (X symmetric)
-    team_gemm_nt(tm, A, js.Vt, A, d, ld);   // B = T1 Vt'
+    // B = V X V' (rows of Vt are the previous eigenvectors): T1 = Vt X, then
+    // B' = Vt T1' (= B for symmetric X) with the odd-ld operand on the right
+    team_gemm_nt(tm, js.Vt, ldv, A, lda, A, lda, d);
+    team_gemm_nt(tm, js.Vt, ldv, A, lda, A, lda, d);
     for (int e = tm.rank; e < d * d; e += tm.size()) {
       const int a = e / d, bcol = e - a * d;
       if (a < bcol) {
-        const double s = 0.5 * (A[a * ld + bcol] + A[bcol * ld + a]);
-        A[a * ld + bcol] = s;
-        A[bcol * ld + a] = s;
+        const double s = 0.5 * (A[a * lda + bcol] + A[bcol * lda + a]);
+        A[a * lda + bcol] = s;
+        A[bcol * lda + a] = s;
       }
     }
     tm.sync();
@@ -498,12 +543,12 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   if (MODE == CONE_HOT && tm.rank == 0 && W.sweeps) W.sweeps[k] = sw;
   // non-finite eigenvalue -> EigenFailure (symmat.py:162-163)
   double nb = 0.0;
-  for (int i = tm.rank; i < d; i += tm.size()) nb += isfinite(A[i * ld + i]) ? 0.0 : 1.0;
+  for (int i = tm.rank; i < d; i += tm.size()) nb += isfinite(A[i * lda + i]) ? 0.0 : 1.0;
   const bool bad = team_sum(tm, nb, js.red) > 0.0;
   if (bad && tm.rank == 0) atomicOr(W.err, 1);
   if (MODE == CONE_MINEIG) {
     double mn = CUDART_INF;
-    for (int i = 0; i < d; ++i) mn = fmin(mn, A[i * ld + i]);
+    for (int i = 0; i < d; ++i) mn = fmin(mn, A[i * lda + i]);
     if (tm.rank == 0) ca.out[k] = mn;
     tm.sync();
     return;
@@ -511,9 +556,9 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   if (MODE == CONE_HOT && ca.warm) {
     for (int e = tm.rank; e < d * d; e += tm.size()) {
       const int a = e / d, bcol = e - a * d;
-      W.vstore[off + e] = js.Vt[a * ld + bcol];
+      W.vstore[off + e] = js.Vt[a * ldv + bcol];
     }
-    if (tm.rank == 0) W.vvalid[k] = bad ? 0 : 1;
+    if (tm.rank == 0) W.vvalid[k] = bad ? 0 : (warm ? age + 1 : 1);
   }
   if (MODE == CONE_HOT) {
     psd_rebuild(tm, js, d, [&](int a, int bcol, double v) {
@@ -533,7 +578,7 @@ constexpr int kConeBlock = 512;  // threads per CTA team (d > 32)
 // one warp per clique (d <= 32); dynamic smem = warps * scratch(dpmax)
 template <int MODE>
 __global__ void __launch_bounds__(kBlock) k_cone_warp(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   const int wid = threadIdx.x >> 5;
   const int gw = blockIdx.x * (blockDim.x >> 5) + wid;
   if (gw >= ca.count) return;
@@ -547,7 +592,7 @@ __global__ void __launch_bounds__(kBlock) k_cone_warp(DevProblem P, DevState S, 
 // one CTA per clique (d > 32)
 template <int MODE>
 __global__ void __launch_bounds__(kConeBlock, 2) k_cone_block(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   if ((int)blockIdx.x >= ca.count) return;
   BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
   cone_one<MODE>(tm, P, S, W, ca, ca.ids[blockIdx.x], smem);
