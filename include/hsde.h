@@ -59,7 +59,26 @@ typedef struct hsde_problem_desc {
   const int32_t *clique_sizes;   /* [p]                                             */
   const int32_t *slot_cov;       /* [n_d] covered position of each clique slot
                                      (graphs.py:184-187 gather_index, compressed)  */
+  /* ---- sharding (paper_1611_01828_b200/shard.py); zero / NULL on one GPU ---- */
+  const double *cover_counts;    /* [n_c] GLOBAL cover counts D (NULL: from slot_cov) */
+  const uint8_t *owned;          /* [n_c] 1 if this shard owns the coordinate (NULL: all) */
+  int32_t n_sep;                 /* global separator count |S|                      */
+  int32_t n_sep_local;           /* separator coordinates this shard touches        */
+  const int32_t *sep_local;      /* [n_sep_local] local covered index               */
+  const int32_t *sep_pos;        /* [n_sep_local] position in the global list S     */
+  int32_t follower;              /* 1 on every shard but the lead (replicated y, tau
+                                    are counted once, by the lead)                  */
 } hsde_problem_desc;
+
+/* Multi-GPU communicator: one shard per rank, NCCL all-reduce over NVLink.
+ * The unique id comes from hsde_nccl_unique_id on rank 0, broadcast by the
+ * caller (e.g. torch.distributed). */
+#define HSDE_NCCL_ID_BYTES 128
+typedef struct hsde_comm {
+  int32_t world;
+  int32_t rank;
+  uint8_t nccl_id[HSDE_NCCL_ID_BYTES];
+} hsde_comm;
 
 typedef struct hsde_settings {
   double alpha;              /* over-relaxation in [1,2)        (solver.py:84)     */
@@ -81,6 +100,8 @@ typedef struct hsde_info_t {
   double zeta_scale;         /* 1 + zeta . M^{-1} zeta           (solver.py:269)    */
   int32_t schur_diagonal;    /* S = I + A P^{-1} A' is diagonal                     */
   int32_t max_clique;
+  int32_t n_shards;          /* shards held by this handle                          */
+  int32_t mode;              /* 0 single GPU, 1 emulated shards (one GPU), 2 NCCL   */
 } hsde_info_t;
 
 typedef struct hsde_handle hsde_t;
@@ -90,6 +111,17 @@ typedef struct hsde_handle hsde_t;
  * factors S = I + A P^{-1} A' (cuSOLVER, fp64) and stores S^{-1}, solves
  * M zeta on the device.  The caller may free the desc buffers on return. */
 int hsde_create(const hsde_problem_desc *desc, const hsde_settings *settings, hsde_t **out);
+
+/* Sharded variant: `nshards` shard descriptions.  With comm
+ * and comm->world > 1: NCCL mode, exactly one shard (this rank's).  Without
+ * comm and nshards > 1: all shards on one device with device-side reductions
+ * (emulation; same kernels, same three all-reduce points). */
+int hsde_create_sharded(const hsde_problem_desc *descs, int32_t nshards,
+                        const hsde_settings *settings, const hsde_comm *comm, hsde_t **out);
+int hsde_nccl_unique_id(uint8_t *out);  /* HSDE_NCCL_ID_BYTES bytes */
+int hsde_shard_total(const hsde_t *h, int32_t shard, int64_t *total);
+int hsde_set_state_shard(hsde_t *h, int32_t shard, const double *u, const double *w);
+int hsde_get_state_shard(hsde_t *h, int32_t shard, double *u, double *w);
 void hsde_destroy(hsde_t *h);
 const char *hsde_last_error(const hsde_t *h);  /* h may be NULL: last create error */
 int hsde_info(const hsde_t *h, hsde_info_t *out);

@@ -31,8 +31,10 @@ EXPORTED = (
     "hsde_get_state", "hsde_reset_state", "hsde_iterate", "hsde_check", "hsde_certificate",
     "hsde_affine_project", "hsde_solve_inner", "hsde_project_cone", "hsde_residuals",
     "hsde_get_minv_zeta", "hsde_time_iterations", "hsde_profile_iterations",
-    "hsde_profile_name", "hsde_sync", "hsde_set_alpha", "hsde_stats",
+    "hsde_profile_name", "hsde_sync", "hsde_set_alpha", "hsde_stats", "hsde_create_sharded",
+    "hsde_nccl_unique_id", "hsde_shard_total", "hsde_set_state_shard", "hsde_get_state_shard",
 )
+HSDE_NCCL_ID_BYTES = 128
 
 _dp = C.POINTER(C.c_double)
 _i64p = C.POINTER(C.c_int64)
@@ -46,7 +48,14 @@ class ProblemDesc(C.Structure):
         ("a_row_ptr", _i64p), ("a_col", _i32p), ("a_val", _dp),
         ("c", _dp), ("b", _dp),
         ("clique_offsets", _i64p), ("clique_sizes", _i32p), ("slot_cov", _i32p),
+        ("cover_counts", _dp), ("owned", C.POINTER(C.c_uint8)), ("n_sep", C.c_int32),
+        ("n_sep_local", C.c_int32), ("sep_local", _i32p), ("sep_pos", _i32p),
+        ("follower", C.c_int32),
     ]
+
+
+class Comm(C.Structure):
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_uint8 * 128)]
 
 
 class Settings(C.Structure):
@@ -62,7 +71,7 @@ class Info(C.Structure):
         ("total", C.c_int64), ("n_c", C.c_int32), ("m", C.c_int32), ("p", C.c_int32),
         ("n_d", C.c_int64), ("nnz", C.c_int64), ("sigma_c", C.c_double),
         ("sigma_b", C.c_double), ("zeta_scale", C.c_double), ("schur_diagonal", C.c_int32),
-        ("max_clique", C.c_int32),
+        ("max_clique", C.c_int32), ("n_shards", C.c_int32), ("mode", C.c_int32),
     ]
 
 
@@ -102,6 +111,12 @@ def load() -> C.CDLL:
         "hsde_sync": (C.c_int, [vp]),
         "hsde_set_alpha": (C.c_int, [vp, C.c_double]),
         "hsde_stats": (C.c_int, [vp, _dp]),
+        "hsde_create_sharded": (C.c_int, [C.POINTER(ProblemDesc), C.c_int32, C.POINTER(Settings),
+                                          C.POINTER(Comm), C.POINTER(vp)]),
+        "hsde_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+        "hsde_shard_total": (C.c_int, [vp, C.c_int32, C.POINTER(C.c_int64)]),
+        "hsde_set_state_shard": (C.c_int, [vp, C.c_int32, _dp, _dp]),
+        "hsde_get_state_shard": (C.c_int, [vp, C.c_int32, _dp, _dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -133,12 +148,54 @@ class Handle:
     """Owns one device-resident problem + ADMM state (one hsde_t)."""
 
     def __init__(self, cp, *, alpha=1.6, tol=1e-4, infeas_tau_tol=1e-9, infeas_kappa_tol=1e-6,
-                 check_interval=20, normalize=True, device=0, flags=0):
+                 check_interval=20, normalize=True, device=0, flags=0, shards=None, comm=None):
+        """One problem on one device (`cp`), or sharded (`shards`, list of
+        paper_1611_01828_b200.shard.Shard): all shards emulated on this device
+        (comm None) or this rank's single shard with an NCCL communicator
+        (comm = (world, rank, nccl_id bytes))."""
         lib = load()
         self._lib = lib
         self.cp = cp
+        keep = []
+        parts = shards if shards is not None else [None]
+        descs = (ProblemDesc * len(parts))()
+        for i, sh in enumerate(parts):
+            self._fill_desc(descs[i], cp if sh is None else sh.problem, sh, keep)
+        st = Settings(alpha=alpha, tol=tol, infeas_tau_tol=infeas_tau_tol,
+                      infeas_kappa_tol=infeas_kappa_tol, check_interval=check_interval,
+                      normalize=1 if normalize else 0, device=device, flags=flags)
+        cm = None
+        if comm is not None:
+            cm = Comm(world=int(comm[0]), rank=int(comm[1]))
+            C.memmove(cm.nccl_id, bytes(comm[2]), HSDE_NCCL_ID_BYTES)
+        h = C.c_void_p()
+        rc = lib.hsde_create_sharded(descs, len(parts), C.byref(st),
+                                     C.byref(cm) if cm is not None else None, C.byref(h))
+        if rc != HSDE_OK:
+            raise_for(rc, lib.hsde_last_error(None).decode())
+        self._h = h
+        del keep  # the library copied everything
+        inf = Info()
+        lib.hsde_info(h, C.byref(inf))
+        self.n_shards = int(inf.n_shards)
+        self.mode = int(inf.mode)
+        self.totals = []
+        for g in range(self.n_shards):
+            t = C.c_int64()
+            lib.hsde_shard_total(h, g, C.byref(t))
+            self.totals.append(int(t.value))
+        self.total = self.totals[0]
+        self.sigma_c = float(inf.sigma_c)
+        self.sigma_b = float(inf.sigma_b)
+        self.zeta_scale = float(inf.zeta_scale)
+        self.schur_diagonal = bool(inf.schur_diagonal)
+        self.max_clique = int(inf.max_clique)
+        self.alpha = alpha
+
+    @staticmethod
+    def _fill_desc(desc, cp, sh, keep):
         A = cp.A
-        self._keep = keep = {
+        arrs = {
             "rp": np.ascontiguousarray(A.indptr, dtype=np.int64),
             "col": np.ascontiguousarray(A.indices, dtype=np.int32),
             "val": np.ascontiguousarray(A.data, dtype=np.float64),
@@ -148,30 +205,29 @@ class Handle:
             "sz": np.ascontiguousarray(cp.sizes, dtype=np.int32),
             "sc": np.ascontiguousarray(cp.slot_cov, dtype=np.int32),
         }
-        desc = ProblemDesc(
-            n=cp.n, m=cp.m, n_c=cp.N_c, p=cp.p, n_d=cp.n_d, nnz=int(A.nnz),
-            a_row_ptr=_ptr(keep["rp"], C.c_int64), a_col=_ptr(keep["col"], C.c_int32),
-            a_val=_ptr(keep["val"], C.c_double), c=_ptr(keep["c"], C.c_double),
-            b=_ptr(keep["b"], C.c_double), clique_offsets=_ptr(keep["off"], C.c_int64),
-            clique_sizes=_ptr(keep["sz"], C.c_int32), slot_cov=_ptr(keep["sc"], C.c_int32))
-        st = Settings(alpha=alpha, tol=tol, infeas_tau_tol=infeas_tau_tol,
-                      infeas_kappa_tol=infeas_kappa_tol, check_interval=check_interval,
-                      normalize=1 if normalize else 0, device=device, flags=flags)
-        h = C.c_void_p()
-        rc = lib.hsde_create(C.byref(desc), C.byref(st), C.byref(h))
-        if rc != HSDE_OK:
-            raise_for(rc, lib.hsde_last_error(None).decode())
-        self._h = h
-        self._keep = None  # library copied everything
-        inf = Info()
-        lib.hsde_info(h, C.byref(inf))
-        self.total = int(inf.total)
-        self.sigma_c = float(inf.sigma_c)
-        self.sigma_b = float(inf.sigma_b)
-        self.zeta_scale = float(inf.zeta_scale)
-        self.schur_diagonal = bool(inf.schur_diagonal)
-        self.max_clique = int(inf.max_clique)
-        self.alpha = alpha
+        keep.append(arrs)
+        desc.n, desc.m, desc.n_c, desc.p = cp.n, cp.m, cp.N_c, cp.p
+        desc.n_d, desc.nnz = cp.n_d, int(A.nnz)
+        desc.a_row_ptr = _ptr(arrs["rp"], C.c_int64)
+        desc.a_col = _ptr(arrs["col"], C.c_int32)
+        desc.a_val = _ptr(arrs["val"], C.c_double)
+        desc.c = _ptr(arrs["c"], C.c_double)
+        desc.b = _ptr(arrs["b"], C.c_double)
+        desc.clique_offsets = _ptr(arrs["off"], C.c_int64)
+        desc.clique_sizes = _ptr(arrs["sz"], C.c_int32)
+        desc.slot_cov = _ptr(arrs["sc"], C.c_int32)
+        if sh is not None:
+            arrs["D"] = np.ascontiguousarray(sh.D, dtype=np.float64)
+            arrs["own"] = np.ascontiguousarray(sh.owned, dtype=np.uint8)
+            arrs["sl"] = np.ascontiguousarray(sh.sep_local, dtype=np.int32)
+            arrs["sp"] = np.ascontiguousarray(sh.sep_pos, dtype=np.int32)
+            desc.cover_counts = _ptr(arrs["D"], C.c_double)
+            desc.owned = _ptr(arrs["own"], C.c_uint8)
+            desc.n_sep = int(sh.n_sep)
+            desc.n_sep_local = int(arrs["sl"].size)
+            desc.sep_local = _ptr(arrs["sl"], C.c_int32)
+            desc.sep_pos = _ptr(arrs["sp"], C.c_int32)
+            desc.follower = 0 if sh.rank == 0 else 1
 
     # -- plumbing -------------------------------------------------------------
     def _rc(self, rc):
@@ -206,11 +262,18 @@ class Handle:
         w = self._vec(w, self.total)
         self._rc(self._lib.hsde_set_state(self._h, _ptr(u, C.c_double), _ptr(w, C.c_double)))
 
-    def get_state(self):
-        u = np.empty(self.total)
-        w = np.empty(self.total)
-        self._rc(self._lib.hsde_get_state(self._h, _ptr(u, C.c_double), _ptr(w, C.c_double)))
+    def get_state(self, shard: int = 0):
+        u = np.empty(self.totals[shard])
+        w = np.empty(self.totals[shard])
+        self._rc(self._lib.hsde_get_state_shard(self._h, shard, _ptr(u, C.c_double),
+                                                _ptr(w, C.c_double)))
         return u, w
+
+    def set_state_shard(self, shard: int, u, w):
+        u = self._vec(u, self.totals[shard])
+        w = self._vec(w, self.totals[shard])
+        self._rc(self._lib.hsde_set_state_shard(self._h, shard, _ptr(u, C.c_double),
+                                                _ptr(w, C.c_double)))
 
     def reset_state(self):
         self._rc(self._lib.hsde_reset_state(self._h))
@@ -283,6 +346,15 @@ class Handle:
             if name:
                 out[name] = float(ms[i])
         return out, int(nl.value)
+
+
+def nccl_unique_id() -> bytes:
+    lib = load()
+    buf = (C.c_uint8 * HSDE_NCCL_ID_BYTES)()
+    rc = lib.hsde_nccl_unique_id(buf)
+    if rc != HSDE_OK:
+        raise_for(rc, lib.hsde_last_error(None).decode())
+    return bytes(buf)
 
 
 def exported_symbols() -> list[str]:

@@ -1,15 +1,28 @@
 // hsde_capi.cu -- C ABI (include/hsde.h) over the sm_100a kernels.
 //
 // Host responsibilities: validate and derive the device layout once
-// (CSC of A, row segments, cover lists, P^{-1}, normalisation), assemble and
-// factor the m x m Schur matrix S = I + A P^{-1} A' on the device
-// (solver.py:248-283: dense chunks + cuBLAS DGEMM, cuSOLVER Cholesky, explicit
-// S^{-1}), solve M zeta with the device inner solve, capture the iteration
-// as a CUDA graph, and run the residual / certificate reductions.
+// (CSC of A, row segments over owned columns, cover lists, P^{-1},
+// normalisation), assemble and factor the m x m Schur matrix
+// S = I + A P^{-1} A' on the device (solver.py:248-283: dense column chunks +
+// cuBLAS DGEMM, cuSOLVER Cholesky, explicit S^{-1}), solve M zeta with the
+// device inner solve, capture the iteration as a CUDA graph, and run the
+// residual / certificate reductions.
+//
+// A handle holds one or more *shards* (shard.py / SURVEY 8(e)).  Shards meet
+// at three all-reduce points per iteration (separator pull-scatter partials,
+// partial A t, partial c.ua):
+//   single GPU     -- one shard, no reduction;
+//   NCCL           -- one shard per rank, ncclAllReduce on the handle's stream
+//                     (captured in the iteration graph);
+//   emulated       -- all shards of one problem on one device, reductions by a
+//                     device kernel summing the shard buffers in rank order
+//                     (tests the sharded kernels on one GPU without ranks that
+//                     wait on each other).
 
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -30,53 +43,78 @@ std::string g_create_error;
 
 enum ProfSlot {
   PS_PREP = 0, PS_RHS, PS_SPMV, PS_SCHUR, PS_UA, PS_SCALARS, PS_CONE_WARP, PS_CONE_BLOCK,
-  PS_XUPD, PS_SNAPSHOT, PS_COUNT
+  PS_XUPD, PS_COMM, PS_COUNT
 };
 const char *kProfNames[HSDE_PROFILE_SLOTS] = {
     "k_prep_ry", "k_rhs", "k_spmv_seg", "k_schur", "k_ua", "k_scalars", "k_cone_warp",
-    "k_cone_block", "k_xupd", "snapshot", "", "", "", "", "", ""};
+    "k_cone_block", "k_xupd", "allreduce", "", "", "", "", "", ""};
 
 struct ConePlan {
   int *ids = nullptr;
   int count = 0;
   int dpmax = 0;
   size_t smem = 0;
-  double *gscratch = nullptr;  // when the scratch exceeds shared memory
-  int per_block = 0;           // warps per CTA (warp plan)
+  int per_block = 0;  // warps per CTA (warp plan)
 };
 
+enum Mode { MODE_SINGLE = 0, MODE_EMULATED = 1, MODE_NCCL = 2 };
+enum Buf { BUF_SEP = 0, BUF_Q, BUF_RED, BUF_CHK, BUF_SCHUR, BUF_MINEIG, BUF_COUNT };
+
+// sum (or min) the G shard buffers element-wise, result written back to all
+__global__ void k_reduce_ptrs(double *const *ptrs, int G, int64_t n, int64_t off, int op_min) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double s = ptrs[0][off + k];
+    for (int g = 1; g < G; ++g) s = op_min ? fmin(s, ptrs[g][off + k]) : s + ptrs[g][off + k];
+    for (int g = 0; g < G; ++g) ptrs[g][off + k] = s;
+  }
+}
+
 }  // namespace
+
+struct ShardDev {
+  DevProblem P{};
+  DevState S{};
+  DevWork W{};
+  ConePlan warp_plan, block_plan;
+  double *d_zeta = nullptr;       // [T-1] (c, 0, -b, 0) normalised
+  double *d_prev_u = nullptr, *d_prev_w = nullptr;
+  double *d_tmp = nullptr, *d_tmp2 = nullptr, *d_tmp3 = nullptr;  // [T] scratch
+  double *d_hv = nullptr;         // [n_c] pull-scatter scratch
+  double *d_qseg2 = nullptr;
+  double *d_c_orig = nullptr, *d_b_orig = nullptr;
+  double *d_consts = nullptr;     // [0] sigma_b [1] sigma_c
+  double *d_chk = nullptr;        // [64] check sums
+  double *d_mineig = nullptr;     // [p]
+  double *d_schur = nullptr;      // [m*m] partial / factored Schur (owned)
+  int grid_heavy = 0, grid_nc = 1, grid_nd = 1, grid_m = 1, grid_T = 1, grid_seg = 1, grid_schur = 1;
+  size_t schur_smem = 0;
+  std::vector<int> sizes;         // clique sizes (host copy)
+  int64_t maxcol = 0;
+  double nc2_owned = 0;           // sum of c^2 over owned coordinates (original units)
+};
 
 struct hsde_handle {
   int dev = 0;
   cudaStream_t st = nullptr;
   hsde_settings set{};
   hsde_info_t info{};
-  DevProblem P{};
-  DevState S{};
-  DevWork W{};
   std::vector<void *> bufs;
   std::string err;
-  ConePlan warp_plan, block_plan;
-  // extra device buffers
-  double *d_zeta = nullptr;       // [T-1] (c, 0, -b, 0) normalised
-  double *d_prev_u = nullptr, *d_prev_w = nullptr;
-  double *d_tmp = nullptr, *d_tmp2 = nullptr, *d_tmp3 = nullptr;  // [T] scratch
-  double *d_qseg2 = nullptr;
-  double *d_c_orig = nullptr, *d_b_orig = nullptr;
-  double *d_consts = nullptr;     // [0] sigma_b [1] sigma_c [2] 1.0
-  double *d_chk = nullptr;        // [64] check sums
-  double *d_mineig = nullptr;     // [p]
-  double *h_chk = nullptr;        // pinned [64]
-  int grid_heavy = 0;
-  int grid_nc = 1, grid_nd = 1, grid_m = 1, grid_T = 1, grid_seg = 1, grid_schur = 1;
-  size_t schur_smem = 0;
-  double norm_b = 0, norm_c = 0;  // of the iterated (normalised) data
-  // graphs
+  std::vector<ShardDev> sh;
+  int mode = MODE_SINGLE;
+  ncclComm_t nccl = nullptr;
+  int world = 1, rank = 0;
+  double **d_ptrs[BUF_COUNT] = {};  // emulation pointer tables
+  double *h_chk = nullptr;          // pinned [64]
+  double norm_b = 0, norm_c = 0;    // of the iterated (normalised) data
+  int n_sep = 0;
+  bool schur_diag = false;
   cudaGraphExec_t g1 = nullptr, gci = nullptr;
   int gci_len = 0;
   bool factor = true;
-  bool warm = true;               // warm-started eigensolves (HSDE_FLAG_COLD_EIG clears)
+  bool warm = true;
+  bool multi() const { return mode != MODE_SINGLE; }
 };
 
 #define CK(call)                                                                      \
@@ -97,6 +135,12 @@ struct hsde_handle {
     }                                                                                 \
   } while (0)
 
+#define RC(x)            \
+  do {                   \
+    int rc_ = (x);       \
+    if (rc_) return rc_; \
+  } while (0)
+
 namespace {
 
 template <class T>
@@ -114,8 +158,7 @@ int dalloc(hsde_handle *h, T **p, size_t n) {
 
 template <class T>
 int dupload(hsde_handle *h, T **p, const T *src, size_t n) {
-  int rc = dalloc(h, p, n);
-  if (rc) return rc;
+  RC(dalloc(h, p, n));
   if (n) {
     cudaError_t e = cudaMemcpy(*p, src, n * sizeof(T), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
@@ -133,12 +176,42 @@ int grid_for(int64_t n, int cap = 148 * 8) {
   return (int)g;
 }
 
-// densify columns [c0, c1) of A (CSC) into Dm (m x w, col-major) and Ds = Dm diag(p_inv)
+double *buf_ptr(ShardDev &s, int which) {
+  switch (which) {
+    case BUF_SEP: return s.W.sepbuf;
+    case BUF_Q: return s.W.qbuf;
+    case BUF_RED: return s.W.red;
+    case BUF_CHK: return s.d_chk;
+    case BUF_SCHUR: return s.d_schur;
+    default: return s.d_mineig;
+  }
+}
+
+// All-reduce `n` doubles of buffer `which` (+offset) across shards / ranks.
+int reduce(hsde_handle *h, int which, int64_t n, int64_t off = 0, bool op_min = false) {
+  if (!h->multi() || n <= 0) return 0;
+  if (h->mode == MODE_NCCL) {
+    double *b = buf_ptr(h->sh[0], which) + off;
+    ncclResult_t r = ncclAllReduce(b, b, (size_t)n, ncclDouble, op_min ? ncclMin : ncclSum, h->nccl, h->st);
+    if (r != ncclSuccess) {
+      h->err = std::string("ncclAllReduce: ") + ncclGetErrorString(r);
+      return HSDE_ERR_CUDA;
+    }
+    return 0;
+  }
+  const int G = (int)h->sh.size();
+  k_reduce_ptrs<<<grid_for(n), kBlock, 0, h->st>>>(h->d_ptrs[which], G, n, off, op_min ? 1 : 0);
+  CKL();
+  return 0;
+}
+
+// densify owned columns [c0, c1) of A (CSC) into Dm (m x w, col-major) and Ds = Dm diag(p_inv)
 __global__ void k_densify(DevProblem P, int c0, int c1, double *Dm, double *Ds) {
   const int64_t w = c1 - c0;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < w;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int l = c0 + (int)k;
+    if (!owns(P, l)) continue;
     for (int64_t e = P.at_cp[l]; e < P.at_cp[l + 1]; ++e) {
       const int i = P.at_row[e];
       Dm[i + k * P.m] = P.at_val[e];
@@ -172,104 +245,226 @@ __global__ void k_finite_check(const double *x, int64_t n, int *flag) {
     if (!isfinite(x[k])) atomicOr(flag, 1);
 }
 
-// cone launches
-int launch_cone(hsde_handle *h, int mode, const ConePlan &pl, bool block, const double *in,
-                double *out, double in_scale, cudaStream_t st) {
+// S_ii partial = sum over owned columns of (A_il p_l) A_il (diagonal case)
+__global__ void k_diag_schur(DevProblem P, double *diag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = P.a_rp[i]; k < P.a_rp[i + 1]; ++k)
+      s += (P.a_val[k] * P.p_inv[P.a_col[k]]) * P.a_val[k];
+    diag[i] = s;
+  }
+}
+
+__global__ void k_diag_finish(double *diag, int m, int *flag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const double s = diag[i] + 1.0;
+    if (!(s > 0.0) || !isfinite(s)) atomicOr(flag, 1);
+    diag[i] = 1.0 / s;
+  }
+}
+
+// cone launches (one shard)
+int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool block,
+                const double *in, double *out, double in_scale, cudaStream_t st) {
   if (pl.count == 0) return 0;
   ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0};
   if (!block) {
     const int grid = (pl.count + pl.per_block - 1) / pl.per_block;
     const int thr = pl.per_block * 32;
-    if (mode == CONE_HOT) k_cone_warp<CONE_HOT><<<grid, thr, pl.smem, st>>>(h->P, h->S, h->W, ca);
-    else if (mode == CONE_PLAIN) k_cone_warp<CONE_PLAIN><<<grid, thr, pl.smem, st>>>(h->P, h->S, h->W, ca);
-    else k_cone_warp<CONE_MINEIG><<<grid, thr, pl.smem, st>>>(h->P, h->S, h->W, ca);
+    if (mode == CONE_HOT) k_cone_warp<CONE_HOT><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
+    else if (mode == CONE_PLAIN) k_cone_warp<CONE_PLAIN><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
+    else k_cone_warp<CONE_MINEIG><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
   } else {
-    if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(h->P, h->S, h->W, ca);
-    else if (mode == CONE_PLAIN) k_cone_block<CONE_PLAIN><<<pl.count, kConeBlock, pl.smem, st>>>(h->P, h->S, h->W, ca);
-    else k_cone_block<CONE_MINEIG><<<pl.count, kConeBlock, pl.smem, st>>>(h->P, h->S, h->W, ca);
+    if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
+    else if (mode == CONE_PLAIN) k_cone_block<CONE_PLAIN><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
+    else k_cone_block<CONE_MINEIG><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
   }
-  CKL();
-  return 0;
-}
-
-// The inner solve of _solve_inner_parts (solver.py:203-245) on explicit vectors:
-// rho (T-1, layout x|s|y|v) -> u12 (T-1).  uy by the explicit CSR pass.
-int inner_explicit(hsde_handle *h, const double *rho, double *u12, cudaStream_t st) {
-  const DevProblem &P = h->P;
-  const double *rx = rho, *rs = rho + P.n_c, *ry = rho + P.n_c + P.n_d,
-               *rv = rho + P.n_c + P.n_d + P.m;
-  k_rhs<false><<<h->grid_nc + h->grid_heavy, kBlock, 0, st>>>(P, h->S, h->W, rx, rs, ry, rv, h->grid_nc);
-  CKL();
-  k_spmv_seg<<<h->grid_seg, kBlock, 0, st>>>(P, h->W.t, h->W.qseg);
-  CKL();
-  k_schur<<<h->grid_schur, kBlock, h->schur_smem, st>>>(P, h->W.qseg, h->W.qp);
-  CKL();
-  k_ua<false><<<h->grid_nc, kBlock, 0, st>>>(P, h->W, h->W.qp);
-  CKL();
-  double *ua = u12, *ub = u12 + P.n_c, *uy = u12 + P.n_c + P.n_d, *uv = uy + P.m;
-  CK(cudaMemcpyAsync(ua, h->W.ua, sizeof(double) * P.n_c, cudaMemcpyDeviceToDevice, st));
-  k_slot_out<<<h->grid_nd, kBlock, 0, st>>>(P, rs, rv, ua, ub, uv);
-  CKL();
-  k_spmv_seg<<<h->grid_seg, kBlock, 0, st>>>(P, ua, h->d_qseg2);
-  CKL();
-  k_uy_from_seg<<<h->grid_m, kBlock, 0, st>>>(P, h->d_qseg2, ry, uy);
   CKL();
   return 0;
 }
 
 // ordered dot of two device vectors into out (device scalar)
-int dev_dot(hsde_handle *h, const double *a, const double *b, int64_t n, double *out,
-            cudaStream_t st) {
+int dev_dot(hsde_handle *h, ShardDev &s, const double *a, const double *b, int64_t n, double *out) {
   const int g = grid_for(n);
-  k_dot_part<<<g, kBlock, 0, st>>>(a, b, n, h->W.part);
+  k_dot_part<<<g, kBlock, 0, h->st>>>(a, b, n, s.W.part);
   CKL();
-  k_sum_parts<<<1, 1024, 0, st>>>(h->W.part, g, out);
+  k_sum_parts<<<1, 1024, 0, h->st>>>(s.W.part, g, out);
   CKL();
   return 0;
 }
 
-// one hot iteration (solver.py:375-395), eager launches; prof events optional
-int launch_iteration(hsde_handle *h, cudaStream_t st, cudaEvent_t *ev = nullptr, int *launches = nullptr) {
-  const DevProblem &P = h->P;
-  int slot = 0;
-  auto mark = [&](int s) {
-    if (ev) cudaEventRecord(ev[s], st);
-    slot = s;
-  };
-  (void)slot;
-  if (ev) cudaEventRecord(ev[PS_COUNT], st);
-  k_rhs<true><<<h->grid_nc + h->grid_heavy, kBlock, 0, st>>>(P, h->S, h->W, nullptr, nullptr, nullptr,
-                                                             nullptr, h->grid_nc);
+int dev_dot_owned(hsde_handle *h, ShardDev &s, const double *a, const double *b, double *out) {
+  k_dot_owned_part<<<s.grid_nc, kBlock, 0, h->st>>>(s.P, a, b, s.W.part);
   CKL();
-  mark(PS_RHS);
-  k_spmv_seg<<<h->grid_seg, kBlock, 0, st>>>(P, h->W.t, h->W.qseg);
+  k_sum_parts<<<1, 1024, 0, h->st>>>(s.W.part, s.grid_nc, out);
   CKL();
-  mark(PS_SPMV);
-  k_schur<<<h->grid_schur, kBlock, h->schur_smem, st>>>(P, h->W.qseg, h->W.qp);
-  CKL();
-  mark(PS_SCHUR);
-  k_ua<true><<<h->grid_nc, kBlock, 0, st>>>(P, h->W, h->W.qp);
-  CKL();
-  const bool exact = (h->set.flags & HSDE_FLAG_EXACT_UY) != 0;
-  if (exact) {
-    // uy = rho_y - A ua by an explicit CSR pass (solver.py:240-241)
-    k_spmv_seg<<<h->grid_seg, kBlock, 0, st>>>(P, h->W.ua, h->d_qseg2);
-    CKL();
-    k_rowsum_seg<<<h->grid_m, kBlock, 0, st>>>(P, h->d_qseg2, h->d_tmp3);
+  return 0;
+}
+
+// The inner solve of _solve_inner_parts (solver.py:203-245) on explicit
+// vectors, all shards: rho (T-1 per shard, x|s|y|v) -> u12.  uy by the
+// identity A ua = S^{-1} A t, or (exact_uy, single shard) the explicit CSR
+// pass uy = wy - A ua of solver.py:240-241.
+int inner_dist(hsde_handle *h, const std::vector<const double *> &rho,
+               const std::vector<double *> &u12, bool exact_uy) {
+  cudaStream_t st = h->st;
+  const int G = (int)h->sh.size();
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    const DevProblem &P = s.P;
+    const double *rx = rho[g], *rs = rho[g] + P.n_c, *ry = rho[g] + P.n_c + P.n_d,
+                 *rv = rho[g] + P.n_c + P.n_d + P.m;
+    if (h->n_sep) {
+      k_zero<<<grid_for(h->n_sep), kBlock, 0, st>>>(s.W.sepbuf, h->n_sep);
+      CKL();
+    }
+    k_rhs<false><<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(P, s.S, s.W, rx, rs, ry, rv, s.grid_nc);
     CKL();
   }
+  RC(reduce(h, BUF_SEP, h->n_sep));
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    const DevProblem &P = s.P;
+    const double *rx = rho[g], *ry = rho[g] + P.n_c + P.n_d;
+    if (P.n_sep_local) {
+      k_sep_finish<false><<<grid_for(P.n_sep_local), kBlock, 0, st>>>(P, s.S, s.W, rx, ry);
+      CKL();
+    }
+    k_spmv_seg<<<s.grid_seg, kBlock, 0, st>>>(P, s.W.t, s.W.qseg);
+    CKL();
+    if (h->multi()) {
+      k_rowsum_seg<<<s.grid_m, kBlock, 0, st>>>(P, s.W.qseg, s.W.qbuf);
+      CKL();
+    }
+  }
+  RC(reduce(h, BUF_Q, h->sh[0].P.m));
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    const DevProblem &P = s.P;
+    const double *rs = rho[g] + P.n_c, *ry = rho[g] + P.n_c + P.n_d, *rv = ry + P.m;
+    k_schur<<<s.grid_schur, kBlock, s.schur_smem, st>>>(P, s.W.qseg, h->multi() ? s.W.qbuf : nullptr,
+                                                        s.W.qp);
+    CKL();
+    k_ua<false><<<s.grid_nc, kBlock, 0, st>>>(P, s.W, s.W.qp);
+    CKL();
+    double *ua = u12[g], *ub = u12[g] + P.n_c, *uy = u12[g] + P.n_c + P.n_d, *uv = uy + P.m;
+    CK(cudaMemcpyAsync(ua, s.W.ua, sizeof(double) * P.n_c, cudaMemcpyDeviceToDevice, st));
+    k_slot_out<<<s.grid_nd, kBlock, 0, st>>>(P, rs, rv, ua, ub, uv);
+    CKL();
+    if (exact_uy) {
+      k_spmv_seg<<<s.grid_seg, kBlock, 0, st>>>(P, ua, s.d_qseg2);
+      CKL();
+      k_uy_from_seg<<<s.grid_m, kBlock, 0, st>>>(P, s.d_qseg2, nullptr, ry, uy);
+      CKL();
+    } else {
+      k_uy_from_seg<<<s.grid_m, kBlock, 0, st>>>(P, nullptr, s.W.qp, ry, uy);  // uy = rho_y - q'
+      CKL();
+    }
+  }
+  return 0;
+}
+
+// one hot iteration (solver.py:375-395) over all shards, eager launches;
+// profiling events optional (phases summed over shards)
+int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = nullptr) {
+  cudaStream_t st = h->st;
+  const int G = (int)h->sh.size();
+  const bool exact = (h->set.flags & HSDE_FLAG_EXACT_UY) != 0 && !h->multi();
+  int nl = 0;
+  auto mark = [&](int s) {
+    if (ev) cudaEventRecord(ev[s], st);
+  };
+  mark(PS_COUNT);
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    if (h->n_sep) {
+      k_zero<<<grid_for(h->n_sep), kBlock, 0, st>>>(s.W.sepbuf, h->n_sep);
+      CKL();
+      ++nl;
+    }
+    k_rhs<true><<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(s.P, s.S, s.W, nullptr, nullptr, nullptr,
+                                                            nullptr, s.grid_nc);
+    CKL();
+    ++nl;
+  }
+  mark(PS_RHS);
+  RC(reduce(h, BUF_SEP, h->n_sep));
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    if (s.P.n_sep_local) {
+      k_sep_finish<true><<<grid_for(s.P.n_sep_local), kBlock, 0, st>>>(s.P, s.S, s.W, nullptr, nullptr);
+      CKL();
+      ++nl;
+    }
+    k_spmv_seg<<<s.grid_seg, kBlock, 0, st>>>(s.P, s.W.t, s.W.qseg);
+    CKL();
+    ++nl;
+    if (h->multi()) {
+      k_rowsum_seg<<<s.grid_m, kBlock, 0, st>>>(s.P, s.W.qseg, s.W.qbuf);
+      CKL();
+      ++nl;
+    }
+  }
+  mark(PS_SPMV);
+  RC(reduce(h, BUF_Q, h->sh[0].P.m));
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    k_schur<<<s.grid_schur, kBlock, s.schur_smem, st>>>(s.P, s.W.qseg, h->multi() ? s.W.qbuf : nullptr,
+                                                        s.W.qp);
+    CKL();
+    ++nl;
+  }
+  mark(PS_SCHUR);
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    k_ua<true><<<s.grid_nc, kBlock, 0, st>>>(s.P, s.W, s.W.qp);
+    CKL();
+    ++nl;
+    if (h->multi()) {
+      k_sum_parts<<<1, 1024, 0, st>>>(s.W.part, s.grid_nc, s.W.red);
+      CKL();
+      ++nl;
+    }
+    if (exact) {
+      // uy = rho_y - A ua by an explicit CSR pass (solver.py:240-241)
+      k_spmv_seg<<<s.grid_seg, kBlock, 0, st>>>(s.P, s.W.ua, s.d_qseg2);
+      CKL();
+      k_rowsum_seg<<<s.grid_m, kBlock, 0, st>>>(s.P, s.d_qseg2, s.d_tmp3);
+      CKL();
+      nl += 2;
+    }
+  }
   mark(PS_UA);
-  k_scalars<<<1, 1024, 0, st>>>(P, h->S, h->W, h->grid_nc, exact ? 1 : 0, h->d_tmp3);
-  CKL();
+  RC(reduce(h, BUF_RED, 1));
+  mark(PS_COMM);
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    k_scalars<<<1, 1024, 0, st>>>(s.P, s.S, s.W, s.grid_nc, exact ? 1 : 0, s.d_tmp3,
+                                  h->multi() ? s.W.red : nullptr);
+    CKL();
+    ++nl;
+  }
   mark(PS_SCALARS);
-  if (launch_cone(h, CONE_HOT, h->warp_plan, false, nullptr, nullptr, 1.0, st)) return HSDE_ERR_CUDA;
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    RC(launch_cone(h, s, CONE_HOT, s.warp_plan, false, nullptr, nullptr, 1.0, st));
+    nl += s.warp_plan.count > 0;
+  }
   mark(PS_CONE_WARP);
-  if (launch_cone(h, CONE_HOT, h->block_plan, true, nullptr, nullptr, 1.0, st)) return HSDE_ERR_CUDA;
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    RC(launch_cone(h, s, CONE_HOT, s.block_plan, true, nullptr, nullptr, 1.0, st));
+    nl += s.block_plan.count > 0;
+  }
   mark(PS_CONE_BLOCK);
-  k_xupd<<<h->grid_nc, kBlock, 0, st>>>(P, h->S, h->W);
-  CKL();
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    k_xupd<<<s.grid_nc, kBlock, 0, st>>>(s.P, s.S, s.W);
+    CKL();
+    ++nl;
+  }
   mark(PS_XUPD);
-  if (launches) *launches += 6 + (h->warp_plan.count > 0) + (h->block_plan.count > 0) + (exact ? 2 : 0);
+  if (launches) *launches += nl;
   return 0;
 }
 
@@ -277,7 +472,7 @@ int build_graph(hsde_handle *h, int iters, cudaGraphExec_t *out) {
   cudaGraph_t g;
   CK(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
   int rc = 0;
-  for (int i = 0; i < iters && !rc; ++i) rc = launch_iteration(h, h->st);
+  for (int i = 0; i < iters && !rc; ++i) rc = launch_iteration(h);
   cudaError_t e = cudaStreamEndCapture(h->st, &g);
   if (rc) return rc;
   if (e != cudaSuccess) {
@@ -293,19 +488,34 @@ int build_graph(hsde_handle *h, int iters, cudaGraphExec_t *out) {
   return 0;
 }
 
+int rebuild_graphs(hsde_handle *h) {
+  if (h->g1) cudaGraphExecDestroy(h->g1);
+  if (h->gci) cudaGraphExecDestroy(h->gci);
+  h->g1 = h->gci = nullptr;
+  RC(build_graph(h, 1, &h->g1));
+  if (h->gci_len > 1) RC(build_graph(h, h->gci_len, &h->gci));
+  return 0;
+}
+
 int check_err_flag(hsde_handle *h) {
-  int flag = 0;
-  CK(cudaMemcpyAsync(&flag, h->W.err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-  CK(cudaStreamSynchronize(h->st));
-  if (flag) {
-    CK(cudaMemsetAsync(h->W.err, 0, sizeof(int), h->st));
+  int any = 0;
+  for (auto &s : h->sh) {
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, s.W.err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (flag) {
+      CK(cudaMemsetAsync(s.W.err, 0, sizeof(int), h->st));
+      any = 1;
+    }
+  }
+  if (any) {
     h->err = "batched eigendecomposition produced non-finite eigenvalues";
     return HSDE_ERR_EIGEN;
   }
   return 0;
 }
 
-int setup_cone_plans(hsde_handle *h, const int32_t *sizes, int p) {
+int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
   std::vector<int> wids, bids;
   int dpw = 2, dpb = 2;
   for (int k = 0; k < p; ++k) {
@@ -322,45 +532,43 @@ int setup_cone_plans(hsde_handle *h, const int32_t *sizes, int p) {
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev);
   if (maxsm <= 0) maxsm = 227 * 1024;
-  // warp plan
-  h->warp_plan.count = (int)wids.size();
-  h->warp_plan.dpmax = dpw;
+  s.warp_plan.count = (int)wids.size();
+  s.warp_plan.dpmax = dpw;
   const size_t per_warp = (size_t)jacobi_scratch_doubles(dpw) * sizeof(double);
   int pb = 8;
   while (pb > 1 && per_warp * pb > (size_t)maxsm) pb >>= 1;
-  h->warp_plan.per_block = pb;
-  h->warp_plan.smem = per_warp * pb;
+  s.warp_plan.per_block = pb;
+  s.warp_plan.smem = per_warp * pb;
   if (!wids.empty()) {
-    if (dupload(h, &h->warp_plan.ids, wids.data(), wids.size())) return HSDE_ERR_CUDA;
-    CK(cudaFuncSetAttribute(k_cone_warp<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->warp_plan.smem));
-    CK(cudaFuncSetAttribute(k_cone_warp<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->warp_plan.smem));
-    CK(cudaFuncSetAttribute(k_cone_warp<CONE_MINEIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->warp_plan.smem));
+    RC(dupload(h, &s.warp_plan.ids, wids.data(), wids.size()));
+    const int sm = (int)s.warp_plan.smem;
+    CK(cudaFuncSetAttribute(k_cone_warp<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute(k_cone_warp<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute(k_cone_warp<CONE_MINEIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   }
-  h->block_plan.count = (int)bids.size();
-  h->block_plan.dpmax = dpb;
+  s.block_plan.count = (int)bids.size();
+  s.block_plan.dpmax = dpb;
   const size_t per_blk = (size_t)jacobi_scratch_doubles(dpb) * sizeof(double);
   if (!bids.empty()) {
     if (per_blk > (size_t)maxsm) {
       h->err = "clique of order " + std::to_string(dpb) + " exceeds the shared-memory Jacobi path";
       return HSDE_ERR_ARG;
     }
-    h->block_plan.smem = per_blk;
-    if (dupload(h, &h->block_plan.ids, bids.data(), bids.size())) return HSDE_ERR_CUDA;
-    CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per_blk));
-    CK(cudaFuncSetAttribute(k_cone_block<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per_blk));
-    CK(cudaFuncSetAttribute(k_cone_block<CONE_MINEIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per_blk));
+    s.block_plan.smem = per_blk;
+    RC(dupload(h, &s.block_plan.ids, bids.data(), bids.size()));
+    const int sm = (int)per_blk;
+    CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute(k_cone_block<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute(k_cone_block<CONE_MINEIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   }
   return 0;
 }
 
-// Dense Schur S = I + A P^{-1} A' (solver.py:250-255) -> S^{-1}
-int setup_schur_dense(hsde_handle *h) {
-  const int m = h->P.m;
-  const int n_c = h->P.n_c;
-  double *S = nullptr, *X = nullptr;
-  if (dalloc(h, &S, (size_t)m * m)) return HSDE_ERR_CUDA;
-  CK(cudaMemsetAsync(S, 0, sizeof(double) * m * m, h->st));
-  // chunked dense GEMM
+// Partial S = sum over owned columns of A diag(p_inv) A' (dense chunks + DGEMM)
+int schur_partial_dense(hsde_handle *h, ShardDev &s) {
+  const int m = s.P.m, n_c = s.P.n_c;
+  RC(dalloc(h, &s.d_schur, (size_t)m * m));
+  CK(cudaMemsetAsync(s.d_schur, 0, sizeof(double) * m * m, h->st));
   const size_t budget = 256ull << 20;  // bytes per densified chunk
   int wc = (int)std::max<size_t>(1, budget / (sizeof(double) * (size_t)m));
   wc = std::min(wc, std::max(n_c, 1));
@@ -374,39 +582,44 @@ int setup_schur_dense(hsde_handle *h) {
   }
   cublasSetStream(cb, h->st);
   const double one = 1.0;
-  for (int c0 = 0; c0 < n_c; c0 += wc) {
+  int rc = 0;
+  for (int c0 = 0; c0 < n_c && !rc; c0 += wc) {
     const int c1 = std::min(n_c, c0 + wc);
     const int w = c1 - c0;
     CK(cudaMemsetAsync(Dm, 0, sizeof(double) * (size_t)m * w, h->st));
     CK(cudaMemsetAsync(Ds, 0, sizeof(double) * (size_t)m * w, h->st));
-    k_densify<<<grid_for(w), kBlock, 0, h->st>>>(h->P, c0, c1, Dm, Ds);
+    k_densify<<<grid_for(w), kBlock, 0, h->st>>>(s.P, c0, c1, Dm, Ds);
     CKL();
-    // S += Ds * Dm'
-    if (cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, m, m, w, &one, Ds, m, Dm, m, &one, S, m) !=
+    if (cublasDgemm(cb, CUBLAS_OP_N, CUBLAS_OP_T, m, m, w, &one, Ds, m, Dm, m, &one, s.d_schur, m) !=
         CUBLAS_STATUS_SUCCESS) {
       h->err = "cublasDgemm failed";
-      cublasDestroy(cb);
-      return HSDE_ERR_CUDA;
+      rc = HSDE_ERR_CUDA;
     }
   }
-  cublasDestroy(cb);
-  k_add_identity<<<grid_for(m), kBlock, 0, h->st>>>(S, m);
-  CKL();
   CK(cudaStreamSynchronize(h->st));
+  cublasDestroy(cb);
   cudaFree(Dm);
   cudaFree(Ds);
-  // finite check (cho_factor on non-finite data fails: solver.py:254-259)
-  k_finite_check<<<grid_for((int64_t)m * m), kBlock, 0, h->st>>>(S, (int64_t)m * m, h->W.err);
+  return rc;
+}
+
+// reduced S (in the shard's d_schur) -> S^{-1} (cuSOLVER Cholesky, potrs on I)
+int schur_factor(hsde_handle *h, ShardDev &s) {
+  const int m = s.P.m;
+  double *S = s.d_schur;
+  k_add_identity<<<grid_for(m), kBlock, 0, h->st>>>(S, m);
+  CKL();
+  k_finite_check<<<grid_for((int64_t)m * m), kBlock, 0, h->st>>>(S, (int64_t)m * m, s.W.err);
   CKL();
   int flag = 0;
-  CK(cudaMemcpy(&flag, h->W.err, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(&flag, s.W.err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
   if (flag) {
-    CK(cudaMemset(h->W.err, 0, sizeof(int)));
+    CK(cudaMemset(s.W.err, 0, sizeof(int)));
     h->err = "Cholesky of the " + std::to_string(m) + " x " + std::to_string(m) +
              " reduced system failed: non-finite entries";
     return HSDE_ERR_FACTOR;
   }
-  // Cholesky (lower) and explicit inverse via potrs on the identity
   cusolverDnHandle_t cs;
   if (cusolverDnCreate(&cs) != CUSOLVER_STATUS_SUCCESS) {
     h->err = "cusolverDnCreate failed";
@@ -431,7 +644,8 @@ int setup_schur_dense(hsde_handle *h) {
              " reduced system failed: leading minor " + std::to_string(info) + " not positive";
     return HSDE_ERR_FACTOR;
   }
-  if (dalloc(h, &X, (size_t)m * m)) return HSDE_ERR_CUDA;
+  double *X = nullptr;
+  RC(dalloc(h, &X, (size_t)m * m));
   k_identity<<<grid_for((int64_t)m * m), kBlock, 0, h->st>>>(X, m);
   CKL();
   cusolverDnDpotrs(cs, CUBLAS_FILL_MODE_LOWER, m, m, S, m, X, m, dinfo);
@@ -439,26 +653,79 @@ int setup_schur_dense(hsde_handle *h) {
   cudaFree(work);
   cudaFree(dinfo);
   cusolverDnDestroy(cs);
-  // S^{-1} symmetrised, row-major == col-major
-  k_symmetrize<<<grid_for((int64_t)m * m), kBlock, 0, h->st>>>(X, m, S);
+  k_symmetrize<<<grid_for((int64_t)m * m), kBlock, 0, h->st>>>(X, m, S);  // S^{-1}, symmetric
   CKL();
-  h->P.sinv = S;
-  h->P.schur_diag = 0;
+  s.P.sinv = S;
+  s.P.schur_diag = 0;
+  return 0;
+}
+
+int setup_schur(hsde_handle *h) {
+  const int G = (int)h->sh.size();
+  const int m = h->sh[0].P.m;
+  for (auto &s : h->sh) {
+    if (h->schur_diag) {
+      RC(dalloc(h, &s.d_schur, std::max(m, 1)));
+      k_diag_schur<<<grid_for(m), kBlock, 0, h->st>>>(s.P, s.d_schur);
+      CKL();
+    } else {
+      RC(schur_partial_dense(h, s));
+    }
+  }
+  if (h->mode == MODE_EMULATED) {
+    std::vector<double *> p(G);
+    for (int g = 0; g < G; ++g) p[g] = h->sh[g].d_schur;
+    RC(dupload(h, &h->d_ptrs[BUF_SCHUR], p.data(), G));
+  }
+  RC(reduce(h, BUF_SCHUR, h->schur_diag ? (int64_t)m : (int64_t)m * m));
+  for (auto &s : h->sh) {
+    if (!h->schur_diag) {
+      RC(schur_factor(h, s));
+      continue;
+    }
+    k_diag_finish<<<grid_for(m), kBlock, 0, h->st>>>(s.d_schur, m, s.W.err);
+    CKL();
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, s.W.err, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    if (flag) {
+      CK(cudaMemset(s.W.err, 0, sizeof(int)));
+      h->err = "Cholesky of the " + std::to_string(m) + " x " + std::to_string(m) +
+               " reduced system failed: diagonal entry not positive";
+      return HSDE_ERR_FACTOR;
+    }
+    s.P.sinv = s.d_schur;
+    s.P.schur_diag = 1;
+  }
   return 0;
 }
 
 int compute_minv_zeta(hsde_handle *h) {
-  const DevProblem &P = h->P;
-  double *mz = nullptr;
-  if (dalloc(h, &mz, (size_t)(P.total - 1))) return HSDE_ERR_CUDA;
-  int rc = inner_explicit(h, h->d_zeta, mz, h->st);
-  if (rc) return rc;
-  h->P.mz = mz;
-  rc = dev_dot(h, h->d_zeta, mz, P.total - 1, h->d_chk, h->st);
-  if (rc) return rc;
-  double zmz = 0;
-  CK(cudaMemcpyAsync(&zmz, h->d_chk, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  const int G = (int)h->sh.size();
+  std::vector<const double *> rho(G);
+  std::vector<double *> out(G);
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    double *mz = nullptr;
+    RC(dalloc(h, &mz, (size_t)(s.P.total - 1)));
+    rho[g] = s.d_zeta;
+    out[g] = mz;
+  }
+  // single GPU keeps the reference's explicit uy = wy - A ua (solver.py:240-241)
+  RC(inner_dist(h, rho, out, !h->multi()));
+  // zeta . M zeta = c . mz_x (owned) - b . mz_y (replicated: lead shard)
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    s.P.mz = out[g];
+    RC(dev_dot_owned(h, s, s.P.c, out[g], s.W.red + 0));
+    RC(dev_dot(h, s, s.P.b, out[g] + s.P.n_c + s.P.n_d, s.P.m, s.W.red + 1));
+    if (!s.P.lead) CK(cudaMemsetAsync(s.W.red + 1, 0, sizeof(double), h->st));
+  }
+  RC(reduce(h, BUF_RED, 2));
+  double r[2];
+  CK(cudaMemcpyAsync(r, h->sh[0].W.red, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
+  const double zmz = r[0] - r[1];
   const double zs = 1.0 + zmz;  // solver.py:269
   if (!(zs > 0)) {
     char buf[128];
@@ -466,105 +733,92 @@ int compute_minv_zeta(hsde_handle *h) {
     h->err = buf;
     return HSDE_ERR_FACTOR;
   }
-  h->P.zmz = zmz;
-  h->P.zeta_scale = zs;
+  for (auto &s : h->sh) {
+    s.P.zmz = zmz;
+    s.P.zeta_scale = zs;
+  }
   h->info.zeta_scale = zs;
   return 0;
 }
 
 int init_state(hsde_handle *h) {
-  const int64_t T = h->P.total;
-  CK(cudaMemsetAsync(h->S.u, 0, sizeof(double) * T, h->st));
-  CK(cudaMemsetAsync(h->S.w, 0, sizeof(double) * T, h->st));
-  const double one = 1.0;
-  CK(cudaMemcpyAsync(h->S.u + T - 1, &one, sizeof(double), cudaMemcpyHostToDevice, h->st));
-  CK(cudaMemcpyAsync(h->S.w + T - 1, &one, sizeof(double), cudaMemcpyHostToDevice, h->st));
-  CK(cudaMemcpyAsync(h->d_prev_u, h->S.u, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
-  CK(cudaMemcpyAsync(h->d_prev_w, h->S.w, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
-  CK(cudaMemsetAsync(h->W.vvalid, 0, sizeof(int) * std::max(h->P.p, 1), h->st));
-  CK(cudaStreamSynchronize(h->st));
+  for (auto &s : h->sh) {
+    const int64_t T = s.P.total;
+    CK(cudaMemsetAsync(s.S.u, 0, sizeof(double) * T, h->st));
+    CK(cudaMemsetAsync(s.S.w, 0, sizeof(double) * T, h->st));
+    const double one = 1.0;
+    CK(cudaMemcpyAsync(s.S.u + T - 1, &one, sizeof(double), cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(s.S.w + T - 1, &one, sizeof(double), cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemcpyAsync(s.d_prev_u, s.S.u, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(s.d_prev_w, s.S.w, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemsetAsync(s.W.vvalid, 0, sizeof(int) * std::max(s.P.p, 1), h->st));
+    CK(cudaStreamSynchronize(h->st));
+  }
   return 0;
 }
 
-}  // namespace
+// ---- per-shard construction -------------------------------------------------------
 
-extern "C" {
-
-const char *hsde_last_error(const hsde_t *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
-
-int hsde_create(const hsde_problem_desc *d, const hsde_settings *s, hsde_t **out) {
-  g_create_error.clear();
-  if (!d || !s || !out) {
-    g_create_error = "null argument";
-    return HSDE_ERR_ARG;
-  }
-  *out = nullptr;
-  if (d->m < 0 || d->n_c < 0 || d->p < 0 || d->n_d < 0 || d->nnz < 0) {
-    g_create_error = "negative dimension";
-    return HSDE_ERR_ARG;
-  }
-  if (!(s->alpha >= 1.0 && s->alpha < 2.0)) {
-    g_create_error = "alpha must lie in [1, 2)";
-    return HSDE_ERR_ARG;
-  }
-  hsde_handle *h = new hsde_handle();
-  h->set = *s;
-  h->dev = s->device;
-  h->factor = !(s->flags & HSDE_FLAG_NO_FACTOR);
-  h->warm = !(s->flags & HSDE_FLAG_COLD_EIG);
-  auto fail = [&](int rc) {
-    g_create_error = h->err;
-    hsde_destroy(h);
-    return rc;
-  };
-  cudaError_t e = cudaSetDevice(h->dev);
-  if (e != cudaSuccess) {
-    h->err = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
-    return fail(HSDE_ERR_CUDA);
-  }
-  if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) {
-    h->err = "stream create failed";
-    return fail(HSDE_ERR_CUDA);
-  }
+int validate(hsde_handle *h, const hsde_problem_desc *d) {
   const int m = d->m, n_c = d->n_c, p = d->p;
   const int64_t n_d = d->n_d, nnz = d->nnz;
-  // ---- validate
+  if (m < 0 || n_c < 0 || p < 0 || n_d < 0 || nnz < 0) {
+    h->err = "negative dimension";
+    return HSDE_ERR_ARG;
+  }
   if (d->a_row_ptr[0] != 0 || d->a_row_ptr[m] != nnz) {
     h->err = "a_row_ptr inconsistent with nnz";
-    return fail(HSDE_ERR_ARG);
+    return HSDE_ERR_ARG;
   }
   for (int i = 0; i < m; ++i) {
     if (d->a_row_ptr[i + 1] < d->a_row_ptr[i]) {
       h->err = "a_row_ptr not monotone";
-      return fail(HSDE_ERR_ARG);
+      return HSDE_ERR_ARG;
     }
     for (int64_t k = d->a_row_ptr[i]; k < d->a_row_ptr[i + 1]; ++k) {
       const int c = d->a_col[k];
       if (c < 0 || c >= n_c || (k > d->a_row_ptr[i] && c <= d->a_col[k - 1])) {
         h->err = "a_col out of range or not strictly ascending in row " + std::to_string(i);
-        return fail(HSDE_ERR_ARG);
+        return HSDE_ERR_ARG;
       }
     }
   }
   if (d->clique_offsets[0] != 0 || d->clique_offsets[p] != n_d) {
     h->err = "clique offsets inconsistent with n_d";
-    return fail(HSDE_ERR_ARG);
+    return HSDE_ERR_ARG;
   }
-  int maxd = 0;
   for (int k = 0; k < p; ++k) {
     const int64_t dk = d->clique_sizes[k];
     if (dk < 1 || d->clique_offsets[k + 1] - d->clique_offsets[k] != dk * dk) {
       h->err = "clique size / offset mismatch at clique " + std::to_string(k);
-      return fail(HSDE_ERR_ARG);
+      return HSDE_ERR_ARG;
     }
-    maxd = std::max<int>(maxd, (int)dk);
   }
   for (int64_t j = 0; j < n_d; ++j)
     if (d->slot_cov[j] < 0 || d->slot_cov[j] >= n_c) {
       h->err = "slot_cov out of range";
-      return fail(HSDE_ERR_ARG);
+      return HSDE_ERR_ARG;
     }
-  // ---- derived host structures
+  if (d->n_sep_local > 0 && (!d->sep_local || !d->sep_pos)) {
+    h->err = "separator lists missing";
+    return HSDE_ERR_ARG;
+  }
+  for (int i = 0; i < d->n_sep_local; ++i)
+    if (d->sep_local[i] < 0 || d->sep_local[i] >= n_c || d->sep_pos[i] < 0 ||
+        d->sep_pos[i] >= d->n_sep) {
+      h->err = "separator index out of range";
+      return HSDE_ERR_ARG;
+    }
+  return 0;
+}
+
+// upload shard data (everything that does not depend on normalisation)
+int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
+  const int m = d->m, n_c = d->n_c, p = d->p;
+  const int64_t n_d = d->n_d, nnz = d->nnz;
+  std::vector<unsigned char> owned(n_c, 1);
+  if (d->owned)
+    for (int c = 0; c < n_c; ++c) owned[c] = d->owned[c] ? 1 : 0;
   // CSC (transpose) by counting sort; rows ascending within a column
   std::vector<int64_t> at_cp(n_c + 1, 0);
   for (int64_t k = 0; k < nnz; ++k) at_cp[d->a_col[k] + 1]++;
@@ -580,14 +834,28 @@ int hsde_create(const hsde_problem_desc *d, const hsde_settings *s, hsde_t **out
         at_val[q] = d->a_val[k];
       }
   }
-  int64_t maxcol = 0;
-  for (int c = 0; c < n_c; ++c) maxcol = std::max(maxcol, at_cp[c + 1] - at_cp[c]);
+  for (int c = 0; c < n_c; ++c)
+    if (owned[c]) s.maxcol = std::max(s.maxcol, at_cp[c + 1] - at_cp[c]);
+  // CSR over owned columns (the only columns this shard adds into A t)
+  std::vector<int64_t> rp(m + 1, 0);
+  std::vector<int> col;
+  std::vector<double> val;
+  col.reserve(nnz);
+  val.reserve(nnz);
+  for (int i = 0; i < m; ++i) {
+    for (int64_t k = d->a_row_ptr[i]; k < d->a_row_ptr[i + 1]; ++k)
+      if (owned[d->a_col[k]]) {
+        col.push_back(d->a_col[k]);
+        val.push_back(d->a_val[k]);
+      }
+    rp[i + 1] = (int64_t)col.size();
+  }
   // row segments
   std::vector<int> seg_row, row_seg(m + 1, 0);
   std::vector<int64_t> seg_beg;
   for (int i = 0; i < m; ++i) {
     row_seg[i] = (int)seg_row.size();
-    for (int64_t k = d->a_row_ptr[i]; k < d->a_row_ptr[i + 1]; k += kSegNnz) {
+    for (int64_t k = rp[i]; k < rp[i + 1]; k += kSegNnz) {
       seg_row.push_back(i);
       seg_beg.push_back(k);
     }
@@ -605,62 +873,68 @@ int hsde_create(const hsde_problem_desc *d, const hsde_settings *s, hsde_t **out
   for (int c = 0; c < n_c; ++c)
     if (cov_ptr[c + 1] - cov_ptr[c] > kHeavy) heavy.push_back(c);
   std::vector<double> p_inv(n_c);
-  for (int c = 0; c < n_c; ++c)
-    p_inv[c] = 1.0 / (1.0 + 0.5 * (double)(cov_ptr[c + 1] - cov_ptr[c]));  // solver.py:250
-  // normalisation (solver.py:659-665)
-  double nc2 = 0, nb2 = 0;
-  for (int c = 0; c < n_c; ++c) nc2 += d->c[c] * d->c[c];
-  for (int i = 0; i < m; ++i) nb2 += d->b[i] * d->b[i];
-  double sc = 1.0, sb = 1.0;
-  if (s->normalize) {
-    const double ncn = std::sqrt(nc2), nbn = std::sqrt(nb2);
-    sc = ncn > 0 ? 1.0 / ncn : 1.0;
-    sb = nbn > 0 ? 1.0 / nbn : 1.0;
+  for (int c = 0; c < n_c; ++c) {
+    const double D = d->cover_counts ? d->cover_counts[c] : (double)(cov_ptr[c + 1] - cov_ptr[c]);
+    p_inv[c] = 1.0 / (1.0 + 0.5 * D);  // solver.py:250 (global cover counts)
   }
-  std::vector<double> cint(n_c), bint(m);
-  for (int c = 0; c < n_c; ++c) cint[c] = sc == 1.0 ? d->c[c] : sc * d->c[c];
-  for (int i = 0; i < m; ++i) bint[i] = sb == 1.0 ? d->b[i] : sb * d->b[i];
-  double nci = 0, nbi = 0;
-  for (int c = 0; c < n_c; ++c) nci += cint[c] * cint[c];
-  for (int i = 0; i < m; ++i) nbi += bint[i] * bint[i];
-  h->norm_c = std::sqrt(nci);
-  h->norm_b = std::sqrt(nbi);
-  // diagonal Schur detection: no two rows share a column
-  const bool sdiag = maxcol <= 1;
+  std::vector<int> sep_of;
+  if (d->n_sep > 0) {
+    sep_of.assign(n_c, -1);
+    for (int i = 0; i < d->n_sep_local; ++i) sep_of[d->sep_local[i]] = d->sep_pos[i];
+  }
+  s.nc2_owned = 0;
+  for (int c = 0; c < n_c; ++c)
+    if (owned[c]) s.nc2_owned += d->c[c] * d->c[c];
+  s.sizes.assign(d->clique_sizes, d->clique_sizes + p);
   // ---- device problem
-  DevProblem &P = h->P;
+  DevProblem &P = s.P;
   P.m = m;
   P.n_c = n_c;
   P.p = p;
   P.n_d = n_d;
   P.nnz = nnz;
   P.total = (int64_t)n_c + 2 * n_d + m + 1;
-  P.alpha = s->alpha;
+  P.alpha = h->set.alpha;
   P.nseg = (int)seg_row.size();
-  int rc = 0;
+  P.n_sep = d->n_sep;
+  P.n_sep_local = d->n_sep_local;
+  P.lead = d->follower ? 0 : 1;
   int64_t *a_rp = nullptr, *at_cp_d = nullptr, *seg_beg_d = nullptr, *cl_off = nullptr;
   int *a_col = nullptr, *at_row_d = nullptr, *seg_row_d = nullptr, *row_seg_d = nullptr;
   int *cov_ptr_d = nullptr, *cov_slot_d = nullptr, *slot_cov_d = nullptr, *cl_size = nullptr;
-  double *a_val = nullptr, *at_val_d = nullptr, *c_d = nullptr, *b_d = nullptr, *pinv_d = nullptr;
-  if ((rc = dupload(h, &a_rp, d->a_row_ptr, m + 1)) || (rc = dupload(h, &a_col, d->a_col, nnz)) ||
-      (rc = dupload(h, &a_val, d->a_val, nnz)) || (rc = dupload(h, &at_cp_d, at_cp.data(), n_c + 1)) ||
-      (rc = dupload(h, &at_row_d, at_row.data(), nnz)) || (rc = dupload(h, &at_val_d, at_val.data(), nnz)) ||
-      (rc = dupload(h, &seg_row_d, seg_row.data(), seg_row.size())) ||
-      (rc = dupload(h, &seg_beg_d, seg_beg.data(), seg_beg.size())) ||
-      (rc = dupload(h, &row_seg_d, row_seg.data(), m + 1)) ||
-      (rc = dupload(h, &cov_ptr_d, cov_ptr.data(), n_c + 1)) ||
-      (rc = dupload(h, &cov_slot_d, cov_slot.data(), n_d)) ||
-      (rc = dupload(h, &slot_cov_d, d->slot_cov, n_d)) ||
-      (rc = dupload(h, &cl_off, d->clique_offsets, p + 1)) ||
-      (rc = dupload(h, &cl_size, d->clique_sizes, p)) || (rc = dupload(h, &c_d, cint.data(), n_c)) ||
-      (rc = dupload(h, &b_d, bint.data(), m)) || (rc = dupload(h, &pinv_d, p_inv.data(), n_c)) ||
-      (rc = dupload(h, &h->d_c_orig, d->c, n_c)) || (rc = dupload(h, &h->d_b_orig, d->b, m)))
-    return fail(rc);
-  int *heavy_d = nullptr;
-  if ((rc = dupload(h, &heavy_d, heavy.data(), heavy.size()))) return fail(rc);
-  P.heavy = heavy_d;
-  P.n_heavy = (int)heavy.size();
-  h->grid_heavy = (P.n_heavy + (kBlock / 32) - 1) / (kBlock / 32);
+  int *heavy_d = nullptr, *sep_of_d = nullptr, *sep_local_d = nullptr, *sep_pos_d = nullptr;
+  unsigned char *owned_d = nullptr;
+  double *a_val = nullptr, *at_val_d = nullptr, *pinv_d = nullptr;
+  RC(dupload(h, &a_rp, rp.data(), m + 1));
+  RC(dupload(h, &a_col, col.data(), col.size()));
+  RC(dupload(h, &a_val, val.data(), val.size()));
+  RC(dupload(h, &at_cp_d, at_cp.data(), n_c + 1));
+  RC(dupload(h, &at_row_d, at_row.data(), nnz));
+  RC(dupload(h, &at_val_d, at_val.data(), nnz));
+  RC(dupload(h, &seg_row_d, seg_row.data(), seg_row.size()));
+  RC(dupload(h, &seg_beg_d, seg_beg.data(), seg_beg.size()));
+  RC(dupload(h, &row_seg_d, row_seg.data(), m + 1));
+  RC(dupload(h, &cov_ptr_d, cov_ptr.data(), n_c + 1));
+  RC(dupload(h, &cov_slot_d, cov_slot.data(), n_d));
+  RC(dupload(h, &slot_cov_d, d->slot_cov, n_d));
+  RC(dupload(h, &cl_off, d->clique_offsets, p + 1));
+  RC(dupload(h, &cl_size, d->clique_sizes, p));
+  RC(dupload(h, &pinv_d, p_inv.data(), n_c));
+  RC(dupload(h, &s.d_c_orig, d->c, n_c));
+  RC(dupload(h, &s.d_b_orig, d->b, m));
+  RC(dupload(h, &heavy_d, heavy.data(), heavy.size()));
+  if (d->owned) {
+    RC(dupload(h, &owned_d, owned.data(), n_c));
+    P.owned = owned_d;
+  }
+  if (d->n_sep > 0) {
+    RC(dupload(h, &sep_of_d, sep_of.data(), n_c));
+    RC(dupload(h, &sep_local_d, d->sep_local, d->n_sep_local));
+    RC(dupload(h, &sep_pos_d, d->sep_pos, d->n_sep_local));
+    P.sep_of = sep_of_d;
+    P.sep_local = sep_local_d;
+    P.sep_pos = sep_pos_d;
+  }
   P.a_rp = a_rp;
   P.a_col = a_col;
   P.a_val = a_val;
@@ -675,106 +949,268 @@ int hsde_create(const hsde_problem_desc *d, const hsde_settings *s, hsde_t **out
   P.slot_cov = slot_cov_d;
   P.cl_off = cl_off;
   P.cl_size = cl_size;
-  P.c = c_d;
-  P.b = b_d;
   P.p_inv = pinv_d;
-  const double consts[4] = {sb, sc, 1.0, 0.0};
-  if ((rc = dupload(h, &h->d_consts, consts, 4))) return fail(rc);
-  // zeta (solver.py:264)
-  {
-    std::vector<double> z(P.total - 1, 0.0);
-    for (int c = 0; c < n_c; ++c) z[c] = cint[c];
-    for (int i = 0; i < m; ++i) z[n_c + n_d + i] = -bint[i];
-    if ((rc = dupload(h, &h->d_zeta, z.data(), z.size()))) return fail(rc);
-  }
+  P.heavy = heavy_d;
+  P.n_heavy = (int)heavy.size();
   // state + work
   const int64_t T = P.total;
-  if ((rc = dalloc(h, &h->S.u, T)) || (rc = dalloc(h, &h->S.w, T)) ||
-      (rc = dalloc(h, &h->d_prev_u, T)) || (rc = dalloc(h, &h->d_prev_w, T)) ||
-      (rc = dalloc(h, &h->d_tmp, T)) || (rc = dalloc(h, &h->d_tmp2, T)) ||
-      (rc = dalloc(h, &h->d_tmp3, T)) || (rc = dalloc(h, &h->W.t, n_c)) ||
-      (rc = dalloc(h, &h->W.ua, n_c)) || (rc = dalloc(h, &h->W.ry, m)) ||
-      (rc = dalloc(h, &h->W.qseg, P.nseg)) || (rc = dalloc(h, &h->d_qseg2, P.nseg)) ||
-      (rc = dalloc(h, &h->W.qp, m)) || (rc = dalloc(h, &h->W.uy, m)) ||
-      (rc = dalloc(h, &h->W.part, kMaxParts)) || (rc = dalloc(h, &h->W.scal, S_COUNT)) ||
-      (rc = dalloc(h, &h->W.err, 1)) || (rc = dalloc(h, &h->d_chk, 64)) ||
-      (rc = dalloc(h, &h->d_mineig, std::max(p, 1))) || (rc = dalloc(h, &h->W.vstore, n_d)) ||
-      (rc = dalloc(h, &h->W.vvalid, std::max(p, 1))) || (rc = dalloc(h, &h->W.sweeps, std::max(p, 1))))
-    return fail(rc);
-  if (cudaMemset(h->W.vvalid, 0, sizeof(int) * std::max(p, 1)) != cudaSuccess ||
-      cudaMemset(h->W.sweeps, 0, sizeof(int) * std::max(p, 1)) != cudaSuccess)
-    return fail(HSDE_ERR_CUDA);
-  if (cudaMemset(h->W.err, 0, sizeof(int)) != cudaSuccess) return fail(HSDE_ERR_CUDA);
-  if (cudaMallocHost(&h->h_chk, 64 * sizeof(double)) != cudaSuccess) {
-    h->err = "cudaMallocHost failed";
-    return fail(HSDE_ERR_CUDA);
-  }
-  h->grid_nc = grid_for(n_c);
-  h->grid_nd = grid_for(n_d);
-  h->grid_m = grid_for(m);
-  h->grid_T = grid_for(T);
-  h->grid_seg = std::max(1, (int)((P.nseg * 32LL + kBlock - 1) / kBlock));
-  h->schur_smem = sizeof(double) * std::max(m, 1);
-  h->grid_schur = sdiag ? grid_for(m, 64) : std::min(148 * 2, std::max(1, (m + 7) / 8));
-  if (h->schur_smem > 48 * 1024) {
+  RC(dalloc(h, &s.S.u, T));
+  RC(dalloc(h, &s.S.w, T));
+  RC(dalloc(h, &s.d_prev_u, T));
+  RC(dalloc(h, &s.d_prev_w, T));
+  RC(dalloc(h, &s.d_tmp, T));
+  RC(dalloc(h, &s.d_tmp2, T));
+  RC(dalloc(h, &s.d_tmp3, T));
+  RC(dalloc(h, &s.d_hv, n_c));
+  RC(dalloc(h, &s.W.t, n_c));
+  RC(dalloc(h, &s.W.ua, n_c));
+  RC(dalloc(h, &s.W.ry, m));
+  RC(dalloc(h, &s.W.qseg, P.nseg));
+  RC(dalloc(h, &s.d_qseg2, P.nseg));
+  RC(dalloc(h, &s.W.qp, m));
+  RC(dalloc(h, &s.W.uy, m));
+  RC(dalloc(h, &s.W.part, kMaxParts));
+  RC(dalloc(h, &s.W.scal, S_COUNT));
+  RC(dalloc(h, &s.W.err, 1));
+  RC(dalloc(h, &s.d_chk, 64));
+  RC(dalloc(h, &s.d_mineig, std::max(p, 1)));
+  RC(dalloc(h, &s.W.vstore, n_d));
+  RC(dalloc(h, &s.W.vvalid, std::max(p, 1)));
+  RC(dalloc(h, &s.W.sweeps, std::max(p, 1)));
+  RC(dalloc(h, &s.W.sepbuf, std::max(d->n_sep, 1)));
+  RC(dalloc(h, &s.W.qbuf, std::max(m, 1)));
+  RC(dalloc(h, &s.W.red, 8));
+  CK(cudaMemset(s.W.err, 0, sizeof(int)));
+  CK(cudaMemset(s.W.vvalid, 0, sizeof(int) * std::max(p, 1)));
+  CK(cudaMemset(s.W.sweeps, 0, sizeof(int) * std::max(p, 1)));
+  CK(cudaMemset(s.d_chk, 0, sizeof(double) * 64));
+  s.grid_nc = grid_for(n_c);
+  s.grid_nd = grid_for(n_d);
+  s.grid_m = grid_for(m);
+  s.grid_T = grid_for(T);
+  s.grid_heavy = (P.n_heavy + (kBlock / 32) - 1) / (kBlock / 32);
+  s.grid_seg = std::max(1, (int)((P.nseg * 32LL + kBlock - 1) / kBlock));
+  s.schur_smem = sizeof(double) * std::max(m, 1);
+  s.grid_schur = 1;
+  if (s.schur_smem > 48 * 1024) {
     if (cudaFuncSetAttribute(k_schur, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)h->schur_smem) != cudaSuccess) {
+                             (int)s.schur_smem) != cudaSuccess) {
       h->err = "m too large for the shared-memory Schur apply";
-      return fail(HSDE_ERR_ARG);
+      return HSDE_ERR_ARG;
     }
   }
-  if ((rc = setup_cone_plans(h, d->clique_sizes, p))) return fail(rc);
-  // ---- Schur complement (solver.py:250-255)
+  RC(setup_cone_plans(h, s, d->clique_sizes, p));
+  return 0;
+}
+
+// normalised data (after the global |c| is known)
+int set_data(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d, double sc, double sb) {
+  const int m = d->m, n_c = d->n_c;
+  const int64_t n_d = d->n_d;
+  std::vector<double> cint(n_c), bint(m);
+  for (int c = 0; c < n_c; ++c) cint[c] = sc == 1.0 ? d->c[c] : sc * d->c[c];
+  for (int i = 0; i < m; ++i) bint[i] = sb == 1.0 ? d->b[i] : sb * d->b[i];
+  double *c_d = nullptr, *b_d = nullptr;
+  RC(dupload(h, &c_d, cint.data(), n_c));
+  RC(dupload(h, &b_d, bint.data(), m));
+  s.P.c = c_d;
+  s.P.b = b_d;
+  const double consts[4] = {sb, sc, 1.0, 0.0};
+  RC(dupload(h, &s.d_consts, consts, 4));
+  std::vector<double> z(s.P.total - 1, 0.0);  // zeta (solver.py:264)
+  for (int c = 0; c < n_c; ++c) z[c] = cint[c];
+  for (int i = 0; i < m; ++i) z[n_c + n_d + i] = -bint[i];
+  RC(dupload(h, &s.d_zeta, z.data(), z.size()));
+  return 0;
+}
+
+int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings *st,
+                const hsde_comm *comm, hsde_handle *h) {
+  cudaError_t e = cudaSetDevice(h->dev);
+  if (e != cudaSuccess) {
+    h->err = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+    return HSDE_ERR_CUDA;
+  }
+  if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) {
+    h->err = "stream create failed";
+    return HSDE_ERR_CUDA;
+  }
+  if (comm && comm->world > 1) {
+    if (nshards != 1) {
+      h->err = "NCCL mode takes exactly one shard per rank";
+      return HSDE_ERR_ARG;
+    }
+    h->mode = MODE_NCCL;
+    h->world = comm->world;
+    h->rank = comm->rank;
+    ncclUniqueId id;
+    static_assert(sizeof(id.internal) == HSDE_NCCL_ID_BYTES, "nccl id size");
+    memcpy(id.internal, comm->nccl_id, HSDE_NCCL_ID_BYTES);
+    ncclResult_t r = ncclCommInitRank(&h->nccl, comm->world, id, comm->rank);
+    if (r != ncclSuccess) {
+      h->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      return HSDE_ERR_CUDA;
+    }
+  } else if (nshards > 1) {
+    h->mode = MODE_EMULATED;
+  }
+  const int m = descs[0].m;
+  h->n_sep = descs[0].n_sep;
+  for (int g = 0; g < nshards; ++g) {
+    RC(validate(h, &descs[g]));
+    if (descs[g].m != m || descs[g].n_sep != h->n_sep) {
+      h->err = "shards disagree on m or the separator count";
+      return HSDE_ERR_ARG;
+    }
+  }
+  h->sh.resize(nshards);
+  for (int g = 0; g < nshards; ++g) RC(build_shard(h, h->sh[g], &descs[g]));
+  if (h->mode == MODE_EMULATED) {
+    const int bufs[] = {BUF_SEP, BUF_Q, BUF_RED, BUF_CHK, BUF_MINEIG};
+    for (int b : bufs) {
+      std::vector<double *> p(nshards);
+      for (int g = 0; g < nshards; ++g) p[g] = buf_ptr(h->sh[g], b);
+      RC(dupload(h, &h->d_ptrs[b], p.data(), nshards));
+    }
+  }
+  // ---- global scalars: |c|^2 over owners; diagonal-Schur test (each owned
+  // column has <= 1 nonzero on every shard; reduced as a count of violators)
+  for (auto &s : h->sh) {
+    const double v[2] = {s.nc2_owned, s.maxcol > 1 ? 1.0 : 0.0};
+    CK(cudaMemcpy(s.W.red, v, sizeof v, cudaMemcpyHostToDevice));
+  }
+  RC(reduce(h, BUF_RED, 2));
+  double gv[2];
+  CK(cudaMemcpyAsync(gv, h->sh[0].W.red, sizeof gv, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  h->schur_diag = gv[1] == 0.0;
+  for (auto &s : h->sh)
+    s.grid_schur = h->schur_diag ? grid_for(m, 64) : std::min(148 * 2, std::max(1, (m + 7) / 8));
+  const double *bsrc = descs[0].b;
+  double nb2 = 0;
+  for (int i = 0; i < m; ++i) nb2 += bsrc[i] * bsrc[i];
+  double sc = 1.0, sb = 1.0;
+  if (st->normalize) {
+    const double ncn = std::sqrt(gv[0]), nbn = std::sqrt(nb2);
+    sc = ncn > 0 ? 1.0 / ncn : 1.0;  // solver.py:659-665
+    sb = nbn > 0 ? 1.0 / nbn : 1.0;
+  }
+  for (int g = 0; g < nshards; ++g) RC(set_data(h, h->sh[g], &descs[g], sc, sb));
+  // norms of the iterated data (residual denominators, solver.py:417-423)
+  {
+    double nci = 0;
+    for (auto &s : h->sh) {
+      std::vector<double> cc(s.P.n_c);
+      CK(cudaMemcpy(cc.data(), s.P.c, sizeof(double) * s.P.n_c, cudaMemcpyDeviceToHost));
+      std::vector<unsigned char> ow(s.P.n_c, 1);
+      if (s.P.owned) CK(cudaMemcpy(ow.data(), s.P.owned, s.P.n_c, cudaMemcpyDeviceToHost));
+      for (int c = 0; c < s.P.n_c; ++c)
+        if (ow[c]) nci += cc[c] * cc[c];
+    }
+    double *red = h->sh[0].W.red;
+    for (auto &s : h->sh) CK(cudaMemset(s.W.red, 0, sizeof(double)));
+    CK(cudaMemcpy(red, &nci, sizeof(double), cudaMemcpyHostToDevice));
+    if (h->mode == MODE_NCCL) {
+      RC(reduce(h, BUF_RED, 1));
+      CK(cudaMemcpyAsync(&nci, red, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+    }
+    h->norm_c = std::sqrt(nci);
+    double nbi = 0;
+    for (int i = 0; i < m; ++i) {
+      const double bi = sb == 1.0 ? bsrc[i] : sb * bsrc[i];
+      nbi += bi * bi;
+    }
+    h->norm_b = std::sqrt(nbi);
+  }
   if (h->factor) {
-    if (sdiag) {
-      std::vector<double> sinv(m);
-      for (int i = 0; i < m; ++i) {
-        double sii = 0.0;
-        for (int64_t k = d->a_row_ptr[i]; k < d->a_row_ptr[i + 1]; ++k)
-          sii += (d->a_val[k] * p_inv[d->a_col[k]]) * d->a_val[k];
-        sii += 1.0;
-        if (!(sii > 0) || !std::isfinite(sii)) {
-          h->err = "Cholesky of the " + std::to_string(m) + " x " + std::to_string(m) +
-                   " reduced system failed: diagonal entry not positive";
-          return fail(HSDE_ERR_FACTOR);
-        }
-        sinv[i] = 1.0 / sii;
-      }
-      double *sinv_d = nullptr;
-      if ((rc = dupload(h, &sinv_d, sinv.data(), m))) return fail(rc);
-      P.sinv = sinv_d;
-      P.schur_diag = 1;
-    } else if ((rc = setup_schur_dense(h))) {
-      return fail(rc);
-    }
-    if ((rc = compute_minv_zeta(h))) return fail(rc);
+    RC(setup_schur(h));
+    RC(compute_minv_zeta(h));
   } else {
-    P.schur_diag = 1;
-    P.sinv = pinv_d;  // unused placeholder
-    P.mz = h->d_zeta;
-    P.zeta_scale = 1.0;
+    for (auto &s : h->sh) {
+      s.P.schur_diag = 1;
+      s.P.sinv = s.P.p_inv;  // unused placeholder
+      s.P.mz = s.d_zeta;
+      s.P.zeta_scale = 1.0;
+    }
   }
-  if ((rc = init_state(h))) return fail(rc);
-  // info
-  h->info.total = T;
-  h->info.n_c = n_c;
+  RC(init_state(h));
+  int maxd = 0;
+  for (auto &s : h->sh)
+    for (int d : s.sizes) maxd = std::max(maxd, d);
+  h->info.total = h->sh[0].P.total;
+  h->info.n_c = descs[0].n_c;
   h->info.m = m;
-  h->info.p = p;
-  h->info.n_d = n_d;
-  h->info.nnz = nnz;
+  h->info.p = descs[0].p;
+  h->info.n_d = descs[0].n_d;
+  h->info.nnz = descs[0].nnz;
   h->info.sigma_c = sc;
   h->info.sigma_b = sb;
-  h->info.schur_diagonal = sdiag ? 1 : 0;
+  h->info.schur_diagonal = h->schur_diag ? 1 : 0;
   h->info.max_clique = maxd;
+  h->info.n_shards = nshards;
+  h->info.mode = h->mode;
   if (h->factor) {
-    if ((rc = build_graph(h, 1, &h->g1))) return fail(rc);
     // graph of check_interval - 1 iterations: hsde_iterate(check_interval)
     // = one replay + snapshot + the single-iteration graph
-    h->gci_len = std::max(1, s->check_interval - 1);
-    if (h->gci_len > 1 && (rc = build_graph(h, h->gci_len, &h->gci))) return fail(rc);
+    h->gci_len = std::max(1, st->check_interval - 1);
+    RC(rebuild_graphs(h));
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *hsde_last_error(const hsde_t *h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+int hsde_nccl_unique_id(uint8_t *out) {
+  if (!out) return HSDE_ERR_ARG;
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    g_create_error = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+    return HSDE_ERR_CUDA;
+  }
+  memcpy(out, id.internal, HSDE_NCCL_ID_BYTES);
+  return HSDE_OK;
+}
+
+int hsde_create_sharded(const hsde_problem_desc *descs, int32_t nshards, const hsde_settings *s,
+                        const hsde_comm *comm, hsde_t **out) {
+  g_create_error.clear();
+  if (!descs || !s || !out || nshards < 1) {
+    g_create_error = "null argument";
+    return HSDE_ERR_ARG;
+  }
+  *out = nullptr;
+  if (!(s->alpha >= 1.0 && s->alpha < 2.0)) {
+    g_create_error = "alpha must lie in [1, 2)";
+    return HSDE_ERR_ARG;
+  }
+  hsde_handle *h = new hsde_handle();
+  h->set = *s;
+  h->dev = s->device;
+  h->factor = !(s->flags & HSDE_FLAG_NO_FACTOR);
+  h->warm = !(s->flags & HSDE_FLAG_COLD_EIG);
+  if (cudaMallocHost(&h->h_chk, 64 * sizeof(double)) != cudaSuccess) {
+    g_create_error = "cudaMallocHost failed";
+    delete h;
+    return HSDE_ERR_CUDA;
+  }
+  const int rc = create_impl(descs, nshards, s, comm, h);
+  if (rc) {
+    g_create_error = h->err;
+    hsde_destroy(h);
+    return rc;
   }
   *out = h;
   return HSDE_OK;
+}
+
+int hsde_create(const hsde_problem_desc *desc, const hsde_settings *settings, hsde_t **out) {
+  return hsde_create_sharded(desc, 1, settings, nullptr, out);
 }
 
 void hsde_destroy(hsde_t *h) {
@@ -783,6 +1219,7 @@ void hsde_destroy(hsde_t *h) {
   if (h->st) cudaStreamSynchronize(h->st);
   if (h->g1) cudaGraphExecDestroy(h->g1);
   if (h->gci) cudaGraphExecDestroy(h->gci);
+  if (h->nccl) ncclCommDestroy(h->nccl);
   for (void *p : h->bufs) cudaFree(p);
   if (h->h_chk) cudaFreeHost(h->h_chk);
   if (h->st) cudaStreamDestroy(h->st);
@@ -795,28 +1232,42 @@ int hsde_info(const hsde_t *h, hsde_info_t *out) {
   return HSDE_OK;
 }
 
-int hsde_set_state(hsde_t *h, const double *u, const double *w) {
-  if (!h || !u || !w) return HSDE_ERR_ARG;
+int hsde_shard_total(const hsde_t *h, int32_t g, int64_t *total) {
+  if (!h || !total || g < 0 || g >= (int)h->sh.size()) return HSDE_ERR_ARG;
+  *total = h->sh[g].P.total;
+  return HSDE_OK;
+}
+
+int hsde_set_state_shard(hsde_t *h, int32_t g, const double *u, const double *w) {
+  if (!h || !u || !w || g < 0 || g >= (int)h->sh.size()) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  const int64_t T = h->P.total;
-  CK(cudaMemcpyAsync(h->S.u, u, sizeof(double) * T, cudaMemcpyHostToDevice, h->st));
-  CK(cudaMemcpyAsync(h->S.w, w, sizeof(double) * T, cudaMemcpyHostToDevice, h->st));
-  CK(cudaMemcpyAsync(h->d_prev_u, h->S.u, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
-  CK(cudaMemcpyAsync(h->d_prev_w, h->S.w, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
-  CK(cudaMemsetAsync(h->W.vvalid, 0, sizeof(int) * std::max(h->P.p, 1), h->st));
+  ShardDev &s = h->sh[g];
+  const int64_t T = s.P.total;
+  CK(cudaMemcpyAsync(s.S.u, u, sizeof(double) * T, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(s.S.w, w, sizeof(double) * T, cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemcpyAsync(s.d_prev_u, s.S.u, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaMemcpyAsync(s.d_prev_w, s.S.w, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaMemsetAsync(s.W.vvalid, 0, sizeof(int) * std::max(s.P.p, 1), h->st));
   CK(cudaStreamSynchronize(h->st));
   return HSDE_OK;
 }
 
-int hsde_get_state(hsde_t *h, double *u, double *w) {
-  if (!h) return HSDE_ERR_ARG;
+int hsde_get_state_shard(hsde_t *h, int32_t g, double *u, double *w) {
+  if (!h || g < 0 || g >= (int)h->sh.size()) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  const int64_t T = h->P.total;
-  if (u) CK(cudaMemcpyAsync(u, h->S.u, sizeof(double) * T, cudaMemcpyDeviceToHost, h->st));
-  if (w) CK(cudaMemcpyAsync(w, h->S.w, sizeof(double) * T, cudaMemcpyDeviceToHost, h->st));
+  ShardDev &s = h->sh[g];
+  const int64_t T = s.P.total;
+  if (u) CK(cudaMemcpyAsync(u, s.S.u, sizeof(double) * T, cudaMemcpyDeviceToHost, h->st));
+  if (w) CK(cudaMemcpyAsync(w, s.S.w, sizeof(double) * T, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   return HSDE_OK;
 }
+
+int hsde_set_state(hsde_t *h, const double *u, const double *w) {
+  return hsde_set_state_shard(h, 0, u, w);
+}
+
+int hsde_get_state(hsde_t *h, double *u, double *w) { return hsde_get_state_shard(h, 0, u, w); }
 
 int hsde_reset_state(hsde_t *h) {
   if (!h) return HSDE_ERR_ARG;
@@ -826,26 +1277,22 @@ int hsde_reset_state(hsde_t *h) {
 
 int hsde_set_alpha(hsde_t *h, double alpha) {
   if (!h || !(alpha >= 1.0 && alpha < 2.0)) return HSDE_ERR_ARG;
-  if (alpha == h->P.alpha) return HSDE_OK;
+  if (alpha == h->sh[0].P.alpha) return HSDE_OK;
   cudaSetDevice(h->dev);
   CK(cudaStreamSynchronize(h->st));
-  h->P.alpha = alpha;
+  for (auto &s : h->sh) s.P.alpha = alpha;
   h->set.alpha = alpha;
-  if (h->g1) cudaGraphExecDestroy(h->g1);
-  if (h->gci) cudaGraphExecDestroy(h->gci);
-  h->g1 = h->gci = nullptr;
-  int rc = build_graph(h, 1, &h->g1);
-  if (!rc && h->gci_len > 1) rc = build_graph(h, h->gci_len, &h->gci);
-  return rc;
+  return h->factor ? rebuild_graphs(h) : 0;
 }
 
 int hsde_iterate(hsde_t *h, int32_t k) {
   if (!h || k < 0 || !h->factor) return HSDE_ERR_ARG;
   if (k == 0) return HSDE_OK;
   cudaSetDevice(h->dev);
-  const int64_t T = h->P.total;
-  k_prep_ry<<<h->grid_m, kBlock, 0, h->st>>>(h->P, h->S, h->W);
-  CKL();
+  for (auto &s : h->sh) {
+    k_prep_ry<<<s.grid_m, kBlock, 0, h->st>>>(s.P, s.S, s.W);
+    CKL();
+  }
   int left = k - 1;  // the last iteration runs after the snapshot
   while (h->gci && left >= h->gci_len) {
     CK(cudaGraphLaunch(h->gci, h->st));
@@ -855,8 +1302,11 @@ int hsde_iterate(hsde_t *h, int32_t k) {
     CK(cudaGraphLaunch(h->g1, h->st));
     --left;
   }
-  CK(cudaMemcpyAsync(h->d_prev_u, h->S.u, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
-  CK(cudaMemcpyAsync(h->d_prev_w, h->S.w, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
+  for (auto &s : h->sh) {
+    const int64_t T = s.P.total;
+    CK(cudaMemcpyAsync(s.d_prev_u, s.S.u, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaMemcpyAsync(s.d_prev_w, s.S.w, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
+  }
   CK(cudaGraphLaunch(h->g1, h->st));
   return HSDE_OK;
 }
@@ -868,36 +1318,64 @@ int hsde_sync(hsde_t *h) {
   return check_err_flag(h);
 }
 
-// residual sums of a stacked vector `u` (device) into d_chk[base..base+6]:
-// |A xt - b|^2, |H xt - st|^2, |st|^2, |A' yt + H' vt - c|^2, c.xt, b.yt
-static int residual_sums(hsde_t *h, const double *u, int base) {
-  const DevProblem &P = h->P;
+// Residual sums of the stacked states (all shards) into d_chk[0..5]:
+// |A xt - b|^2 (lead), |H xt - st|^2, |st|^2, |A' yt + H' vt - c|^2 (owned),
+// c.xt (owned), b.yt (lead).  The caller reduces d_chk across shards.
+static int residual_sums(hsde_t *h, const std::vector<const double *> &us) {
   cudaStream_t st = h->st;
-  const int64_t T = P.total;
-  double *ut = h->d_tmp2;
-  // tilde = u / tau (solver.py:413-416)
-  k_div_copy<<<h->grid_T, kBlock, 0, st>>>(u, u + T - 1, 1.0, T - 1, ut);
-  CKL();
-  const double *xt = ut, *stv = ut + P.n_c, *yt = ut + P.n_c + P.n_d, *vt = yt + P.m;
-  double *chk = h->d_chk + base;
-  k_spmv_seg<<<h->grid_seg, kBlock, 0, st>>>(P, xt, h->d_qseg2);
-  CKL();
-  k_rowres_part<<<h->grid_m, kBlock, 0, st>>>(P, h->d_qseg2, P.b, h->W.part);
-  CKL();
-  k_sum_parts<<<1, 1024, 0, st>>>(h->W.part, h->grid_m, chk + 0);
-  CKL();
-  double *pa = h->W.part, *pb = h->W.part + 2048;
-  k_cons_part<<<h->grid_nd, kBlock, 0, st>>>(P, xt, stv, pa, pb);
-  CKL();
-  k_sum_parts<<<1, 1024, 0, st>>>(pa, h->grid_nd, chk + 1);
-  k_sum_parts<<<1, 1024, 0, st>>>(pb, h->grid_nd, chk + 2);
-  CKL();
-  k_dres_part<<<h->grid_nc, kBlock, 0, st>>>(P, yt, vt, P.c, h->W.part);
-  CKL();
-  k_sum_parts<<<1, 1024, 0, st>>>(h->W.part, h->grid_nc, chk + 3);
-  CKL();
-  if (dev_dot(h, P.c, xt, P.n_c, chk + 4, st)) return HSDE_ERR_CUDA;
-  if (dev_dot(h, P.b, yt, P.m, chk + 5, st)) return HSDE_ERR_CUDA;
+  const int G = (int)h->sh.size();
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    const DevProblem &P = s.P;
+    const int64_t T = P.total;
+    const double *u = us[g];
+    double *ut = s.d_tmp2;
+    k_div_copy<<<s.grid_T, kBlock, 0, st>>>(u, u + T - 1, 1.0, T - 1, ut);  // solver.py:413-416
+    CKL();
+    const double *xt = ut, *stv = ut + P.n_c, *yt = ut + P.n_c + P.n_d, *vt = yt + P.m;
+    k_spmv_seg<<<s.grid_seg, kBlock, 0, st>>>(P, xt, s.d_qseg2);
+    CKL();
+    k_rowsum_seg<<<s.grid_m, kBlock, 0, st>>>(P, s.d_qseg2, s.W.qbuf);
+    CKL();
+    double *pa = s.W.part, *pb = s.W.part + 2048;
+    k_cons_part<<<s.grid_nd, kBlock, 0, st>>>(P, xt, stv, pa, pb);
+    CKL();
+    k_sum_parts<<<1, 1024, 0, st>>>(pa, s.grid_nd, s.d_chk + 1);
+    k_sum_parts<<<1, 1024, 0, st>>>(pb, s.grid_nd, s.d_chk + 2);
+    CKL();
+    if (h->n_sep) {
+      k_zero<<<grid_for(h->n_sep), kBlock, 0, st>>>(s.W.sepbuf, h->n_sep);
+      CKL();
+    }
+    k_pull<<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(P, s.W, vt, s.d_hv, s.grid_nc);
+    CKL();
+    RC(dev_dot_owned(h, s, P.c, xt, s.d_chk + 4));
+    RC(dev_dot(h, s, P.b, yt, P.m, s.d_chk + 5));
+    if (!P.lead) CK(cudaMemsetAsync(s.d_chk + 5, 0, sizeof(double), st));
+  }
+  RC(reduce(h, BUF_Q, h->sh[0].P.m));
+  RC(reduce(h, BUF_SEP, h->n_sep));
+  for (int g = 0; g < G; ++g) {
+    ShardDev &s = h->sh[g];
+    const DevProblem &P = s.P;
+    const double *yt = s.d_tmp2 + P.n_c + P.n_d;
+    if (P.n_sep_local) {
+      k_sep_store<<<grid_for(P.n_sep_local), kBlock, 0, st>>>(P, s.W, s.d_hv);
+      CKL();
+    }
+    k_dres_part<<<s.grid_nc, kBlock, 0, st>>>(P, yt, s.d_hv, P.c, s.W.part);
+    CKL();
+    k_sum_parts<<<1, 1024, 0, st>>>(s.W.part, s.grid_nc, s.d_chk + 3);
+    CKL();
+    if (P.lead) {
+      k_rowres_part<<<s.grid_m, kBlock, 0, st>>>(P, nullptr, s.W.qbuf, P.b, s.W.part);
+      CKL();
+      k_sum_parts<<<1, 1024, 0, st>>>(s.W.part, s.grid_m, s.d_chk + 0);
+      CKL();
+    } else {
+      CK(cudaMemsetAsync(s.d_chk + 0, 0, sizeof(double), st));
+    }
+  }
   return 0;
 }
 
@@ -915,21 +1393,26 @@ static void finish_residuals(const hsde_t *h, const double *v, double *out3) {
 int hsde_check(hsde_t *h, double *out) {
   if (!h || !out) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  const DevProblem &P = h->P;
-  const int64_t T = P.total;
   cudaStream_t st = h->st;
-  // merit |u - prev.u| + |w - prev.w| (solver.py:721-723)
-  k_diff2_part<<<h->grid_T, kBlock, 0, st>>>(h->S.u, h->d_prev_u, T, h->W.part);
-  CKL();
-  k_sum_parts<<<1, 1024, 0, st>>>(h->W.part, h->grid_T, h->d_chk + 10);
-  k_diff2_part<<<h->grid_T, kBlock, 0, st>>>(h->S.w, h->d_prev_w, T, h->W.part);
-  CKL();
-  k_sum_parts<<<1, 1024, 0, st>>>(h->W.part, h->grid_T, h->d_chk + 11);
-  CK(cudaMemcpyAsync(h->d_chk + 12, h->S.u + T - 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(h->d_chk + 13, h->S.w + T - 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
-  int rc = residual_sums(h, h->S.u, 0);
-  if (rc) return rc;
-  CK(cudaMemcpyAsync(h->h_chk, h->d_chk, 16 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  std::vector<const double *> us;
+  for (auto &s : h->sh) {
+    // merit |u - prev.u| + |w - prev.w| (solver.py:721-723)
+    k_merit_part<<<s.grid_T, kBlock, 0, st>>>(s.P, s.S.u, s.d_prev_u, s.W.part);
+    CKL();
+    k_sum_parts<<<1, 1024, 0, st>>>(s.W.part, s.grid_T, s.d_chk + 10);
+    k_merit_part<<<s.grid_T, kBlock, 0, st>>>(s.P, s.S.w, s.d_prev_w, s.W.part);
+    CKL();
+    k_sum_parts<<<1, 1024, 0, st>>>(s.W.part, s.grid_T, s.d_chk + 11);
+    CKL();
+    us.push_back(s.S.u);
+  }
+  RC(residual_sums(h, us));
+  RC(reduce(h, BUF_CHK, 12));
+  ShardDev &s0 = h->sh[0];
+  const int64_t T0 = s0.P.total;
+  CK(cudaMemcpyAsync(h->h_chk, s0.d_chk, 12 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->h_chk + 12, s0.S.u + T0 - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h->h_chk + 13, s0.S.w + T0 - 1, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const double *v = h->h_chk;
   const double tau = v[12], kappa = v[13];
@@ -952,18 +1435,23 @@ int hsde_check(hsde_t *h, double *out) {
 
 int hsde_residuals(hsde_t *h, const double *u, double *out3) {
   if (!h || !u || !out3) return HSDE_ERR_ARG;
+  if (h->multi()) {
+    h->err = "hsde_residuals: single-shard handles only";
+    return HSDE_ERR_ARG;
+  }
   cudaSetDevice(h->dev);
-  const int64_t T = h->P.total;
+  ShardDev &s = h->sh[0];
+  const int64_t T = s.P.total;
   if (!(u[T - 1] > h->set.infeas_tau_tol)) {
     char buf[64];
     snprintf(buf, sizeof buf, "tau = %g is numerically zero", u[T - 1]);
     h->err = buf;
     return HSDE_ERR_TAUZERO;
   }
-  CK(cudaMemcpyAsync(h->d_tmp, u, sizeof(double) * T, cudaMemcpyHostToDevice, h->st));
-  int rc = residual_sums(h, h->d_tmp, 0);
-  if (rc) return rc;
-  CK(cudaMemcpyAsync(h->h_chk, h->d_chk, 16 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaMemcpyAsync(s.d_tmp, u, sizeof(double) * T, cudaMemcpyHostToDevice, h->st));
+  std::vector<const double *> us{s.d_tmp};
+  RC(residual_sums(h, us));
+  CK(cudaMemcpyAsync(h->h_chk, s.d_chk, 16 * sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   finish_residuals(h, h->h_chk, out3);
   return HSDE_OK;
@@ -972,95 +1460,149 @@ int hsde_residuals(hsde_t *h, const double *u, double *out3) {
 int hsde_certificate(hsde_t *h, double *out) {
   if (!h || !out) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  const DevProblem &P = h->P;
   cudaStream_t st = h->st;
-  const int64_t T = P.total;
+  const int G = (int)h->sh.size();
   const double nan = std::numeric_limits<double>::quiet_NaN();
   for (int i = 0; i < HSDE_CERT_LEN; ++i) out[i] = nan;
-  // unscale (solver.py:668-687): x, s / sigma_b ; y, v / sigma_c
-  double *uu = h->d_tmp;
-  k_div_copy<<<h->grid_T, kBlock, 0, st>>>(h->S.u, h->d_consts + 0, 1.0, P.n_c + P.n_d, uu);
-  k_div_copy<<<h->grid_T, kBlock, 0, st>>>(h->S.u + P.n_c + P.n_d, h->d_consts + 1, 1.0,
-                                            P.m + P.n_d, uu + P.n_c + P.n_d);
-  CKL();
-  const double *x = uu, *y = uu + P.n_c + P.n_d;
-  if (dev_dot(h, h->d_b_orig, y, P.m, h->d_chk + 20, st)) return HSDE_ERR_CUDA;
-  if (dev_dot(h, h->d_c_orig, x, P.n_c, h->d_chk + 21, st)) return HSDE_ERR_CUDA;
-  CK(cudaMemcpyAsync(h->h_chk, h->d_chk + 20, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  // unscale (solver.py:668-687): x, s / sigma_b ; y, v / sigma_c ; then b.y, c.x
+  for (auto &s : h->sh) {
+    const DevProblem &P = s.P;
+    double *uu = s.d_tmp;
+    k_div_copy<<<s.grid_T, kBlock, 0, st>>>(s.S.u, s.d_consts + 0, 1.0, P.n_c + P.n_d, uu);
+    k_div_copy<<<s.grid_T, kBlock, 0, st>>>(s.S.u + P.n_c + P.n_d, s.d_consts + 1, 1.0, P.m + P.n_d,
+                                            uu + P.n_c + P.n_d);
+    CKL();
+    RC(dev_dot(h, s, s.d_b_orig, uu + P.n_c + P.n_d, P.m, s.d_chk + 20));
+    if (!P.lead) CK(cudaMemsetAsync(s.d_chk + 20, 0, sizeof(double), st));
+    RC(dev_dot_owned(h, s, s.d_c_orig, uu, s.d_chk + 21));
+  }
+  RC(reduce(h, BUF_CHK, 2, 20));
+  CK(cudaMemcpyAsync(h->h_chk, h->sh[0].d_chk + 20, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const double by = h->h_chk[0], cx = h->h_chk[1];
   out[0] = by;
   out[1] = cx;
-  double *t2 = h->d_tmp2;
+  // min clique eigenvalue over all shards of the stacked blocks
+  auto min_eig = [&](const std::vector<const double *> &blocks, double *res) -> int {
+    for (int g = 0; g < G; ++g) {
+      ShardDev &s = h->sh[g];
+      RC(launch_cone(h, s, CONE_MINEIG, s.warp_plan, false, blocks[g], s.d_mineig, 1.0, st));
+      RC(launch_cone(h, s, CONE_MINEIG, s.block_plan, true, blocks[g], s.d_mineig, 1.0, st));
+    }
+    double mn = std::numeric_limits<double>::infinity();
+    for (auto &s : h->sh) {
+      std::vector<double> me(s.P.p);
+      if (s.P.p)
+        CK(cudaMemcpyAsync(me.data(), s.d_mineig, sizeof(double) * s.P.p, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (double e : me) mn = std::min(mn, e);
+    }
+    if (h->mode == MODE_NCCL) {
+      CK(cudaMemcpyAsync(h->sh[0].d_mineig, &mn, sizeof(double), cudaMemcpyHostToDevice, st));
+      RC(reduce(h, BUF_MINEIG, 1, 0, /*min=*/true));
+      CK(cudaMemcpyAsync(&mn, h->sh[0].d_mineig, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    *res = mn;
+    return 0;
+  };
   if (by > 0) {
     // yt = y / by, vt = v / by ; |A' yt + H' vt| ; min eig of vt blocks
-    k_div_copy<<<h->grid_T, kBlock, 0, st>>>(y, h->d_chk + 20, 1.0, P.m + P.n_d, t2);
-    CKL();
-    const double *yt = t2, *vt = t2 + P.m;
-    k_dres_part<<<h->grid_nc, kBlock, 0, st>>>(P, yt, vt, nullptr, h->W.part);
-    CKL();
-    k_sum_parts<<<1, 1024, 0, st>>>(h->W.part, h->grid_nc, h->d_chk + 22);
-    CKL();
-    if (launch_cone(h, CONE_MINEIG, h->warp_plan, false, vt, h->d_mineig, 1.0, st)) return HSDE_ERR_CUDA;
-    if (launch_cone(h, CONE_MINEIG, h->block_plan, true, vt, h->d_mineig, 1.0, st)) return HSDE_ERR_CUDA;
-    std::vector<double> me(P.p);
-    CK(cudaMemcpyAsync(h->h_chk + 22, h->d_chk + 22, sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (P.p) CK(cudaMemcpyAsync(me.data(), h->d_mineig, sizeof(double) * P.p, cudaMemcpyDeviceToHost, st));
+    std::vector<const double *> vts;
+    for (auto &s : h->sh) {
+      const DevProblem &P = s.P;
+      double *y = s.d_tmp + P.n_c + P.n_d, *t2 = s.d_tmp2;
+      k_div_copy<<<s.grid_T, kBlock, 0, st>>>(y, s.d_chk + 20, 1.0, P.m + P.n_d, t2);
+      CKL();
+      if (h->n_sep) {
+        k_zero<<<grid_for(h->n_sep), kBlock, 0, st>>>(s.W.sepbuf, h->n_sep);
+        CKL();
+      }
+      k_pull<<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(P, s.W, t2 + P.m, s.d_hv, s.grid_nc);
+      CKL();
+      vts.push_back(t2 + P.m);
+    }
+    RC(reduce(h, BUF_SEP, h->n_sep));
+    for (auto &s : h->sh) {
+      const DevProblem &P = s.P;
+      if (P.n_sep_local) {
+        k_sep_store<<<grid_for(P.n_sep_local), kBlock, 0, st>>>(P, s.W, s.d_hv);
+        CKL();
+      }
+      k_dres_part<<<s.grid_nc, kBlock, 0, st>>>(P, s.d_tmp2, s.d_hv, nullptr, s.W.part);
+      CKL();
+      k_sum_parts<<<1, 1024, 0, st>>>(s.W.part, s.grid_nc, s.d_chk + 22);
+      CKL();
+    }
+    RC(reduce(h, BUF_CHK, 1, 22));
+    double mn;
+    RC(min_eig(vts, &mn));
+    CK(cudaMemcpyAsync(h->h_chk + 22, h->sh[0].d_chk + 22, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    double mn = std::numeric_limits<double>::infinity();
-    for (double e : me) mn = std::min(mn, e);
     out[2] = std::sqrt(h->h_chk[22]);
     out[3] = mn;
   }
   if (cx < 0) {
     // xt = x / (-cx), st = s / (-cx) ; |A xt| ; |H xt - st| ; min eig of H xt
-    k_div_copy<<<h->grid_T, kBlock, 0, st>>>(x, h->d_chk + 21, -1.0, P.n_c + P.n_d, t2);
-    CKL();
-    const double *xt = t2, *stv = t2 + P.n_c;
-    k_spmv_seg<<<h->grid_seg, kBlock, 0, st>>>(P, xt, h->d_qseg2);
-    k_rowres_part<<<h->grid_m, kBlock, 0, st>>>(P, h->d_qseg2, nullptr, h->W.part);
-    k_sum_parts<<<1, 1024, 0, st>>>(h->W.part, h->grid_m, h->d_chk + 23);
-    CKL();
-    double *pa = h->W.part, *pb = h->W.part + 2048;
-    k_cons_part<<<h->grid_nd, kBlock, 0, st>>>(P, xt, stv, pa, pb);
-    k_sum_parts<<<1, 1024, 0, st>>>(pa, h->grid_nd, h->d_chk + 24);
-    CKL();
-    double *hx = h->d_tmp3;
-    k_gather<<<h->grid_nd, kBlock, 0, st>>>(P, xt, hx);
-    CKL();
-    if (launch_cone(h, CONE_MINEIG, h->warp_plan, false, hx, h->d_mineig, 1.0, st)) return HSDE_ERR_CUDA;
-    if (launch_cone(h, CONE_MINEIG, h->block_plan, true, hx, h->d_mineig, 1.0, st)) return HSDE_ERR_CUDA;
-    std::vector<double> me(P.p);
-    CK(cudaMemcpyAsync(h->h_chk + 23, h->d_chk + 23, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (P.p) CK(cudaMemcpyAsync(me.data(), h->d_mineig, sizeof(double) * P.p, cudaMemcpyDeviceToHost, st));
+    std::vector<const double *> hxs;
+    for (auto &s : h->sh) {
+      const DevProblem &P = s.P;
+      double *t2 = s.d_tmp2;
+      k_div_copy<<<s.grid_T, kBlock, 0, st>>>(s.d_tmp, s.d_chk + 21, -1.0, P.n_c + P.n_d, t2);
+      CKL();
+      const double *xt = t2, *stv = t2 + P.n_c;
+      k_spmv_seg<<<s.grid_seg, kBlock, 0, st>>>(P, xt, s.d_qseg2);
+      k_rowsum_seg<<<s.grid_m, kBlock, 0, st>>>(P, s.d_qseg2, s.W.qbuf);
+      CKL();
+      double *pa = s.W.part, *pb = s.W.part + 2048;
+      k_cons_part<<<s.grid_nd, kBlock, 0, st>>>(P, xt, stv, pa, pb);
+      k_sum_parts<<<1, 1024, 0, st>>>(pa, s.grid_nd, s.d_chk + 24);
+      CKL();
+      double *hx = s.d_tmp3;
+      k_gather<<<s.grid_nd, kBlock, 0, st>>>(P, xt, hx);
+      CKL();
+      hxs.push_back(hx);
+    }
+    RC(reduce(h, BUF_Q, h->sh[0].P.m));
+    for (auto &s : h->sh) {
+      const DevProblem &P = s.P;
+      if (P.lead) {
+        k_rowres_part<<<s.grid_m, kBlock, 0, st>>>(P, nullptr, s.W.qbuf, nullptr, s.W.part);
+        k_sum_parts<<<1, 1024, 0, st>>>(s.W.part, s.grid_m, s.d_chk + 23);
+        CKL();
+      } else {
+        CK(cudaMemsetAsync(s.d_chk + 23, 0, sizeof(double), st));
+      }
+    }
+    RC(reduce(h, BUF_CHK, 2, 23));
+    double mn;
+    RC(min_eig(hxs, &mn));
+    CK(cudaMemcpyAsync(h->h_chk + 23, h->sh[0].d_chk + 23, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    double mn = std::numeric_limits<double>::infinity();
-    for (double e : me) mn = std::min(mn, e);
     out[4] = std::sqrt(h->h_chk[23]);
     out[5] = std::sqrt(h->h_chk[24]);
     out[6] = mn;
   }
-  (void)T;
   return check_err_flag(h);
 }
 
 int hsde_affine_project(hsde_t *h, const double *w, double *u) {
-  if (!h || !w || !u || !h->factor) return HSDE_ERR_ARG;
+  if (!h || !w || !u || !h->factor || h->multi()) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  const DevProblem &P = h->P;
+  ShardDev &s = h->sh[0];
+  const DevProblem &P = s.P;
   cudaStream_t st = h->st;
   const int64_t T = P.total;
-  double *dw = h->d_tmp, *rho = h->d_tmp2, *du = h->d_tmp3;
+  double *dw = s.d_tmp, *rho = s.d_tmp2, *du = s.d_tmp3;
   CK(cudaMemcpyAsync(dw, w, sizeof(double) * T, cudaMemcpyHostToDevice, st));
-  k_rho<<<h->grid_T, kBlock, 0, st>>>(P, dw, rho);  // solver.py:301
+  k_rho<<<s.grid_T, kBlock, 0, st>>>(P, dw, rho);  // solver.py:301
   CKL();
-  int rc = inner_explicit(h, rho, du, st);
-  if (rc) return rc;
-  if ((rc = dev_dot(h, h->d_zeta, du, T - 1, h->W.scal + S_ZU, st))) return rc;  // :315
-  k_shift_apply<<<h->grid_T, kBlock, 0, st>>>(P, du, h->W.scal + S_ZU);         // :316
+  RC(inner_dist(h, {rho}, {du}, true));
+  RC(dev_dot(h, s, s.d_zeta, du, T - 1, s.W.scal + S_ZU));             // :315
+  k_shift_apply<<<s.grid_T, kBlock, 0, st>>>(P, du, s.W.scal + S_ZU);  // :316
   CKL();
-  if ((rc = dev_dot(h, h->d_zeta, du, T - 1, h->W.scal + S_UTAU, st))) return rc;
-  k_tau_out<<<1, 32, 0, st>>>(dw, T, h->W.scal + S_UTAU, du);                    // :317
+  RC(dev_dot(h, s, s.d_zeta, du, T - 1, s.W.scal + S_UTAU));
+  k_tau_out<<<1, 32, 0, st>>>(dw, T, s.W.scal + S_UTAU, du);           // :317
   CKL();
   CK(cudaMemcpyAsync(u, du, sizeof(double) * T, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -1068,32 +1610,33 @@ int hsde_affine_project(hsde_t *h, const double *w, double *u) {
 }
 
 int hsde_solve_inner(hsde_t *h, const double *w12, double *u12) {
-  if (!h || !w12 || !u12 || !h->factor) return HSDE_ERR_ARG;
+  if (!h || !w12 || !u12 || !h->factor || h->multi()) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  const int64_t T = h->P.total;
-  CK(cudaMemcpyAsync(h->d_tmp2, w12, sizeof(double) * (T - 1), cudaMemcpyHostToDevice, h->st));
-  int rc = inner_explicit(h, h->d_tmp2, h->d_tmp3, h->st);
-  if (rc) return rc;
-  CK(cudaMemcpyAsync(u12, h->d_tmp3, sizeof(double) * (T - 1), cudaMemcpyDeviceToHost, h->st));
+  ShardDev &s = h->sh[0];
+  const int64_t T = s.P.total;
+  CK(cudaMemcpyAsync(s.d_tmp2, w12, sizeof(double) * (T - 1), cudaMemcpyHostToDevice, h->st));
+  RC(inner_dist(h, {s.d_tmp2}, {s.d_tmp3}, true));
+  CK(cudaMemcpyAsync(u12, s.d_tmp3, sizeof(double) * (T - 1), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   return HSDE_OK;
 }
 
 int hsde_project_cone(hsde_t *h, const double *in, double *out) {
-  if (!h || !in || !out) return HSDE_ERR_ARG;
+  if (!h || !in || !out || h->multi()) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  const DevProblem &P = h->P;
+  ShardDev &s = h->sh[0];
+  const DevProblem &P = s.P;
   const int64_t T = P.total;
   cudaStream_t st = h->st;
-  CK(cudaMemcpyAsync(h->d_tmp, in, sizeof(double) * T, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(h->d_tmp2, h->d_tmp, sizeof(double) * T, cudaMemcpyDeviceToDevice, st));
-  const double *sin = h->d_tmp + P.n_c;
-  double *sout = h->d_tmp2 + P.n_c;
-  if (launch_cone(h, CONE_PLAIN, h->warp_plan, false, sin, sout, 1.0, st)) return HSDE_ERR_CUDA;
-  if (launch_cone(h, CONE_PLAIN, h->block_plan, true, sin, sout, 1.0, st)) return HSDE_ERR_CUDA;
-  k_tau_clamp<<<1, 32, 0, st>>>(h->d_tmp, T, h->d_tmp2);
+  CK(cudaMemcpyAsync(s.d_tmp, in, sizeof(double) * T, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(s.d_tmp2, s.d_tmp, sizeof(double) * T, cudaMemcpyDeviceToDevice, st));
+  const double *sin = s.d_tmp + P.n_c;
+  double *sout = s.d_tmp2 + P.n_c;
+  RC(launch_cone(h, s, CONE_PLAIN, s.warp_plan, false, sin, sout, 1.0, st));
+  RC(launch_cone(h, s, CONE_PLAIN, s.block_plan, true, sin, sout, 1.0, st));
+  k_tau_clamp<<<1, 32, 0, st>>>(s.d_tmp, T, s.d_tmp2);
   CKL();
-  CK(cudaMemcpyAsync(out, h->d_tmp2, sizeof(double) * T, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out, s.d_tmp2, sizeof(double) * T, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return check_err_flag(h);
 }
@@ -1101,7 +1644,7 @@ int hsde_project_cone(hsde_t *h, const double *in, double *out) {
 int hsde_get_minv_zeta(hsde_t *h, double *out) {
   if (!h || !out || !h->factor) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  CK(cudaMemcpy(out, h->P.mz, sizeof(double) * (h->P.total - 1), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, h->sh[0].P.mz, sizeof(double) * (h->sh[0].P.total - 1), cudaMemcpyDeviceToHost));
   return HSDE_OK;
 }
 
@@ -1113,8 +1656,7 @@ int hsde_time_iterations(hsde_t *h, int32_t k, float *ms) {
   CK(cudaEventCreate(&b));
   CK(cudaStreamSynchronize(h->st));
   CK(cudaEventRecord(a, h->st));
-  int rc = hsde_iterate(h, k);
-  if (rc) return rc;
+  RC(hsde_iterate(h, k));
   CK(cudaEventRecord(b, h->st));
   CK(cudaEventSynchronize(b));
   CK(cudaEventElapsedTime(ms, a, b));
@@ -1130,18 +1672,17 @@ int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches) 
   for (auto &e : ev) CK(cudaEventCreate(&e));
   for (int i = 0; i < HSDE_PROFILE_SLOTS; ++i) ms[i] = 0.f;
   int nl = 0;
-  k_prep_ry<<<h->grid_m, kBlock, 0, h->st>>>(h->P, h->S, h->W);
-  CKL();
-  ++nl;
+  for (auto &s : h->sh) {
+    k_prep_ry<<<s.grid_m, kBlock, 0, h->st>>>(s.P, s.S, s.W);
+    CKL();
+    ++nl;
+  }
+  const int order[] = {PS_COUNT, PS_RHS, PS_SPMV, PS_SCHUR, PS_UA, PS_COMM, PS_SCALARS,
+                       PS_CONE_WARP, PS_CONE_BLOCK, PS_XUPD};
   for (int it = 0; it < k; ++it) {
-    // record all slot events so unused slots have zero duration
-    for (int s = 0; s <= PS_COUNT; ++s) CK(cudaEventRecord(ev[s], h->st));
-    int rc = launch_iteration(h, h->st, ev, &nl);
-    if (rc) return rc;
+    RC(launch_iteration(h, ev, &nl));
     CK(cudaEventSynchronize(ev[PS_XUPD]));
-    const int order[] = {PS_COUNT, PS_RHS, PS_SPMV, PS_SCHUR, PS_UA, PS_SCALARS, PS_CONE_WARP,
-                         PS_CONE_BLOCK, PS_XUPD};
-    for (int q = 1; q < 9; ++q) {
+    for (int q = 1; q < 10; ++q) {
       float t = 0.f;
       CK(cudaEventElapsedTime(&t, ev[order[q - 1]], ev[order[q]]));
       ms[order[q]] += t;
@@ -1155,21 +1696,22 @@ int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches) 
 int hsde_stats(hsde_t *h, double *out) {
   if (!h || !out) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  std::vector<int> sw(std::max(h->P.p, 1));
-  CK(cudaMemcpyAsync(sw.data(), h->W.sweeps, sizeof(int) * sw.size(), cudaMemcpyDeviceToHost, h->st));
-  CK(cudaStreamSynchronize(h->st));
-  double sum = 0, mx = 0, sum_big = 0, n_big = 0;
-  std::vector<int> sizes(h->P.p);
-  if (h->P.p) CK(cudaMemcpy(sizes.data(), h->P.cl_size, sizeof(int) * h->P.p, cudaMemcpyDeviceToHost));
-  for (int k = 0; k < h->P.p; ++k) {
-    sum += sw[k];
-    mx = std::max(mx, (double)sw[k]);
-    if (sizes[k] > 32) {
-      sum_big += sw[k];
-      n_big += 1;
+  double sum = 0, mx = 0, sum_big = 0, n_big = 0, n = 0;
+  for (auto &s : h->sh) {
+    std::vector<int> sw(std::max(s.P.p, 1));
+    CK(cudaMemcpyAsync(sw.data(), s.W.sweeps, sizeof(int) * sw.size(), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    for (int k = 0; k < s.P.p; ++k) {
+      sum += sw[k];
+      n += 1;
+      mx = std::max(mx, (double)sw[k]);
+      if (s.sizes[k] > 32) {
+        sum_big += sw[k];
+        n_big += 1;
+      }
     }
   }
-  out[0] = h->P.p ? sum / h->P.p : 0.0;
+  out[0] = n ? sum / n : 0.0;
   out[1] = mx;
   out[2] = n_big ? sum_big / n_big : 0.0;
   out[3] = h->warm ? 1.0 : 0.0;

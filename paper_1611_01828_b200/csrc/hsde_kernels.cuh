@@ -60,6 +60,14 @@ struct DevProblem {
   const int *slot_cov; // [n_d]
   int n_heavy;         // covered coordinates with > kHeavy slots
   const int *heavy;    // [n_heavy]
+  // sharding; single GPU: n_sep = 0, owned = null
+  int n_sep;           // global separator count |S|
+  int n_sep_local;     // separator coordinates this shard touches
+  const int *sep_of;   // [n_c] position in S or -1 (null when n_sep == 0)
+  const int *sep_local;// [n_sep_local] local covered index
+  const int *sep_pos;  // [n_sep_local] position in S
+  const unsigned char *owned;  // [n_c] 1 if this shard owns the coordinate (null: all)
+  int lead;            // 1 on the shard that contributes replicated terms (y, tau)
   const int64_t *cl_off;
   const int *cl_size;
   // data of the iterated (normalised) problem
@@ -88,7 +96,14 @@ struct DevWork {
   double *vstore;      // [n_d] eigenvectors of the last projection (warm start)
   int *vvalid;         // [p]   vstore holds a valid basis for clique k
   int *sweeps;         // [p]   Jacobi sweeps of the last projection (stats)
+  double *sepbuf;      // [n_sep] separator partials (all-reduced)
+  double *qbuf;        // [m]     partial A t (all-reduced)
+  double *red;         // [8]     scalar partials (all-reduced)
 };
+
+__device__ __forceinline__ bool owns(const DevProblem &P, int l) {
+  return P.owned == nullptr || P.owned[l];
+}
 
 // ---------------------------------------------------------------------------
 // helpers
@@ -161,6 +176,10 @@ __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWor
       if (je - jb > kHeavy) continue;
       double sg = 0.0, sv = 0.0;
       for (int e = jb; e < je; ++e) rhs_slot<FROM_STATE>(P, S, rs, rv, P.cov_slot[e], sg, sv);
+      if (P.n_sep && P.sep_of[l] >= 0) {  // separator: partial, finished after the all-reduce
+        W.sepbuf[P.sep_of[l]] = sg * 0.5 + sv;
+        continue;
+      }
       double aty = 0.0;
       const int64_t cb = P.at_cp[l], ce = P.at_cp[l + 1];
 #pragma unroll 4
@@ -184,11 +203,39 @@ __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWor
   sg = warp_sum(sg);
   sv = warp_sum(sv);
   aty = warp_sum(aty);
+  if (P.n_sep && P.sep_of[l] >= 0) {
+    if (lane == 0) W.sepbuf[P.sep_of[l]] = sg * 0.5 + sv;
+    return;
+  }
   if (lane == 0) {
     const double rx_l = FROM_STATE ? (S.u[l] + S.w[l]) - atau * P.c[l] : rx[l];
     const double r = ((sg * 0.5 + sv) + aty) + rx_l;
     W.t[l] = r * P.p_inv[l];
   }
+}
+
+// t of the separator coordinates once their pull-scatter partials are all-reduced
+template <bool FROM_STATE>
+__global__ void k_sep_finish(DevProblem P, DevState S, DevWork W, const double *rx,
+                             const double *ry) {
+  double atau = 0.0;
+  if (FROM_STATE) {
+    atau = S.u[P.total - 1] + S.w[P.total - 1];
+    ry = W.ry;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_sep_local; i += gridDim.x * blockDim.x) {
+    const int l = P.sep_local[i];
+    double aty = 0.0;
+    for (int64_t e = P.at_cp[l]; e < P.at_cp[l + 1]; ++e) aty += P.at_val[e] * __ldg(ry + P.at_row[e]);
+    const double rx_l = FROM_STATE ? (S.u[l] + S.w[l]) - atau * P.c[l] : rx[l];
+    W.t[l] = ((W.sepbuf[P.sep_pos[i]] + aty) + rx_l) * P.p_inv[l];
+  }
+}
+
+__global__ void k_zero(double *x, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    x[k] = 0.0;
 }
 
 // rho_y for the first iteration after a state change: (u_y + w_y) + a_tau b
@@ -219,11 +266,16 @@ __global__ void __launch_bounds__(kBlock) k_spmv_seg(DevProblem P, const double 
 // q' = S^{-1} q.  Every CTA rebuilds q from the segment partials (ordered),
 // then one warp per output row of the symmetric inverse.
 __global__ void __launch_bounds__(kBlock) k_schur(DevProblem P, const double *__restrict__ qseg,
+                                                   const double *__restrict__ qfull,
                                                    double *__restrict__ qp) {
   extern __shared__ double qs[];
   for (int i = threadIdx.x; i < P.m; i += blockDim.x) {
     double q = 0.0;
-    for (int s = P.row_seg[i]; s < P.row_seg[i + 1]; ++s) q += qseg[s];
+    if (qfull) {
+      q = qfull[i];  // already reduced (sharded)
+    } else {
+      for (int s = P.row_seg[i]; s < P.row_seg[i + 1]; ++s) q += qseg[s];
+    }
     qs[i] = q;
   }
   __syncthreads();
@@ -254,7 +306,7 @@ __global__ void __launch_bounds__(kBlock) k_ua(DevProblem P, DevWork W, const do
     for (int64_t e = cb; e < ce; ++e) atq += P.at_val[e] * __ldg(qp + P.at_row[e]);
     const double ua = W.t[l] - atq * P.p_inv[l];
     W.ua[l] = ua;
-    if (WITH_DOT) dot += P.c[l] * ua;
+    if (WITH_DOT && owns(P, l)) dot += P.c[l] * ua;
   }
   if (WITH_DOT) {
     dot = block_sum(dot, sh);
@@ -268,13 +320,16 @@ __global__ void __launch_bounds__(kBlock) k_ua(DevProblem P, DevWork W, const do
 // projection and dual update (:391-394), y update, next rho_y.
 
 __global__ void __launch_bounds__(1024) k_scalars(DevProblem P, DevState S, DevWork W, int nparts,
-                                                  int exact_uy, const double *__restrict__ auy) {
+                                                  int exact_uy, const double *__restrict__ auy,
+                                                  const double *__restrict__ cua_red) {
   __shared__ double sh[32];
   __shared__ double bc[4];
   const int64_t yo = P.n_c + P.n_d;
   double a = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += blockDim.x) a += W.part[i];
-  const double cua = block_sum(a, sh);
+  if (!cua_red)
+    for (int i = threadIdx.x; i < nparts; i += blockDim.x) a += W.part[i];
+  double cua = block_sum(a, sh);
+  if (cua_red) cua = cua_red[0];  // all-reduced over shards (thread 0 uses it)
   double bu = 0.0;
   for (int i = threadIdx.x; i < P.m; i += blockDim.x) {
     // uy = rho_y - A ua (solver.py:240-241); identity A ua = q' unless exact
@@ -359,11 +414,15 @@ __global__ void k_slot_out(DevProblem P, const double *rs, const double *rv, con
   }
 }
 
-// uy = wy - A ua, rows reduced from segments (solver.py:240-241)
-__global__ void k_uy_from_seg(DevProblem P, const double *qseg, const double *wy, double *uy) {
+// uy = wy - A ua (solver.py:240-241): A ua reduced from row segments, or the
+// identity A ua = q' = S^{-1} A t when qfull is given
+__global__ void k_uy_from_seg(DevProblem P, const double *qseg, const double *qfull,
+                              const double *wy, double *uy) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m; i += gridDim.x * blockDim.x) {
     double q = 0.0;
-    for (int s = P.row_seg[i]; s < P.row_seg[i + 1]; ++s) q += qseg[s];
+    if (qfull) q = qfull[i];
+    else
+      for (int s = P.row_seg[i]; s < P.row_seg[i + 1]; ++s) q += qseg[s];
     uy[i] = wy[i] - q;
   }
 }
@@ -408,19 +467,85 @@ __global__ void k_shift_apply(DevProblem P, double *u12, const double *scal_zu) 
     u12[k] -= shift * P.mz[k];
 }
 
-// residual pieces (solver.py:398-429, :455-505) on explicit vectors:
-//   per covered l: (A' y + H' v - c)_l  (c optional)
-__global__ void __launch_bounds__(kBlock) k_dres_part(DevProblem P, const double *y, const double *v,
+// residual pieces (solver.py:398-429, :455-505) on explicit vectors.
+// hv = H' v (pull scatter over the covering slots); separator coordinates
+// leave a partial in W.sepbuf for the all-reduce (then k_sep_store).
+__global__ void __launch_bounds__(kBlock) k_pull(DevProblem P, DevWork W, const double *v,
+                                                 double *hv, int nb_light) {
+  if ((int)blockIdx.x < nb_light) {
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < P.n_c; l += nb_light * blockDim.x) {
+      const int jb = P.cov_ptr[l], je = P.cov_ptr[l + 1];
+      if (je - jb > kHeavy) continue;
+      double acc = 0.0;
+      for (int e = jb; e < je; ++e) acc += v[P.cov_slot[e]];
+      if (P.n_sep && P.sep_of[l] >= 0) W.sepbuf[P.sep_of[l]] = acc;
+      else hv[l] = acc;
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int hw = ((int)blockIdx.x - nb_light) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (hw >= P.n_heavy) return;
+  const int l = P.heavy[hw];
+  double acc = 0.0;
+  for (int e = P.cov_ptr[l] + lane; e < P.cov_ptr[l + 1]; e += 32) acc += v[P.cov_slot[e]];
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    if (P.n_sep && P.sep_of[l] >= 0) W.sepbuf[P.sep_of[l]] = acc;
+    else hv[l] = acc;
+  }
+}
+
+__global__ void k_sep_store(DevProblem P, DevWork W, double *hv) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_sep_local; i += gridDim.x * blockDim.x)
+    hv[P.sep_local[i]] = W.sepbuf[P.sep_pos[i]];
+}
+
+// per owned covered l: (A' y + hv - c)_l^2   (c optional)
+__global__ void __launch_bounds__(kBlock) k_dres_part(DevProblem P, const double *y, const double *hv,
                                                       const double *c, double *part) {
   __shared__ double sh[32];
   double acc = 0.0;
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < P.n_c; l += gridDim.x * blockDim.x) {
+    if (!owns(P, l)) continue;
     double aty = 0.0;
     for (int64_t e = P.at_cp[l]; e < P.at_cp[l + 1]; ++e) aty += P.at_val[e] * y[P.at_row[e]];
-    double hv = 0.0;
-    for (int e = P.cov_ptr[l]; e < P.cov_ptr[l + 1]; ++e) hv += v[P.cov_slot[e]];
-    const double r = c ? (aty + hv) - c[l] : aty + hv;
+    const double r = c ? (aty + hv[l]) - c[l] : aty + hv[l];
     acc += r * r;
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// block partials of sum over owned l of a[l] * b[l]
+__global__ void __launch_bounds__(kBlock) k_dot_owned_part(DevProblem P, const double *a,
+                                                           const double *b, double *part) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < P.n_c; l += gridDim.x * blockDim.x)
+    if (owns(P, l)) acc += a[l] * b[l];
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// merit pieces |u - prev|^2 over the stacked vector: x owned, s/v local,
+// y / tau only on the lead shard (replicated there)
+__global__ void __launch_bounds__(kBlock) k_merit_part(DevProblem P, const double *a,
+                                                       const double *b, double *part) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  const int64_t yo = P.n_c + P.n_d, vo = yo + P.m;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < P.total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    bool use;
+    if (k < P.n_c) use = owns(P, (int)k);
+    else if (k >= yo && k < vo) use = P.lead;
+    else if (k == P.total - 1) use = P.lead;
+    else use = true;
+    if (use) {
+      const double d = a[k] - b[k];
+      acc += d * d;
+    }
   }
   acc = block_sum(acc, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
@@ -461,12 +586,15 @@ __global__ void k_gather(DevProblem P, const double *x, double *out) {
 
 // row residual (A x)_i - b_i with A x from segments; b may be null
 __global__ void __launch_bounds__(kBlock) k_rowres_part(DevProblem P, const double *qseg,
-                                                        const double *bvec, double *part) {
+                                                        const double *qfull, const double *bvec,
+                                                        double *part) {
   __shared__ double sh[32];
   double acc = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m; i += gridDim.x * blockDim.x) {
     double q = 0.0;
-    for (int s = P.row_seg[i]; s < P.row_seg[i + 1]; ++s) q += qseg[s];
+    if (qfull) q = qfull[i];
+    else
+      for (int s = P.row_seg[i]; s < P.row_seg[i + 1]; ++s) q += qseg[s];
     const double r = bvec ? q - bvec[i] : q;
     acc += r * r;
   }

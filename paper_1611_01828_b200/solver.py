@@ -439,28 +439,63 @@ def _cert_decision(cert: np.ndarray, tol: float):
 
 
 class _Session:
-    """One device handle driven through a solve (shared by solve/recover)."""
+    """One device handle driven through a solve (shared by solve/recover).
 
-    def __init__(self, dp, settings: SolverSettings, normalize: bool):
+    ``shards``: run the clique-sharded algorithm -- an int G
+    emulates G shards on this device; ``comm=(world, rank, nccl_id)`` runs this
+    rank's shard of ``shard.make_shards(cp, world)`` with NCCL.
+    """
+
+    def __init__(self, dp, settings: SolverSettings, normalize: bool, shards=None, comm=None):
+        from .shard import make_shards
+
         self.dp = dp
         self.cp = dp if isinstance(dp, CompressedProblem) else compress(dp)
         self.n2 = self.cp.N_c if isinstance(dp, CompressedProblem) else int(dp.n) ** 2
         self.mapper = _Mapper(self.cp, self.n2)
         self.settings = settings
-        self.h = _lib.Handle(
-            self.cp, alpha=settings.alpha, tol=settings.tol,
-            infeas_tau_tol=settings.infeas_tau_tol, infeas_kappa_tol=settings.infeas_kappa_tol,
-            check_interval=settings.check_interval, normalize=normalize,
-            device=_device(settings))
+        self.shards = None
+        self.comm = comm
+        kw = dict(alpha=settings.alpha, tol=settings.tol, infeas_tau_tol=settings.infeas_tau_tol,
+                  infeas_kappa_tol=settings.infeas_kappa_tol,
+                  check_interval=settings.check_interval, normalize=normalize,
+                  device=_device(settings))
+        if comm is not None:
+            world, rank = int(comm[0]), int(comm[1])
+            self.shards = make_shards(self.cp, world)
+            self.h = _lib.Handle(self.cp, shards=[self.shards[rank]], comm=comm, **kw)
+        elif shards:
+            self.shards = make_shards(self.cp, int(shards))
+            self.h = _lib.Handle(self.cp, shards=self.shards, **kw)
+        else:
+            self.h = _lib.Handle(self.cp, **kw)
         self.sigma_c, self.sigma_b = self.h.sigma_c, self.h.sigma_b
 
+    def raw_state(self):
+        """Global compressed (u, w) of the normalised problem."""
+        from .shard import gather_state
+
+        if self.shards is None:
+            return self.h.get_state()
+        if self.comm is None:
+            parts = [self.h.get_state(g) for g in range(len(self.shards))]
+        else:
+            import torch.distributed as dist
+
+            mine = self.h.get_state(0)
+            parts = [None] * int(self.comm[0])
+            dist.all_gather_object(parts, mine)
+        u = gather_state(self.cp, self.shards, [p[0] for p in parts])
+        w = gather_state(self.cp, self.shards, [p[1] for p in parts])
+        return u, w
+
     def state_ref_layout(self) -> HsdeState:
-        u, w = self.h.get_state()
+        u, w = self.raw_state()
         return HsdeState(self.mapper.up(u), self.mapper.up(w))
 
     def unscaled(self):
         """Compressed unscaled iterate (solver.py:668-687)."""
-        u, w = self.h.get_state()
+        u, w = self.raw_state()
         cp = self.cp
         if self.sigma_c != 1.0 or self.sigma_b != 1.0:
             for vec in (u, w):
@@ -561,17 +596,22 @@ def _classify(sess: _Session, chk: np.ndarray, iterations: int, timing: Timing) 
 
 
 def solve_decomposed(dp, settings: SolverSettings | None = None, iteration_callback=None,
-                     setup_elapsed: float = 0.0) -> SolverReport:
+                     setup_elapsed: float = 0.0, *, shards: int | None = None,
+                     comm=None) -> SolverReport:
     """Run the ADMM loop on the B200 (solver.py:690-772).
 
     ``dp`` is a reference-layout ``DecomposedProblem`` (the reference's own or
     :class:`paper_1611_01828_b200.problem.DecomposedProblem`) or a
     :class:`CompressedProblem`.  Iterations run back to back on the device
     (CUDA-graph replay); the host syncs once per ``check_interval``.
+
+    Extensions (keyword-only): ``comm=(world, rank, nccl_id)`` runs this rank's
+    clique shard with NCCL all-reduce (one process per GPU, see
+    paper_1611_01828_b200.multigpu); ``shards=G`` emulates G shards on one GPU.
     """
     settings = settings or SolverSettings()
     t0 = time.perf_counter()
-    sess = _Session(dp, settings, settings.normalize)
+    sess = _Session(dp, settings, settings.normalize, shards=shards, comm=comm)
     setup_s = setup_elapsed + (time.perf_counter() - t0)
     layout = sess.cp if isinstance(dp, CompressedProblem) else build_hsde(dp)[1]
     tracker = _MeritTracker()
