@@ -229,7 +229,7 @@ def run_reference(args):
         "metric": METRIC, "impl": "reference", "value": s["rate"], "unit": "iterations/s",
         "n_gpus": args.gpus, "steps": s["iterations"], "warmup": 0,
         "ms_per_step": 1e3 * s["loop_s"] / s["iterations"], "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CONFIG_NAMES[args.config], **config_stats(cp),
                    "l2": "working set > L2 (A alone 0.92 GB in CSR+CSC)"},
         "cpu_baseline": {"value": s["rate"], "unit": "iterations/s", "cores": s["threads"],
@@ -255,13 +255,23 @@ def run_ours(args):
     dev = local if world > 1 else 0
     torch.cuda.set_device(dev)
     dist = None
+    comm = None
+    cp = make_config(args.config)
     if world > 1:
         import torch.distributed as dist
 
+        from paper_1611_01828_b200.multigpu import init_comm
+        from paper_1611_01828_b200.shard import make_shards
+
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    cp = make_config(args.config)
+        comm = init_comm()
+        shards = make_shards(cp, world)
     # --- value: device-resident iterations (CUDA-graph replay) -------------------
-    h = _lib.Handle(cp, device=dev)
+    if comm is None:
+        h = _lib.Handle(cp, device=dev)
+    else:
+        # this rank's clique shard; three ncclAllReduce per iteration
+        h = _lib.Handle(cp, shards=[shards[rank]], comm=comm, device=dev)
     h.iterate(args.warmup)
     h.sync()
     sampler = ClockSampler(dev)
@@ -278,7 +288,7 @@ def run_ours(args):
         t = torch.tensor([t_local], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_local = float(t.item())
-    value = world * args.steps / t_local
+    value = args.steps / t_local  # iterations/s of the whole (sharded) problem
     # --- roofline: per-kernel CUDA events over a few eager iterations ------------
     prof_iters = 5
     prof, launches = h.profile_iterations(prof_iters)
@@ -292,10 +302,11 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_local / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator of BASELINE config; SURVEY 8d RNG order)",
             "config": {"workload": CONFIG_NAMES[args.config], **config_stats(cp),
-                       "parallelism": "single GPU" if world == 1 else f"replicas x{world}",
+                       "parallelism": "single GPU" if world == 1 else
+                       f"clique shards x{world} (NCCL all-reduce: separators, A t, c.ua)",
                        "l2": "no flush: per-iteration working set (A CSR+CSC 0.92 GB) > 126 MB L2"},
             "clocks": clocks,
             "gpu_launches": int(round(gpu_launches_per_iter * args.steps)) + 1,
@@ -306,11 +317,16 @@ def run_ours(args):
             line["roofline"] = dict(roofs[dominant], kernel=dominant)
             line["roofline_all"] = roofs
     # --- e2e: public API on host data, default to-tolerance solve ------------------
-    if rank == 0 and not args.no_e2e:
+    if not args.no_e2e:
         torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
         t0 = time.perf_counter()
-        rep = H.solve_decomposed(cp, H.SolverSettings(device=dev))
+        # a fresh NCCL unique id per communicator
+        rep = H.solve_decomposed(cp, H.SolverSettings(device=dev),
+                                 comm=init_comm() if comm is not None else None)
         wall = time.perf_counter() - t0
+    if rank == 0 and not args.no_e2e:
         nbytes = (cp.A.data.nbytes + cp.A.indices.nbytes // 2 + 8 * (cp.m + 1) + 8 * cp.N_c
                   + 8 * cp.m + 8 * (cp.p + 1) + 4 * cp.p + 4 * cp.n_d)
         checks = (rep.iterations + 19) // 20
@@ -326,7 +342,7 @@ def run_ours(args):
                                "objective_primal": rep.objective_primal,
                                "objective_dual": rep.objective_dual}
     # --- other configs (small, latency-bound): iterations/s ----------------------------
-    if rank == 0 and not args.no_extras:
+    if rank == 0 and world == 1 and not args.no_extras:
         extra = {}
         for c in (0, 1, 2, 3):
             if c == args.config:

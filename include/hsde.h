@@ -113,7 +113,7 @@ typedef struct hsde_handle hsde_t;
 int hsde_create(const hsde_problem_desc *desc, const hsde_settings *settings, hsde_t **out);
 
 /* Sharded variant: `nshards` shard descriptions.  With comm
- * and comm->world > 1: NCCL mode, exactly one shard (this rank's).  Without
+ * (world >= 1): NCCL mode, exactly one shard (this rank's).  Without
  * comm and nshards > 1: all shards on one device with device-side reductions
  * (emulation; same kernels, same three all-reduce points). */
 int hsde_create_sharded(const hsde_problem_desc *descs, int32_t nshards,

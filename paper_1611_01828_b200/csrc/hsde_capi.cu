@@ -541,7 +541,7 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
   s.warp_plan.smem = per_warp * pb;
   if (!wids.empty()) {
     RC(dupload(h, &s.warp_plan.ids, wids.data(), wids.size()));
-    const int sm = (int)s.warp_plan.smem;
+    const int sm = maxsm;  // attribute is per kernel, shared by every shard / handle
     CK(cudaFuncSetAttribute(k_cone_warp<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_warp<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_warp<CONE_MINEIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -556,7 +556,7 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
     }
     s.block_plan.smem = per_blk;
     RC(dupload(h, &s.block_plan.ids, bids.data(), bids.size()));
-    const int sm = (int)per_blk;
+    const int sm = maxsm;
     CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_MINEIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -1035,7 +1035,7 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
     h->err = "stream create failed";
     return HSDE_ERR_CUDA;
   }
-  if (comm && comm->world > 1) {
+  if (comm && comm->world >= 1) {  // explicit communicator: NCCL (a 1-rank comm is valid)
     if (nshards != 1) {
       h->err = "NCCL mode takes exactly one shard per rank";
       return HSDE_ERR_ARG;

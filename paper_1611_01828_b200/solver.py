@@ -479,6 +479,8 @@ class _Session:
             return self.h.get_state()
         if self.comm is None:
             parts = [self.h.get_state(g) for g in range(len(self.shards))]
+        elif int(self.comm[0]) == 1:
+            parts = [self.h.get_state(0)]
         else:
             import torch.distributed as dist
 

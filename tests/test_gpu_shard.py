@@ -57,3 +57,24 @@ def test_emulated_shards_to_tolerance(golden_dir, cfg, G):
     else:
         ref = z["tol_obj"]
         assert abs(rep.objective_primal - ref[0]) <= 1e-6 * abs(ref[0])
+
+
+def test_nccl_path_single_rank():
+    """The NCCL code path (unique id, communicator, ncclAllReduce captured in
+    the iteration graph) on a 1-rank communicator: must equal the plain path."""
+    from paper_1611_01828_b200 import _lib
+
+    cp = make_config(0)
+    comm = (1, 0, _lib.nccl_unique_id())
+    a, la = _run(cp, 100)
+    got, logs = {}, []
+
+    def cb(info):
+        logs.append((info.iteration, info.pres, info.dres, info.gap))
+        if info.iteration == 100:
+            got["u"] = info.state.u.copy()
+
+    H.solve_decomposed(cp, H.SolverSettings(max_iters=100, tol=1e-300), iteration_callback=cb,
+                       comm=comm)
+    assert rel(got["u"], a["u"]) <= 1e-12
+    assert np.allclose(np.array(logs)[:, 1:4], la[:, 1:4], rtol=1e-9)
