@@ -196,18 +196,19 @@ def _compare_state(z, cp, u, w, tol):
     if "fixed_u" in z.files:
         assert rel(u, z["fixed_u"]) <= tol
         assert rel(w, z["fixed_w"]) <= tol
-    else:
-        for name, vec in (("u", u), ("w", w)):
-            idx, val = z[f"fixed_{name}_idx"], z[f"fixed_{name}_val"]
-            scale = max(np.linalg.norm(z[f"fixed_{name}_norms"][:4]), 1e-300)
-            assert np.linalg.norm(vec[idx] - val) <= tol * scale * math.sqrt(idx.size / vec.size) + 1e-300
-            norms = np.array([np.linalg.norm(vec[sl]) for sl in (cp.sl_x, cp.sl_s, cp.sl_y, cp.sl_v)]
-                             + [vec[-1]])
-            ref = z[f"fixed_{name}_norms"]
-            assert np.allclose(norms, ref, rtol=tol, atol=tol * scale)
+        return
+    # large configs: 4096 seeded sample entries + per-segment norms
+    for name, vec in (("u", u), ("w", w)):
+        idx, val = z[f"fixed_{name}_idx"], z[f"fixed_{name}_val"]
+        assert rel(vec[idx], val) <= tol, name
+        norms = np.array([np.linalg.norm(vec[sl]) for sl in (cp.sl_x, cp.sl_s, cp.sl_y, cp.sl_v)]
+                         + [vec[-1]])
+        ref = z[f"fixed_{name}_norms"]
+        scale = np.linalg.norm(ref)
+        assert np.all(np.abs(norms - ref) <= tol * scale), (name, norms, ref)
 
 
-@pytest.mark.parametrize("cfg", [0, 1, 2])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
 def test_config_fixed_iterations(golden_dir, cfg):
     """Iterates after 500 iterations within 1e-8 relative of the reference."""
     z = np.load(golden_dir / f"cfg{cfg}_reference.npz")
@@ -221,7 +222,7 @@ def test_config_fixed_iterations(golden_dir, cfg):
     assert np.allclose(logs[finite, 1:4], ref[finite, 1:4], rtol=1e-6)
 
 
-@pytest.mark.parametrize("cfg", [0, 1, 2])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
 def test_config_to_tolerance(golden_dir, cfg):
     z = np.load(golden_dir / f"cfg{cfg}_reference.npz")
     rep = H.solve_decomposed(make_config(cfg), H.SolverSettings())
