@@ -42,6 +42,8 @@ extern "C" {
                                   instead of the identity A ua = S^{-1} A t        */
 #define HSDE_FLAG_NO_FACTOR 2  /* skip the Schur factorisation (residual-only handle) */
 #define HSDE_FLAG_COLD_EIG 4   /* no warm start of the clique eigensolves             */
+#define HSDE_FLAG_REFINE 8     /* d > 32: warm Jacobi to 1e-4, then eigenbasis
+                                  refinement (Ogita-Aishima) in a second kernel     */
 
 typedef struct hsde_problem_desc {
   int64_t n;                 /* ambient matrix order (informational)              */
@@ -172,10 +174,16 @@ int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches);
 const char *hsde_profile_name(int32_t slot);
 int hsde_sync(hsde_t *h);
 /* Eigensolver statistics of the last hot projection:
- * out[0] mean Jacobi sweeps per clique, out[1] max, out[2] mean over d > 32,
- * out[3] 1 if warm starts are enabled. */
-#define HSDE_STATS_LEN 4
+ * out[0] mean Jacobi sweeps per Jacobi-solved clique, out[1] max, out[2] mean
+ * over d > 32, out[3] 1 if warm starts are enabled, out[4] fraction of cliques
+ * solved by warm-start refinement, out[5] mean refinement steps. */
+#define HSDE_STATS_LEN 6
 int hsde_stats(hsde_t *h, double *out);
+/* Diagnostics: off-diagonal norm history (relative, per sweep) of the last
+ * hot projection of one clique: out[0] = 1 if warm-started, out[1..] = |off|/|A|
+ * after each sweep (-1 past the last).  `clique` selects the clique traced by
+ * subsequent iterations. */
+int hsde_debug_jacobi(hsde_t *h, int32_t clique, double *out64);
 
 #ifdef __cplusplus
 }

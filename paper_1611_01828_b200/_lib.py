@@ -21,7 +21,8 @@ HSDE_OK, HSDE_ERR_CUDA, HSDE_ERR_EIGEN, HSDE_ERR_FACTOR, HSDE_ERR_ARG, HSDE_ERR_
 HSDE_FLAG_EXACT_UY = 1
 HSDE_FLAG_NO_FACTOR = 2
 HSDE_FLAG_COLD_EIG = 4
-HSDE_STATS_LEN = 4
+HSDE_FLAG_REFINE = 8
+HSDE_STATS_LEN = 6
 HSDE_CHECK_LEN = 8
 HSDE_CERT_LEN = 7
 HSDE_PROFILE_SLOTS = 16
@@ -33,6 +34,7 @@ EXPORTED = (
     "hsde_get_minv_zeta", "hsde_time_iterations", "hsde_profile_iterations",
     "hsde_profile_name", "hsde_sync", "hsde_set_alpha", "hsde_stats", "hsde_create_sharded",
     "hsde_nccl_unique_id", "hsde_shard_total", "hsde_set_state_shard", "hsde_get_state_shard",
+    "hsde_debug_jacobi",
 )
 HSDE_NCCL_ID_BYTES = 128
 
@@ -117,6 +119,7 @@ def load() -> C.CDLL:
         "hsde_shard_total": (C.c_int, [vp, C.c_int32, C.POINTER(C.c_int64)]),
         "hsde_set_state_shard": (C.c_int, [vp, C.c_int32, _dp, _dp]),
         "hsde_get_state_shard": (C.c_int, [vp, C.c_int32, _dp, _dp]),
+        "hsde_debug_jacobi": (C.c_int, [vp, C.c_int32, _dp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -328,7 +331,13 @@ class Handle:
         out = np.empty(HSDE_STATS_LEN)
         self._rc(self._lib.hsde_stats(self._h, _ptr(out, C.c_double)))
         return {"mean_sweeps": float(out[0]), "max_sweeps": float(out[1]),
-                "mean_sweeps_large": float(out[2]), "warm_start": bool(out[3])}
+                "mean_sweeps_large": float(out[2]), "warm_start": bool(out[3]),
+                "refined_fraction": float(out[4]), "mean_refine_steps": float(out[5])}
+
+    def debug_jacobi(self, clique: int = 0) -> np.ndarray:
+        out = np.empty(64)
+        self._rc(self._lib.hsde_debug_jacobi(self._h, int(clique), _ptr(out, C.c_double)))
+        return out
 
     # -- measurement ---------------------------------------------------------------------
     def time_iterations(self, k: int) -> float:

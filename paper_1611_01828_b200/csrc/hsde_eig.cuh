@@ -80,6 +80,7 @@ struct JacobiScratch {
   double *tt, *lam, *red;
   int *offtab, *pos, *flag;
   int lda, ldv;
+  double *dbg;  // optional off-norm history (diagnostics)
 };
 
 __host__ __device__ inline int64_t jacobi_scratch_doubles(int dp) {
@@ -105,6 +106,7 @@ __device__ inline JacobiScratch jacobi_carve(double *base, int dp) {
   s.offtab = reinterpret_cast<int *>(s.red + 32);
   s.pos = s.offtab + half * (half - 1) / 2;
   s.flag = s.pos + dp + 1;
+  s.dbg = nullptr;
   return s;
 }
 
@@ -172,7 +174,9 @@ __device__ __forceinline__ void jacobi_vupdate(const Team &tm, JacobiScratch &js
 // Cyclic Jacobi on the symmetric A (dp x dp, padded); rotations accumulate
 // into the rows of Vt.  Returns the number of sweeps performed.
 template <class Team>
-__device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp) {
+__device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
+                             bool *first_order = nullptr, double switch_rel = 0.0,
+                             bool *switched = nullptr) {
   double *A = js.A;
   const int lda = js.lda, half = dp / 2, noff = half * (half - 1) / 2;
   const int nch = (d + 3) >> 2;
@@ -185,8 +189,21 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp) {
   const double stop2 = norm2 * 1.925929944387236e-34;      // (2^-56 |A|_F)^2
   int sweep = 0, round = 0;
   bool pending = false;
+  // first-order exit: off <= 1e-12 |A|_F (see psd_rebuild_first_order)
+  const double fo2 = norm2 * 1e-24;
+  if (first_order) *first_order = false;
+  if (switched) *switched = false;
+  const double sw2 = norm2 * switch_rel * switch_rel;
   for (; sweep < kMaxSweeps; ++sweep) {
     if (!(off2 > stop2)) break;  // also stops on NaN
+    if (first_order && off2 <= fo2) {
+      *first_order = true;
+      break;
+    }
+    if (switched && off2 <= sw2) {  // hand over to the refinement
+      *switched = true;
+      break;
+    }
     if (tm.rank == 0) js.flag[0] = 0;
     tm.sync();
     for (int r = 0; r < dp - 1; ++r, ++round) {
@@ -247,6 +264,7 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp) {
     const int rotated = js.flag[0];
     double n2;
     jacobi_norms(tm, js, dp, n2, off2);  // (team barriers inside)
+    if (js.dbg && tm.rank == 0 && sweep < 63) js.dbg[1 + sweep] = sqrt(off2 / norm2);
     if (!rotated) {
       ++sweep;
       break;  // every pair below the rotation threshold
@@ -336,7 +354,7 @@ __device__ void team_gemm_tn_sym(const Team &tm, const double *W, int ldw, const
   }
   for (int k = 0; k < r; ++k) {
     double w[4], x[4];
-    const int vk = vrow[k] * ldv;
+    const int vk = (vrow ? vrow[k] : k) * ldv;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       w[a] = W[k * ldw + ci[a]];
@@ -420,6 +438,89 @@ __device__ void psd_rebuild(const Team &tm, JacobiScratch &js, int d, Emit emit)
   tm.sync();
 }
 
+// out = L * R   (out[i][j] = sum_k L[i][k] R[k][j]); out may alias L.
+template <class Team>
+__device__ void team_gemm_nn(const Team &tm, const double *L, int ldl, const double *R, int ldr,
+                             double *out, int ldo, int d) {
+  const int nt = (d + 3) >> 2;
+  const int t = tm.rank;
+  const bool active = t < nt * nt;
+  const int u = active ? t / nt : 0, v = active ? t - u * nt : 0;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  if (active) {
+    int ri[4], cj[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      ri[a] = min(u + nt * a, d - 1) * ldl;
+      cj[a] = min(v + nt * a, d - 1);
+    }
+    for (int k = 0; k < d; ++k) {
+      double l[4], r[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        l[a] = L[ri[a] + k];
+        r[a] = R[k * ldr + cj[a]];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(l[a], r[b], acc[a][b]);
+    }
+  }
+  tm.sync();
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = u + nt * a, j = v + nt * b;
+        if (i < d && j < d) out[i * ldo + j] = acc[a][b];
+      }
+  }
+  tm.sync();
+}
+
+// First-order projection of a nearly diagonal B = D + E (CTA teams):
+//   P(B) = P(D) + L_D(E) + O(|E|^2 / gap),  L_D(E)_ij = E_ij (l_i+ - l_j+) / (l_i - l_j)
+// (the Frechet derivative of the spectral function max(., 0); the divided
+// difference is 1 between positive, 0 between non-positive eigenvalues).  It
+// is exact within same-sign pairs and its error is bounded by ~|E| overall;
+// the sweeps stop here only when |E|_F <= 1e-12 |A|_F.  P = V' M V with
+// M = diag(l+) + L_D(E) by two team GEMMs.
+template <class Team, class Emit>
+__device__ void psd_rebuild_first_order(const Team &tm, JacobiScratch &js, int d, Emit emit) {
+  double *A = js.A;
+  const int lda = js.lda, ldv = js.ldv;
+  for (int i = tm.rank; i < d; i += tm.size()) js.lam[i] = A[i * lda + i];
+  tm.sync();
+  for (int e = tm.rank; e < d * d; e += tm.size()) {
+    const int i = e / d, j = e - i * d;
+    const double li = js.lam[i], lj = js.lam[j];
+    double m;
+    if (i == j) {
+      m = li > 0.0 ? li : 0.0;
+    } else {
+      double dd;
+      if (li > 0.0 && lj > 0.0) dd = 1.0;
+      else if (li <= 0.0 && lj <= 0.0) dd = 0.0;
+      else dd = (fmax(li, 0.0) - fmax(lj, 0.0)) / (li - lj);
+      m = A[i * lda + j] * dd;
+    }
+    A[i * lda + j] = m;  // each element read and written by one thread
+  }
+  tm.sync();
+  team_gemm_nn(tm, A, lda, js.Vt, ldv, A, lda, d);  // T = M Vt
+  team_gemm_tn_sym(tm, js.Vt, ldv, A, lda, nullptr, d, d, [&](int i, int j, double v) {
+    emit(i, j, v);
+    if (i != j) emit(j, i, v);
+  });
+  tm.sync();
+}
+
 // ---------------------------------------------------------------------------
 // cone kernels
 
@@ -433,6 +534,7 @@ struct ConeArgs {
   double *out;      // PLAIN: stacked output; MINEIG: per-clique min eigenvalue [p]
   double in_scale;
   int warm;         // HOT: use / refresh the per-clique eigenvector store
+  int refine;       // HOT, CTA teams: hand warm cliques to k_cone_refine at 1e-4
 };
 
 // Hot-path load of slot j: builds arg_s and performs the v / w_v update and
@@ -490,6 +592,13 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   double *A = js.A;
   const int age = (MODE == CONE_HOT && ca.warm) ? W.vvalid[k] : 0;
   const bool warm = age > 0 && age < kWarmMaxAge && ((d + 3) >> 2) * ((d + 3) >> 2) <= tm.size();
+  if (MODE == CONE_HOT && W.dbg && k == W.dbg_clique) {
+    js.dbg = W.dbg;
+    if (tm.rank == 0) {
+      for (int i = 0; i < 64; ++i) W.dbg[i] = -1.0;
+      W.dbg[0] = warm ? 1.0 : 0.0;
+    }
+  }
   jacobi_prepare(tm, js, dp, !warm);
   // load (raw) and the previous eigenvectors (warm)
   for (int e = tm.rank; e < d * d; e += tm.size()) {
@@ -539,7 +648,26 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
     }
     tm.sync();
   }
-  const int sw = jacobi_sweeps(tm, js, d, dp);
+  // first-order exit for CTA teams whose GEMM tiles fit (not for MINEIG)
+  bool first_order = false, switched = false;
+  const bool fo_ok = MODE != CONE_MINEIG && tm.size() > 32 &&
+                     ((d + 3) >> 2) * ((d + 3) >> 2) <= tm.size();
+  const bool handoff_ok = MODE == CONE_HOT && warm && ca.refine;
+  const int sw = jacobi_sweeps(tm, js, d, dp, fo_ok ? &first_order : nullptr,
+                               handoff_ok ? 1e-4 : 0.0, handoff_ok ? &switched : nullptr);
+  if (MODE == CONE_HOT && ca.refine && tm.rank == 0) W.handoff[k] = switched ? 1 : 0;
+  if (switched) {
+    // stage 2 (k_cone_refine) finishes: basis to the store, w_s holds -arg_s
+    for (int e = tm.rank; e < d * d; e += tm.size()) {
+      const int a = e / d, bcol = e - a * d;
+      W.vstore[off + e] = js.Vt[a * ldv + bcol];
+    }
+    if (tm.rank == 0) {
+      W.vvalid[k] = age + 1;
+      if (W.sweeps) W.sweeps[k] = sw;
+    }
+    return;
+  }
   if (MODE == CONE_HOT && tm.rank == 0 && W.sweeps) W.sweeps[k] = sw;
   // non-finite eigenvalue -> EigenFailure (symmat.py:162-163)
   double nb = 0.0;
@@ -560,16 +688,18 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
     }
     if (tm.rank == 0) W.vvalid[k] = bad ? 0 : (warm ? age + 1 : 1);
   }
-  if (MODE == CONE_HOT) {
-    psd_rebuild(tm, js, d, [&](int a, int bcol, double v) {
-      const int64_t j = so + off + (int64_t)a * d + bcol;
-      S.u[j] = v;
-      S.w[j] += v;
-    });
+  auto emit_hot = [&](int a, int bcol, double v) {
+    const int64_t j = so + off + (int64_t)a * d + bcol;
+    S.u[j] = v;
+    S.w[j] += v;
+  };
+  auto emit_plain = [&](int a, int bcol, double v) { ca.out[off + (int64_t)a * d + bcol] = v; };
+  if (first_order) {
+    if (MODE == CONE_HOT) psd_rebuild_first_order(tm, js, d, emit_hot);
+    else psd_rebuild_first_order(tm, js, d, emit_plain);
   } else {
-    psd_rebuild(tm, js, d, [&](int a, int bcol, double v) {
-      ca.out[off + (int64_t)a * d + bcol] = v;
-    });
+    if (MODE == CONE_HOT) psd_rebuild(tm, js, d, emit_hot);
+    else psd_rebuild(tm, js, d, emit_plain);
   }
 }
 
@@ -596,4 +726,295 @@ __global__ void __launch_bounds__(kConeBlock, 2) k_cone_block(DevProblem P, DevS
   if ((int)blockIdx.x >= ca.count) return;
   BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
   cone_one<MODE>(tm, P, S, W, ca, ca.ids[blockIdx.x], smem);
+}
+
+// ---------------------------------------------------------------------------
+// Warm-started refinement of the eigenbasis (CTA teams, hot path).
+//
+// Iterative refinement for the symmetric eigendecomposition (Ogita & Aishima,
+// "Iterative refinement for symmetric eigenvalue decomposition", 2018):
+// from an approximate eigenbasis Xh (here: the previous ADMM iteration's),
+//   G = Xh'Xh, S = Xh' X Xh, lam_k = S_kk / G_kk, R = I - G,
+//   E_kl = (S_kl + lam_l R_kl) / (lam_l - lam_k)   if |lam_k - lam_l| > dlt
+//        = R_kl / 2                                 otherwise (cluster), E_kk = R_kk / 2
+//   Xh <- Xh + Xh E
+// converges quadratically; every step is four d x d GEMMs (register-tiled, fp64
+// FFMA), no barrier-bound rotation rounds.  At convergence the projection is
+// P = Xh M Xh' with M = diag(lam+) + [S_kl dd(lam_k, lam_l)] (divided
+// differences of max(., 0): exact within clusters of one sign, the
+// off-diagonal remainder |S_kl| <= 1e-12 |X| elsewhere).  Not converged within
+// kRefineMax steps -> cold cyclic Jacobi on the same block.
+
+constexpr int kRefineMax = 8;
+
+template <class Team>
+__device__ double team_max(const Team &tm, double v, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (tm.size() <= 32) return v;
+  const int lane = tm.rank & 31, wid = tm.rank >> 5;
+  tm.sync();
+  if (lane == 0) red[wid] = v;
+  tm.sync();
+  double r = 0.0;
+  const int nw = (tm.size() + 31) >> 5;
+  for (int i = 0; i < nw; ++i) r = fmax(r, red[i]);
+  tm.sync();
+  return r;
+}
+
+// acc[i][j] = sum_k opL[i][k] opR[k][j] (opL = TL ? L' : L, opR = TR ? R' : R),
+// 4x4 interleaved register tiles; epi(i, j, acc) after a team barrier.
+template <bool TL, bool TR, class Team, class Epi>
+__device__ void team_gemm(const Team &tm, const double *L, int ldl, const double *R, int ldr, int d,
+                          Epi epi) {
+  const int nt = (d + 3) >> 2;
+  const int t = tm.rank;
+  const bool active = t < nt * nt;
+  const int u = active ? t / nt : 0, v = active ? t - u * nt : 0;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  if (active) {
+    int ci[4], cj[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      ci[a] = min(u + nt * a, d - 1);
+      cj[a] = min(v + nt * a, d - 1);
+    }
+#pragma unroll 4
+    for (int k = 0; k < d; ++k) {
+      double l[4], r[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        l[a] = TL ? L[k * ldl + ci[a]] : L[ci[a] * ldl + k];
+        r[a] = TR ? R[cj[a] * ldr + k] : R[k * ldr + cj[a]];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(l[a], r[b], acc[a][b]);
+    }
+  }
+  tm.sync();
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = u + nt * a, j = v + nt * b;
+        if (i < d && j < d) epi(i, j, acc[a][b]);
+      }
+  }
+  tm.sync();
+}
+
+__host__ __device__ inline int64_t refine_scratch_doubles(int dp) {
+  const int64_t lda = dp + 1;
+  const int64_t n = 4 * dp * lda + dp + 32 + 8;
+  const int64_t j = jacobi_scratch_doubles(dp);
+  return n > j ? n : j;
+}
+
+// one CTA per clique: warm-started Jacobi sweeps down to 1e-4 |A|, then the
+// quadratically convergent refinement; cold Jacobi on failure.
+__host__ __device__ inline int64_t hybrid_scratch_doubles(int dp) {
+  const int64_t lda = dp + 1, ldv = jacobi_ldv(dp);
+  const int64_t half = dp / 2, noff = half * (half - 1) / 2;
+  const int64_t tables = 8 * half + half + dp + 32 + (noff + dp + 3 + 1) / 2 + 2;
+  const int64_t rt = dp * lda > tables ? dp * lda : tables;
+  return dp * lda + dp * lda + dp * (ldv > lda ? ldv : lda) + rt + dp + 32 + 8;
+}
+
+// Stage 2 of the hot CTA path: cliques handed over by stage-1 Jacobi
+// (off <= 1e-4 |A|) are finished by the refinement; X is re-read from w_s
+// (= -arg_s after the stage-1 load), the basis from the store.
+__global__ void __launch_bounds__(kConeBlock, 1) k_cone_refine(DevProblem P, DevState S, DevWork W,
+                                                               ConeArgs ca) {
+  extern __shared__ __align__(16) double smem[];
+  if ((int)blockIdx.x >= ca.count) return;
+  const int k = ca.ids[blockIdx.x];
+  if (!W.handoff[k]) return;
+  BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
+  const int T = tm.size();
+  const int d = P.cl_size[k];
+  const int64_t off = P.cl_off[k];
+  const int64_t so = P.n_c;
+  const int dp = d + (d & 1), lda = dp + 1, ldv = jacobi_ldv(dp);
+  const int half = dp / 2;
+  // regions: X | RA (Xt / Jacobi A) | RV (B2 / Jacobi Vt) | RT (B3 / tables) | lam, red
+  double *X = smem, *RA = X + dp * lda, *RV = RA + dp * lda;
+  double *RT = RV + dp * (ldv > lda ? ldv : lda);
+  const int64_t tables = 8 * half + half + dp + 32 + (half * (half - 1) / 2 + dp + 3 + 1) / 2 + 2;
+  double *lam = RT + (dp * lda > tables ? dp * lda : tables), *red = lam + dp;
+  for (int e = tm.rank; e < d * d; e += T) {
+    const int a = e / d, b = e - a * d;
+    X[a * lda + b] = -S.w[so + off + e];
+    RA[a * lda + b] = W.vstore[off + e];
+  }
+  if (d & 1)
+    for (int e = tm.rank; e < dp; e += T) {
+      X[d * lda + e] = 0.0;
+      X[e * lda + d] = 0.0;
+    }
+  tm.sync();
+  for (int e = tm.rank; e < d * d; e += T) {  // sym = 0.5 (B + B')  (symmat.py:157)
+    const int a = e / d, b = e - a * d;
+    if (a < b) {
+      const double s = 0.5 * (X[a * lda + b] + X[b * lda + a]);
+      X[a * lda + b] = s;
+      X[b * lda + a] = s;
+    }
+  }
+  tm.sync();
+  double loc = 0.0;
+  for (int e = tm.rank; e < d * d; e += T) {
+    const int a = e / d, b = e - a * d;
+    loc += X[a * lda + b] * X[a * lda + b];
+  }
+  const double xnorm = sqrt(team_sum(tm, loc, red));
+  auto emit_val = [&](int a, int b, double v) {
+    const int64_t j = so + off + (int64_t)a * d + b;
+    S.u[j] = v;
+    S.w[j] += v;
+  };
+  bool refined = false;
+  int steps = 0;
+  double *Xt = RA, *B2 = RV, *B3 = RT;
+  {
+    for (; steps < kRefineMax; ++steps) {
+      team_gemm<false, true>(tm, X, lda, Xt, lda, d, [&](int i, int j, double a) { B2[i * lda + j] = a; });
+      team_gemm<false, false>(tm, Xt, lda, B2, lda, d, [&](int i, int j, double a) { B3[i * lda + j] = a; });
+      team_gemm<false, true>(tm, Xt, lda, Xt, lda, d, [&](int i, int j, double a) { B2[i * lda + j] = a; });
+      for (int i = tm.rank; i < d; i += T) lam[i] = B3[i * lda + i] / B2[i * lda + i];
+      tm.sync();
+      double s2 = 0.0, r2 = 0.0, orth = 0.0;
+      for (int e = tm.rank; e < d * d; e += T) {
+        const int i = e / d, j = e - i * d;
+        const double g = B2[i * lda + j] - (i == j ? 1.0 : 0.0);
+        const double s = i == j ? B3[i * lda + i] - lam[i] : B3[i * lda + j];
+        s2 += s * s;
+        r2 += g * g;
+        orth = fmax(orth, fabs(g));
+      }
+      s2 = team_sum(tm, s2, red);
+      r2 = team_sum(tm, r2, red);
+      orth = team_max(tm, orth, red);
+      const double dlt = 2.0 * (sqrt(s2) + xnorm * sqrt(r2));
+      // separated pairs: |S_kl| must vanish (first-order M error S^2 / gap);
+      // clustered pairs of one sign are exact in M whatever S_kl; clustered
+      // pairs of opposite signs have |lam| <= dlt and must be negligible
+      double offs = 0.0, offz = 0.0;
+      for (int e = tm.rank; e < d * d; e += T) {
+        const int i = e / d, j = e - i * d;
+        if (i == j) continue;
+        if (fabs(lam[i] - lam[j]) > dlt) {
+          offs = fmax(offs, fabs(B3[i * lda + j]));
+        } else if ((lam[i] > 0.0) != (lam[j] > 0.0)) {
+          offz = fmax(offz, fmax(fabs(B3[i * lda + j]), fmax(fabs(lam[i]), fabs(lam[j]))));
+        }
+      }
+      offs = team_max(tm, offs, red);
+      offz = team_max(tm, offz, red);
+      if (W.dbg && k == W.dbg_clique && tm.rank == 0 && steps < 15) {
+        W.dbg[0] = -2.0;
+        W.dbg[1 + 4 * steps] = offs / xnorm;
+        W.dbg[2 + 4 * steps] = orth;
+        W.dbg[3 + 4 * steps] = dlt / xnorm;
+        W.dbg[4 + 4 * steps] = offz / xnorm;
+      }
+      if (!(offs == offs) || !(orth == orth) || !(dlt == dlt)) break;  // NaN -> Jacobi
+      if (offs <= 1e-12 * xnorm && offz <= 1e-10 * xnorm && orth <= 1e-12) {
+        refined = true;
+        break;
+      }
+      if (dlt > 1e-2 * xnorm) break;  // not in the refinement regime
+      for (int e = tm.rank; e < d * d; e += T) {
+        const int i = e / d, j = e - i * d;
+        const double r = (i == j ? 1.0 : 0.0) - B2[i * lda + j];
+        double ev;
+        if (i == j) ev = 0.5 * r;
+        else if (fabs(lam[i] - lam[j]) > dlt)
+          ev = (B3[i * lda + j] + lam[j] * r) / (lam[j] - lam[i]);
+        else
+          ev = 0.5 * r;
+        B2[i * lda + j] = ev;
+      }
+      tm.sync();
+      team_gemm<true, false>(tm, B2, lda, Xt, lda, d, [&](int i, int j, double a) { Xt[i * lda + j] += a; });
+    }
+  }
+  double nb = 0.0;
+  if (refined) {
+    // M = diag(lam+) + [S_kl dd(lam_k, lam_l)] (B3), T = M Xt (B2), P = Xt' T
+    for (int e = tm.rank; e < d * d; e += T) {
+      const int i = e / d, j = e - i * d;
+      const double li = lam[i], lj = lam[j];
+      double m;
+      if (i == j) {
+        m = li > 0.0 ? li : 0.0;
+      } else {
+        double dd;
+        if (li > 0.0 && lj > 0.0) dd = 1.0;
+        else if (li <= 0.0 && lj <= 0.0) dd = 0.0;
+        else dd = (fmax(li, 0.0) - fmax(lj, 0.0)) / (li - lj);
+        m = B3[i * lda + j] * dd;
+      }
+      B3[i * lda + j] = m;
+    }
+    for (int i = tm.rank; i < d; i += T) nb += isfinite(lam[i]) ? 0.0 : 1.0;
+    tm.sync();
+    team_gemm<false, false>(tm, B3, lda, Xt, lda, d, [&](int i, int j, double a) { B2[i * lda + j] = a; });
+    team_gemm_tn_sym(tm, Xt, lda, B2, lda, nullptr, d, d, [&](int i, int j, double v) {
+      emit_val(i, j, v);
+      if (i != j) emit_val(j, i, v);
+    });
+    for (int e = tm.rank; e < d * d; e += T) {
+      const int a = e / d, b = e - a * d;
+      W.vstore[off + e] = Xt[a * lda + b];
+    }
+    if (tm.rank == 0 && W.sweeps) W.sweeps[k] = 100 * (W.sweeps[k] + 1) + steps;
+  } else {
+    // refinement failed: cold cyclic Jacobi from X in this CTA
+    JacobiScratch js;
+    js.lda = lda;
+    js.ldv = ldv;
+    js.A = RA;
+    js.Vt = RV;
+    js.rot = reinterpret_cast<double2 *>(RT);
+    js.idx = reinterpret_cast<int4 *>(js.rot + 2 * half);
+    js.tt = reinterpret_cast<double *>(js.idx + 2 * half);
+    js.lam = js.tt + half;
+    js.red = js.lam + dp;
+    js.offtab = reinterpret_cast<int *>(js.red + 32);
+    js.pos = js.offtab + half * (half - 1) / 2;
+    js.flag = js.pos + dp + 1;
+    js.dbg = nullptr;
+    jacobi_prepare(tm, js, dp, true);
+    for (int e = tm.rank; e < dp * dp; e += T) {
+      const int a = e / dp, b = e - a * dp;
+      RA[a * lda + b] = X[a * lda + b];
+    }
+    tm.sync();
+    bool first_order = false;
+    const int sw = jacobi_sweeps(tm, js, d, dp, &first_order);
+    for (int i = tm.rank; i < d; i += T) nb += isfinite(js.A[i * lda + i]) ? 0.0 : 1.0;
+    for (int e = tm.rank; e < d * d; e += T) {
+      const int a = e / d, b = e - a * d;
+      W.vstore[off + e] = js.Vt[a * ldv + b];
+    }
+    if (first_order) psd_rebuild_first_order(tm, js, d, emit_val);
+    else psd_rebuild(tm, js, d, emit_val);
+    if (tm.rank == 0) {
+      if (W.sweeps) W.sweeps[k] += sw;
+      W.vvalid[k] = 1;
+    }
+  }
+  const bool bad = team_sum(tm, nb, red) > 0.0;
+  if (bad && tm.rank == 0) {
+    W.vvalid[k] = 0;
+    atomicOr(W.err, 1);
+  }
 }

@@ -99,6 +99,9 @@ struct DevWork {
   double *sepbuf;      // [n_sep] separator partials (all-reduced)
   double *qbuf;        // [m]     partial A t (all-reduced)
   double *red;         // [8]     scalar partials (all-reduced)
+  int *handoff;        // [p]     1: stage-1 Jacobi handed the clique to the refinement kernel
+  double *dbg;         // [64]    Jacobi off-norm history of one clique (diagnostics)
+  int dbg_clique;
 };
 
 __device__ __forceinline__ bool owns(const DevProblem &P, int l) {
