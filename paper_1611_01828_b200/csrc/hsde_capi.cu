@@ -115,6 +115,7 @@ struct hsde_handle {
   int gci_len = 0;
   bool factor = true;
   bool warm = true;
+  bool refine = false;  // two-stage Jacobi + refinement (HSDE_FLAG_REFINE)
   bool multi() const { return mode != MODE_SINGLE; }
 };
 

@@ -293,3 +293,21 @@ def test_warm_started_eigensolves_match_cold_and_oracle():
 
     O.solve(cp, O.OracleSettings(max_iters=200, tol=1e-300), callback=cb)
     assert rel(res[0][0], ref["u"]) <= 1e-8
+
+
+def test_refinement_path_matches_jacobi():
+    """HSDE_FLAG_REFINE (Jacobi to 1e-4 + Ogita-Aishima refinement) vs the default
+    warm Jacobi after 150 iterations of d = 40 cliques."""
+    from paper_1611_01828_b200 import _lib
+    from paper_1611_01828_b200.synthetic import block_arrow
+
+    cp = block_arrow(12, 24, 16, 50, 0.05, 7, "ctapath")
+    res = []
+    for flags in (0, _lib.HSDE_FLAG_REFINE):
+        h = _lib.Handle(cp, flags=flags)
+        h.iterate(150)
+        res.append(h.get_state()[0])
+        if flags:
+            assert h.stats()["refined_fraction"] > 0.0
+        h.close()
+    assert rel(res[1], res[0]) <= 1e-9
