@@ -327,16 +327,16 @@ int inner_dist(hsde_handle *h, const std::vector<const double *> &rho,
       k_zero<<<grid_for(h->n_sep), kBlock, 0, st>>>(s.W.sepbuf, h->n_sep);
       CKL();
     }
-    k_rhs<false><<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(P, s.S, s.W, rx, rs, ry, rv, s.grid_nc);
+    k_rhs<false><<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(P, s.S, s.W, rx, rs, rv, s.grid_nc);
     CKL();
   }
   RC(reduce(h, BUF_SEP, h->n_sep));
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
     const DevProblem &P = s.P;
-    const double *rx = rho[g], *ry = rho[g] + P.n_c + P.n_d;
+    const double *rx = rho[g];
     if (P.n_sep_local) {
-      k_sep_finish<false><<<grid_for(P.n_sep_local), kBlock, 0, st>>>(P, s.S, s.W, rx, ry);
+      k_sep_finish<false><<<grid_for(P.n_sep_local), kBlock, 0, st>>>(P, s.S, s.W, rx);
       CKL();
     }
     k_spmv_seg<<<s.grid_seg, kBlock, 0, st>>>(P, s.W.t, s.W.qseg);
@@ -352,7 +352,7 @@ int inner_dist(hsde_handle *h, const std::vector<const double *> &rho,
     const DevProblem &P = s.P;
     const double *rs = rho[g] + P.n_c, *ry = rho[g] + P.n_c + P.n_d, *rv = ry + P.m;
     k_schur<<<s.grid_schur, kBlock, s.schur_smem, st>>>(P, s.W.qseg, h->multi() ? s.W.qbuf : nullptr,
-                                                        s.W.qp);
+                                                        ry, s.W.qp);
     CKL();
     k_ua<false><<<s.grid_nc, kBlock, 0, st>>>(P, s.W, s.W.qp);
     CKL();
@@ -366,7 +366,7 @@ int inner_dist(hsde_handle *h, const std::vector<const double *> &rho,
       k_uy_from_seg<<<s.grid_m, kBlock, 0, st>>>(P, s.d_qseg2, nullptr, ry, uy);
       CKL();
     } else {
-      k_uy_from_seg<<<s.grid_m, kBlock, 0, st>>>(P, nullptr, s.W.qp, ry, uy);  // uy = rho_y - q'
+      k_uy_from_seg<<<s.grid_m, kBlock, 0, st>>>(P, nullptr, s.W.qp, ry, uy);  // uy = -g
       CKL();
     }
   }
@@ -392,7 +392,7 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
       ++nl;
     }
     k_rhs<true><<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(s.P, s.S, s.W, nullptr, nullptr, nullptr,
-                                                            nullptr, s.grid_nc);
+                                                            s.grid_nc);
     CKL();
     ++nl;
   }
@@ -401,7 +401,7 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
     if (s.P.n_sep_local) {
-      k_sep_finish<true><<<grid_for(s.P.n_sep_local), kBlock, 0, st>>>(s.P, s.S, s.W, nullptr, nullptr);
+      k_sep_finish<true><<<grid_for(s.P.n_sep_local), kBlock, 0, st>>>(s.P, s.S, s.W, nullptr);
       CKL();
       ++nl;
     }
@@ -419,7 +419,7 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
     k_schur<<<s.grid_schur, kBlock, s.schur_smem, st>>>(s.P, s.W.qseg, h->multi() ? s.W.qbuf : nullptr,
-                                                        s.W.qp);
+                                                        s.W.ry, s.W.qp);
     CKL();
     ++nl;
   }

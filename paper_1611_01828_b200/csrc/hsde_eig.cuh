@@ -811,12 +811,6 @@ __device__ void team_gemm(const Team &tm, const double *L, int ldl, const double
   tm.sync();
 }
 
-__host__ __device__ inline int64_t refine_scratch_doubles(int dp) {
-  const int64_t lda = dp + 1;
-  const int64_t n = 4 * dp * lda + dp + 32 + 8;
-  const int64_t j = jacobi_scratch_doubles(dp);
-  return n > j ? n : j;
-}
 
 // one CTA per clique: warm-started Jacobi sweeps down to 1e-4 |A|, then the
 // quadratically convergent refinement; cold Jacobi on failure.

@@ -4,11 +4,16 @@
 // compressed layout [x n_c | s n_d | y m | v n_d | tau] is, in launch order:
 //
 //   k_rhs      per covered coordinate l: pull-scatter of the clique slots
-//              covering l (graphs.py:249-252, atomic-free), CSC column of A'
-//              (solver.py:226), r and t = P^{-1} r (solver.py:222-231)
-//   k_spmv_seg row-split CSR SpMV q = A t (solver.py:232 `dp.A @ t`)
-//   k_schur    q' = S^{-1} q with the cached inverse (solver.py:232 cho_solve)
-//   k_ua       ua = t - P^{-1} A' q' (solver.py:232-235) + block partials of c.ua
+//              covering l (graphs.py:249-252, atomic-free) and
+//              t0 = P^{-1} (r - A' rho_y)  (solver.py:222-231 without the A' term)
+//   k_spmv_seg row-split CSR SpMV q0 = A t0 (solver.py:232 `dp.A @ t`)
+//   k_schur    g = S^{-1} (q0 - rho_y) with the cached inverse
+//   k_ua       ua = t0 - P^{-1} A' g + block partials of c.ua
+//
+//   With S = I + A P^{-1} A' this is the reference's block elimination
+//   (t = t0 + P^{-1} A' rho_y, q' = S^{-1} A t, ua = t - P^{-1} A' q',
+//   solver.py:231-235) rearranged: q' = g + rho_y, ua = t0 - P^{-1} A' g and
+//   uy = rho_y - A ua = rho_y - q' = -g.  Two passes over A instead of three.
 //   k_scalars  one CTA: zeta.u12, shift, tau/kappa, y update (solver.py:315-317,
 //              388-394), next iteration's rho_y
 //   k_cone     per clique: ub, uv, relaxation, PSD projection (symmat.py:153-165)
@@ -139,8 +144,8 @@ __device__ __forceinline__ double relax(double uhat, double uold, double alpha) 
 }
 
 // ---------------------------------------------------------------------------
-// k_rhs: r = 0.5 H'(rho_s - rho_v) + H' rho_v + A' rho_y + rho_x ; t = P^{-1} r
-// (solver.py:222-231).  FROM_STATE: rho comes from the state u + w and a_tau
+// k_rhs: r0 = 0.5 H'(rho_s - rho_v) + H' rho_v + rho_x ; t0 = P^{-1} r0
+// (solver.py:222-231 less the A' rho_y term, folded into k_schur).  FROM_STATE: rho comes from the state u + w and a_tau
 // (affine_project :300-301 fused); otherwise from explicit vectors.
 
 // Covered coordinates with more than kHeavy covering slots (e.g. the arrow
@@ -167,12 +172,9 @@ __device__ __forceinline__ void rhs_slot(const DevProblem &P, const DevState &S,
 template <bool FROM_STATE>
 __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWork W,
                                                 const double *rx, const double *rs,
-                                                const double *ry, const double *rv, int nb_light) {
+                                                const double *rv, int nb_light) {
   double atau = 0.0;
-  if (FROM_STATE) {
-    atau = S.u[P.total - 1] + S.w[P.total - 1];
-    ry = W.ry;
-  }
+  if (FROM_STATE) atau = S.u[P.total - 1] + S.w[P.total - 1];
   if ((int)blockIdx.x < nb_light) {
     for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < P.n_c; l += nb_light * blockDim.x) {
       const int jb = P.cov_ptr[l], je = P.cov_ptr[l + 1];
@@ -183,12 +185,8 @@ __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWor
         W.sepbuf[P.sep_of[l]] = sg * 0.5 + sv;
         continue;
       }
-      double aty = 0.0;
-      const int64_t cb = P.at_cp[l], ce = P.at_cp[l + 1];
-#pragma unroll 4
-      for (int64_t e = cb; e < ce; ++e) aty += P.at_val[e] * __ldg(ry + P.at_row[e]);
       const double rx_l = FROM_STATE ? (S.u[l] + S.w[l]) - atau * P.c[l] : rx[l];
-      const double r = ((sg * 0.5 + sv) + aty) + rx_l;
+      const double r = (sg * 0.5 + sv) + rx_l;
       W.t[l] = r * P.p_inv[l];
     }
     return;
@@ -198,40 +196,31 @@ __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWor
   const int hw = ((int)blockIdx.x - nb_light) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (hw >= P.n_heavy) return;
   const int l = P.heavy[hw];
-  double sg = 0.0, sv = 0.0, aty = 0.0;
+  double sg = 0.0, sv = 0.0;
   for (int e = P.cov_ptr[l] + lane; e < P.cov_ptr[l + 1]; e += 32)
     rhs_slot<FROM_STATE>(P, S, rs, rv, P.cov_slot[e], sg, sv);
-  for (int64_t e = P.at_cp[l] + lane; e < P.at_cp[l + 1]; e += 32)
-    aty += P.at_val[e] * __ldg(ry + P.at_row[e]);
   sg = warp_sum(sg);
   sv = warp_sum(sv);
-  aty = warp_sum(aty);
   if (P.n_sep && P.sep_of[l] >= 0) {
     if (lane == 0) W.sepbuf[P.sep_of[l]] = sg * 0.5 + sv;
     return;
   }
   if (lane == 0) {
     const double rx_l = FROM_STATE ? (S.u[l] + S.w[l]) - atau * P.c[l] : rx[l];
-    const double r = ((sg * 0.5 + sv) + aty) + rx_l;
+    const double r = (sg * 0.5 + sv) + rx_l;
     W.t[l] = r * P.p_inv[l];
   }
 }
 
 // t of the separator coordinates once their pull-scatter partials are all-reduced
 template <bool FROM_STATE>
-__global__ void k_sep_finish(DevProblem P, DevState S, DevWork W, const double *rx,
-                             const double *ry) {
+__global__ void k_sep_finish(DevProblem P, DevState S, DevWork W, const double *rx) {
   double atau = 0.0;
-  if (FROM_STATE) {
-    atau = S.u[P.total - 1] + S.w[P.total - 1];
-    ry = W.ry;
-  }
+  if (FROM_STATE) atau = S.u[P.total - 1] + S.w[P.total - 1];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n_sep_local; i += gridDim.x * blockDim.x) {
     const int l = P.sep_local[i];
-    double aty = 0.0;
-    for (int64_t e = P.at_cp[l]; e < P.at_cp[l + 1]; ++e) aty += P.at_val[e] * __ldg(ry + P.at_row[e]);
     const double rx_l = FROM_STATE ? (S.u[l] + S.w[l]) - atau * P.c[l] : rx[l];
-    W.t[l] = ((W.sepbuf[P.sep_pos[i]] + aty) + rx_l) * P.p_inv[l];
+    W.t[l] = (W.sepbuf[P.sep_pos[i]] + rx_l) * P.p_inv[l];
   }
 }
 
@@ -266,11 +255,13 @@ __global__ void __launch_bounds__(kBlock) k_spmv_seg(DevProblem P, const double 
   if (lane == 0) qseg[seg] = acc;
 }
 
-// q' = S^{-1} q.  Every CTA rebuilds q from the segment partials (ordered),
-// then one warp per output row of the symmetric inverse.
+// g = S^{-1} (q0 - rho_y).  Every CTA rebuilds q0 - rho_y from the segment
+// partials (ordered) into shared memory, then one warp per output row of the
+// symmetric inverse.
 __global__ void __launch_bounds__(kBlock) k_schur(DevProblem P, const double *__restrict__ qseg,
                                                    const double *__restrict__ qfull,
-                                                   double *__restrict__ qp) {
+                                                   const double *__restrict__ ry,
+                                                   double *__restrict__ g) {
   extern __shared__ double qs[];
   for (int i = threadIdx.x; i < P.m; i += blockDim.x) {
     double q = 0.0;
@@ -279,12 +270,12 @@ __global__ void __launch_bounds__(kBlock) k_schur(DevProblem P, const double *__
     } else {
       for (int s = P.row_seg[i]; s < P.row_seg[i + 1]; ++s) q += qseg[s];
     }
-    qs[i] = q;
+    qs[i] = q - ry[i];
   }
   __syncthreads();
   if (P.schur_diag) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m; i += gridDim.x * blockDim.x)
-      qp[i] = qs[i] * P.sinv[i];
+      g[i] = qs[i] * P.sinv[i];
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -294,11 +285,12 @@ __global__ void __launch_bounds__(kBlock) k_schur(DevProblem P, const double *__
     double acc = 0.0;
     for (int j = lane; j < P.m; j += 32) acc += row[j] * qs[j];
     acc = warp_sum(acc);
-    if (lane == 0) qp[i] = acc;
+    if (lane == 0) g[i] = acc;
   }
 }
 
-// ua = t - P^{-1} (A' q')  (solver.py:232-235); WITH_DOT: block partials of c.ua
+// ua = t0 - P^{-1} (A' g)  (solver.py:232-235, see the header); WITH_DOT: block
+// partials of c.ua
 template <bool WITH_DOT>
 __global__ void __launch_bounds__(kBlock) k_ua(DevProblem P, DevWork W, const double *__restrict__ qp) {
   __shared__ double sh[32];
@@ -335,8 +327,8 @@ __global__ void __launch_bounds__(1024) k_scalars(DevProblem P, DevState S, DevW
   if (cua_red) cua = cua_red[0];  // all-reduced over shards (thread 0 uses it)
   double bu = 0.0;
   for (int i = threadIdx.x; i < P.m; i += blockDim.x) {
-    // uy = rho_y - A ua (solver.py:240-241); identity A ua = q' unless exact
-    const double uy = W.ry[i] - (exact_uy ? auy[i] : W.qp[i]);
+    // uy = rho_y - A ua (solver.py:240-241); identity rho_y - A ua = -g unless exact
+    const double uy = exact_uy ? W.ry[i] - auy[i] : -W.qp[i];
     W.uy[i] = uy;
     bu += P.b[i] * uy;
   }
@@ -418,14 +410,16 @@ __global__ void k_slot_out(DevProblem P, const double *rs, const double *rv, con
 }
 
 // uy = wy - A ua (solver.py:240-241): A ua reduced from row segments, or the
-// identity A ua = q' = S^{-1} A t when qfull is given
-__global__ void k_uy_from_seg(DevProblem P, const double *qseg, const double *qfull,
+// identity uy = -g when g (k_schur's output) is given
+__global__ void k_uy_from_seg(DevProblem P, const double *qseg, const double *g,
                               const double *wy, double *uy) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m; i += gridDim.x * blockDim.x) {
+    if (g) {
+      uy[i] = -g[i];
+      continue;
+    }
     double q = 0.0;
-    if (qfull) q = qfull[i];
-    else
-      for (int s = P.row_seg[i]; s < P.row_seg[i + 1]; ++s) q += qseg[s];
+    for (int s = P.row_seg[i]; s < P.row_seg[i + 1]; ++s) q += qseg[s];
     uy[i] = wy[i] - q;
   }
 }
