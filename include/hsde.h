@@ -42,8 +42,6 @@ extern "C" {
                                   instead of the identity A ua = S^{-1} A t        */
 #define HSDE_FLAG_NO_FACTOR 2  /* skip the Schur factorisation (residual-only handle) */
 #define HSDE_FLAG_COLD_EIG 4   /* no warm start of the clique eigensolves             */
-#define HSDE_FLAG_REFINE 8     /* d > 32: warm Jacobi to 1e-4, then eigenbasis
-                                  refinement (Ogita-Aishima) in a second kernel     */
 
 typedef struct hsde_problem_desc {
   int64_t n;                 /* ambient matrix order (informational)              */
@@ -175,9 +173,8 @@ const char *hsde_profile_name(int32_t slot);
 int hsde_sync(hsde_t *h);
 /* Eigensolver statistics of the last hot projection:
  * out[0] mean Jacobi sweeps per Jacobi-solved clique, out[1] max, out[2] mean
- * over d > 32, out[3] 1 if warm starts are enabled, out[4] fraction of cliques
- * solved by warm-start refinement, out[5] mean refinement steps. */
-#define HSDE_STATS_LEN 6
+ * over d > 32, out[3] 1 if warm starts are enabled. */
+#define HSDE_STATS_LEN 4
 int hsde_stats(hsde_t *h, double *out);
 /* Diagnostics: off-diagonal norm history (relative, per sweep) of the last
  * hot projection of one clique: out[0] = 1 if warm-started, out[1..] = |off|/|A|

@@ -54,7 +54,6 @@ struct ConePlan {
   int count = 0;
   int dpmax = 0;
   size_t smem = 0;
-  size_t refine_smem = 0;  // > 0: hot path uses the warm-start refinement kernel
   int per_block = 0;       // warps per CTA (warp plan)
 };
 
@@ -115,7 +114,6 @@ struct hsde_handle {
   int gci_len = 0;
   bool factor = true;
   bool warm = true;
-  bool refine = false;  // two-stage Jacobi + refinement (HSDE_FLAG_REFINE)
   bool multi() const { return mode != MODE_SINGLE; }
 };
 
@@ -269,7 +267,7 @@ __global__ void k_diag_finish(double *diag, int m, int *flag) {
 int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool block,
                 const double *in, double *out, double in_scale, cudaStream_t st) {
   if (pl.count == 0) return 0;
-  ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0, 0};
+  ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0};
   if (!block) {
     const int grid = (pl.count + pl.per_block - 1) / pl.per_block;
     const int thr = pl.per_block * 32;
@@ -277,14 +275,7 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
     else if (mode == CONE_PLAIN) k_cone_warp<CONE_PLAIN><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
     else k_cone_warp<CONE_MINEIG><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
   } else {
-    if (mode == CONE_HOT) {
-      ca.refine = pl.refine_smem ? 1 : 0;
-      k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
-      if (ca.refine) {  // stage 2: cliques handed over at 1e-4
-        CKL();
-        k_cone_refine<<<pl.count, kConeBlock, pl.refine_smem, st>>>(s.P, s.S, s.W, ca);
-      }
-    }
+    if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
     else if (mode == CONE_PLAIN) k_cone_block<CONE_PLAIN><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
     else k_cone_block<CONE_MINEIG><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
   }
@@ -569,12 +560,6 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
     CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_MINEIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    const size_t rs = (size_t)hybrid_scratch_doubles(dpb) * sizeof(double);
-    const int ntile = (dpb + 3) / 4;
-    if (h->warm && h->refine && rs <= (size_t)maxsm && ntile * ntile <= kConeBlock) {
-      s.block_plan.refine_smem = rs;
-      CK(cudaFuncSetAttribute(k_cone_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    }
   }
   return 0;
 }
@@ -996,8 +981,6 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   RC(dalloc(h, &s.W.qbuf, std::max(m, 1)));
   RC(dalloc(h, &s.W.red, 8));
   RC(dalloc(h, &s.W.dbg, 64));
-  RC(dalloc(h, &s.W.handoff, std::max(p, 1)));
-  CK(cudaMemset(s.W.handoff, 0, sizeof(int) * std::max(p, 1)));
   s.W.dbg_clique = 0;
   CK(cudaMemset(s.W.err, 0, sizeof(int)));
   CK(cudaMemset(s.W.vvalid, 0, sizeof(int) * std::max(p, 1)));
@@ -1213,7 +1196,6 @@ int hsde_create_sharded(const hsde_problem_desc *descs, int32_t nshards, const h
   h->dev = s->device;
   h->factor = !(s->flags & HSDE_FLAG_NO_FACTOR);
   h->warm = !(s->flags & HSDE_FLAG_COLD_EIG);
-  h->refine = (s->flags & HSDE_FLAG_REFINE) != 0;
   if (cudaMallocHost(&h->h_chk, 64 * sizeof(double)) != cudaSuccess) {
     g_create_error = "cudaMallocHost failed";
     delete h;
@@ -1716,25 +1698,12 @@ int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches) 
 int hsde_stats(hsde_t *h, double *out) {
   if (!h || !out) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  double sum = 0, mx = 0, sum_big = 0, n_big = 0, n = 0, n_ref = 0, ref_steps = 0;
+  double sum = 0, mx = 0, sum_big = 0, n_big = 0, n = 0;
   for (auto &s : h->sh) {
     std::vector<int> sw(std::max(s.P.p, 1));
     CK(cudaMemcpyAsync(sw.data(), s.W.sweeps, sizeof(int) * sw.size(), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     for (int k = 0; k < s.P.p; ++k) {
-      if (sw[k] >= 100) {  // refined: 100 * (jacobi sweeps + 1) + refinement steps
-        n_ref += 1;
-        ref_steps += sw[k] % 100;
-        const int js_ = sw[k] / 100 - 1;
-        sum += js_;
-        n += 1;
-        mx = std::max(mx, (double)js_);
-        if (s.sizes[k] > 32) {
-          sum_big += js_;
-          n_big += 1;
-        }
-        continue;
-      }
       sum += sw[k];
       n += 1;
       mx = std::max(mx, (double)sw[k]);
@@ -1748,8 +1717,6 @@ int hsde_stats(hsde_t *h, double *out) {
   out[1] = mx;
   out[2] = n_big ? sum_big / n_big : 0.0;
   out[3] = h->warm ? 1.0 : 0.0;
-  out[4] = (n + n_ref) ? n_ref / (n + n_ref) : 0.0;
-  out[5] = n_ref ? ref_steps / n_ref : 0.0;
   return HSDE_OK;
 }
 

@@ -64,19 +64,31 @@ __device__ double team_sum(const Team &tm, double v, double *red) {
 }
 
 // player at tournament position `pos` in round r (0 <= r < dp - 1): position 0
-// is fixed, the others rotate (no integer division: pos - 1 + r < 2 (dp - 1))
+// is fixed, the others rotate (no integer division: pos - 1 + r < 2 (dp - 1)).
+// Pair k of round r is (tour_player(k), tour_player(dp - 1 - k)).
 __device__ __forceinline__ int tour_player(int pos, int r, int dp) {
   int x = pos - 1 + r;
   if (x >= dp - 1) x -= dp - 1;
   return pos == 0 ? 0 : 1 + x;
 }
 
-__host__ __device__ inline int jacobi_ldv(int dp) { return (dp + 3) & ~3; }
+// Leading dimensions.  A: lda = 1 (mod 16), so the 8-byte bank of entry
+// (i, j) is (i + j) mod 16 for either orientation -- the 2x2-block updates of
+// one row pair k over consecutive column pairs l touch consecutive players
+// and hit distinct banks.  Vt: ldv = 2 (mod 16), so the rows of consecutive
+// players start in consecutive 16-byte bank groups (16-byte row alignment).
+__host__ __device__ inline int jacobi_lda(int dp) { return ((dp + 15) & ~15) + 1; }
+__host__ __device__ inline int jacobi_ldv(int dp) { return ((dp + 13) & ~15) + 2; }
+
+// upper-triangle position of the symmetric entry {i, j}: during the sweeps only
+// i <= j is stored (the strict lower triangle is refreshed on exit)
+__device__ __forceinline__ int sym_at(int i, int j, int lda) {
+  return i < j ? i * lda + j : j * lda + i;
+}
 
 struct JacobiScratch {
   double *A, *Vt;
-  double2 *rot;   // [2][half] (c, s)
-  int4 *idx;      // [2][half] (p, q, p*lda, q*lda)
+  double *rc, *rs;  // [2][half] rotation cosines / sines (double buffered)
   double *tt, *lam, *red;
   int *offtab, *pos, *flag;
   int lda, ldv;
@@ -84,23 +96,23 @@ struct JacobiScratch {
 };
 
 __host__ __device__ inline int64_t jacobi_scratch_doubles(int dp) {
-  const int64_t lda = dp + 1, ldv = jacobi_ldv(dp), half = dp / 2;
+  const int64_t lda = jacobi_lda(dp), ldv = jacobi_ldv(dp), half = dp / 2;
   const int64_t noff = half * (half - 1) / 2;
   const int64_t ints = noff + dp + 1 + 2;
-  const int64_t n = dp * lda + dp * ldv + 4 * half + 4 * half + half + dp + 32 + (ints + 1) / 2 + 2;
+  const int64_t n = dp * lda + dp * ldv + 4 * half + half + dp + 32 + (ints + 1) / 2 + 2;
   return (n + 1) & ~int64_t(1);  // keep per-warp slices 16-byte aligned
 }
 
 __device__ inline JacobiScratch jacobi_carve(double *base, int dp) {
   JacobiScratch s;
   const int half = dp / 2;
-  s.lda = dp + 1;
+  s.lda = jacobi_lda(dp);
   s.ldv = jacobi_ldv(dp);
   s.A = base;
   s.Vt = s.A + dp * s.lda;  // dp even -> 16-byte aligned
-  s.rot = reinterpret_cast<double2 *>(s.Vt + dp * s.ldv);
-  s.idx = reinterpret_cast<int4 *>(s.rot + 2 * half);
-  s.tt = reinterpret_cast<double *>(s.idx + 2 * half);
+  s.rc = s.Vt + dp * s.ldv;
+  s.rs = s.rc + 2 * half;
+  s.tt = s.rs + 2 * half;
   s.lam = s.tt + half;
   s.red = s.lam + dp;
   s.offtab = reinterpret_cast<int *>(s.red + 32);
@@ -125,61 +137,75 @@ __device__ void jacobi_prepare(const Team &tm, JacobiScratch &js, int dp, bool i
     }
 }
 
+// |A|_F^2 and off(A)^2 from the upper triangle
 template <class Team>
 __device__ void jacobi_norms(const Team &tm, const JacobiScratch &js, int dp, double &norm2,
                              double &off2) {
   double a2 = 0.0, o2 = 0.0;
   for (int e = tm.rank; e < dp * dp; e += tm.size()) {
     const int i = e / dp, j = e - i * dp;
+    if (j < i) continue;
     const double a = js.A[i * js.lda + j];
-    a2 += a * a;
-    if (i != j) o2 += a * a;
+    if (i == j) {
+      a2 += a * a;
+    } else {
+      a2 += 2.0 * (a * a);
+      o2 += 2.0 * (a * a);
+    }
   }
   norm2 = team_sum(tm, a2, js.red);
   off2 = team_sum(tm, o2, js.red);
 }
 
-// apply the rotations of parameter buffer `b` to the eigenvector rows, in
-// 4-column chunks; participating threads [first, team size)
+// Apply the rotations of round r (parameter buffer b) to the eigenvector rows.
+// Item (k, c): pair k, 16-byte column chunks c and c + nh of rows p_k, q_k;
+// consecutive threads take consecutive pairs (rows of consecutive players ->
+// distinct bank groups, see jacobi_ldv).  Threads [first, team size).
 template <class Team>
-__device__ __forceinline__ void jacobi_vupdate(const Team &tm, JacobiScratch &js, int half, int nch,
-                                               int b, int first) {
+__device__ __forceinline__ void jacobi_vupdate(const Team &tm, JacobiScratch &js, int d, int dp,
+                                               int r, int b, int first) {
   const int T = tm.size() - first;
   const int me = tm.rank - first;
   if (me < 0) return;
-  const int total = half * nch;
-  const double2 *rot = js.rot + b * half;
-  const int4 *idx = js.idx + b * half;
-  // (k, ch) of item `it` advanced incrementally (no division in the loop)
-  const int dk = T / nch, dc = T - (T / nch) * nch;
-  int k = me / nch, ch = me - (me / nch) * nch;
-  for (int it = me; it < total; it += T, k += dk, ch += dc) {
-    if (ch >= nch) {
-      ch -= nch;
-      ++k;
+  const int half = dp / 2;
+  const int n2 = (d + 1) >> 1;       // 16-byte chunks per row
+  const int nh = (n2 + 1) >> 1;      // chunk pairs
+  const int total = half * nh;
+  const double *rc = js.rc + b * half, *rs = js.rs + b * half;
+  const int dk = T % half, dc = T / half;
+  int c = me / half, k = me - (me / half) * half;
+  for (int it = me; it < total; it += T, k += dk, c += dc) {
+    if (k >= half) {
+      k -= half;
+      ++c;
     }
-    const double2 cs = rot[k];
-    if (cs.y == 0.0) continue;
-    const int4 pq = idx[k];
-    double2 *vp = reinterpret_cast<double2 *>(js.Vt + pq.x * js.ldv + 4 * ch);
-    double2 *vq = reinterpret_cast<double2 *>(js.Vt + pq.y * js.ldv + 4 * ch);
-    const double2 p0 = vp[0], p1 = vp[1], q0 = vq[0], q1 = vq[1];
-    vp[0] = make_double2(cs.x * p0.x - cs.y * q0.x, cs.x * p0.y - cs.y * q0.y);
-    vp[1] = make_double2(cs.x * p1.x - cs.y * q1.x, cs.x * p1.y - cs.y * q1.y);
-    vq[0] = make_double2(cs.y * p0.x + cs.x * q0.x, cs.y * p0.y + cs.x * q0.y);
-    vq[1] = make_double2(cs.y * p1.x + cs.x * q1.x, cs.y * p1.y + cs.x * q1.y);
+    const double sn = rs[k];
+    if (sn == 0.0) continue;
+    const double cs = rc[k];
+    const int p = tour_player(k, r, dp), q = tour_player(dp - 1 - k, r, dp);
+    double2 *vp = reinterpret_cast<double2 *>(js.Vt + p * js.ldv);
+    double2 *vq = reinterpret_cast<double2 *>(js.Vt + q * js.ldv);
+    const bool two = c + nh < n2;
+    const double2 p0 = vp[c], q0 = vq[c];
+    const double2 p1 = two ? vp[c + nh] : p0, q1 = two ? vq[c + nh] : q0;
+    vp[c] = make_double2(cs * p0.x - sn * q0.x, cs * p0.y - sn * q0.y);
+    vq[c] = make_double2(sn * p0.x + cs * q0.x, sn * p0.y + cs * q0.y);
+    if (two) {
+      vp[c + nh] = make_double2(cs * p1.x - sn * q1.x, cs * p1.y - sn * q1.y);
+      vq[c + nh] = make_double2(sn * p1.x + cs * q1.x, sn * p1.y + cs * q1.y);
+    }
   }
 }
 
 // Cyclic Jacobi on the symmetric A (dp x dp, padded); rotations accumulate
-// into the rows of Vt.  Returns the number of sweeps performed.
+// into the rows of Vt.  Only the upper triangle is maintained during the
+// sweeps; the full symmetric A (diagonal = eigenvalues, off-diagonal = the
+// remainder) is restored on exit.  Returns the number of sweeps performed.
 template <class Team>
 __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
-                             bool *first_order = nullptr, double switch_rel = 0.0,
-                             bool *switched = nullptr) {
+                             bool *first_order = nullptr) {
   double *A = js.A;
   const int lda = js.lda, half = dp / 2, noff = half * (half - 1) / 2;
-  const int nch = (d + 3) >> 2;
   const int T = tm.size();
   // threads that only update eigenvectors during phase P (block teams)
   const int vfirst = (T > 32 && T - ((half + 31) & ~31) >= 64) ? ((half + 31) & ~31) : 0;
@@ -192,26 +218,21 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
   // first-order exit: off <= 1e-12 |A|_F (see psd_rebuild_first_order)
   const double fo2 = norm2 * 1e-24;
   if (first_order) *first_order = false;
-  if (switched) *switched = false;
-  const double sw2 = norm2 * switch_rel * switch_rel;
   for (; sweep < kMaxSweeps; ++sweep) {
     if (!(off2 > stop2)) break;  // also stops on NaN
     if (first_order && off2 <= fo2) {
       *first_order = true;
       break;
     }
-    if (switched && off2 <= sw2) {  // hand over to the refinement
-      *switched = true;
-      break;
-    }
     if (tm.rank == 0) js.flag[0] = 0;
     tm.sync();
     for (int r = 0; r < dp - 1; ++r, ++round) {
       const int b = round & 1;
+      double *rc = js.rc + b * half, *rs = js.rs + b * half;
       // ---- phase P: parameters of round r | eigenvector update of round r-1
       for (int k = tm.rank; k < half; k += T) {
         const int p = tour_player(k, r, dp), q = tour_player(dp - 1 - k, r, dp);
-        const double apq = A[p * lda + q];
+        const double apq = A[sym_at(p, q, lda)];
         double c = 1.0, s = 0.0, t = 0.0;
         if (fabs(apq) > thr) {
           const double diff = A[q * lda + q] - A[p * lda + p];
@@ -222,41 +243,41 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
           s = t * c;
           js.flag[0] = 1;
         }
-        js.rot[b * half + k] = make_double2(c, s);
-        js.idx[b * half + k] = make_int4(p, q, p * lda, q * lda);
+        rc[k] = c;
+        rs[k] = s;
         js.tt[k] = t;
       }
-      if (pending) jacobi_vupdate(tm, js, half, nch, b ^ 1, vfirst);
+      if (pending) jacobi_vupdate(tm, js, d, dp, r == 0 ? dp - 2 : r - 1, b ^ 1, vfirst);
       tm.sync();
-      // ---- phase A: off-diagonal 2x2 blocks and the diagonal blocks
-      const double2 *rot = js.rot + b * half;
-      const int4 *idx = js.idx + b * half;
+      // ---- phase A: off-diagonal 2x2 blocks (upper triangle), then the
+      // diagonal blocks
       for (int it = tm.rank; it < noff; it += T) {
         const int kl = js.offtab[it];
         const int k = kl & 0xffff, l = kl >> 16;
-        const double2 rk = rot[k], rl = rot[l];
-        if (rk.y == 0.0 && rl.y == 0.0) continue;
-        const int4 ik = idx[k], il = idx[l];
-        const double a = A[ik.z + il.x], bb = A[ik.z + il.y];
-        const double cc = A[ik.w + il.x], ee = A[ik.w + il.y];
-        const double r_pp = rk.x * a - rk.y * cc, r_pq = rk.x * bb - rk.y * ee;
-        const double r_qp = rk.y * a + rk.x * cc, r_qq = rk.y * bb + rk.x * ee;
-        const double n_pp = rl.x * r_pp - rl.y * r_pq, n_pq = rl.y * r_pp + rl.x * r_pq;
-        const double n_qp = rl.x * r_qp - rl.y * r_qq, n_qq = rl.y * r_qp + rl.x * r_qq;
-        A[ik.z + il.x] = n_pp; A[il.z + ik.x] = n_pp;
-        A[ik.z + il.y] = n_pq; A[il.w + ik.x] = n_pq;
-        A[ik.w + il.x] = n_qp; A[il.z + ik.y] = n_qp;
-        A[ik.w + il.y] = n_qq; A[il.w + ik.y] = n_qq;
+        const double sk = rs[k], sl = rs[l];
+        if (sk == 0.0 && sl == 0.0) continue;
+        const double ck = rc[k], cl = rc[l];
+        const int pk = tour_player(k, r, dp), qk = tour_player(dp - 1 - k, r, dp);
+        const int pl = tour_player(l, r, dp), ql = tour_player(dp - 1 - l, r, dp);
+        const int i_pp = sym_at(pk, pl, lda), i_pq = sym_at(pk, ql, lda);
+        const int i_qp = sym_at(qk, pl, lda), i_qq = sym_at(qk, ql, lda);
+        const double a = A[i_pp], bb = A[i_pq], cc = A[i_qp], ee = A[i_qq];
+        const double r_pp = ck * a - sk * cc, r_pq = ck * bb - sk * ee;
+        const double r_qp = sk * a + ck * cc, r_qq = sk * bb + ck * ee;
+        A[i_pp] = cl * r_pp - sl * r_pq;
+        A[i_pq] = sl * r_pp + cl * r_pq;
+        A[i_qp] = cl * r_qp - sl * r_qq;
+        A[i_qq] = sl * r_qp + cl * r_qq;
       }
       for (int k = tm.rank; k < half; k += T) {
         const double t = js.tt[k];
         if (t == 0.0) continue;
-        const int4 ik = idx[k];
-        const double apq = A[ik.z + ik.y];
-        A[ik.z + ik.x] -= t * apq;
-        A[ik.w + ik.y] += t * apq;
-        A[ik.z + ik.y] = 0.0;
-        A[ik.w + ik.x] = 0.0;
+        const int p = tour_player(k, r, dp), q = tour_player(dp - 1 - k, r, dp);
+        const int ipq = sym_at(p, q, lda);
+        const double apq = A[ipq];
+        A[p * lda + p] -= t * apq;
+        A[q * lda + q] += t * apq;
+        A[ipq] = 0.0;
       }
       pending = true;
       tm.sync();
@@ -270,10 +291,13 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
       break;  // every pair below the rotation threshold
     }
   }
-  if (pending) {
-    jacobi_vupdate(tm, js, half, nch, (round - 1) & 1, 0);
-    tm.sync();
+  if (pending) jacobi_vupdate(tm, js, d, dp, (round - 1) % (dp - 1), (round - 1) & 1, 0);
+  // restore the strict lower triangle
+  for (int e = tm.rank; e < dp * dp; e += T) {
+    const int i = e / dp, j = e - i * dp;
+    if (j < i) A[i * lda + j] = A[j * lda + i];
   }
+  tm.sync();
   return sweep;
 }
 
@@ -534,7 +558,6 @@ struct ConeArgs {
   double *out;      // PLAIN: stacked output; MINEIG: per-clique min eigenvalue [p]
   double in_scale;
   int warm;         // HOT: use / refresh the per-clique eigenvector store
-  int refine;       // HOT, CTA teams: hand warm cliques to k_cone_refine at 1e-4
 };
 
 // Hot-path load of slot j: builds arg_s and performs the v / w_v update and
@@ -649,25 +672,10 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
     tm.sync();
   }
   // first-order exit for CTA teams whose GEMM tiles fit (not for MINEIG)
-  bool first_order = false, switched = false;
+  bool first_order = false;
   const bool fo_ok = MODE != CONE_MINEIG && tm.size() > 32 &&
                      ((d + 3) >> 2) * ((d + 3) >> 2) <= tm.size();
-  const bool handoff_ok = MODE == CONE_HOT && warm && ca.refine;
-  const int sw = jacobi_sweeps(tm, js, d, dp, fo_ok ? &first_order : nullptr,
-                               handoff_ok ? 1e-4 : 0.0, handoff_ok ? &switched : nullptr);
-  if (MODE == CONE_HOT && ca.refine && tm.rank == 0) W.handoff[k] = switched ? 1 : 0;
-  if (switched) {
-    // stage 2 (k_cone_refine) finishes: basis to the store, w_s holds -arg_s
-    for (int e = tm.rank; e < d * d; e += tm.size()) {
-      const int a = e / d, bcol = e - a * d;
-      W.vstore[off + e] = js.Vt[a * ldv + bcol];
-    }
-    if (tm.rank == 0) {
-      W.vvalid[k] = age + 1;
-      if (W.sweeps) W.sweeps[k] = sw;
-    }
-    return;
-  }
+  const int sw = jacobi_sweeps(tm, js, d, dp, fo_ok ? &first_order : nullptr);
   if (MODE == CONE_HOT && tm.rank == 0 && W.sweeps) W.sweeps[k] = sw;
   // non-finite eigenvalue -> EigenFailure (symmat.py:162-163)
   double nb = 0.0;
@@ -726,289 +734,4 @@ __global__ void __launch_bounds__(kConeBlock, 2) k_cone_block(DevProblem P, DevS
   if ((int)blockIdx.x >= ca.count) return;
   BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
   cone_one<MODE>(tm, P, S, W, ca, ca.ids[blockIdx.x], smem);
-}
-
-// ---------------------------------------------------------------------------
-// Warm-started refinement of the eigenbasis (CTA teams, hot path).
-//
-// Iterative refinement for the symmetric eigendecomposition (Ogita & Aishima,
-// "Iterative refinement for symmetric eigenvalue decomposition", 2018):
-// from an approximate eigenbasis Xh (here: the previous ADMM iteration's),
-//   G = Xh'Xh, S = Xh' X Xh, lam_k = S_kk / G_kk, R = I - G,
-//   E_kl = (S_kl + lam_l R_kl) / (lam_l - lam_k)   if |lam_k - lam_l| > dlt
-//        = R_kl / 2                                 otherwise (cluster), E_kk = R_kk / 2
-//   Xh <- Xh + Xh E
-// converges quadratically; every step is four d x d GEMMs (register-tiled, fp64
-// FFMA), no barrier-bound rotation rounds.  At convergence the projection is
-// P = Xh M Xh' with M = diag(lam+) + [S_kl dd(lam_k, lam_l)] (divided
-// differences of max(., 0): exact within clusters of one sign, the
-// off-diagonal remainder |S_kl| <= 1e-12 |X| elsewhere).  Not converged within
-// kRefineMax steps -> cold cyclic Jacobi on the same block.
-
-constexpr int kRefineMax = 8;
-
-template <class Team>
-__device__ double team_max(const Team &tm, double v, double *red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if (tm.size() <= 32) return v;
-  const int lane = tm.rank & 31, wid = tm.rank >> 5;
-  tm.sync();
-  if (lane == 0) red[wid] = v;
-  tm.sync();
-  double r = 0.0;
-  const int nw = (tm.size() + 31) >> 5;
-  for (int i = 0; i < nw; ++i) r = fmax(r, red[i]);
-  tm.sync();
-  return r;
-}
-
-// acc[i][j] = sum_k opL[i][k] opR[k][j] (opL = TL ? L' : L, opR = TR ? R' : R),
-// 4x4 interleaved register tiles; epi(i, j, acc) after a team barrier.
-template <bool TL, bool TR, class Team, class Epi>
-__device__ void team_gemm(const Team &tm, const double *L, int ldl, const double *R, int ldr, int d,
-                          Epi epi) {
-  const int nt = (d + 3) >> 2;
-  const int t = tm.rank;
-  const bool active = t < nt * nt;
-  const int u = active ? t / nt : 0, v = active ? t - u * nt : 0;
-  double acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  if (active) {
-    int ci[4], cj[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      ci[a] = min(u + nt * a, d - 1);
-      cj[a] = min(v + nt * a, d - 1);
-    }
-#pragma unroll 4
-    for (int k = 0; k < d; ++k) {
-      double l[4], r[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        l[a] = TL ? L[k * ldl + ci[a]] : L[ci[a] * ldl + k];
-        r[a] = TR ? R[cj[a] * ldr + k] : R[k * ldr + cj[a]];
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(l[a], r[b], acc[a][b]);
-    }
-  }
-  tm.sync();
-  if (active) {
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int i = u + nt * a, j = v + nt * b;
-        if (i < d && j < d) epi(i, j, acc[a][b]);
-      }
-  }
-  tm.sync();
-}
-
-
-// one CTA per clique: warm-started Jacobi sweeps down to 1e-4 |A|, then the
-// quadratically convergent refinement; cold Jacobi on failure.
-__host__ __device__ inline int64_t hybrid_scratch_doubles(int dp) {
-  const int64_t lda = dp + 1, ldv = jacobi_ldv(dp);
-  const int64_t half = dp / 2, noff = half * (half - 1) / 2;
-  const int64_t tables = 8 * half + half + dp + 32 + (noff + dp + 3 + 1) / 2 + 2;
-  const int64_t rt = dp * lda > tables ? dp * lda : tables;
-  return dp * lda + dp * lda + dp * (ldv > lda ? ldv : lda) + rt + dp + 32 + 8;
-}
-
-// Stage 2 of the hot CTA path: cliques handed over by stage-1 Jacobi
-// (off <= 1e-4 |A|) are finished by the refinement; X is re-read from w_s
-// (= -arg_s after the stage-1 load), the basis from the store.
-__global__ void __launch_bounds__(kConeBlock, 1) k_cone_refine(DevProblem P, DevState S, DevWork W,
-                                                               ConeArgs ca) {
-  extern __shared__ __align__(16) double smem[];
-  if ((int)blockIdx.x >= ca.count) return;
-  const int k = ca.ids[blockIdx.x];
-  if (!W.handoff[k]) return;
-  BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
-  const int T = tm.size();
-  const int d = P.cl_size[k];
-  const int64_t off = P.cl_off[k];
-  const int64_t so = P.n_c;
-  const int dp = d + (d & 1), lda = dp + 1, ldv = jacobi_ldv(dp);
-  const int half = dp / 2;
-  // regions: X | RA (Xt / Jacobi A) | RV (B2 / Jacobi Vt) | RT (B3 / tables) | lam, red
-  double *X = smem, *RA = X + dp * lda, *RV = RA + dp * lda;
-  double *RT = RV + dp * (ldv > lda ? ldv : lda);
-  const int64_t tables = 8 * half + half + dp + 32 + (half * (half - 1) / 2 + dp + 3 + 1) / 2 + 2;
-  double *lam = RT + (dp * lda > tables ? dp * lda : tables), *red = lam + dp;
-  for (int e = tm.rank; e < d * d; e += T) {
-    const int a = e / d, b = e - a * d;
-    X[a * lda + b] = -S.w[so + off + e];
-    RA[a * lda + b] = W.vstore[off + e];
-  }
-  if (d & 1)
-    for (int e = tm.rank; e < dp; e += T) {
-      X[d * lda + e] = 0.0;
-      X[e * lda + d] = 0.0;
-    }
-  tm.sync();
-  for (int e = tm.rank; e < d * d; e += T) {  // sym = 0.5 (B + B')  (symmat.py:157)
-    const int a = e / d, b = e - a * d;
-    if (a < b) {
-      const double s = 0.5 * (X[a * lda + b] + X[b * lda + a]);
-      X[a * lda + b] = s;
-      X[b * lda + a] = s;
-    }
-  }
-  tm.sync();
-  double loc = 0.0;
-  for (int e = tm.rank; e < d * d; e += T) {
-    const int a = e / d, b = e - a * d;
-    loc += X[a * lda + b] * X[a * lda + b];
-  }
-  const double xnorm = sqrt(team_sum(tm, loc, red));
-  auto emit_val = [&](int a, int b, double v) {
-    const int64_t j = so + off + (int64_t)a * d + b;
-    S.u[j] = v;
-    S.w[j] += v;
-  };
-  bool refined = false;
-  int steps = 0;
-  double *Xt = RA, *B2 = RV, *B3 = RT;
-  {
-    for (; steps < kRefineMax; ++steps) {
-      team_gemm<false, true>(tm, X, lda, Xt, lda, d, [&](int i, int j, double a) { B2[i * lda + j] = a; });
-      team_gemm<false, false>(tm, Xt, lda, B2, lda, d, [&](int i, int j, double a) { B3[i * lda + j] = a; });
-      team_gemm<false, true>(tm, Xt, lda, Xt, lda, d, [&](int i, int j, double a) { B2[i * lda + j] = a; });
-      for (int i = tm.rank; i < d; i += T) lam[i] = B3[i * lda + i] / B2[i * lda + i];
-      tm.sync();
-      double s2 = 0.0, r2 = 0.0, orth = 0.0;
-      for (int e = tm.rank; e < d * d; e += T) {
-        const int i = e / d, j = e - i * d;
-        const double g = B2[i * lda + j] - (i == j ? 1.0 : 0.0);
-        const double s = i == j ? B3[i * lda + i] - lam[i] : B3[i * lda + j];
-        s2 += s * s;
-        r2 += g * g;
-        orth = fmax(orth, fabs(g));
-      }
-      s2 = team_sum(tm, s2, red);
-      r2 = team_sum(tm, r2, red);
-      orth = team_max(tm, orth, red);
-      const double dlt = 2.0 * (sqrt(s2) + xnorm * sqrt(r2));
-      // separated pairs: |S_kl| must vanish (first-order M error S^2 / gap);
-      // clustered pairs of one sign are exact in M whatever S_kl; clustered
-      // pairs of opposite signs have |lam| <= dlt and must be negligible
-      double offs = 0.0, offz = 0.0;
-      for (int e = tm.rank; e < d * d; e += T) {
-        const int i = e / d, j = e - i * d;
-        if (i == j) continue;
-        if (fabs(lam[i] - lam[j]) > dlt) {
-          offs = fmax(offs, fabs(B3[i * lda + j]));
-        } else if ((lam[i] > 0.0) != (lam[j] > 0.0)) {
-          offz = fmax(offz, fmax(fabs(B3[i * lda + j]), fmax(fabs(lam[i]), fabs(lam[j]))));
-        }
-      }
-      offs = team_max(tm, offs, red);
-      offz = team_max(tm, offz, red);
-      if (W.dbg && k == W.dbg_clique && tm.rank == 0 && steps < 15) {
-        W.dbg[0] = -2.0;
-        W.dbg[1 + 4 * steps] = offs / xnorm;
-        W.dbg[2 + 4 * steps] = orth;
-        W.dbg[3 + 4 * steps] = dlt / xnorm;
-        W.dbg[4 + 4 * steps] = offz / xnorm;
-      }
-      if (!(offs == offs) || !(orth == orth) || !(dlt == dlt)) break;  // NaN -> Jacobi
-      if (offs <= 1e-12 * xnorm && offz <= 1e-10 * xnorm && orth <= 1e-12) {
-        refined = true;
-        break;
-      }
-      if (dlt > 1e-2 * xnorm) break;  // not in the refinement regime
-      for (int e = tm.rank; e < d * d; e += T) {
-        const int i = e / d, j = e - i * d;
-        const double r = (i == j ? 1.0 : 0.0) - B2[i * lda + j];
-        double ev;
-        if (i == j) ev = 0.5 * r;
-        else if (fabs(lam[i] - lam[j]) > dlt)
-          ev = (B3[i * lda + j] + lam[j] * r) / (lam[j] - lam[i]);
-        else
-          ev = 0.5 * r;
-        B2[i * lda + j] = ev;
-      }
-      tm.sync();
-      team_gemm<true, false>(tm, B2, lda, Xt, lda, d, [&](int i, int j, double a) { Xt[i * lda + j] += a; });
-    }
-  }
-  double nb = 0.0;
-  if (refined) {
-    // M = diag(lam+) + [S_kl dd(lam_k, lam_l)] (B3), T = M Xt (B2), P = Xt' T
-    for (int e = tm.rank; e < d * d; e += T) {
-      const int i = e / d, j = e - i * d;
-      const double li = lam[i], lj = lam[j];
-      double m;
-      if (i == j) {
-        m = li > 0.0 ? li : 0.0;
-      } else {
-        double dd;
-        if (li > 0.0 && lj > 0.0) dd = 1.0;
-        else if (li <= 0.0 && lj <= 0.0) dd = 0.0;
-        else dd = (fmax(li, 0.0) - fmax(lj, 0.0)) / (li - lj);
-        m = B3[i * lda + j] * dd;
-      }
-      B3[i * lda + j] = m;
-    }
-    for (int i = tm.rank; i < d; i += T) nb += isfinite(lam[i]) ? 0.0 : 1.0;
-    tm.sync();
-    team_gemm<false, false>(tm, B3, lda, Xt, lda, d, [&](int i, int j, double a) { B2[i * lda + j] = a; });
-    team_gemm_tn_sym(tm, Xt, lda, B2, lda, nullptr, d, d, [&](int i, int j, double v) {
-      emit_val(i, j, v);
-      if (i != j) emit_val(j, i, v);
-    });
-    for (int e = tm.rank; e < d * d; e += T) {
-      const int a = e / d, b = e - a * d;
-      W.vstore[off + e] = Xt[a * lda + b];
-    }
-    if (tm.rank == 0 && W.sweeps) W.sweeps[k] = 100 * (W.sweeps[k] + 1) + steps;
-  } else {
-    // refinement failed: cold cyclic Jacobi from X in this CTA
-    JacobiScratch js;
-    js.lda = lda;
-    js.ldv = ldv;
-    js.A = RA;
-    js.Vt = RV;
-    js.rot = reinterpret_cast<double2 *>(RT);
-    js.idx = reinterpret_cast<int4 *>(js.rot + 2 * half);
-    js.tt = reinterpret_cast<double *>(js.idx + 2 * half);
-    js.lam = js.tt + half;
-    js.red = js.lam + dp;
-    js.offtab = reinterpret_cast<int *>(js.red + 32);
-    js.pos = js.offtab + half * (half - 1) / 2;
-    js.flag = js.pos + dp + 1;
-    js.dbg = nullptr;
-    jacobi_prepare(tm, js, dp, true);
-    for (int e = tm.rank; e < dp * dp; e += T) {
-      const int a = e / dp, b = e - a * dp;
-      RA[a * lda + b] = X[a * lda + b];
-    }
-    tm.sync();
-    bool first_order = false;
-    const int sw = jacobi_sweeps(tm, js, d, dp, &first_order);
-    for (int i = tm.rank; i < d; i += T) nb += isfinite(js.A[i * lda + i]) ? 0.0 : 1.0;
-    for (int e = tm.rank; e < d * d; e += T) {
-      const int a = e / d, b = e - a * d;
-      W.vstore[off + e] = js.Vt[a * ldv + b];
-    }
-    if (first_order) psd_rebuild_first_order(tm, js, d, emit_val);
-    else psd_rebuild(tm, js, d, emit_val);
-    if (tm.rank == 0) {
-      if (W.sweeps) W.sweeps[k] += sw;
-      W.vvalid[k] = 1;
-    }
-  }
-  const bool bad = team_sum(tm, nb, red) > 0.0;
-  if (bad && tm.rank == 0) {
-    W.vvalid[k] = 0;
-    atomicOr(W.err, 1);
-  }
 }

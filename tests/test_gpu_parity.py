@@ -295,19 +295,32 @@ def test_warm_started_eigensolves_match_cold_and_oracle():
     assert rel(res[0][0], ref["u"]) <= 1e-8
 
 
-def test_refinement_path_matches_jacobi():
-    """HSDE_FLAG_REFINE (Jacobi to 1e-4 + Ogita-Aishima refinement) vs the default
-    warm Jacobi after 150 iterations of d = 40 cliques."""
-    from paper_1611_01828_b200 import _lib
-    from paper_1611_01828_b200.synthetic import block_arrow
+def test_project_cone_clique_orders():
+    """PSD projection of random symmetric blocks over the clique orders the two
+    Jacobi teams cover (warp d <= 32, CTA d > 32, odd and even, up to the
+    shared-memory limit) against numpy's eigh projection (symmat.py:153-165)."""
+    import scipy.sparse as sp
 
-    cp = block_arrow(12, 24, 16, 50, 0.05, 7, "ctapath")
-    res = []
-    for flags in (0, _lib.HSDE_FLAG_REFINE):
-        h = _lib.Handle(cp, flags=flags)
-        h.iterate(150)
-        res.append(h.get_state()[0])
-        if flags:
-            assert h.stats()["refined_fraction"] > 0.0
-        h.close()
-    assert rel(res[1], res[0]) <= 1e-9
+    from paper_1611_01828_b200.problem import CliqueDecomposition, DecomposedProblem
+
+    sizes = [2, 3, 7, 16, 17, 31, 32, 33, 40, 47, 64, 80, 81, 96, 113]
+    n = sum(sizes)
+    cl, o = [], 0
+    for d in sizes:
+        cl.append(list(range(o, o + d)))
+        o += d
+    dec = CliqueDecomposition.build(n, cl)
+    A = sp.csr_matrix(([1.0], ([0], [0])), shape=(1, n * n))
+    dp = DecomposedProblem(n=n, m=1, c=np.eye(n).ravel(), A=A, b=np.ones(1), dec=dec,
+                           block_dims=(n,))
+    _, layout = H.build_hsde(dp)
+    rng = np.random.default_rng(5)
+    u = rng.normal(size=layout.total)
+    got = H.project_cone(u, layout)
+    s_in, s_out = u[layout.sl_s], got[layout.sl_s]
+    for k, d in enumerate(sizes):
+        o0, o1 = dec.offsets[k], dec.offsets[k + 1]
+        b = s_in[o0:o1].reshape(d, d)
+        w, v = np.linalg.eigh(0.5 * (b + b.T))
+        want = (v * np.maximum(w, 0.0)) @ v.T
+        assert rel(s_out[o0:o1], want.ravel()) <= 1e-12, d
