@@ -10,8 +10,8 @@ from .errors import EigenFailure, FactorizationFailure, TauZero
 from .problem import (CliqueDecomposition, CompressedProblem, DecomposedProblem, compress,
                       expand_to_mirror)
 from .report import (STATUS_DUAL_INFEASIBLE, STATUS_MAX_ITERS, STATUS_OPTIMAL,
-                     STATUS_PRIMAL_INFEASIBLE, ProblemStats, Residuals, SolverReport, Timing,
-                     emit_report, read_report)
+                     STATUS_PRIMAL_INFEASIBLE, PatternEntries, ProblemStats, Residuals,
+                     SolverReport, Timing, emit_report, read_report)
 from .solver import (HsdeState, IterationInfo, KktCache, QOperator, SolverSettings,
                      VariableLayout, affine_project, build_hsde, initial_state, iterate,
                      project_cone, recover, residuals, setup_cache, solve_decomposed,
@@ -22,7 +22,7 @@ __version__ = "0.1.0"
 __all__ = [
     "CliqueDecomposition", "CompressedProblem", "DecomposedProblem", "EigenFailure",
     "FactorizationFailure", "HsdeState", "IterationInfo", "KktCache", "ProblemStats",
-    "QOperator", "Residuals", "STATUS_DUAL_INFEASIBLE", "STATUS_MAX_ITERS", "STATUS_OPTIMAL",
+    "PatternEntries", "QOperator", "Residuals", "STATUS_DUAL_INFEASIBLE", "STATUS_MAX_ITERS", "STATUS_OPTIMAL",
     "STATUS_PRIMAL_INFEASIBLE", "SolverReport", "SolverSettings", "TauZero", "Timing",
     "VariableLayout", "affine_project", "build_hsde", "compress", "emit_report",
     "expand_to_mirror", "initial_state", "iterate", "project_cone", "read_report", "recover",

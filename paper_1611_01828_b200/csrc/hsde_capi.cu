@@ -25,7 +25,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <limits>
@@ -35,11 +37,28 @@
 #include "../../include/hsde.h"
 #include "hsde_kernels.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 using namespace hsde;
 
 namespace {
 
 std::string g_create_error;
+
+// HSDE_TIMING=1: setup phase times on stderr (device synchronised per phase)
+struct SetupTimer {
+  bool on = std::getenv("HSDE_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void operator()(const char *what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hsde setup] %-18s %8.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
 
 enum ProfSlot {
   PS_PREP = 0, PS_RHS, PS_SPMV, PS_SCHUR, PS_UA, PS_SCALARS, PS_CONE_WARP, PS_CONE_BLOCK,
@@ -813,43 +832,159 @@ int validate(hsde_handle *h, const hsde_problem_desc *d) {
 }
 
 // upload shard data (everything that does not depend on normalisation)
+// ---- device construction of the CSC of A (rows ascending within a column)
+__global__ void k_row_of(const int64_t *rp, int m, int *row_of) {
+  for (int i = blockIdx.x; i < m; i += gridDim.x)
+    for (int64_t k = rp[i] + threadIdx.x; k < rp[i + 1]; k += blockDim.x) row_of[k] = i;
+}
+
+__global__ void k_iota(int *x, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    x[k] = (int)k;
+}
+
+__global__ void k_col_count(const int *col, int64_t nnz, unsigned long long *cnt) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + col[k] + 1, 1ull);  // integer counts: order-independent
+}
+
+__global__ void k_csc_gather(const int *perm, const int *row_of, const double *val, int64_t nnz,
+                             int *at_row, double *at_val) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int e = perm[k];
+    at_row[k] = row_of[e];
+    at_val[k] = val[e];
+  }
+}
+
+__global__ void k_maxcol(const int64_t *cp, int n_c, const unsigned char *owned,
+                         unsigned long long *mx) {
+  unsigned long long best = 0;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_c; c += gridDim.x * blockDim.x)
+    if (!owned || owned[c]) best = max(best, (unsigned long long)(cp[c + 1] - cp[c]));
+  atomicMax(mx, best);
+}
+
+int build_csc_device(hsde_handle *h, int m, int n_c, int64_t nnz, const int64_t *rp, const int *col,
+                     const double *val, int64_t **at_cp, int **at_row, double **at_val) {
+  RC(dalloc(h, at_cp, n_c + 1));
+  RC(dalloc(h, at_row, nnz));
+  RC(dalloc(h, at_val, nnz));
+  unsigned long long *cnt = reinterpret_cast<unsigned long long *>(*at_cp);
+  CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (n_c + 1), h->st));
+  if (nnz == 0) return 0;
+  if (nnz > INT32_MAX) {
+    h->err = "nnz(A) above 2^31 is not supported";
+    return HSDE_ERR_ARG;
+  }
+  const int g = 148 * 8;
+  k_col_count<<<g, kBlock, 0, h->st>>>(col, nnz, cnt);
+  CKL();
+  size_t tb = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, cnt, cnt, n_c + 1, h->st);
+  int *row_of = nullptr, *idx = nullptr, *perm = nullptr, *keys_out = nullptr;
+  void *tmp = nullptr;
+  size_t tb2 = 0;
+  int end_bit = 1;
+  while ((1ll << end_bit) < (long long)n_c) ++end_bit;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb2, col, keys_out, idx, perm, (int)nnz, 0, end_bit, h->st);
+  CK(cudaMalloc(&tmp, std::max(tb, tb2)));
+  CK(cudaMalloc(&row_of, sizeof(int) * nnz));
+  CK(cudaMalloc(&idx, sizeof(int) * nnz));
+  CK(cudaMalloc(&perm, sizeof(int) * nnz));
+  CK(cudaMalloc(&keys_out, sizeof(int) * nnz));
+  cub::DeviceScan::InclusiveSum(tmp, tb, cnt, cnt, n_c + 1, h->st);
+  k_row_of<<<std::min(m, 148 * 8), kBlock, 0, h->st>>>(rp, m, row_of);
+  k_iota<<<g, kBlock, 0, h->st>>>(idx, nnz);
+  CKL();
+  // stable: equal columns keep CSR (row-ascending) order
+  cub::DeviceRadixSort::SortPairs(tmp, tb2, col, keys_out, idx, perm, (int)nnz, 0, end_bit, h->st);
+  k_csc_gather<<<g, kBlock, 0, h->st>>>(perm, row_of, val, nnz, *at_row, *at_val);
+  CKL();
+  CK(cudaStreamSynchronize(h->st));
+  cudaFree(tmp);
+  cudaFree(row_of);
+  cudaFree(idx);
+  cudaFree(perm);
+  cudaFree(keys_out);
+  return 0;
+}
+
 int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
+  SetupTimer tick;
   const int m = d->m, n_c = d->n_c, p = d->p;
   const int64_t n_d = d->n_d, nnz = d->nnz;
   std::vector<unsigned char> owned(n_c, 1);
   if (d->owned)
     for (int c = 0; c < n_c; ++c) owned[c] = d->owned[c] ? 1 : 0;
-  // CSC (transpose) by counting sort; rows ascending within a column
-  std::vector<int64_t> at_cp(n_c + 1, 0);
-  for (int64_t k = 0; k < nnz; ++k) at_cp[d->a_col[k] + 1]++;
-  for (int c = 0; c < n_c; ++c) at_cp[c + 1] += at_cp[c];
-  std::vector<int> at_row(nnz);
-  std::vector<double> at_val(nnz);
-  {
-    std::vector<int64_t> pos(at_cp.begin(), at_cp.end() - 1);
-    for (int i = 0; i < m; ++i)
-      for (int64_t k = d->a_row_ptr[i]; k < d->a_row_ptr[i + 1]; ++k) {
-        const int64_t q = pos[d->a_col[k]]++;
-        at_row[q] = i;
-        at_val[q] = d->a_val[k];
-      }
-  }
-  for (int c = 0; c < n_c; ++c)
-    if (owned[c]) s.maxcol = std::max(s.maxcol, at_cp[c + 1] - at_cp[c]);
-  // CSR over owned columns (the only columns this shard adds into A t)
+  // A on the device: the CSR as given (all columns on a single shard, the
+  // owned columns of a shard), then the CSC by a stable device radix sort
+  int64_t *a_rp = nullptr, *at_cp_d = nullptr;
+  int *a_col = nullptr, *at_row_d = nullptr;
+  double *a_val = nullptr, *at_val_d = nullptr;
   std::vector<int64_t> rp(m + 1, 0);
-  std::vector<int> col;
-  std::vector<double> val;
-  col.reserve(nnz);
-  val.reserve(nnz);
-  for (int i = 0; i < m; ++i) {
-    for (int64_t k = d->a_row_ptr[i]; k < d->a_row_ptr[i + 1]; ++k)
-      if (owned[d->a_col[k]]) {
-        col.push_back(d->a_col[k]);
-        val.push_back(d->a_val[k]);
-      }
-    rp[i + 1] = (int64_t)col.size();
+  if (!d->owned) {
+    rp.assign(d->a_row_ptr, d->a_row_ptr + m + 1);
+    RC(dupload(h, &a_rp, d->a_row_ptr, m + 1));
+    RC(dupload(h, &a_col, d->a_col, nnz));
+    RC(dupload(h, &a_val, d->a_val, nnz));
+    RC(build_csc_device(h, m, n_c, nnz, a_rp, a_col, a_val, &at_cp_d, &at_row_d, &at_val_d));
+  } else {
+    // CSC over all local columns (A' g is needed on every local coordinate)
+    int64_t *f_rp = nullptr;
+    int *f_col = nullptr;
+    double *f_val = nullptr;
+    CK(cudaMalloc(&f_rp, sizeof(int64_t) * (m + 1)));
+    CK(cudaMalloc(&f_col, sizeof(int) * std::max<int64_t>(nnz, 1)));
+    CK(cudaMalloc(&f_val, sizeof(double) * std::max<int64_t>(nnz, 1)));
+    CK(cudaMemcpy(f_rp, d->a_row_ptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(f_col, d->a_col, sizeof(int) * nnz, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(f_val, d->a_val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+    const int rc = build_csc_device(h, m, n_c, nnz, f_rp, f_col, f_val, &at_cp_d, &at_row_d, &at_val_d);
+    cudaFree(f_rp);
+    cudaFree(f_col);
+    cudaFree(f_val);
+    RC(rc);
+    // CSR over the owned columns (the only columns this shard adds into A t)
+    std::vector<int> col;
+    std::vector<double> val;
+    col.reserve(nnz);
+    val.reserve(nnz);
+    for (int i = 0; i < m; ++i) {
+      for (int64_t k = d->a_row_ptr[i]; k < d->a_row_ptr[i + 1]; ++k)
+        if (owned[d->a_col[k]]) {
+          col.push_back(d->a_col[k]);
+          val.push_back(d->a_val[k]);
+        }
+      rp[i + 1] = (int64_t)col.size();
+    }
+    RC(dupload(h, &a_rp, rp.data(), m + 1));
+    RC(dupload(h, &a_col, col.data(), col.size()));
+    RC(dupload(h, &a_val, val.data(), val.size()));
   }
+  {
+    // longest owned column (diagonal-Schur test)
+    unsigned long long *mx = nullptr;
+    CK(cudaMalloc(&mx, sizeof(unsigned long long)));
+    CK(cudaMemset(mx, 0, sizeof(unsigned long long)));
+    unsigned char *own_tmp = nullptr;
+    if (d->owned) {
+      CK(cudaMalloc(&own_tmp, n_c));
+      CK(cudaMemcpy(own_tmp, owned.data(), n_c, cudaMemcpyHostToDevice));
+    }
+    k_maxcol<<<grid_for(n_c), kBlock, 0, h->st>>>(at_cp_d, n_c, own_tmp, mx);
+    CKL();
+    unsigned long long hm = 0;
+    CK(cudaMemcpyAsync(&hm, mx, sizeof hm, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    s.maxcol = (int64_t)hm;
+    cudaFree(mx);
+    if (own_tmp) cudaFree(own_tmp);
+  }
+  tick("  A CSR+CSC (device)");
   // row segments
   std::vector<int> seg_row, row_seg(m + 1, 0);
   std::vector<int64_t> seg_beg;
@@ -861,6 +996,7 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
     }
   }
   row_seg[m] = (int)seg_row.size();
+  tick("  host CSR+segments");
   // cover lists (stable by slot) and cover counts D
   std::vector<int> cov_ptr(n_c + 1, 0), cov_slot(n_d);
   for (int64_t j = 0; j < n_d; ++j) cov_ptr[d->slot_cov[j] + 1]++;
@@ -886,6 +1022,7 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   for (int c = 0; c < n_c; ++c)
     if (owned[c]) s.nc2_owned += d->c[c] * d->c[c];
   s.sizes.assign(d->clique_sizes, d->clique_sizes + p);
+  tick("  host covers");
   // ---- device problem
   DevProblem &P = s.P;
   P.m = m;
@@ -899,18 +1036,12 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   P.n_sep = d->n_sep;
   P.n_sep_local = d->n_sep_local;
   P.lead = d->follower ? 0 : 1;
-  int64_t *a_rp = nullptr, *at_cp_d = nullptr, *seg_beg_d = nullptr, *cl_off = nullptr;
-  int *a_col = nullptr, *at_row_d = nullptr, *seg_row_d = nullptr, *row_seg_d = nullptr;
+  int64_t *seg_beg_d = nullptr, *cl_off = nullptr;
+  int *seg_row_d = nullptr, *row_seg_d = nullptr;
   int *cov_ptr_d = nullptr, *cov_slot_d = nullptr, *slot_cov_d = nullptr, *cl_size = nullptr;
   int *heavy_d = nullptr, *sep_of_d = nullptr, *sep_local_d = nullptr, *sep_pos_d = nullptr;
   unsigned char *owned_d = nullptr;
-  double *a_val = nullptr, *at_val_d = nullptr, *pinv_d = nullptr;
-  RC(dupload(h, &a_rp, rp.data(), m + 1));
-  RC(dupload(h, &a_col, col.data(), col.size()));
-  RC(dupload(h, &a_val, val.data(), val.size()));
-  RC(dupload(h, &at_cp_d, at_cp.data(), n_c + 1));
-  RC(dupload(h, &at_row_d, at_row.data(), nnz));
-  RC(dupload(h, &at_val_d, at_val.data(), nnz));
+  double *pinv_d = nullptr;
   RC(dupload(h, &seg_row_d, seg_row.data(), seg_row.size()));
   RC(dupload(h, &seg_beg_d, seg_beg.data(), seg_beg.size()));
   RC(dupload(h, &row_seg_d, row_seg.data(), m + 1));
@@ -952,6 +1083,7 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   P.p_inv = pinv_d;
   P.heavy = heavy_d;
   P.n_heavy = (int)heavy.size();
+  tick("  uploads");
   // state + work
   const int64_t T = P.total;
   RC(dalloc(h, &s.S.u, T));
@@ -1056,6 +1188,8 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
   } else if (nshards > 1) {
     h->mode = MODE_EMULATED;
   }
+  SetupTimer tick;
+  tick("context+stream");
   const int m = descs[0].m;
   h->n_sep = descs[0].n_sep;
   for (int g = 0; g < nshards; ++g) {
@@ -1065,8 +1199,10 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
       return HSDE_ERR_ARG;
     }
   }
+  tick("validate");
   h->sh.resize(nshards);
   for (int g = 0; g < nshards; ++g) RC(build_shard(h, h->sh[g], &descs[g]));
+  tick("build_shard");
   if (h->mode == MODE_EMULATED) {
     const int bufs[] = {BUF_SEP, BUF_Q, BUF_RED, BUF_CHK, BUF_MINEIG};
     for (int b : bufs) {
@@ -1098,6 +1234,7 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
     sb = nbn > 0 ? 1.0 / nbn : 1.0;
   }
   for (int g = 0; g < nshards; ++g) RC(set_data(h, h->sh[g], &descs[g], sc, sb));
+  tick("set_data");
   // norms of the iterated data (residual denominators, solver.py:417-423)
   {
     double nci = 0;
@@ -1125,9 +1262,12 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
     }
     h->norm_b = std::sqrt(nbi);
   }
+  tick("norms");
   if (h->factor) {
     RC(setup_schur(h));
+    tick("setup_schur");
     RC(compute_minv_zeta(h));
+    tick("minv_zeta");
   } else {
     for (auto &s : h->sh) {
       s.P.schur_diag = 1;
@@ -1137,6 +1277,7 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
     }
   }
   RC(init_state(h));
+  tick("init_state");
   int maxd = 0;
   for (auto &s : h->sh)
     for (int d : s.sizes) maxd = std::max(maxd, d);
@@ -1157,6 +1298,7 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
     // = one replay + snapshot + the single-iteration graph
     h->gci_len = std::max(1, st->check_interval - 1);
     RC(rebuild_graphs(h));
+    tick("graphs");
   }
   return 0;
 }

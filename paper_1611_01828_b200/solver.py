@@ -31,7 +31,8 @@ from . import _lib
 from .errors import EigenFailure, FactorizationFailure, TauZero
 from .problem import CompressedProblem, compress
 from .report import (STATUS_DUAL_INFEASIBLE, STATUS_MAX_ITERS, STATUS_OPTIMAL,
-                     STATUS_PRIMAL_INFEASIBLE, ProblemStats, Residuals, SolverReport, Timing)
+                     STATUS_PRIMAL_INFEASIBLE, PatternEntries, ProblemStats, Residuals, SolverReport,
+                     Timing)
 
 logger = logging.getLogger(__name__)
 
@@ -508,29 +509,42 @@ class _Session:
         return u, w
 
 
-def _pattern_entries(cp: CompressedProblem, dp, xc: np.ndarray) -> list:
-    """[block, i, j, value] rows (1-based, block-local) on the aggregate pattern
-    plus the diagonal (solver.py:443-452); ``xc`` is a covered-coordinate vector."""
+def _pattern_index(cp: CompressedProblem, dp):
+    """Block-local (block, i, j) of the aggregate pattern plus the diagonal
+    (solver.py:443-452), and where each entry sits in the covered vector.
+    Cached on ``cp``: x and z share it."""
+    key = "pattern_index"
+    if key in cp._cache:
+        return cp._cache[key]
     n = cp.n
     if isinstance(dp, CompressedProblem) or getattr(dp, "aggregate", None) is None:
         edges = cp.aggregate_edges if cp.aggregate_edges is not None else np.zeros((0, 2), np.int64)
     else:
         edges = np.asarray(sorted(dp.aggregate.edges), dtype=np.int64).reshape(-1, 2)
     diag = np.arange(n, dtype=np.int64)
-    pairs = np.concatenate([edges, np.stack([diag, diag], axis=1)])
+    pairs = np.concatenate([np.asarray(edges, dtype=np.int64).reshape(-1, 2),
+                            np.stack([diag, diag], axis=1)])
     code = np.unique(pairs[:, 0] * n + pairs[:, 1])
     gi, gj = code // n, code % n
     flat = gj * n + gi
     pos = np.searchsorted(cp.covered, flat)
     pos_c = np.minimum(pos, max(cp.N_c - 1, 0))
     hit = (pos < cp.N_c) & (cp.covered[pos_c] == flat) if cp.N_c else np.zeros(flat.size, bool)
-    vals = np.where(hit, xc[pos_c] if cp.N_c else 0.0, 0.0)
     dims = np.abs(np.asarray(cp.block_dims or (n,), dtype=np.int64))
     starts = np.concatenate([[0], np.cumsum(dims)])
     bi = np.searchsorted(starts, gi, side="right") - 1
     bj = np.searchsorted(starts, gj, side="right") - 1
-    li, lj = gi - starts[bi], gj - starts[bj]
-    return [[int(b) + 1, int(a) + 1, int(c) + 1, float(v)] for b, a, c, v in zip(bi, li, lj, vals)]
+    out = (bi + 1, gi - starts[bi] + 1, gj - starts[bj] + 1, pos_c, hit)
+    cp._cache[key] = out
+    return out
+
+
+def _pattern_entries(cp: CompressedProblem, dp, xc: np.ndarray) -> PatternEntries:
+    """[block, i, j, value] rows (1-based, block-local) on the aggregate pattern
+    plus the diagonal (solver.py:443-452); ``xc`` is a covered-coordinate vector."""
+    b, i, j, pos_c, hit = _pattern_index(cp, dp)
+    vals = np.where(hit, xc[pos_c] if cp.N_c else 0.0, 0.0)
+    return PatternEntries(b, i, j, vals)
 
 
 def _problem_stats(cp: CompressedProblem, dp) -> ProblemStats:

@@ -100,6 +100,26 @@ def test_certificate_decision_rules():
     assert _cert_decision(np.array([-1.0, -2.0, nan, nan, 1e-6, 1e-3, 0.0]), 1e-4) is None
 
 
+def test_pattern_entries_behave_as_rows():
+    """Solution rows held as arrays serialise exactly like the reference's lists."""
+    import json
+
+    from paper_1611_01828_b200.report import PatternEntries
+
+    rows = [[1, 1, 1, 0.5], [1, 2, 1, -0.25], [2, 3, 3, 1e-300]]
+    pe = PatternEntries(*zip(*rows))
+    assert len(pe) == 3 and pe[1] == rows[1] and pe[1:] == rows[1:] and list(pe) == rows
+    assert pe == rows and rows == pe and pe == PatternEntries(*zip(*rows))
+    timing, stats = Timing(0.1, 0.2, 0.3, 0.01), ProblemStats(3, 1, [3], 1, 3, 3, 9)
+    mk = lambda e: SolverReport(status="Optimal", objective_primal=1.0, objective_dual=1.0,
+                                iterations=20, residuals=Residuals(1e-5, 1e-5, 1e-5),
+                                timing=timing, problem=stats, tol=1e-4,
+                                solution={"x_entries": e, "y": [1.0]})
+    assert emit_report(mk(pe)) == emit_report(mk(rows))
+    assert json.loads(emit_report(mk(pe)))["solution"]["x_entries"] == rows
+    assert read_report(emit_report(mk(pe))) == mk(pe)
+
+
 def test_report_json_roundtrip():
     rep = SolverReport(status="Optimal", objective_primal=1.0, objective_dual=1.0, iterations=20,
                        residuals=Residuals(1e-5, 1e-5, 1e-5), timing=Timing(0.1, 0.2, 0.3, 0.01),
