@@ -583,6 +583,105 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
   return 0;
 }
 
+// Partial S = A diag(p_inv) A' over the owned columns, sparse and row-wise:
+// warp (i, part) walks its share of row i's CSR (ascending column l) and adds
+//   S[i][j] += (a_il a_jl) p_l   for every nonzero a_jl of column l (CSC)
+// into a shared-memory row (the rows j of one column are distinct: no
+// conflicts); parts are summed in order by k_schur_parts_sum.  Deterministic,
+// and bitwise symmetric (a_il a_jl = a_jl a_il).  Work ~ sum_l nnz(col l)^2
+// instead of the dense m^2 n_c.
+constexpr int kSchurParts = 8;
+constexpr int kSchurBatch = 4;  // columns whose loads are in flight together
+
+__global__ void __launch_bounds__(256) k_schur_rows(DevProblem P, int wpb, double *part) {
+  extern __shared__ double srow[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w >= wpb) return;
+  const int task = blockIdx.x * wpb + w;
+  const int i = task / kSchurParts, sp = task - (task / kSchurParts) * kSchurParts;
+  if (i >= P.m) return;
+  const int m = P.m;
+  double *row = srow + (size_t)w * m;
+  for (int j = lane; j < m; j += 32) row[j] = 0.0;
+  __syncwarp();
+  const int64_t rb = P.a_rp[i], len = P.a_rp[i + 1] - rb;
+  const int64_t kb = rb + len * sp / kSchurParts, ke = rb + len * (sp + 1) / kSchurParts;
+  for (int64_t k0 = kb; k0 < ke; k0 += kSchurBatch) {
+    int64_t cb = 0, ce = 0;
+    double a = 0.0, pl = 0.0;
+    if (lane < kSchurBatch && k0 + lane < ke) {
+      const int l = P.a_col[k0 + lane];
+      a = P.a_val[k0 + lane];  // a_il
+      pl = P.p_inv[l];
+      cb = P.at_cp[l];
+      ce = P.at_cp[l + 1];
+    }
+    int jq[kSchurBatch];
+    double aq[kSchurBatch], pq[kSchurBatch];
+    int64_t cbq[kSchurBatch], ceq[kSchurBatch];
+#pragma unroll
+    for (int q = 0; q < kSchurBatch; ++q) {
+      cbq[q] = __shfl_sync(0xffffffffu, cb, q);
+      ceq[q] = __shfl_sync(0xffffffffu, ce, q);
+      aq[q] = __shfl_sync(0xffffffffu, a, q);
+      pq[q] = __shfl_sync(0xffffffffu, pl, q);
+    }
+    double av[kSchurBatch];
+#pragma unroll
+    for (int q = 0; q < kSchurBatch; ++q) {
+      const int64_t e = cbq[q] + lane;
+      jq[q] = e < ceq[q] ? P.at_row[e] : -1;
+      av[q] = e < ceq[q] ? P.at_val[e] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kSchurBatch; ++q) {
+      if (jq[q] >= 0) row[jq[q]] += (aq[q] * av[q]) * pq[q];
+      __syncwarp();
+      for (int64_t e = cbq[q] + 32 + lane; e < ceq[q]; e += 32)  // long columns
+        row[P.at_row[e]] += (aq[q] * P.at_val[e]) * pq[q];
+      __syncwarp();
+    }
+  }
+  double *out = part + ((size_t)sp * m + i) * m;
+  for (int j = lane; j < m; j += 32) out[j] = row[j];
+}
+
+__global__ void k_schur_parts_sum(const double *part, int64_t mm, double *S) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < mm;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double a = 0.0;
+    for (int s = 0; s < kSchurParts; ++s) a += part[(size_t)s * mm + k];
+    S[k] = a;
+  }
+}
+
+// sparse row-wise partial Schur when a row of S fits in shared memory
+int schur_partial_sparse(hsde_handle *h, ShardDev &s, bool *done) {
+  *done = false;
+  const int m = s.P.m;
+  const size_t row_bytes = sizeof(double) * (size_t)m;
+  const int wpb = (int)std::min<size_t>(8, (200u << 10) / std::max<size_t>(row_bytes, 1));
+  if (wpb < 1 || m == 0) return 0;
+  SetupTimer tick;
+  RC(dalloc(h, &s.d_schur, (size_t)m * m));
+  double *part = nullptr;
+  CK(cudaMalloc(&part, sizeof(double) * (size_t)kSchurParts * m * m));
+  tick("    schur alloc");
+  const size_t smem = row_bytes * wpb;
+  CK(cudaFuncSetAttribute(k_schur_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t tasks = (int64_t)m * kSchurParts;
+  k_schur_rows<<<(unsigned)((tasks + wpb - 1) / wpb), wpb * 32, smem, h->st>>>(s.P, wpb, part);
+  CKL();
+  tick("    schur rows");
+  k_schur_parts_sum<<<grid_for((int64_t)m * m), kBlock, 0, h->st>>>(part, (int64_t)m * m, s.d_schur);
+  CKL();
+  CK(cudaStreamSynchronize(h->st));
+  cudaFree(part);
+  tick("    schur sum+free");
+  *done = true;
+  return 0;
+}
+
 // Partial S = sum over owned columns of A diag(p_inv) A' (dense chunks + DGEMM)
 int schur_partial_dense(hsde_handle *h, ShardDev &s) {
   const int m = s.P.m, n_c = s.P.n_c;
@@ -624,6 +723,7 @@ int schur_partial_dense(hsde_handle *h, ShardDev &s) {
 
 // reduced S (in the shard's d_schur) -> S^{-1} (cuSOLVER Cholesky, potrs on I)
 int schur_factor(hsde_handle *h, ShardDev &s) {
+  SetupTimer tick;
   const int m = s.P.m;
   double *S = s.d_schur;
   k_add_identity<<<grid_for(m), kBlock, 0, h->st>>>(S, m);
@@ -651,6 +751,7 @@ int schur_factor(hsde_handle *h, ShardDev &s) {
   int *dinfo = nullptr;
   CK(cudaMalloc(&work, sizeof(double) * std::max(lwork, 1)));
   CK(cudaMalloc(&dinfo, sizeof(int)));
+  tick("    potrf setup");
   cusolverDnDpotrf(cs, CUBLAS_FILL_MODE_LOWER, m, S, m, work, lwork, dinfo);
   int info = 0;
   CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, h->st));
@@ -674,6 +775,7 @@ int schur_factor(hsde_handle *h, ShardDev &s) {
   cusolverDnDestroy(cs);
   k_symmetrize<<<grid_for((int64_t)m * m), kBlock, 0, h->st>>>(X, m, S);  // S^{-1}, symmetric
   CKL();
+  tick("    potrf+potrs");
   s.P.sinv = S;
   s.P.schur_diag = 0;
   return 0;
@@ -688,7 +790,9 @@ int setup_schur(hsde_handle *h) {
       k_diag_schur<<<grid_for(m), kBlock, 0, h->st>>>(s.P, s.d_schur);
       CKL();
     } else {
-      RC(schur_partial_dense(h, s));
+      bool done = false;
+      RC(schur_partial_sparse(h, s, &done));
+      if (!done) RC(schur_partial_dense(h, s));
     }
   }
   if (h->mode == MODE_EMULATED) {
@@ -794,14 +898,8 @@ int validate(hsde_handle *h, const hsde_problem_desc *d) {
       h->err = "a_row_ptr not monotone";
       return HSDE_ERR_ARG;
     }
-    for (int64_t k = d->a_row_ptr[i]; k < d->a_row_ptr[i + 1]; ++k) {
-      const int c = d->a_col[k];
-      if (c < 0 || c >= n_c || (k > d->a_row_ptr[i] && c <= d->a_col[k - 1])) {
-        h->err = "a_col out of range or not strictly ascending in row " + std::to_string(i);
-        return HSDE_ERR_ARG;
-      }
-    }
   }
+  // column indices are checked on the device after the upload (check_csr_device)
   if (d->clique_offsets[0] != 0 || d->clique_offsets[p] != n_d) {
     h->err = "clique offsets inconsistent with n_d";
     return HSDE_ERR_ARG;
@@ -832,6 +930,33 @@ int validate(hsde_handle *h, const hsde_problem_desc *d) {
 }
 
 // upload shard data (everything that does not depend on normalisation)
+// a_col in range and strictly ascending within each row; first bad row or -1
+__global__ void k_check_csr(const int64_t *rp, const int *col, int m, int n_c, int *bad_row) {
+  for (int i = blockIdx.x; i < m; i += gridDim.x)
+    for (int64_t k = rp[i] + threadIdx.x; k < rp[i + 1]; k += blockDim.x) {
+      const int c = col[k];
+      if (c < 0 || c >= n_c || (k > rp[i] && c <= col[k - 1])) atomicMin(bad_row, i);
+    }
+}
+
+int check_csr_device(hsde_handle *h, const int64_t *rp, const int *col, int m, int n_c) {
+  int *bad = nullptr;
+  CK(cudaMalloc(&bad, sizeof(int)));
+  const int init = INT32_MAX;
+  CK(cudaMemcpy(bad, &init, sizeof(int), cudaMemcpyHostToDevice));
+  if (m > 0) k_check_csr<<<std::min(m, 148 * 8), kBlock, 0, h->st>>>(rp, col, m, n_c, bad);
+  CKL();
+  int hb = INT32_MAX;
+  CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  cudaFree(bad);
+  if (hb != INT32_MAX) {
+    h->err = "a_col out of range or not strictly ascending in row " + std::to_string(hb);
+    return HSDE_ERR_ARG;
+  }
+  return 0;
+}
+
 // ---- device construction of the CSC of A (rows ascending within a column)
 __global__ void k_row_of(const int64_t *rp, int m, int *row_of) {
   for (int i = blockIdx.x; i < m; i += gridDim.x)
@@ -870,9 +995,11 @@ __global__ void k_maxcol(const int64_t *cp, int n_c, const unsigned char *owned,
 
 int build_csc_device(hsde_handle *h, int m, int n_c, int64_t nnz, const int64_t *rp, const int *col,
                      const double *val, int64_t **at_cp, int **at_row, double **at_val) {
+  SetupTimer tick;
   RC(dalloc(h, at_cp, n_c + 1));
   RC(dalloc(h, at_row, nnz));
   RC(dalloc(h, at_val, nnz));
+  tick("    csc alloc");
   unsigned long long *cnt = reinterpret_cast<unsigned long long *>(*at_cp);
   CK(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (n_c + 1), h->st));
   if (nnz == 0) return 0;
@@ -896,6 +1023,7 @@ int build_csc_device(hsde_handle *h, int m, int n_c, int64_t nnz, const int64_t 
   CK(cudaMalloc(&idx, sizeof(int) * nnz));
   CK(cudaMalloc(&perm, sizeof(int) * nnz));
   CK(cudaMalloc(&keys_out, sizeof(int) * nnz));
+  tick("    csc tmp alloc");
   cub::DeviceScan::InclusiveSum(tmp, tb, cnt, cnt, n_c + 1, h->st);
   k_row_of<<<std::min(m, 148 * 8), kBlock, 0, h->st>>>(rp, m, row_of);
   k_iota<<<g, kBlock, 0, h->st>>>(idx, nnz);
@@ -905,11 +1033,13 @@ int build_csc_device(hsde_handle *h, int m, int n_c, int64_t nnz, const int64_t 
   k_csc_gather<<<g, kBlock, 0, h->st>>>(perm, row_of, val, nnz, *at_row, *at_val);
   CKL();
   CK(cudaStreamSynchronize(h->st));
+  tick("    csc sort+gather");
   cudaFree(tmp);
   cudaFree(row_of);
   cudaFree(idx);
   cudaFree(perm);
   cudaFree(keys_out);
+  tick("    csc free");
   return 0;
 }
 
@@ -931,6 +1061,8 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
     RC(dupload(h, &a_rp, d->a_row_ptr, m + 1));
     RC(dupload(h, &a_col, d->a_col, nnz));
     RC(dupload(h, &a_val, d->a_val, nnz));
+    tick("  A upload");
+    RC(check_csr_device(h, a_rp, a_col, m, n_c));
     RC(build_csc_device(h, m, n_c, nnz, a_rp, a_col, a_val, &at_cp_d, &at_row_d, &at_val_d));
   } else {
     // CSC over all local columns (A' g is needed on every local coordinate)
@@ -943,7 +1075,8 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
     CK(cudaMemcpy(f_rp, d->a_row_ptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(f_col, d->a_col, sizeof(int) * nnz, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(f_val, d->a_val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
-    const int rc = build_csc_device(h, m, n_c, nnz, f_rp, f_col, f_val, &at_cp_d, &at_row_d, &at_val_d);
+    int rc = check_csr_device(h, f_rp, f_col, m, n_c);
+    if (!rc) rc = build_csc_device(h, m, n_c, nnz, f_rp, f_col, f_val, &at_cp_d, &at_row_d, &at_val_d);
     cudaFree(f_rp);
     cudaFree(f_col);
     cudaFree(f_val);

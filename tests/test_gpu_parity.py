@@ -160,6 +160,22 @@ def test_factorization_failure_on_bad_data():
         H.setup_cache(dp)
 
 
+def test_malformed_constraint_matrix_rejected():
+    """Column indices out of order (validated on the device after the upload)."""
+    import dataclasses
+
+    from paper_1611_01828_b200 import _lib
+
+    cp = make_config(0)
+    A = cp.A.copy()
+    row = 3
+    b, e = A.indptr[row], A.indptr[row + 1]
+    A.indices[b:e] = A.indices[b:e][::-1].copy()
+    bad = dataclasses.replace(cp, A=A, _cache={})
+    with pytest.raises(ValueError, match="row 3"):
+        _lib.Handle(bad)
+
+
 def test_eigen_failure_on_nan():
     from paper_1611_01828_b200.problem import CliqueDecomposition, DecomposedProblem
     import scipy.sparse as sp
