@@ -162,12 +162,37 @@ struct hsde_handle {
 
 namespace {
 
+// Device memory comes from the device's stream-ordered pool, which keeps
+// freed blocks (release threshold raised once): a second solve in the same
+// process reuses the first one's memory instead of mapping new pages.
+void retain_pool(int dev) {
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
+// pool allocation usable from any stream on return
+cudaError_t pool_malloc(hsde_handle *h, void **p, size_t bytes) {
+  cudaError_t e = cudaMallocAsync(p, std::max<size_t>(bytes, 1), h->st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->st);
+  return e;
+}
+
+void pool_free(hsde_handle *h, void *p) {
+  if (p) cudaFreeAsync(p, h->st);
+}
+
 template <class T>
 int dalloc(hsde_handle *h, T **p, size_t n) {
   void *q = nullptr;
-  cudaError_t e = cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T));
+  cudaError_t e = pool_malloc(h, &q, std::max<size_t>(n, 1) * sizeof(T));
   if (e != cudaSuccess) {
-    h->err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+    h->err = std::string("cudaMallocAsync: ") + cudaGetErrorString(e);
     return HSDE_ERR_CUDA;
   }
   h->bufs.push_back(q);
@@ -665,7 +690,7 @@ int schur_partial_sparse(hsde_handle *h, ShardDev &s, bool *done) {
   SetupTimer tick;
   RC(dalloc(h, &s.d_schur, (size_t)m * m));
   double *part = nullptr;
-  CK(cudaMalloc(&part, sizeof(double) * (size_t)kSchurParts * m * m));
+  CK(pool_malloc(h, (void **)&part, sizeof(double) * (size_t)kSchurParts * m * m));
   tick("    schur alloc");
   const size_t smem = row_bytes * wpb;
   CK(cudaFuncSetAttribute(k_schur_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -676,7 +701,7 @@ int schur_partial_sparse(hsde_handle *h, ShardDev &s, bool *done) {
   k_schur_parts_sum<<<grid_for((int64_t)m * m), kBlock, 0, h->st>>>(part, (int64_t)m * m, s.d_schur);
   CKL();
   CK(cudaStreamSynchronize(h->st));
-  cudaFree(part);
+  pool_free(h, part);
   tick("    schur sum+free");
   *done = true;
   return 0;
@@ -691,8 +716,8 @@ int schur_partial_dense(hsde_handle *h, ShardDev &s) {
   int wc = (int)std::max<size_t>(1, budget / (sizeof(double) * (size_t)m));
   wc = std::min(wc, std::max(n_c, 1));
   double *Dm = nullptr, *Ds = nullptr;
-  CK(cudaMalloc(&Dm, sizeof(double) * (size_t)m * wc));
-  CK(cudaMalloc(&Ds, sizeof(double) * (size_t)m * wc));
+  CK(pool_malloc(h, (void **)&Dm, sizeof(double) * (size_t)m * wc));
+  CK(pool_malloc(h, (void **)&Ds, sizeof(double) * (size_t)m * wc));
   cublasHandle_t cb;
   if (cublasCreate(&cb) != CUBLAS_STATUS_SUCCESS) {
     h->err = "cublasCreate failed";
@@ -716,8 +741,8 @@ int schur_partial_dense(hsde_handle *h, ShardDev &s) {
   }
   CK(cudaStreamSynchronize(h->st));
   cublasDestroy(cb);
-  cudaFree(Dm);
-  cudaFree(Ds);
+  pool_free(h, Dm);
+  pool_free(h, Ds);
   return rc;
 }
 
@@ -749,16 +774,16 @@ int schur_factor(hsde_handle *h, ShardDev &s) {
   cusolverDnDpotrf_bufferSize(cs, CUBLAS_FILL_MODE_LOWER, m, S, m, &lwork);
   double *work = nullptr;
   int *dinfo = nullptr;
-  CK(cudaMalloc(&work, sizeof(double) * std::max(lwork, 1)));
-  CK(cudaMalloc(&dinfo, sizeof(int)));
+  CK(pool_malloc(h, (void **)&work, sizeof(double) * std::max(lwork, 1)));
+  CK(pool_malloc(h, (void **)&dinfo, sizeof(int)));
   tick("    potrf setup");
   cusolverDnDpotrf(cs, CUBLAS_FILL_MODE_LOWER, m, S, m, work, lwork, dinfo);
   int info = 0;
   CK(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   if (info != 0) {
-    cudaFree(work);
-    cudaFree(dinfo);
+    pool_free(h, work);
+    pool_free(h, dinfo);
     cusolverDnDestroy(cs);
     h->err = "Cholesky of the " + std::to_string(m) + " x " + std::to_string(m) +
              " reduced system failed: leading minor " + std::to_string(info) + " not positive";
@@ -770,8 +795,8 @@ int schur_factor(hsde_handle *h, ShardDev &s) {
   CKL();
   cusolverDnDpotrs(cs, CUBLAS_FILL_MODE_LOWER, m, m, S, m, X, m, dinfo);
   CK(cudaStreamSynchronize(h->st));
-  cudaFree(work);
-  cudaFree(dinfo);
+  pool_free(h, work);
+  pool_free(h, dinfo);
   cusolverDnDestroy(cs);
   k_symmetrize<<<grid_for((int64_t)m * m), kBlock, 0, h->st>>>(X, m, S);  // S^{-1}, symmetric
   CKL();
@@ -941,7 +966,7 @@ __global__ void k_check_csr(const int64_t *rp, const int *col, int m, int n_c, i
 
 int check_csr_device(hsde_handle *h, const int64_t *rp, const int *col, int m, int n_c) {
   int *bad = nullptr;
-  CK(cudaMalloc(&bad, sizeof(int)));
+  CK(pool_malloc(h, (void **)&bad, sizeof(int)));
   const int init = INT32_MAX;
   CK(cudaMemcpy(bad, &init, sizeof(int), cudaMemcpyHostToDevice));
   if (m > 0) k_check_csr<<<std::min(m, 148 * 8), kBlock, 0, h->st>>>(rp, col, m, n_c, bad);
@@ -949,7 +974,7 @@ int check_csr_device(hsde_handle *h, const int64_t *rp, const int *col, int m, i
   int hb = INT32_MAX;
   CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
-  cudaFree(bad);
+  pool_free(h, bad);
   if (hb != INT32_MAX) {
     h->err = "a_col out of range or not strictly ascending in row " + std::to_string(hb);
     return HSDE_ERR_ARG;
@@ -1018,11 +1043,11 @@ int build_csc_device(hsde_handle *h, int m, int n_c, int64_t nnz, const int64_t 
   int end_bit = 1;
   while ((1ll << end_bit) < (long long)n_c) ++end_bit;
   cub::DeviceRadixSort::SortPairs(nullptr, tb2, col, keys_out, idx, perm, (int)nnz, 0, end_bit, h->st);
-  CK(cudaMalloc(&tmp, std::max(tb, tb2)));
-  CK(cudaMalloc(&row_of, sizeof(int) * nnz));
-  CK(cudaMalloc(&idx, sizeof(int) * nnz));
-  CK(cudaMalloc(&perm, sizeof(int) * nnz));
-  CK(cudaMalloc(&keys_out, sizeof(int) * nnz));
+  CK(pool_malloc(h, (void **)&tmp, std::max(tb, tb2)));
+  CK(pool_malloc(h, (void **)&row_of, sizeof(int) * nnz));
+  CK(pool_malloc(h, (void **)&idx, sizeof(int) * nnz));
+  CK(pool_malloc(h, (void **)&perm, sizeof(int) * nnz));
+  CK(pool_malloc(h, (void **)&keys_out, sizeof(int) * nnz));
   tick("    csc tmp alloc");
   cub::DeviceScan::InclusiveSum(tmp, tb, cnt, cnt, n_c + 1, h->st);
   k_row_of<<<std::min(m, 148 * 8), kBlock, 0, h->st>>>(rp, m, row_of);
@@ -1034,11 +1059,11 @@ int build_csc_device(hsde_handle *h, int m, int n_c, int64_t nnz, const int64_t 
   CKL();
   CK(cudaStreamSynchronize(h->st));
   tick("    csc sort+gather");
-  cudaFree(tmp);
-  cudaFree(row_of);
-  cudaFree(idx);
-  cudaFree(perm);
-  cudaFree(keys_out);
+  pool_free(h, tmp);
+  pool_free(h, row_of);
+  pool_free(h, idx);
+  pool_free(h, perm);
+  pool_free(h, keys_out);
   tick("    csc free");
   return 0;
 }
@@ -1069,17 +1094,17 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
     int64_t *f_rp = nullptr;
     int *f_col = nullptr;
     double *f_val = nullptr;
-    CK(cudaMalloc(&f_rp, sizeof(int64_t) * (m + 1)));
-    CK(cudaMalloc(&f_col, sizeof(int) * std::max<int64_t>(nnz, 1)));
-    CK(cudaMalloc(&f_val, sizeof(double) * std::max<int64_t>(nnz, 1)));
+    CK(pool_malloc(h, (void **)&f_rp, sizeof(int64_t) * (m + 1)));
+    CK(pool_malloc(h, (void **)&f_col, sizeof(int) * std::max<int64_t>(nnz, 1)));
+    CK(pool_malloc(h, (void **)&f_val, sizeof(double) * std::max<int64_t>(nnz, 1)));
     CK(cudaMemcpy(f_rp, d->a_row_ptr, sizeof(int64_t) * (m + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(f_col, d->a_col, sizeof(int) * nnz, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(f_val, d->a_val, sizeof(double) * nnz, cudaMemcpyHostToDevice));
     int rc = check_csr_device(h, f_rp, f_col, m, n_c);
     if (!rc) rc = build_csc_device(h, m, n_c, nnz, f_rp, f_col, f_val, &at_cp_d, &at_row_d, &at_val_d);
-    cudaFree(f_rp);
-    cudaFree(f_col);
-    cudaFree(f_val);
+    pool_free(h, f_rp);
+    pool_free(h, f_col);
+    pool_free(h, f_val);
     RC(rc);
     // CSR over the owned columns (the only columns this shard adds into A t)
     std::vector<int> col;
@@ -1101,11 +1126,11 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   {
     // longest owned column (diagonal-Schur test)
     unsigned long long *mx = nullptr;
-    CK(cudaMalloc(&mx, sizeof(unsigned long long)));
+    CK(pool_malloc(h, (void **)&mx, sizeof(unsigned long long)));
     CK(cudaMemset(mx, 0, sizeof(unsigned long long)));
     unsigned char *own_tmp = nullptr;
     if (d->owned) {
-      CK(cudaMalloc(&own_tmp, n_c));
+      CK(pool_malloc(h, (void **)&own_tmp, n_c));
       CK(cudaMemcpy(own_tmp, owned.data(), n_c, cudaMemcpyHostToDevice));
     }
     k_maxcol<<<grid_for(n_c), kBlock, 0, h->st>>>(at_cp_d, n_c, own_tmp, mx);
@@ -1114,8 +1139,8 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
     CK(cudaMemcpyAsync(&hm, mx, sizeof hm, cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
     s.maxcol = (int64_t)hm;
-    cudaFree(mx);
-    if (own_tmp) cudaFree(own_tmp);
+    pool_free(h, mx);
+    pool_free(h, own_tmp);
   }
   tick("  A CSR+CSC (device)");
   // row segments
@@ -1302,6 +1327,7 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
     h->err = "stream create failed";
     return HSDE_ERR_CUDA;
   }
+  retain_pool(h->dev);
   if (comm && comm->world >= 1) {  // explicit communicator: NCCL (a 1-rank comm is valid)
     if (nshards != 1) {
       h->err = "NCCL mode takes exactly one shard per rank";
@@ -1497,7 +1523,8 @@ void hsde_destroy(hsde_t *h) {
   if (h->g1) cudaGraphExecDestroy(h->g1);
   if (h->gci) cudaGraphExecDestroy(h->gci);
   if (h->nccl) ncclCommDestroy(h->nccl);
-  for (void *p : h->bufs) cudaFree(p);
+  for (void *p : h->bufs) pool_free(h, p);
+  if (h->st) cudaStreamSynchronize(h->st);
   if (h->h_chk) cudaFreeHost(h->h_chk);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;

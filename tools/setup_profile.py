@@ -10,7 +10,7 @@ from paper_1611_01828_b200 import _lib  # noqa: E402
 from paper_1611_01828_b200.synthetic import make_config  # noqa: E402
 
 cp = make_config(int(sys.argv[1]) if len(sys.argv) > 1 else 4)
-for rep in range(3):
+for rep in range(5):
     t = time.perf_counter()
     h = _lib.Handle(cp)
     t1 = time.perf_counter()
