@@ -137,6 +137,23 @@ __device__ void jacobi_prepare(const Team &tm, JacobiScratch &js, int dp, bool i
     }
 }
 
+// min over the team, returned to every member
+template <class Team>
+__device__ double team_min(const Team &tm, double v, double *red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (tm.size() <= 32) return v;
+  const int lane = tm.rank & 31, wid = tm.rank >> 5;
+  tm.sync();
+  if (lane == 0) red[wid] = v;
+  tm.sync();
+  double r = red[0];
+  const int nw = (tm.size() + 31) >> 5;
+  for (int i = 1; i < nw; ++i) r = fmin(r, red[i]);
+  tm.sync();
+  return r;
+}
+
 // |A|_F^2 and off(A)^2 from the upper triangle
 template <class Team>
 __device__ void jacobi_norms(const Team &tm, const JacobiScratch &js, int dp, double &norm2,
@@ -215,14 +232,22 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
   const double stop2 = norm2 * 1.925929944387236e-34;      // (2^-56 |A|_F)^2
   int sweep = 0, round = 0;
   bool pending = false;
-  // first-order exit: off <= 1e-12 |A|_F (see psd_rebuild_first_order)
-  const double fo2 = norm2 * 1e-24;
+  // First-order exit (psd_rebuild_first_order): its error is O(off^2 / g),
+  // g the smallest |diagonal| (no eigenvalue closer to 0 can change sign while
+  // off <= g / 1000).  Exit once off^2 <= 1e-17 |A|_F g: projection error
+  // ~1e-17 |A|_F, the accuracy of a converged sweep.
   if (first_order) *first_order = false;
+  const double fo_scale = 1e-17 * sqrt(norm2);
   for (; sweep < kMaxSweeps; ++sweep) {
     if (!(off2 > stop2)) break;  // also stops on NaN
-    if (first_order && off2 <= fo2) {
-      *first_order = true;
-      break;
+    if (first_order) {
+      double g = CUDART_INF;
+      for (int i = tm.rank; i < d; i += T) g = fmin(g, fabs(A[i * lda + i]));
+      g = team_min(tm, g, js.red);
+      if (off2 <= fo_scale * g && off2 <= 1e-6 * g * g) {
+        *first_order = true;
+        break;
+      }
     }
     if (tm.rank == 0) js.flag[0] = 0;
     tm.sync();
@@ -509,11 +534,11 @@ __device__ void team_gemm_nn(const Team &tm, const double *L, int ldl, const dou
 }
 
 // First-order projection of a nearly diagonal B = D + E (CTA teams):
-//   P(B) = P(D) + L_D(E) + O(|E|^2 / gap),  L_D(E)_ij = E_ij (l_i+ - l_j+) / (l_i - l_j)
+//   P(B) = P(D) + L_D(E) + O(|E|^2 / g),  L_D(E)_ij = E_ij (l_i+ - l_j+) / (l_i - l_j)
 // (the Frechet derivative of the spectral function max(., 0); the divided
-// difference is 1 between positive, 0 between non-positive eigenvalues).  It
-// is exact within same-sign pairs and its error is bounded by ~|E| overall;
-// the sweeps stop here only when |E|_F <= 1e-12 |A|_F.  P = V' M V with
+// difference is 1 between positive, 0 between non-positive eigenvalues), g the
+// smallest |l_i|.  It is exact within same-sign pairs; jacobi_sweeps stops for
+// it only when |E|_F^2 <= 1e-17 |A|_F g and |E|_F <= g / 1000.  P = V' M V with
 // M = diag(l+) + L_D(E) by two team GEMMs.
 template <class Team, class Emit>
 __device__ void psd_rebuild_first_order(const Team &tm, JacobiScratch &js, int d, Emit emit) {
