@@ -102,6 +102,8 @@ typedef struct hsde_info_t {
   int32_t max_clique;
   int32_t n_shards;          /* shards held by this handle                          */
   int32_t mode;              /* 0 single GPU, 1 emulated shards (one GPU), 2 NCCL   */
+  int32_t half_passes;       /* 1: A passes over mirror pairs (A_ij = A_ji columns) */
+  int32_t reserved;
 } hsde_info_t;
 
 typedef struct hsde_handle hsde_t;

@@ -73,6 +73,7 @@ class Info(C.Structure):
         ("n_d", C.c_int64), ("nnz", C.c_int64), ("sigma_c", C.c_double),
         ("sigma_b", C.c_double), ("zeta_scale", C.c_double), ("schur_diagonal", C.c_int32),
         ("max_clique", C.c_int32), ("n_shards", C.c_int32), ("mode", C.c_int32),
+        ("half_passes", C.c_int32), ("reserved", C.c_int32),
     ]
 
 
@@ -192,6 +193,7 @@ class Handle:
         self.zeta_scale = float(inf.zeta_scale)
         self.schur_diagonal = bool(inf.schur_diagonal)
         self.max_clique = int(inf.max_clique)
+        self.half_passes = bool(inf.half_passes)
         self.alpha = alpha
 
     @staticmethod

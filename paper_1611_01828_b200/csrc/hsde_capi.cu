@@ -107,6 +107,7 @@ struct ShardDev {
   double *d_mineig = nullptr;     // [p]
   double *d_schur = nullptr;      // [m*m] partial / factored Schur (owned)
   int grid_heavy = 0, grid_nc = 1, grid_nd = 1, grid_m = 1, grid_T = 1, grid_seg = 1, grid_schur = 1;
+  int grid_ua = 1;  // k_ua / k_ua_half grid = number of c.ua block partials
   size_t schur_smem = 0;
   std::vector<int> sizes;         // clique sizes (host copy)
   int64_t maxcol = 0;
@@ -345,6 +346,49 @@ int dev_dot_owned(hsde_handle *h, ShardDev &s, const double *a, const double *b,
   return 0;
 }
 
+// q0 = A t0 of one shard: tile partials + ordered row sums into W.qbuf (half
+// passes), or row-segment partials in W.qseg (+ W.qbuf when sharded)
+int launch_aq(hsde_handle *h, ShardDev &s, cudaStream_t st, int *nl) {
+  const DevProblem &P = s.P;
+  if (P.half) {
+    k_pair_sum<<<grid_for(P.n_pair), kBlock, 0, st>>>(P, s.W.t, s.W.xq);
+    CKL();
+    k_spmv_half<<<P.rt_ntile * kRowTileSplit, kBlock, 0, st>>>(P, s.W.xq, s.W.rtpart);
+    CKL();
+    k_rowsum_tiles<<<grid_for((int64_t)P.m * 32), kBlock, 0, st>>>(P, s.W.rtpart, s.W.qbuf);
+    CKL();
+    *nl += 3;
+    return 0;
+  }
+  k_spmv_seg<<<s.grid_seg, kBlock, 0, st>>>(P, s.W.t, s.W.qseg);
+  CKL();
+  ++*nl;
+  if (h->multi()) {
+    k_rowsum_seg<<<s.grid_m, kBlock, 0, st>>>(P, s.W.qseg, s.W.qbuf);
+    CKL();
+    ++*nl;
+  }
+  return 0;
+}
+
+// k_schur reads the reduced q0 from W.qbuf unless it sums row segments itself
+bool q_in_buf(const hsde_handle *h, const ShardDev &s) { return s.P.half || h->multi(); }
+
+// ua = t0 - P^{-1} A' g (+ block partials of c.ua)
+int launch_ua(hsde_handle *h, ShardDev &s, cudaStream_t st, bool with_dot) {
+  const DevProblem &P = s.P;
+  if (P.half) {
+    const size_t sm = sizeof(double) * (size_t)P.m;
+    if (with_dot) k_ua_half<true><<<s.grid_ua, kBlock, sm, st>>>(P, s.W, s.W.qp);
+    else k_ua_half<false><<<s.grid_ua, kBlock, sm, st>>>(P, s.W, s.W.qp);
+  } else {
+    if (with_dot) k_ua<true><<<s.grid_ua, kBlock, 0, st>>>(P, s.W, s.W.qp);
+    else k_ua<false><<<s.grid_ua, kBlock, 0, st>>>(P, s.W, s.W.qp);
+  }
+  CKL();
+  return 0;
+}
+
 // The inner solve of _solve_inner_parts (solver.py:203-245) on explicit
 // vectors, all shards: rho (T-1 per shard, x|s|y|v) -> u12.  uy by the
 // identity A ua = S^{-1} A t, or (exact_uy, single shard) the explicit CSR
@@ -374,23 +418,18 @@ int inner_dist(hsde_handle *h, const std::vector<const double *> &rho,
       k_sep_finish<false><<<grid_for(P.n_sep_local), kBlock, 0, st>>>(P, s.S, s.W, rx);
       CKL();
     }
-    k_spmv_seg<<<s.grid_seg, kBlock, 0, st>>>(P, s.W.t, s.W.qseg);
-    CKL();
-    if (h->multi()) {
-      k_rowsum_seg<<<s.grid_m, kBlock, 0, st>>>(P, s.W.qseg, s.W.qbuf);
-      CKL();
-    }
+    int nl = 0;
+    RC(launch_aq(h, s, st, &nl));
   }
   RC(reduce(h, BUF_Q, h->sh[0].P.m));
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
     const DevProblem &P = s.P;
     const double *rs = rho[g] + P.n_c, *ry = rho[g] + P.n_c + P.n_d, *rv = ry + P.m;
-    k_schur<<<s.grid_schur, kBlock, s.schur_smem, st>>>(P, s.W.qseg, h->multi() ? s.W.qbuf : nullptr,
+    k_schur<<<s.grid_schur, kBlock, s.schur_smem, st>>>(P, s.W.qseg, q_in_buf(h, s) ? s.W.qbuf : nullptr,
                                                         ry, s.W.qp);
     CKL();
-    k_ua<false><<<s.grid_nc, kBlock, 0, st>>>(P, s.W, s.W.qp);
-    CKL();
+    RC(launch_ua(h, s, st, false));
     double *ua = u12[g], *ub = u12[g] + P.n_c, *uy = u12[g] + P.n_c + P.n_d, *uv = uy + P.m;
     CK(cudaMemcpyAsync(ua, s.W.ua, sizeof(double) * P.n_c, cudaMemcpyDeviceToDevice, st));
     k_slot_out<<<s.grid_nd, kBlock, 0, st>>>(P, rs, rv, ua, ub, uv);
@@ -440,20 +479,13 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
       CKL();
       ++nl;
     }
-    k_spmv_seg<<<s.grid_seg, kBlock, 0, st>>>(s.P, s.W.t, s.W.qseg);
-    CKL();
-    ++nl;
-    if (h->multi()) {
-      k_rowsum_seg<<<s.grid_m, kBlock, 0, st>>>(s.P, s.W.qseg, s.W.qbuf);
-      CKL();
-      ++nl;
-    }
+    RC(launch_aq(h, s, st, &nl));
   }
   mark(PS_SPMV);
   RC(reduce(h, BUF_Q, h->sh[0].P.m));
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
-    k_schur<<<s.grid_schur, kBlock, s.schur_smem, st>>>(s.P, s.W.qseg, h->multi() ? s.W.qbuf : nullptr,
+    k_schur<<<s.grid_schur, kBlock, s.schur_smem, st>>>(s.P, s.W.qseg, q_in_buf(h, s) ? s.W.qbuf : nullptr,
                                                         s.W.ry, s.W.qp);
     CKL();
     ++nl;
@@ -461,11 +493,10 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
   mark(PS_SCHUR);
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
-    k_ua<true><<<s.grid_nc, kBlock, 0, st>>>(s.P, s.W, s.W.qp);
-    CKL();
+    RC(launch_ua(h, s, st, true));
     ++nl;
     if (h->multi()) {
-      k_sum_parts<<<1, 1024, 0, st>>>(s.W.part, s.grid_nc, s.W.red);
+      k_sum_parts<<<1, 1024, 0, st>>>(s.W.part, s.grid_ua, s.W.red);
       CKL();
       ++nl;
     }
@@ -483,7 +514,7 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
   mark(PS_COMM);
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
-    k_scalars<<<1, 1024, 0, st>>>(s.P, s.S, s.W, s.grid_nc, exact ? 1 : 0, s.d_tmp3,
+    k_scalars<<<1, 1024, 0, st>>>(s.P, s.S, s.W, s.grid_ua, exact ? 1 : 0, s.d_tmp3,
                                   h->multi() ? s.W.red : nullptr);
     CKL();
     ++nl;
@@ -1068,6 +1099,8 @@ int build_csc_device(hsde_handle *h, int m, int n_c, int64_t nnz, const int64_t 
   return 0;
 }
 
+#include "hsde_setup_half.cuh"
+
 int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   SetupTimer tick;
   const int m = d->m, n_c = d->n_c, p = d->p;
@@ -1242,6 +1275,8 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   P.heavy = heavy_d;
   P.n_heavy = (int)heavy.size();
   tick("  uploads");
+  RC(build_half(h, s));
+  tick("  half-pass layouts");
   // state + work
   const int64_t T = P.total;
   RC(dalloc(h, &s.S.u, T));
@@ -1277,6 +1312,15 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   CK(cudaMemset(s.W.sweeps, 0, sizeof(int) * std::max(p, 1)));
   CK(cudaMemset(s.d_chk, 0, sizeof(double) * 64));
   s.grid_nc = grid_for(n_c);
+  s.grid_ua = s.grid_nc;
+  if (P.half) {
+    s.grid_ua = std::max(1, std::min(148 * 8, (P.n_slice + 7) / 8));
+    const int sm = (int)(sizeof(double) * (size_t)m);
+    if (sm > 48 * 1024) {
+      CK(cudaFuncSetAttribute(k_ua_half<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_ua_half<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    }
+  }
   s.grid_nd = grid_for(n_d);
   s.grid_m = grid_for(m);
   s.grid_T = grid_for(T);
@@ -1452,6 +1496,8 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
   h->info.max_clique = maxd;
   h->info.n_shards = nshards;
   h->info.mode = h->mode;
+  h->info.half_passes = 1;
+  for (auto &s : h->sh) h->info.half_passes &= s.P.half;
   if (h->factor) {
     // graph of check_interval - 1 iterations: hsde_iterate(check_interval)
     // = one replay + snapshot + the single-iteration graph

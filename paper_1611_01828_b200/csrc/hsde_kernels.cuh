@@ -75,6 +75,21 @@ struct DevProblem {
   int lead;            // 1 on the shard that contributes replicated terms (y, tau)
   const int64_t *cl_off;
   const int *cl_size;
+  // symmetric half passes: when every column of A equals its
+  // mirror's (A_ij = A_ji, the symmetric constraint matrices of an SDP), the
+  // two A passes run over one column per mirror pair {l, mirror(l)}:
+  //   A t = sum_pairs A_l (t_l + t_mirror),   (A' g)_l = (A' g)_mirror
+  int half;              // 1: enabled
+  int n_pair;
+  const int *pair_l, *pair_m;  // [n_pair] representative (l <= mirror) and mirror
+  int n_slice;           // SELL-32 slices of 32 pairs (A' g)
+  const int64_t *sl_beg; // [n_slice + 1]; element k of lane j at sl_beg[s] + 32 k + j
+  const uint16_t *sl_row;
+  const double *sl_val;
+  int rt_ntile, rt_G;    // row-SELL tiles of kRowTile pairs x groups of 32 rows (A t),
+  const int64_t *rt_beg; // owned pairs only; [rt_ntile * rt_G + 1]
+  const uint16_t *rt_col;// column within the tile
+  const double *rt_val;
   // data of the iterated (normalised) problem
   const double *c, *b, *p_inv;
   // Schur inverse: dense m x m (row-major, symmetric) or diagonal m
@@ -91,6 +106,8 @@ struct DevState {
 
 struct DevWork {
   double *t, *ua;      // [n_c]
+  double *rtpart;      // [m * rt_ntile] tile partials of A t (half passes)
+  double *xq;          // [n_pair] t_l + t_mirror (half passes)
   double *ry;          // [m] rho_y of the current iteration
   double *qseg;        // [nseg]
   double *qp;          // [m]
@@ -302,6 +319,100 @@ __global__ void __launch_bounds__(kBlock) k_ua(DevProblem P, DevWork W, const do
     const double ua = W.t[l] - atq * P.p_inv[l];
     W.ua[l] = ua;
     if (WITH_DOT && owns(P, l)) dot += P.c[l] * ua;
+  }
+  if (WITH_DOT) {
+    dot = block_sum(dot, sh);
+    if (threadIdx.x == 0) W.part[blockIdx.x] = dot;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Half passes over mirror pairs (P.half).  Both stream A in 16-bit-index
+// SELL layouts: every load is a coalesced 32-lane access.
+
+constexpr int kRowTile = 4096;  // pairs per row-SELL tile (16-bit column index)
+constexpr int kRowTileSplit = 4;  // CTAs per tile (row groups split among them)
+
+// pair values x_q = t_l + t_mirror (t_l on the diagonal)
+__global__ void k_pair_sum(DevProblem P, const double *__restrict__ t, double *__restrict__ xq) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < P.n_pair; q += gridDim.x * blockDim.x) {
+    const int l = P.pair_l[q], mm = P.pair_m[q];
+    xq[q] = mm != l ? t[l] + t[mm] : t[l];
+  }
+}
+
+// q0 partials: part[r * ntile + tile] = sum over the tile's owned pairs of
+// A_r,pair x_pair; the tile's pair values are staged in shared memory.
+__global__ void __launch_bounds__(kBlock) k_spmv_half(DevProblem P, const double *__restrict__ xq,
+                                                       double *__restrict__ part) {
+  __shared__ double xs[kRowTile];
+  const int tile = blockIdx.x / kRowTileSplit, rr = blockIdx.x - tile * kRowTileSplit;
+  const int q0 = tile * kRowTile, wn = min(kRowTile, P.n_pair - q0);
+  for (int i = threadIdx.x; i < wn; i += blockDim.x) xs[i] = xq[q0 + i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int G = P.rt_G;
+  for (int gr = rr * nw + (threadIdx.x >> 5); gr < G; gr += kRowTileSplit * nw) {
+    const int64_t b = P.rt_beg[(int64_t)tile * G + gr], e = P.rt_beg[(int64_t)tile * G + gr + 1];
+    double a0 = 0.0, a1 = 0.0;
+    int64_t k = b + lane;
+#pragma unroll 4
+    for (; k + 32 < e; k += 64) {
+      a0 += __ldcs(P.rt_val + k) * xs[__ldcs(P.rt_col + k)];
+      a1 += __ldcs(P.rt_val + k + 32) * xs[__ldcs(P.rt_col + k + 32)];
+    }
+    if (k < e) a0 += __ldcs(P.rt_val + k) * xs[__ldcs(P.rt_col + k)];
+    const int r = gr * 32 + lane;
+    if (r < P.m) part[(int64_t)r * P.rt_ntile + tile] = a0 + a1;
+  }
+}
+
+// q0_r = ordered sum of the row's tile partials (one warp per row)
+__global__ void k_rowsum_tiles(DevProblem P, const double *__restrict__ part, double *__restrict__ q) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < P.m; r += warps) {
+    double a = 0.0;
+    for (int t = lane; t < P.rt_ntile; t += 32) a += part[(int64_t)r * P.rt_ntile + t];
+    a = warp_sum(a);
+    if (lane == 0) q[r] = a;
+  }
+}
+
+// ua = t0 - P^{-1} A' g over mirror pairs (one warp per SELL slice, lane =
+// pair), g staged in shared memory; WITH_DOT: block partials of c.ua (owned)
+template <bool WITH_DOT>
+__global__ void __launch_bounds__(kBlock) k_ua_half(DevProblem P, DevWork W, const double *__restrict__ g) {
+  extern __shared__ double sg[];
+  __shared__ double sh[32];
+  for (int i = threadIdx.x; i < P.m; i += blockDim.x) sg[i] = g[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  double dot = 0.0;
+  for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < P.n_slice; sl += warps) {
+    const int64_t b = P.sl_beg[sl], e = P.sl_beg[sl + 1];
+    double a0 = 0.0, a1 = 0.0;
+    int64_t k = b + lane;
+#pragma unroll 4
+    for (; k + 32 < e; k += 64) {
+      a0 += __ldcs(P.sl_val + k) * sg[__ldcs(P.sl_row + k)];
+      a1 += __ldcs(P.sl_val + k + 32) * sg[__ldcs(P.sl_row + k + 32)];
+    }
+    if (k < e) a0 += __ldcs(P.sl_val + k) * sg[__ldcs(P.sl_row + k)];
+    const double atg = a0 + a1;
+    const int q = sl * 32 + lane;
+    if (q < P.n_pair) {
+      const int l = P.pair_l[q], mm = P.pair_m[q];
+      const double ul = W.t[l] - atg * P.p_inv[l];
+      W.ua[l] = ul;
+      if (WITH_DOT && owns(P, l)) dot += P.c[l] * ul;
+      if (mm != l) {
+        const double um = W.t[mm] - atg * P.p_inv[mm];
+        W.ua[mm] = um;
+        if (WITH_DOT && owns(P, mm)) dot += P.c[mm] * um;
+      }
+    }
   }
   if (WITH_DOT) {
     dot = block_sum(dot, sh);

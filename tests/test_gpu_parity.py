@@ -340,3 +340,48 @@ def test_project_cone_clique_orders():
         w, v = np.linalg.eigh(0.5 * (b + b.T))
         want = (v * np.maximum(w, 0.0)) @ v.T
         assert rel(s_out[o0:o1], want.ravel()) <= 1e-12, d
+
+
+@pytest.mark.parametrize("cfg", [0, 2, 4])
+def test_half_passes_match_full_passes(cfg, monkeypatch):
+    """A passes over mirror pairs (symmetric constraint matrices) vs the
+    full-column passes: same iterate after 60 iterations to 1e-10."""
+    from paper_1611_01828_b200 import _lib
+
+    cp = make_config(cfg)
+    res = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("HSDE_NO_HALF", "1")
+        h = _lib.Handle(cp)
+        assert h.half_passes == (not off)
+        h.iterate(60)
+        res.append(h.get_state()[0])
+        h.close()
+    assert rel(res[0], res[1]) <= 1e-10
+
+
+def test_half_passes_off_for_nonsymmetric_columns():
+    """One A_ij != A_ji entry disables the half passes; the result still
+    matches the oracle."""
+    import dataclasses
+
+    from paper_1611_01828_b200 import _lib
+
+    cp = make_config(0)
+    A = cp.A.copy()
+    A.data[5] += 0.25
+    bad = dataclasses.replace(cp, A=A, _cache={})
+    h = _lib.Handle(bad)
+    assert not h.half_passes
+    h.iterate(100)
+    u = h.get_state()[0]
+    h.close()
+    ref = {}
+
+    def cb(k, p, d, g, tau, kap, uu, w):
+        if k == 100:
+            ref["u"] = uu.copy()
+
+    O.solve(bad, O.OracleSettings(max_iters=100, tol=1e-300), callback=cb)
+    assert rel(u, ref["u"]) <= 1e-9
