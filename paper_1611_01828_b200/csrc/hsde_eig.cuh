@@ -89,6 +89,7 @@ __device__ __forceinline__ int sym_at(int i, int j, int lda) {
 struct JacobiScratch {
   double *A, *Vt;
   double *rc, *rs;  // [2][half] rotation cosines / sines (double buffered)
+  int2 *pq;         // [2][half] players (p, q) of each pair (double buffered)
   double *tt, *lam, *red;
   int *offtab, *pos, *flag;
   int lda, ldv;
@@ -99,7 +100,7 @@ __host__ __device__ inline int64_t jacobi_scratch_doubles(int dp) {
   const int64_t lda = jacobi_lda(dp), ldv = jacobi_ldv(dp), half = dp / 2;
   const int64_t noff = half * (half - 1) / 2;
   const int64_t ints = noff + dp + 1 + 2;
-  const int64_t n = dp * lda + dp * ldv + 4 * half + half + dp + 32 + (ints + 1) / 2 + 2;
+  const int64_t n = dp * lda + dp * ldv + 4 * half + 2 * half + half + dp + 32 + (ints + 1) / 2 + 2;
   return (n + 1) & ~int64_t(1);  // keep per-warp slices 16-byte aligned
 }
 
@@ -112,7 +113,8 @@ __device__ inline JacobiScratch jacobi_carve(double *base, int dp) {
   s.Vt = s.A + dp * s.lda;  // dp even -> 16-byte aligned
   s.rc = s.Vt + dp * s.ldv;
   s.rs = s.rc + 2 * half;
-  s.tt = s.rs + 2 * half;
+  s.pq = reinterpret_cast<int2 *>(s.rs + 2 * half);
+  s.tt = reinterpret_cast<double *>(s.pq + 2 * half);
   s.lam = s.tt + half;
   s.red = s.lam + dp;
   s.offtab = reinterpret_cast<int *>(s.red + 32);
@@ -174,21 +176,22 @@ __device__ void jacobi_norms(const Team &tm, const JacobiScratch &js, int dp, do
   off2 = team_sum(tm, o2, js.red);
 }
 
-// Apply the rotations of round r (parameter buffer b) to the eigenvector rows.
-// Item (k, c): pair k, 16-byte column chunks c and c + nh of rows p_k, q_k;
-// consecutive threads take consecutive pairs (rows of consecutive players ->
-// distinct bank groups, see jacobi_ldv).  Threads [first, team size).
+// Apply the rotations of parameter buffer b (one round) to the eigenvector
+// rows.  Item (k, c): pair k, 16-byte column chunks c + j nq (j < 4) of rows
+// p_k, q_k; consecutive threads take consecutive pairs (rows of consecutive
+// players -> distinct bank groups, see jacobi_ldv).  Threads [first, size).
 template <class Team>
 __device__ __forceinline__ void jacobi_vupdate(const Team &tm, JacobiScratch &js, int d, int dp,
-                                               int r, int b, int first) {
+                                               int b, int first) {
   const int T = tm.size() - first;
   const int me = tm.rank - first;
   if (me < 0) return;
   const int half = dp / 2;
-  const int n2 = (d + 1) >> 1;       // 16-byte chunks per row
-  const int nh = (n2 + 1) >> 1;      // chunk pairs
-  const int total = half * nh;
+  const int n2 = (d + 1) >> 1;   // 16-byte chunks per row
+  const int nq = (n2 + 3) >> 2;  // items per pair
+  const int total = half * nq;
   const double *rc = js.rc + b * half, *rs = js.rs + b * half;
+  const int2 *pq = js.pq + b * half;
   const int dk = T % half, dc = T / half;
   int c = me / half, k = me - (me / half) * half;
   for (int it = me; it < total; it += T, k += dk, c += dc) {
@@ -196,20 +199,18 @@ __device__ __forceinline__ void jacobi_vupdate(const Team &tm, JacobiScratch &js
       k -= half;
       ++c;
     }
-    const double sn = rs[k];
-    if (sn == 0.0) continue;
-    const double cs = rc[k];
-    const int p = tour_player(k, r, dp), q = tour_player(dp - 1 - k, r, dp);
-    double2 *vp = reinterpret_cast<double2 *>(js.Vt + p * js.ldv);
-    double2 *vq = reinterpret_cast<double2 *>(js.Vt + q * js.ldv);
-    const bool two = c + nh < n2;
-    const double2 p0 = vp[c], q0 = vq[c];
-    const double2 p1 = two ? vp[c + nh] : p0, q1 = two ? vq[c + nh] : q0;
-    vp[c] = make_double2(cs * p0.x - sn * q0.x, cs * p0.y - sn * q0.y);
-    vq[c] = make_double2(sn * p0.x + cs * q0.x, sn * p0.y + cs * q0.y);
-    if (two) {
-      vp[c + nh] = make_double2(cs * p1.x - sn * q1.x, cs * p1.y - sn * q1.y);
-      vq[c + nh] = make_double2(sn * p1.x + cs * q1.x, sn * p1.y + cs * q1.y);
+    const double sn = rs[k], cs = rc[k];
+    const int2 pk = pq[k];
+    double2 *vp = reinterpret_cast<double2 *>(js.Vt + pk.x * js.ldv);
+    double2 *vq = reinterpret_cast<double2 *>(js.Vt + pk.y * js.ldv);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cc = c + j * nq;
+      if (cc < n2) {
+        const double2 p0 = vp[cc], q0 = vq[cc];
+        vp[cc] = make_double2(cs * p0.x - sn * q0.x, cs * p0.y - sn * q0.y);
+        vq[cc] = make_double2(sn * p0.x + cs * q0.x, sn * p0.y + cs * q0.y);
+      }
     }
   }
 }
@@ -254,6 +255,7 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
     for (int r = 0; r < dp - 1; ++r, ++round) {
       const int b = round & 1;
       double *rc = js.rc + b * half, *rs = js.rs + b * half;
+      int2 *pq = js.pq + b * half;
       // ---- phase P: parameters of round r | eigenvector update of round r-1
       for (int k = tm.rank; k < half; k += T) {
         const int p = tour_player(k, r, dp), q = tour_player(dp - 1 - k, r, dp);
@@ -270,22 +272,20 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
         }
         rc[k] = c;
         rs[k] = s;
+        pq[k] = make_int2(p, q);
         js.tt[k] = t;
       }
-      if (pending) jacobi_vupdate(tm, js, d, dp, r == 0 ? dp - 2 : r - 1, b ^ 1, vfirst);
+      if (pending) jacobi_vupdate(tm, js, d, dp, b ^ 1, vfirst);
       tm.sync();
       // ---- phase A: off-diagonal 2x2 blocks (upper triangle), then the
       // diagonal blocks
       for (int it = tm.rank; it < noff; it += T) {
         const int kl = js.offtab[it];
         const int k = kl & 0xffff, l = kl >> 16;
-        const double sk = rs[k], sl = rs[l];
-        if (sk == 0.0 && sl == 0.0) continue;
-        const double ck = rc[k], cl = rc[l];
-        const int pk = tour_player(k, r, dp), qk = tour_player(dp - 1 - k, r, dp);
-        const int pl = tour_player(l, r, dp), ql = tour_player(dp - 1 - l, r, dp);
-        const int i_pp = sym_at(pk, pl, lda), i_pq = sym_at(pk, ql, lda);
-        const int i_qp = sym_at(qk, pl, lda), i_qq = sym_at(qk, ql, lda);
+        const double sk = rs[k], sl = rs[l], ck = rc[k], cl = rc[l];
+        const int2 PK = pq[k], PL = pq[l];
+        const int i_pp = sym_at(PK.x, PL.x, lda), i_pq = sym_at(PK.x, PL.y, lda);
+        const int i_qp = sym_at(PK.y, PL.x, lda), i_qq = sym_at(PK.y, PL.y, lda);
         const double a = A[i_pp], bb = A[i_pq], cc = A[i_qp], ee = A[i_qq];
         const double r_pp = ck * a - sk * cc, r_pq = ck * bb - sk * ee;
         const double r_qp = sk * a + ck * cc, r_qq = sk * bb + ck * ee;
@@ -297,11 +297,11 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
       for (int k = tm.rank; k < half; k += T) {
         const double t = js.tt[k];
         if (t == 0.0) continue;
-        const int p = tour_player(k, r, dp), q = tour_player(dp - 1 - k, r, dp);
-        const int ipq = sym_at(p, q, lda);
+        const int2 PK = pq[k];
+        const int ipq = sym_at(PK.x, PK.y, lda);
         const double apq = A[ipq];
-        A[p * lda + p] -= t * apq;
-        A[q * lda + q] += t * apq;
+        A[PK.x * lda + PK.x] -= t * apq;
+        A[PK.y * lda + PK.y] += t * apq;
         A[ipq] = 0.0;
       }
       pending = true;
@@ -316,7 +316,7 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
       break;  // every pair below the rotation threshold
     }
   }
-  if (pending) jacobi_vupdate(tm, js, d, dp, (round - 1) % (dp - 1), (round - 1) & 1, 0);
+  if (pending) jacobi_vupdate(tm, js, d, dp, (round - 1) & 1, 0);
   // restore the strict lower triangle
   for (int e = tm.rank; e < dp * dp; e += T) {
     const int i = e / dp, j = e - i * dp;

@@ -319,7 +319,7 @@ def test_project_cone_clique_orders():
 
     from paper_1611_01828_b200.problem import CliqueDecomposition, DecomposedProblem
 
-    sizes = [2, 3, 7, 16, 17, 31, 32, 33, 40, 47, 64, 80, 81, 96, 113]
+    sizes = [2, 3, 7, 16, 17, 31, 32, 33, 40, 47, 64, 80, 81, 96, 111]
     n = sum(sizes)
     cl, o = [], 0
     for d in sizes:
