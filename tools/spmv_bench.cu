@@ -141,6 +141,60 @@ __global__ void __launch_bounds__(NW * 32) k_csc_seg2(int n, int m, const int64_
   }
 }
 
+// ---- A' g, SELL-32: slice s of 32 columns, element k of lane j at
+// sb[s] + 32 k + j (padded with zeros to the slice's longest column)
+template <class K>
+__global__ void __launch_bounds__(256) k_sell_col(int n, int m, const int64_t *sb, const K *idx,
+                                                   const double *val, const double *g, double *out) {
+  extern __shared__ double sg[];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) sg[i] = g[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nsl = (n + 31) >> 5;
+  for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < nsl; sl += (gridDim.x * blockDim.x) >> 5) {
+    const int64_t b = sb[sl], e = sb[sl + 1];
+    double a0 = 0.0, a1 = 0.0;
+    int64_t k = b + lane;
+#pragma unroll 4
+    for (; k + 32 < e; k += 64) {
+      a0 += __ldcs(val + k) * sg[__ldcs(idx + k)];
+      a1 += __ldcs(val + k + 32) * sg[__ldcs(idx + k + 32)];
+    }
+    if (k < e) a0 += __ldcs(val + k) * sg[__ldcs(idx + k)];
+    const int l = sl * 32 + lane;
+    if (l < n) out[l] = a0 + a1;
+  }
+}
+
+// ---- A t, row-SELL tiles: tile t of W columns, row group gr of 32 rows;
+// element k of lane j (row 32 gr + j) at tb[t G + gr] + 32 k + j, local column
+// index (16 bit) into the staged x tile; part[row * ntile + t]
+template <int W>
+__global__ void __launch_bounds__(256) k_sell_row(int n, int m, int ntile, const int64_t *tb,
+                                                   const uint16_t *lcol, const double *val,
+                                                   const double *x, double *part, int rg) {
+  __shared__ double xs[W];
+  const int G = (m + 31) >> 5;
+  const int t = blockIdx.x / rg, rr = blockIdx.x - t * rg;
+  const int c0 = t * W, wn = min(W, n - c0);
+  for (int i = threadIdx.x; i < wn; i += blockDim.x) xs[i] = x[c0 + i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int gr = rr * (blockDim.x >> 5) + (threadIdx.x >> 5); gr < G; gr += rg * (blockDim.x >> 5)) {
+    const int64_t b = tb[(int64_t)t * G + gr], e = tb[(int64_t)t * G + gr + 1];
+    double a0 = 0.0, a1 = 0.0;
+    int64_t k = b + lane;
+#pragma unroll 4
+    for (; k + 32 < e; k += 64) {
+      a0 += __ldcs(val + k) * xs[__ldcs(lcol + k)];
+      a1 += __ldcs(val + k + 32) * xs[__ldcs(lcol + k + 32)];
+    }
+    if (k < e) a0 += __ldcs(val + k) * xs[__ldcs(lcol + k)];
+    const int r = gr * 32 + lane;
+    if (r < m) part[(int64_t)r * ntile + t] = a0 + a1;
+  }
+}
+
 // ---- A t: row-split CSR, global gather (current k_spmv_seg)
 __global__ void k_csr_seg(int nseg, const int *seg_row, const int64_t *seg_beg, const int64_t *rp,
                           const int *col, const double *val, const double *x, double *qseg) {
@@ -382,6 +436,76 @@ int main(int argc, char **argv) {
   for (int g : {nsm * 2, nsm * 4, nsm * 8, nsm * 16}) {
     ms = timeit([&] { k_stream<<<g, 256>>>((const double2 *)d_val, nnz / 2, d_y); });
     printf("stream read val g=%d  %8.1f us  %7.0f GB/s\n", g, ms * 1e3, nnz * 8.0 / ms / 1e6);
+  }
+  {
+    // SELL-32 columns
+    const int nsl = (n + 31) / 32;
+    std::vector<int64_t> sb(nsl + 1, 0);
+    for (int sl = 0; sl < nsl; ++sl) {
+      int64_t w = 0;
+      for (int l = sl * 32; l < std::min(n, sl * 32 + 32); ++l) w = std::max(w, cp[l + 1] - cp[l]);
+      sb[sl + 1] = sb[sl] + 32 * w;
+    }
+    std::vector<uint16_t> si(sb[nsl], 0);
+    std::vector<double> sv(sb[nsl], 0.0);
+    for (int l = 0; l < n; ++l) {
+      const int sl = l / 32, j = l % 32;
+      for (int64_t e = cp[l]; e < cp[l + 1]; ++e) {
+        si[sb[sl] + 32 * (e - cp[l]) + j] = (uint16_t)row[e];
+        sv[sb[sl] + 32 * (e - cp[l]) + j] = val[e];
+      }
+    }
+    printf("SELL col padding %.3f\n", (double)sb[nsl] / nnz);
+    int64_t *d_sb = up(sb);
+    uint16_t *d_si = up(si);
+    double *d_sv = up(sv);
+    for (int blocks : {nsm * 4, nsm * 8, nsm * 16}) {
+      ms = timeit([&] { k_sell_col<uint16_t><<<blocks, 256, m * 8>>>(n, m, d_sb, d_si, d_sv, d_g, d_y); });
+      char nm[64];
+      snprintf(nm, 64, "SELL-32 col g=%d", blocks);
+      chk_y(nm, ms, sb[nsl] * 10.0 + 8.0 * n);
+    }
+    // row-SELL tiles
+    constexpr int W2 = 4096;
+    const int nt2 = (n + W2 - 1) / W2, G = (m + 31) / 32;
+    std::vector<std::vector<std::pair<int, double>>> cell((size_t)nt2 * m);
+    for (int l = 0; l < n; ++l)
+      for (int64_t e = cp[l]; e < cp[l + 1]; ++e)
+        cell[(size_t)(l / W2) * m + row[e]].push_back({l % W2, val[e]});
+    std::vector<int64_t> tb((size_t)nt2 * G + 1, 0);
+    for (int t = 0; t < nt2; ++t)
+      for (int gr = 0; gr < G; ++gr) {
+        size_t w = 0;
+        for (int r = gr * 32; r < std::min(m, gr * 32 + 32); ++r) w = std::max(w, cell[(size_t)t * m + r].size());
+        tb[(size_t)t * G + gr + 1] = tb[(size_t)t * G + gr] + 32 * (int64_t)w;
+      }
+    const int64_t tot = tb[(size_t)nt2 * G];
+    std::vector<uint16_t> ti(tot, 0);
+    std::vector<double> tv(tot, 0.0);
+    for (int t = 0; t < nt2; ++t)
+      for (int r = 0; r < m; ++r) {
+        const auto &c = cell[(size_t)t * m + r];
+        const int64_t base = tb[(size_t)t * G + r / 32];
+        for (size_t k = 0; k < c.size(); ++k) {
+          ti[base + 32 * k + r % 32] = (uint16_t)c[k].first;
+          tv[base + 32 * k + r % 32] = c[k].second;
+        }
+      }
+    printf("row-SELL padding %.3f\n", (double)tot / nnz);
+    int64_t *d_tb = up(tb);
+    uint16_t *d_ti = up(ti);
+    double *d_tv = up(tv);
+    for (int rg : {1, 2, 4}) {
+      ms = timeit([&] {
+        k_sell_row<W2><<<nt2 * rg, 256>>>(n, m, nt2, d_tb, d_ti, d_tv, d_x, d_part, rg);
+        k_rowsum<<<(m * 32 + 255) / 256, 256>>>(m, nt2, d_part, d_q);
+      });
+      char nm[64];
+      snprintf(nm, 64, "row-SELL W=4096 rg=%d (+rowsum)", rg);
+      chk_q(nm, ms, tot * 10.0 + 8.0 * n, false);
+    }
+    ms = timeit([&] { k_rowsum<<<(m * 32 + 255) / 256, 256>>>(m, nt2, d_part, d_q); });
+    printf("rowsum only %.1f us\n", ms * 1e3);
   }
   // pure streaming reference: read val once
   ms = timeit([&] { k_csc_thread<<<nsm * 8, 256>>>(0, d_cp, d_row, d_val, d_g, d_y); });
