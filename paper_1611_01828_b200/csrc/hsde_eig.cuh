@@ -25,7 +25,7 @@
 // rotates nothing (absolute accuracy is what the projection needs: the
 // error of P is bounded by the remaining off-diagonal mass).
 //
-// Warm start (CTA teams, hot path): ADMM iterates move slowly, so the
+// Warm start (hot path): ADMM iterates move slowly, so the
 // previous iteration's eigenvectors V nearly diagonalise the new block.  The
 // kernel forms B = V X V' with two register-tiled shared-memory GEMMs and runs
 // Jacobi on B starting from V: ~3 sweeps instead of ~10.  V is refreshed by
@@ -45,6 +45,9 @@ struct BlockTeam {
   __device__ int size() const { return n; }
   __device__ void sync() const { __syncthreads(); }
 };
+// GEMM tiles per thread: a warp covers d <= 32 (8 x 8 tiles of 4 x 4) with two
+template <class Team> struct TeamTiles { static constexpr int value = 1; };
+template <> struct TeamTiles<WarpTeam> { static constexpr int value = 2; };
 
 // sum over the team, returned to every member
 template <class Team>
@@ -328,99 +331,123 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
 
 // ---------------------------------------------------------------------------
 // register-tiled team GEMMs on d x d shared-memory operands.
-// Thread t owns the interleaved 4x4 tile rows {u + nt a}, cols {v + nt b},
-// u = t / nt, v = t % nt, nt = ceil(d / 4): consecutive threads read
-// consecutive rows of R, so R must use an odd leading dimension.
-// Requires nt * nt <= team size.
+// Thread t owns the interleaved 4x4 tiles (u, v) = (q / nt, q % nt) for
+// q = t, t + T, ... (MT tiles at most): rows {u + nt a}, cols {v + nt b},
+// nt = ceil(d / 4); consecutive threads read consecutive rows of R, so R
+// should use an odd leading dimension.  Requires nt * nt <= MT * team size.
+
+template <int MT>
+struct GemmTiles {
+  int u[MT], v[MT];
+  bool on[MT];
+};
+
+template <int MT, class Team>
+__device__ __forceinline__ GemmTiles<MT> gemm_tiles(const Team &tm, int nt) {
+  GemmTiles<MT> g;
+#pragma unroll
+  for (int q = 0; q < MT; ++q) {
+    const int t = tm.rank + q * tm.size();
+    g.on[q] = t < nt * nt;
+    g.u[q] = g.on[q] ? t / nt : 0;
+    g.v[q] = g.on[q] ? t - g.u[q] * nt : 0;
+  }
+  return g;
+}
 
 // out = L * R'   (out[i][j] = sum_k L[i][k] R[j][k]); out may alias L or R.
-template <class Team>
+template <int MT = 1, class Team>
 __device__ void team_gemm_nt(const Team &tm, const double *L, int ldl, const double *R, int ldr,
                              double *out, int ldo, int d) {
   const int nt = (d + 3) >> 2;
-  const int t = tm.rank;
-  const bool active = t < nt * nt;
-  const int u = active ? t / nt : 0, v = active ? t - u * nt : 0;
-  double acc[4][4];
+  const GemmTiles<MT> g = gemm_tiles<MT>(tm, nt);
+  double acc[MT][4][4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  if (active) {
-    int ri[4], rj[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      ri[a] = min(u + nt * a, d - 1) * ldl;
-      rj[a] = min(v + nt * a, d - 1) * ldr;
-    }
-    for (int k = 0; k < d; ++k) {
-      double l[4], r[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        l[a] = L[ri[a] + k];
-        r[a] = R[rj[a] + k];
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(l[a], r[b], acc[a][b]);
-    }
-  }
-  tm.sync();
-  if (active) {
+  for (int q = 0; q < MT; ++q) {
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int i = u + nt * a, j = v + nt * b;
-        if (i < d && j < d) out[i * ldo + j] = acc[a][b];
+      for (int b = 0; b < 4; ++b) acc[q][a][b] = 0.0;
+    if (g.on[q]) {
+      int ri[4], rj[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ri[a] = min(g.u[q] + nt * a, d - 1) * ldl;
+        rj[a] = min(g.v[q] + nt * a, d - 1) * ldr;
       }
+      for (int k = 0; k < d; ++k) {
+        double l[4], r[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          l[a] = L[ri[a] + k];
+          r[a] = R[rj[a] + k];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[q][a][b] = fma(l[a], r[b], acc[q][a][b]);
+      }
+    }
   }
+  tm.sync();
+#pragma unroll
+  for (int q = 0; q < MT; ++q)
+    if (g.on[q]) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = g.u[q] + nt * a, j = g.v[q] + nt * b;
+          if (i < d && j < d) out[i * ldo + j] = acc[q][a][b];
+        }
+    }
   tm.sync();
 }
 
 // P = W' V over the first r rows (P[i][j] = sum_k W[k][i] V[vrow[k]][j]),
 // symmetric output: tiles with u <= v compute; every unordered pair {i, j}
 // is emitted exactly once (caller mirrors).
-template <class Team, class Emit>
+template <int MT = 1, class Team, class Emit>
 __device__ void team_gemm_tn_sym(const Team &tm, const double *W, int ldw, const double *V,
                                  int ldv, const int *vrow, int r, int d, Emit emit) {
   const int nt = (d + 3) >> 2;
-  const int t = tm.rank;
-  if (t >= nt * nt) return;
-  const int u = t / nt, v = t - u * nt;
-  if (u > v) return;
-  double acc[4][4];
+  const GemmTiles<MT> g = gemm_tiles<MT>(tm, nt);
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int q = 0; q < MT; ++q) {
+    if (!g.on[q] || g.u[q] > g.v[q]) continue;
+    const int u = g.u[q], v = g.v[q];
+    double acc[4][4];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  int ci[4], cj[4];
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    ci[a] = min(u + nt * a, d - 1);
-    cj[a] = min(v + nt * a, d - 1);
-  }
-  for (int k = 0; k < r; ++k) {
-    double w[4], x[4];
-    const int vk = (vrow ? vrow[k] : k) * ldv;
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    int ci[4], cj[4];
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      w[a] = W[k * ldw + ci[a]];
-      x[a] = V[vk + cj[a]];
+      ci[a] = min(u + nt * a, d - 1);
+      cj[a] = min(v + nt * a, d - 1);
+    }
+    for (int k = 0; k < r; ++k) {
+      double w[4], x[4];
+      const int vk = (vrow ? vrow[k] : k) * ldv;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        w[a] = W[k * ldw + ci[a]];
+        x[a] = V[vk + cj[a]];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = fma(w[a], x[b], acc[a][b]);
+      for (int b = 0; b < 4; ++b) {
+        const int i = u + nt * a, j = v + nt * b;
+        if (i < d && j < d && (u < v || i <= j)) emit(i, j, acc[a][b]);
+      }
   }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = u + nt * a, j = v + nt * b;
-      if (i < d && j < d && (u < v || i <= j)) emit(i, j, acc[a][b]);
-    }
 }
 
 // compacted positive eigenvalues (warp 0 ballot, ascending position order)
@@ -488,48 +515,51 @@ __device__ void psd_rebuild(const Team &tm, JacobiScratch &js, int d, Emit emit)
 }
 
 // out = L * R   (out[i][j] = sum_k L[i][k] R[k][j]); out may alias L.
-template <class Team>
+template <int MT = 1, class Team>
 __device__ void team_gemm_nn(const Team &tm, const double *L, int ldl, const double *R, int ldr,
                              double *out, int ldo, int d) {
   const int nt = (d + 3) >> 2;
-  const int t = tm.rank;
-  const bool active = t < nt * nt;
-  const int u = active ? t / nt : 0, v = active ? t - u * nt : 0;
-  double acc[4][4];
+  const GemmTiles<MT> g = gemm_tiles<MT>(tm, nt);
+  double acc[MT][4][4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-  if (active) {
-    int ri[4], cj[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      ri[a] = min(u + nt * a, d - 1) * ldl;
-      cj[a] = min(v + nt * a, d - 1);
-    }
-    for (int k = 0; k < d; ++k) {
-      double l[4], r[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        l[a] = L[ri[a] + k];
-        r[a] = R[k * ldr + cj[a]];
-      }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fma(l[a], r[b], acc[a][b]);
-    }
-  }
-  tm.sync();
-  if (active) {
+  for (int q = 0; q < MT; ++q) {
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int i = u + nt * a, j = v + nt * b;
-        if (i < d && j < d) out[i * ldo + j] = acc[a][b];
+      for (int b = 0; b < 4; ++b) acc[q][a][b] = 0.0;
+    if (g.on[q]) {
+      int ri[4], cj[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ri[a] = min(g.u[q] + nt * a, d - 1) * ldl;
+        cj[a] = min(g.v[q] + nt * a, d - 1);
       }
+      for (int k = 0; k < d; ++k) {
+        double l[4], r[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          l[a] = L[ri[a] + k];
+          r[a] = R[k * ldr + cj[a]];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[q][a][b] = fma(l[a], r[b], acc[q][a][b]);
+      }
+    }
   }
+  tm.sync();
+#pragma unroll
+  for (int q = 0; q < MT; ++q)
+    if (g.on[q]) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = g.u[q] + nt * a, j = g.v[q] + nt * b;
+          if (i < d && j < d) out[i * ldo + j] = acc[q][a][b];
+        }
+    }
   tm.sync();
 }
 
@@ -540,7 +570,7 @@ __device__ void team_gemm_nn(const Team &tm, const double *L, int ldl, const dou
 // smallest |l_i|.  It is exact within same-sign pairs; jacobi_sweeps stops for
 // it only when |E|_F^2 <= 1e-17 |A|_F g and |E|_F <= g / 1000.  P = V' M V with
 // M = diag(l+) + L_D(E) by two team GEMMs.
-template <class Team, class Emit>
+template <int MT, class Team, class Emit>
 __device__ void psd_rebuild_first_order(const Team &tm, JacobiScratch &js, int d, Emit emit) {
   double *A = js.A;
   const int lda = js.lda, ldv = js.ldv;
@@ -562,8 +592,8 @@ __device__ void psd_rebuild_first_order(const Team &tm, JacobiScratch &js, int d
     A[i * lda + j] = m;  // each element read and written by one thread
   }
   tm.sync();
-  team_gemm_nn(tm, A, lda, js.Vt, ldv, A, lda, d);  // T = M Vt
-  team_gemm_tn_sym(tm, js.Vt, ldv, A, lda, nullptr, d, d, [&](int i, int j, double v) {
+  team_gemm_nn<MT>(tm, A, lda, js.Vt, ldv, A, lda, d);  // T = M Vt
+  team_gemm_tn_sym<MT>(tm, js.Vt, ldv, A, lda, nullptr, d, d, [&](int i, int j, double v) {
     emit(i, j, v);
     if (i != j) emit(j, i, v);
   });
@@ -639,7 +669,9 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   const int lda = js.lda, ldv = js.ldv;
   double *A = js.A;
   const int age = (MODE == CONE_HOT && ca.warm) ? W.vvalid[k] : 0;
-  const bool warm = age > 0 && age < kWarmMaxAge && ((d + 3) >> 2) * ((d + 3) >> 2) <= tm.size();
+  constexpr int MT = TeamTiles<Team>::value;
+  const int ntile = (d + 3) >> 2;
+  const bool warm = age > 0 && age < kWarmMaxAge && ntile * ntile <= MT * tm.size();
   if (MODE == CONE_HOT && W.dbg && k == W.dbg_clique) {
     js.dbg = W.dbg;
     if (tm.rank == 0) {
@@ -684,8 +716,8 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   if (warm) {
     // B = V X V' (rows of Vt are the previous eigenvectors): T1 = Vt X, then
     // B' = Vt T1' (= B for symmetric X) with the odd-ld operand on the right
-    team_gemm_nt(tm, js.Vt, ldv, A, lda, A, lda, d);
-    team_gemm_nt(tm, js.Vt, ldv, A, lda, A, lda, d);
+    team_gemm_nt<MT>(tm, js.Vt, ldv, A, lda, A, lda, d);
+    team_gemm_nt<MT>(tm, js.Vt, ldv, A, lda, A, lda, d);
     for (int e = tm.rank; e < d * d; e += tm.size()) {
       const int a = e / d, bcol = e - a * d;
       if (a < bcol) {
@@ -698,8 +730,7 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   }
   // first-order exit for CTA teams whose GEMM tiles fit (not for MINEIG)
   bool first_order = false;
-  const bool fo_ok = MODE != CONE_MINEIG && tm.size() > 32 &&
-                     ((d + 3) >> 2) * ((d + 3) >> 2) <= tm.size();
+  const bool fo_ok = MODE != CONE_MINEIG && ntile * ntile <= MT * tm.size();
   const int sw = jacobi_sweeps(tm, js, d, dp, fo_ok ? &first_order : nullptr);
   if (MODE == CONE_HOT && tm.rank == 0 && W.sweeps) W.sweeps[k] = sw;
   // non-finite eigenvalue -> EigenFailure (symmat.py:162-163)
@@ -728,8 +759,8 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   };
   auto emit_plain = [&](int a, int bcol, double v) { ca.out[off + (int64_t)a * d + bcol] = v; };
   if (first_order) {
-    if (MODE == CONE_HOT) psd_rebuild_first_order(tm, js, d, emit_hot);
-    else psd_rebuild_first_order(tm, js, d, emit_plain);
+    if (MODE == CONE_HOT) psd_rebuild_first_order<MT>(tm, js, d, emit_hot);
+    else psd_rebuild_first_order<MT>(tm, js, d, emit_plain);
   } else {
     if (MODE == CONE_HOT) psd_rebuild(tm, js, d, emit_hot);
     else psd_rebuild(tm, js, d, emit_plain);
@@ -747,9 +778,7 @@ __global__ void __launch_bounds__(kBlock) k_cone_warp(DevProblem P, DevState S, 
   if (gw >= ca.count) return;
   double *scratch = smem + (int64_t)wid * jacobi_scratch_doubles(ca.dpmax);
   WarpTeam tm{(int)(threadIdx.x & 31)};
-  ConeArgs c2 = ca;
-  c2.warm = 0;
-  cone_one<MODE>(tm, P, S, W, c2, ca.ids[gw], scratch);
+  cone_one<MODE>(tm, P, S, W, ca, ca.ids[gw], scratch);
 }
 
 // one CTA per clique (d > 32)
