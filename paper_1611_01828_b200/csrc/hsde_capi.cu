@@ -95,7 +95,7 @@ struct ShardDev {
   DevProblem P{};
   DevState S{};
   DevWork W{};
-  ConePlan warp_plan, block_plan;
+  ConePlan warp_plans[3], block_plan;  // warp teams by size class dp <= 8, 16, 32
   double *d_zeta = nullptr;       // [T-1] (c, 0, -b, 0) normalised
   double *d_prev_u = nullptr, *d_prev_w = nullptr;
   double *d_tmp = nullptr, *d_tmp2 = nullptr, *d_tmp3 = nullptr;  // [T] scratch
@@ -117,6 +117,10 @@ struct ShardDev {
 struct hsde_handle {
   int dev = 0;
   cudaStream_t st = nullptr;
+  // parallel branches for the independent cone launches (size classes, shards)
+  static constexpr int kAux = 4;
+  cudaStream_t aux[kAux] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kAux] = {};
   hsde_settings set{};
   hsde_info_t info{};
   std::vector<void *> bufs;
@@ -520,16 +524,45 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
     ++nl;
   }
   mark(PS_SCALARS);
+  // cone projections: the plans (size classes, shards) are independent, so
+  // they run as parallel branches (fork / join on events; captured as graph
+  // edges) -- except under the per-phase profile, which keeps them in order
+  struct ConeJob {
+    ShardDev *s;
+    const ConePlan *pl;
+    bool block;
+  };
+  std::vector<ConeJob> jobs;
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
-    RC(launch_cone(h, s, CONE_HOT, s.warp_plan, false, nullptr, nullptr, 1.0, st));
-    nl += s.warp_plan.count > 0;
+    for (const ConePlan &wp : s.warp_plans)
+      if (wp.count) jobs.push_back({&s, &wp, false});
   }
-  mark(PS_CONE_WARP);
-  for (int g = 0; g < G; ++g) {
-    ShardDev &s = h->sh[g];
-    RC(launch_cone(h, s, CONE_HOT, s.block_plan, true, nullptr, nullptr, 1.0, st));
-    nl += s.block_plan.count > 0;
+  const size_t n_warp_jobs = jobs.size();
+  for (int g = 0; g < G; ++g)
+    if (h->sh[g].block_plan.count) jobs.push_back({&h->sh[g], &h->sh[g].block_plan, true});
+  nl += (int)jobs.size();
+  if (ev || jobs.size() <= 1) {
+    for (size_t j = 0; j < jobs.size(); ++j) {
+      RC(launch_cone(h, *jobs[j].s, CONE_HOT, *jobs[j].pl, jobs[j].block, nullptr, nullptr, 1.0, st));
+      if (j + 1 == n_warp_jobs) mark(PS_CONE_WARP);
+    }
+    if (n_warp_jobs == 0) mark(PS_CONE_WARP);
+  } else {
+    CK(cudaEventRecord(h->ev_fork, st));
+    // the largest job (CTA plan if any, else the last warp class) stays on st
+    for (size_t j = 0; j + 1 < jobs.size(); ++j) {
+      cudaStream_t a = h->aux[j % hsde_handle::kAux];
+      CK(cudaStreamWaitEvent(a, h->ev_fork, 0));
+      RC(launch_cone(h, *jobs[j].s, CONE_HOT, *jobs[j].pl, jobs[j].block, nullptr, nullptr, 1.0, a));
+    }
+    RC(launch_cone(h, *jobs.back().s, CONE_HOT, *jobs.back().pl, jobs.back().block, nullptr, nullptr, 1.0,
+                   st));
+    for (size_t j = 0; j + 1 < jobs.size() && j < (size_t)hsde_handle::kAux; ++j) {
+      CK(cudaEventRecord(h->ev_join[j], h->aux[j]));
+      CK(cudaStreamWaitEvent(st, h->ev_join[j], 0));
+    }
+    mark(PS_CONE_WARP);
   }
   mark(PS_CONE_BLOCK);
   for (int g = 0; g < G; ++g) {
@@ -591,14 +624,15 @@ int check_err_flag(hsde_handle *h) {
 }
 
 int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
-  std::vector<int> wids, bids;
-  int dpw = 2, dpb = 2;
+  // warp teams in three size classes (scratch sized per class), CTA teams
+  std::vector<int> wids[3], bids;
+  const int wcap[3] = {8, 16, 32};
+  int dpb = 2;
   for (int k = 0; k < p; ++k) {
     const int d = sizes[k];
     const int dp = d + (d & 1);
     if (d <= 32) {
-      wids.push_back(k);
-      dpw = std::max(dpw, dp);
+      wids[dp <= 8 ? 0 : dp <= 16 ? 1 : 2].push_back(k);
     } else {
       bids.push_back(k);
       dpb = std::max(dpb, dp);
@@ -607,15 +641,18 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev);
   if (maxsm <= 0) maxsm = 227 * 1024;
-  s.warp_plan.count = (int)wids.size();
-  s.warp_plan.dpmax = dpw;
-  const size_t per_warp = (size_t)jacobi_scratch_doubles(dpw) * sizeof(double);
-  int pb = 8;
-  while (pb > 1 && per_warp * pb > (size_t)maxsm) pb >>= 1;
-  s.warp_plan.per_block = pb;
-  s.warp_plan.smem = per_warp * pb;
-  if (!wids.empty()) {
-    RC(dupload(h, &s.warp_plan.ids, wids.data(), wids.size()));
+  for (int c = 0; c < 3; ++c) {
+    ConePlan &pl = s.warp_plans[c];
+    pl.count = (int)wids[c].size();
+    pl.dpmax = wcap[c];
+    const size_t per_warp = (size_t)jacobi_scratch_doubles(wcap[c]) * sizeof(double);
+    int pb = 8;
+    while (pb > 1 && per_warp * pb > (size_t)maxsm) pb >>= 1;
+    pl.per_block = pb;
+    pl.smem = per_warp * pb;
+    if (!wids[c].empty()) RC(dupload(h, &pl.ids, wids[c].data(), wids[c].size()));
+  }
+  {
     const int sm = maxsm;  // attribute is per kernel, shared by every shard / handle
     CK(cudaFuncSetAttribute(k_cone_warp<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_warp<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -1372,6 +1409,17 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
     return HSDE_ERR_CUDA;
   }
   retain_pool(h->dev);
+  for (int a = 0; a < hsde_handle::kAux; ++a) {
+    if (cudaStreamCreateWithFlags(&h->aux[a], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_join[a], cudaEventDisableTiming) != cudaSuccess) {
+      h->err = "aux stream / event create failed";
+      return HSDE_ERR_CUDA;
+    }
+  }
+  if (cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+    h->err = "event create failed";
+    return HSDE_ERR_CUDA;
+  }
   if (comm && comm->world >= 1) {  // explicit communicator: NCCL (a 1-rank comm is valid)
     if (nshards != 1) {
       h->err = "NCCL mode takes exactly one shard per rank";
@@ -1572,6 +1620,11 @@ void hsde_destroy(hsde_t *h) {
   for (void *p : h->bufs) pool_free(h, p);
   if (h->st) cudaStreamSynchronize(h->st);
   if (h->h_chk) cudaFreeHost(h->h_chk);
+  for (int a = 0; a < hsde_handle::kAux; ++a) {
+    if (h->aux[a]) cudaStreamDestroy(h->aux[a]);
+    if (h->ev_join[a]) cudaEventDestroy(h->ev_join[a]);
+  }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
 }
@@ -1836,7 +1889,8 @@ int hsde_certificate(hsde_t *h, double *out) {
   auto min_eig = [&](const std::vector<const double *> &blocks, double *res) -> int {
     for (int g = 0; g < G; ++g) {
       ShardDev &s = h->sh[g];
-      RC(launch_cone(h, s, CONE_MINEIG, s.warp_plan, false, blocks[g], s.d_mineig, 1.0, st));
+      for (const ConePlan &wp : s.warp_plans)
+        RC(launch_cone(h, s, CONE_MINEIG, wp, false, blocks[g], s.d_mineig, 1.0, st));
       RC(launch_cone(h, s, CONE_MINEIG, s.block_plan, true, blocks[g], s.d_mineig, 1.0, st));
     }
     double mn = std::numeric_limits<double>::infinity();
@@ -1982,7 +2036,7 @@ int hsde_project_cone(hsde_t *h, const double *in, double *out) {
   CK(cudaMemcpyAsync(s.d_tmp2, s.d_tmp, sizeof(double) * T, cudaMemcpyDeviceToDevice, st));
   const double *sin = s.d_tmp + P.n_c;
   double *sout = s.d_tmp2 + P.n_c;
-  RC(launch_cone(h, s, CONE_PLAIN, s.warp_plan, false, sin, sout, 1.0, st));
+  for (const ConePlan &wp : s.warp_plans) RC(launch_cone(h, s, CONE_PLAIN, wp, false, sin, sout, 1.0, st));
   RC(launch_cone(h, s, CONE_PLAIN, s.block_plan, true, sin, sout, 1.0, st));
   k_tau_clamp<<<1, 32, 0, st>>>(s.d_tmp, T, s.d_tmp2);
   CKL();
