@@ -107,16 +107,31 @@ class ClockSampler:
 # algorithmic units per launch
 
 
-def kernel_units(cp, name: str):
-    """(kind, amount) of one launch: kind 'bytes' or 'flops'."""
+def pair_stats(cp):
+    """(pairs, nonzeros of the pair columns) of the symmetric half passes:
+    covered coordinates (i, j) with i <= j and their columns of A."""
+    i, j = np.divmod(cp.covered, cp.n)
+    rep = i <= j
+    counts = np.bincount(cp.A.indices, minlength=cp.N_c)
+    return int(rep.sum()), int(counts[rep].sum())
+
+
+def kernel_units(cp, name: str, half: bool = True):
+    """(kind, amount) of one launch: kind 'bytes' or 'flops' (DESIGN.md 6)."""
     Nc, nd, m, nnz = cp.N_c, cp.n_d, cp.m, int(cp.A.nnz)
     big = cp.sizes[cp.sizes > 32]
     small = cp.sizes[(cp.sizes <= 32) & (cp.sizes > 1)]
-    if name == "k_rhs":
-        return "bytes", 52 * Nc + 36 * nd + 12 * nnz + 8 * m
-    if name == "k_spmv_seg":
+    if half:
+        npair, nnz_p = pair_stats(cp)
+    if name == "k_rhs":  # u, w of x / s / v; cover lists; c, p_inv; t out
+        return "bytes", 44 * Nc + 36 * nd
+    if name == "k_spmv_seg":  # A t: pair sums + 16-bit row-SELL values / columns + row sums
+        if half:
+            return "bytes", 10 * nnz_p + 8 * Nc + 24 * npair
         return "bytes", 12 * nnz + 8 * Nc
-    if name == "k_ua":
+    if name == "k_ua":  # A' g: 16-bit SELL-32 over pairs + t, p_inv, c in, ua out
+        if half:
+            return "bytes", 10 * nnz_p + 8 * npair + 32 * Nc
         return "bytes", 40 * Nc + 12 * nnz
     if name == "k_xupd":
         return "bytes", 48 * Nc
@@ -154,13 +169,13 @@ def load_traffic(name: str):
     return data.get(name)
 
 
-def roofline_for(cp, prof_ms: dict, launches_per_kernel: int, peaks: dict):
-    items = [(ms, name) for name, ms in prof_ms.items() if ms > 0 and kernel_units(cp, name)[0]]
+def roofline_for(cp, prof_ms: dict, launches_per_kernel: int, peaks: dict, half: bool = True):
+    items = [(ms, name) for name, ms in prof_ms.items() if ms > 0 and kernel_units(cp, name, half)[0]]
     if not items:
         return None, None
     out = {}
     for ms, name in sorted(items, reverse=True):
-        kind, amount = kernel_units(cp, name)
+        kind, amount = kernel_units(cp, name, half)
         t = ms / 1e3 / launches_per_kernel
         if kind == "bytes":
             peak = peaks.get("hbm_gbs", 6650.0)
@@ -295,7 +310,8 @@ def run_ours(args):
     eig_stats = h.stats()
     gpu_launches_per_iter = (launches - 1) / prof_iters
     peaks = load_peaks()
-    dominant, roofs = roofline_for(cp, prof, prof_iters, peaks)
+    half = h.half_passes
+    dominant, roofs = roofline_for(cp, prof, prof_iters, peaks, half)
     h.close()
     line = None
     if rank == 0:
@@ -307,7 +323,8 @@ def run_ours(args):
             "config": {"workload": CONFIG_NAMES[args.config], **config_stats(cp),
                        "parallelism": "single GPU" if world == 1 else
                        f"clique shards x{world} (NCCL all-reduce: separators, A t, c.ua)",
-                       "l2": "no flush: per-iteration working set (A CSR+CSC 0.92 GB) > 126 MB L2"},
+                       "l2": "no flush: per-iteration working set (A in SELL layouts ~0.53 GB + state ~0.11 GB) > 126 MB L2",
+                       "half_passes": half},
             "clocks": clocks,
             "gpu_launches": int(round(gpu_launches_per_iter * args.steps)) + 1,
             "kernel_ms_per_iteration": {k: v / prof_iters for k, v in prof.items() if v > 0},

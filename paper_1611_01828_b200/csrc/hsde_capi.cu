@@ -543,11 +543,11 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
     if (h->sh[g].block_plan.count) jobs.push_back({&h->sh[g], &h->sh[g].block_plan, true});
   nl += (int)jobs.size();
   if (ev || jobs.size() <= 1) {
+    if (n_warp_jobs == 0) mark(PS_CONE_WARP);
     for (size_t j = 0; j < jobs.size(); ++j) {
       RC(launch_cone(h, *jobs[j].s, CONE_HOT, *jobs[j].pl, jobs[j].block, nullptr, nullptr, 1.0, st));
       if (j + 1 == n_warp_jobs) mark(PS_CONE_WARP);
     }
-    if (n_warp_jobs == 0) mark(PS_CONE_WARP);
   } else {
     CK(cudaEventRecord(h->ev_fork, st));
     // the largest job (CTA plan if any, else the last warp class) stays on st
