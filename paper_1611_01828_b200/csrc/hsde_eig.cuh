@@ -179,33 +179,47 @@ __device__ void jacobi_norms(const Team &tm, const JacobiScratch &js, int dp, do
   off2 = team_sum(tm, o2, js.red);
 }
 
-// Apply the rotations of parameter buffer b (one round) to the eigenvector
-// rows.  Item (k, c): pair k, 16-byte column chunks c + j nq (j < 4) of rows
-// p_k, q_k; consecutive threads take consecutive pairs (rows of consecutive
-// players -> distinct bank groups, see jacobi_ldv).  Threads [first, size).
+// Eigenvector-update items of one thread: item (k, c) = pair k, 16-byte column
+// chunks c + j nq (j < 4) of rows p_k, q_k; consecutive threads take
+// consecutive pairs (rows of consecutive players -> distinct bank groups, see
+// jacobi_ldv).  The mapping is fixed for a whole solve, so the divisions are
+// done once (VItems), not per round.
+struct VItems {
+  int k0, c0, dk, dc, total, nq, n2;
+  bool on;
+};
+
 template <class Team>
-__device__ __forceinline__ void jacobi_vupdate(const Team &tm, JacobiScratch &js, int d, int dp,
-                                               int b, int first) {
-  const int T = tm.size() - first;
-  const int me = tm.rank - first;
-  if (me < 0) return;
+__device__ __forceinline__ VItems jacobi_vitems(const Team &tm, int d, int dp, int first) {
+  VItems v;
+  const int T = tm.size() - first, me = tm.rank - first;
   const int half = dp / 2;
-  const int n2 = (d + 1) >> 1;   // 16-byte chunks per row
-  const int nq = (n2 + 3) >> 2;  // items per pair
-  const int total = half * nq;
+  v.n2 = (d + 1) >> 1;      // 16-byte chunks per row
+  v.nq = (v.n2 + 3) >> 2;   // items per pair
+  v.total = half * v.nq;
+  v.on = me >= 0 && me < v.total;
+  v.k0 = me >= 0 ? me % half : 0;
+  v.c0 = me >= 0 ? me / half : 0;
+  v.dk = T % half;
+  v.dc = T / half;
+  return v;
+}
+
+// Apply the rotations of parameter buffer b (one round) to the eigenvector rows.
+template <class Team>
+__device__ __forceinline__ void jacobi_vupdate(const Team &tm, JacobiScratch &js, int dp, int b,
+                                               const VItems &vi) {
+  if (!vi.on) return;
+  const int half = dp / 2;
   const double *rc = js.rc + b * half, *rs = js.rs + b * half;
   const int2 *pq = js.pq + b * half;
-  const int dk = T % half, dc = T / half;
-  int c = me / half, k = me - (me / half) * half;
-  for (int it = me; it < total; it += T, k += dk, c += dc) {
-    if (k >= half) {
-      k -= half;
-      ++c;
-    }
+  const int nq = vi.nq, n2 = vi.n2, ldv = js.ldv;
+  int k = vi.k0, c = vi.c0;
+  for (;;) {
     const double sn = rs[k], cs = rc[k];
     const int2 pk = pq[k];
-    double2 *vp = reinterpret_cast<double2 *>(js.Vt + pk.x * js.ldv);
-    double2 *vq = reinterpret_cast<double2 *>(js.Vt + pk.y * js.ldv);
+    double2 *vp = reinterpret_cast<double2 *>(js.Vt + pk.x * ldv);
+    double2 *vq = reinterpret_cast<double2 *>(js.Vt + pk.y * ldv);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int cc = c + j * nq;
@@ -215,6 +229,13 @@ __device__ __forceinline__ void jacobi_vupdate(const Team &tm, JacobiScratch &js
         vq[cc] = make_double2(sn * p0.x + cs * q0.x, sn * p0.y + cs * q0.y);
       }
     }
+    k += vi.dk;
+    c += vi.dc;
+    if (k >= half) {
+      k -= half;
+      ++c;
+    }
+    if (c * half + k >= vi.total) break;
   }
 }
 
@@ -230,6 +251,7 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
   const int T = tm.size();
   // threads that only update eigenvectors during phase P (block teams)
   const int vfirst = (T > 32 && T - ((half + 31) & ~31) >= 64) ? ((half + 31) & ~31) : 0;
+  const VItems vi_p = jacobi_vitems(tm, d, dp, vfirst), vi_all = jacobi_vitems(tm, d, dp, 0);
   double norm2, off2;
   jacobi_norms(tm, js, dp, norm2, off2);
   const double thr = sqrt(norm2) * 8.673617379884035e-19;  // 2^-60 |A|_F
@@ -278,7 +300,7 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
         pq[k] = make_int2(p, q);
         js.tt[k] = t;
       }
-      if (pending) jacobi_vupdate(tm, js, d, dp, b ^ 1, vfirst);
+      if (pending) jacobi_vupdate(tm, js, dp, b ^ 1, vi_p);
       tm.sync();
       // ---- phase A: off-diagonal 2x2 blocks (upper triangle), then the
       // diagonal blocks
@@ -319,7 +341,7 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
       break;  // every pair below the rotation threshold
     }
   }
-  if (pending) jacobi_vupdate(tm, js, d, dp, (round - 1) & 1, 0);
+  if (pending) jacobi_vupdate(tm, js, dp, (round - 1) & 1, vi_all);
   // restore the strict lower triangle
   for (int e = tm.rank; e < dp * dp; e += T) {
     const int i = e / dp, j = e - i * dp;
