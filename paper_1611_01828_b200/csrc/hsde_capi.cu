@@ -410,7 +410,7 @@ int inner_dist(hsde_handle *h, const std::vector<const double *> &rho,
       k_zero<<<grid_for(h->n_sep), kBlock, 0, st>>>(s.W.sepbuf, h->n_sep);
       CKL();
     }
-    k_rhs<false><<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(P, s.S, s.W, rx, rs, rv, s.grid_nc);
+    k_rhs<false><<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(P, s.S, s.W, rx, rs, rv, s.grid_heavy);
     CKL();
   }
   RC(reduce(h, BUF_SEP, h->n_sep));
@@ -470,7 +470,7 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
       ++nl;
     }
     k_rhs<true><<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(s.P, s.S, s.W, nullptr, nullptr, nullptr,
-                                                            s.grid_nc);
+                                                            s.grid_heavy);
     CKL();
     ++nl;
   }

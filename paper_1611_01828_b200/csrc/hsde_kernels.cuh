@@ -187,30 +187,56 @@ __device__ __forceinline__ void rhs_slot(const DevProblem &P, const DevState &S,
 }
 
 template <bool FROM_STATE>
+__device__ __forceinline__ void rhs_finish(const DevProblem &P, const DevState &S, const DevWork &W,
+                                           const double *rx, double atau, int l, double sg, double sv) {
+  if (P.n_sep && P.sep_of[l] >= 0) {  // separator: partial, finished after the all-reduce
+    W.sepbuf[P.sep_of[l]] = sg * 0.5 + sv;
+    return;
+  }
+  const double rx_l = FROM_STATE ? (S.u[l] + S.w[l]) - atau * P.c[l] : rx[l];
+  const double r = (sg * 0.5 + sv) + rx_l;
+  W.t[l] = r * P.p_inv[l];
+}
+
+// Grid = [heavy blocks | light blocks]: the few heavy warps start first.  Light
+// threads take two coordinates per step with their dependent loads (cover
+// range -> slot -> slot values) interleaved.
+template <bool FROM_STATE>
 __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWork W,
                                                 const double *rx, const double *rs,
-                                                const double *rv, int nb_light) {
+                                                const double *rv, int nb_heavy) {
   double atau = 0.0;
   if (FROM_STATE) atau = S.u[P.total - 1] + S.w[P.total - 1];
-  if ((int)blockIdx.x < nb_light) {
-    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < P.n_c; l += nb_light * blockDim.x) {
-      const int jb = P.cov_ptr[l], je = P.cov_ptr[l + 1];
-      if (je - jb > kHeavy) continue;
-      double sg = 0.0, sv = 0.0;
-      for (int e = jb; e < je; ++e) rhs_slot<FROM_STATE>(P, S, rs, rv, P.cov_slot[e], sg, sv);
-      if (P.n_sep && P.sep_of[l] >= 0) {  // separator: partial, finished after the all-reduce
-        W.sepbuf[P.sep_of[l]] = sg * 0.5 + sv;
-        continue;
+  if ((int)blockIdx.x >= nb_heavy) {
+    const int stride = ((int)gridDim.x - nb_heavy) * blockDim.x;
+    for (int l = ((int)blockIdx.x - nb_heavy) * blockDim.x + threadIdx.x; l < P.n_c; l += 2 * stride) {
+      int lq[2], jb[2], je[2];
+      lq[0] = l;
+      lq[1] = l + stride < P.n_c ? l + stride : -1;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        jb[q] = lq[q] >= 0 ? P.cov_ptr[lq[q]] : 0;
+        je[q] = lq[q] >= 0 ? P.cov_ptr[lq[q] + 1] : 0;
       }
-      const double rx_l = FROM_STATE ? (S.u[l] + S.w[l]) - atau * P.c[l] : rx[l];
-      const double r = (sg * 0.5 + sv) + rx_l;
-      W.t[l] = r * P.p_inv[l];
+      int j0[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) j0[q] = (je[q] > jb[q] && je[q] - jb[q] <= kHeavy) ? P.cov_slot[jb[q]] : -1;
+      double sg[2] = {0.0, 0.0}, sv[2] = {0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (j0[q] >= 0) rhs_slot<FROM_STATE>(P, S, rs, rv, j0[q], sg[q], sv[q]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (lq[q] < 0 || je[q] - jb[q] > kHeavy) continue;
+        for (int e = jb[q] + 1; e < je[q]; ++e) rhs_slot<FROM_STATE>(P, S, rs, rv, P.cov_slot[e], sg[q], sv[q]);
+        rhs_finish<FROM_STATE>(P, S, W, rx, atau, lq[q], sg[q], sv[q]);
+      }
     }
     return;
   }
-  // heavy coordinates: one warp each, lanes stride the slot list and the column
+  // heavy coordinates: one warp each, lanes stride the slot list
   const int lane = threadIdx.x & 31;
-  const int hw = ((int)blockIdx.x - nb_light) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int hw = (int)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (hw >= P.n_heavy) return;
   const int l = P.heavy[hw];
   double sg = 0.0, sv = 0.0;
@@ -218,15 +244,7 @@ __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWor
     rhs_slot<FROM_STATE>(P, S, rs, rv, P.cov_slot[e], sg, sv);
   sg = warp_sum(sg);
   sv = warp_sum(sv);
-  if (P.n_sep && P.sep_of[l] >= 0) {
-    if (lane == 0) W.sepbuf[P.sep_of[l]] = sg * 0.5 + sv;
-    return;
-  }
-  if (lane == 0) {
-    const double rx_l = FROM_STATE ? (S.u[l] + S.w[l]) - atau * P.c[l] : rx[l];
-    const double r = (sg * 0.5 + sv) + rx_l;
-    W.t[l] = r * P.p_inv[l];
-  }
+  if (lane == 0) rhs_finish<FROM_STATE>(P, S, W, rx, atau, l, sg, sv);
 }
 
 // t of the separator coordinates once their pull-scatter partials are all-reduced
