@@ -82,14 +82,16 @@ struct DevProblem {
   int half;              // 1: enabled
   int n_pair;
   const int *pair_l, *pair_m;  // [n_pair] representative (l <= mirror) and mirror
-  int n_slice;           // SELL-32 slices of 32 pairs (A' g)
-  const int64_t *sl_beg; // [n_slice + 1]; element k of lane j at sl_beg[s] + 32 k + j
-  const uint16_t *sl_row;
+  int n_slice;           // SELL-32 slices of 32 pairs (A' g), pairs sorted by length
+  const int64_t *sl_beg; // within windows of kSellSigma; [n_slice + 1]; element k of
+  const uint16_t *sl_row;// lane j at sl_beg[s] + 32 k + j
   const double *sl_val;
+  const int *sl_pl, *sl_pm;  // [n_pair] the pair (l, mirror) of SELL position q
   int rt_ntile, rt_G;    // row-SELL tiles of kRowTile pairs x groups of 32 rows (A t),
-  const int64_t *rt_beg; // owned pairs only; [rt_ntile * rt_G + 1]
-  const uint16_t *rt_col;// column within the tile
+  const int64_t *rt_beg; // owned pairs only, rows sorted by length within a tile;
+  const uint16_t *rt_col;// [rt_ntile * rt_G + 1]; column within the tile
   const double *rt_val;
+  const int *rt_row;     // [rt_ntile * m] row of tile position g * 32 + j
   // data of the iterated (normalised) problem
   const double *c, *b, *p_inv;
   // Schur inverse: dense m x m (row-major, symmetric) or diagonal m
@@ -349,6 +351,7 @@ __global__ void __launch_bounds__(kBlock) k_ua(DevProblem P, DevWork W, const do
 // SELL layouts: every load is a coalesced 32-lane access.
 
 constexpr int kRowTile = 4096;  // pairs per row-SELL tile (16-bit column index)
+constexpr int kSellSigma = 1024;  // SELL-32 sorting window (pairs)
 constexpr int kRowTileSplit = 4;  // CTAs per tile (row groups split among them)
 
 // pair values x_q = t_l + t_mirror (t_l on the diagonal)
@@ -380,8 +383,8 @@ __global__ void __launch_bounds__(kBlock) k_spmv_half(DevProblem P, const double
       a1 += __ldcs(P.rt_val + k + 32) * xs[__ldcs(P.rt_col + k + 32)];
     }
     if (k < e) a0 += __ldcs(P.rt_val + k) * xs[__ldcs(P.rt_col + k)];
-    const int r = gr * 32 + lane;
-    if (r < P.m) part[(int64_t)r * P.rt_ntile + tile] = a0 + a1;
+    const int rq = gr * 32 + lane;
+    if (rq < P.m) part[(int64_t)P.rt_row[(int64_t)tile * P.m + rq] * P.rt_ntile + tile] = a0 + a1;
   }
 }
 
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(kBlock) k_ua_half(DevProblem P, DevWork W, con
     const double atg = a0 + a1;
     const int q = sl * 32 + lane;
     if (q < P.n_pair) {
-      const int l = P.pair_l[q], mm = P.pair_m[q];
+      const int l = P.sl_pl[q], mm = P.sl_pm[q];
       const double ul = W.t[l] - atg * P.p_inv[l];
       W.ua[l] = ul;
       if (WITH_DOT && owns(P, l)) dot += P.c[l] * ul;

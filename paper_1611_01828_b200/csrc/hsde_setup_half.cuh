@@ -10,10 +10,13 @@
 //
 //   pairs      representatives l <= mirror(l), ascending
 //   SELL-32    A' g: slice of 32 pairs, element k of lane j at beg + 32 k + j,
-//              16-bit row index, zero padded to the slice's longest column
+//              16-bit row index, zero padded to the slice's longest column;
+//              pairs sorted by column length within windows of kSellSigma
+//              (SELL-C-sigma: padding 1.48 -> 1.02 on config 4)
 //   row-SELL   A t: tiles of kRowTile pairs x groups of 32 rows, element k of
-//              row 32 g + j at beg + 32 k + j, 16-bit column within the tile,
-//              entries of the owned pairs only, ascending column in a row
+//              row position 32 g + j at beg + 32 k + j, 16-bit column within the
+//              tile, entries of the owned pairs only, ascending column in a row;
+//              rows sorted by their tile length within the tile
 
 __global__ void k_mirror_map(DevProblem P, int *mir) {
   for (int k = blockIdx.x; k < P.p; k += gridDim.x) {
@@ -63,20 +66,34 @@ __global__ void k_pair_list(int n_c, const int *mir, const int *rep, const int *
     }
 }
 
-// slice widths (32 * longest column of the slice) and, for the row tiles,
-// the owned-entry count of every pair
-__global__ void k_pair_lengths(DevProblem P, const int *pl, int n_pair, int64_t *slice_w,
-                               int *own_len) {
+// per pair: column length, owned-entry count, and the SELL sort key
+// (window, descending length)
+__global__ void k_pair_lengths(DevProblem P, const int *pl, int n_pair, int *plen, int *own_len,
+                               unsigned *key, int *idx) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pair; q += gridDim.x * blockDim.x) {
+    const int l = pl[q];
+    const int len = (int)(P.at_cp[l + 1] - P.at_cp[l]);
+    plen[q] = len;
+    own_len[q] = owns(P, l) ? len : 0;
+    key[q] = ((unsigned)(q / kSellSigma) << 16) | (unsigned)(65535 - len);
+    idx[q] = q;
+  }
+}
+
+// SELL order: pair of position p, its length; slice widths (32 * longest)
+__global__ void k_sell_order(const int *perm, const int *pl, const int *pm, const int *plen, int n_pair,
+                             int *sl_pl, int *sl_pm, int64_t *slice_w) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const int n_slice = (n_pair + 31) >> 5;
   for (int sl = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sl < n_slice; sl += warps) {
-    const int q = sl * 32 + lane;
+    const int p = sl * 32 + lane;
     int len = 0;
-    if (q < n_pair) {
-      const int l = pl[q];
-      len = (int)(P.at_cp[l + 1] - P.at_cp[l]);
-      own_len[q] = owns(P, l) ? len : 0;
+    if (p < n_pair) {
+      const int q = perm[p];
+      sl_pl[p] = pl[q];
+      sl_pm[p] = pm[q];
+      len = plen[q];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
@@ -84,10 +101,10 @@ __global__ void k_pair_lengths(DevProblem P, const int *pl, int n_pair, int64_t 
   }
 }
 
-__global__ void k_fill_sell(DevProblem P, const int *pl, int n_pair, const int64_t *sl_beg,
+__global__ void k_fill_sell(DevProblem P, const int *sl_pl, int n_pair, const int64_t *sl_beg,
                             uint16_t *sl_row, double *sl_val) {
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n_pair; q += gridDim.x * blockDim.x) {
-    const int l = pl[q];
+    const int l = sl_pl[q];
     const int64_t cb = P.at_cp[l], n = P.at_cp[l + 1] - cb;
     const int64_t base = sl_beg[q >> 5] + (q & 31);
     for (int64_t k = 0; k < n; ++k) {
@@ -120,24 +137,40 @@ __global__ void k_cell_count(const unsigned long long *keys, int64_t n, int *cnt
     atomicAdd(cnt + (keys[e] >> 12), 1);  // integer counts: order-independent
 }
 
-__global__ void k_group_width(const int *cnt, int m, int ntile, int G, int64_t *w) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ntile * G; c += gridDim.x * blockDim.x) {
-    const int t = c / G, g = c - t * G;
-    int mx = 0;
-    for (int r = g * 32; r < min(m, g * 32 + 32); ++r) mx = max(mx, cnt[(int64_t)t * m + r]);
-    w[c] = 32 * (int64_t)mx;
+// row sort keys within each tile: (tile, descending count)
+__global__ void k_row_keys_sort(const int *cnt, int m, int64_t ncell, unsigned long long *key, int *row) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = c / m;
+    key[c] = ((unsigned long long)t << 32) | (unsigned long long)(0xffffffffu - (unsigned)cnt[c]);
+    row[c] = (int)(c - t * m);
+  }
+}
+
+// sorted rows -> inverse positions and the group widths (first row of a group
+// is its longest)
+__global__ void k_row_positions(const int *cnt, const int *rt_row, int m, int ntile, int G, int *rowpos,
+                                int64_t *w) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < (int64_t)ntile * m;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = c / m;
+    const int q = (int)(c - t * m);
+    const int r = rt_row[c];
+    rowpos[t * m + r] = q;
+    if ((q & 31) == 0) w[t * G + (q >> 5)] = 32 * (int64_t)cnt[t * m + r];
   }
 }
 
 __global__ void k_fill_rows(const unsigned long long *keys, const double *vals, int64_t n, int m,
-                            int G, const int64_t *cell_start, const int64_t *rt_beg,
+                            int G, const int64_t *cell_start, const int *rowpos, const int64_t *rt_beg,
                             uint16_t *rt_col, double *rt_val) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long c = keys[e] >> 12;
-    const int t = (int)(c / (unsigned long long)m), r = (int)(c - (unsigned long long)t * m);
+    const int t = (int)(c / (unsigned long long)m);
+    const int q = rowpos[c];
     const int64_t rank = e - cell_start[c];
-    const int64_t dst = rt_beg[(int64_t)t * G + (r >> 5)] + 32 * rank + (r & 31);
+    const int64_t dst = rt_beg[(int64_t)t * G + (q >> 5)] + 32 * rank + (q & 31);
     rt_col[dst] = (uint16_t)(keys[e] & 4095ull);
     rt_val[dst] = vals[e];
   }
@@ -205,19 +238,46 @@ int build_half(hsde_handle *h, ShardDev &s) {
   pool_free(h, rep);
   pool_free(h, pos);
   pool_free(h, flag);
-  // SELL-32 slices (A' g)
+  // SELL-32 slices (A' g), pairs sorted by length within windows (stable)
   const int n_slice = (n_pair + 31) / 32;
   int64_t *sl_beg = nullptr;
-  int *own_len = nullptr;
+  int *own_len = nullptr, *plen = nullptr, *pidx = nullptr, *perm = nullptr, *sl_pl = nullptr,
+      *sl_pm = nullptr;
+  unsigned *pkey = nullptr, *pkey_s = nullptr;
   int64_t *own_pos = nullptr, *slw = nullptr;
   RC(dalloc(h, &sl_beg, n_slice + 1));
+  RC(dalloc(h, &sl_pl, n_pair));
+  RC(dalloc(h, &sl_pm, n_pair));
   CK(pool_malloc(h, (void **)&slw, sizeof(int64_t) * (n_slice + 1)));
   CK(pool_malloc(h, (void **)&own_len, sizeof(int) * (n_pair + 1)));
   CK(pool_malloc(h, (void **)&own_pos, sizeof(int64_t) * (n_pair + 1)));
+  CK(pool_malloc(h, (void **)&plen, sizeof(int) * (n_pair + 1)));
+  CK(pool_malloc(h, (void **)&pidx, sizeof(int) * (n_pair + 1)));
+  CK(pool_malloc(h, (void **)&perm, sizeof(int) * (n_pair + 1)));
+  CK(pool_malloc(h, (void **)&pkey, sizeof(unsigned) * (n_pair + 1)));
+  CK(pool_malloc(h, (void **)&pkey_s, sizeof(unsigned) * (n_pair + 1)));
   CK(cudaMemsetAsync(slw + n_slice, 0, sizeof(int64_t), h->st));
   CK(cudaMemsetAsync(own_len + n_pair, 0, sizeof(int), h->st));
-  k_pair_lengths<<<grid_for((int64_t)n_slice * 32), kBlock, 0, h->st>>>(P, pl, n_pair, slw, own_len);
+  k_pair_lengths<<<grid_for(n_pair), kBlock, 0, h->st>>>(P, pl, n_pair, plen, own_len, pkey, pidx);
   CKL();
+  {
+    int kbits = 16;
+    while ((1ll << (kbits - 16)) <= (long long)(n_pair / kSellSigma)) ++kbits;
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, pkey, pkey_s, pidx, perm, n_pair, 0, kbits, h->st);
+    void *tmp = nullptr;
+    CK(pool_malloc(h, &tmp, tb));
+    cub::DeviceRadixSort::SortPairs(tmp, tb, pkey, pkey_s, pidx, perm, n_pair, 0, kbits, h->st);
+    pool_free(h, tmp);
+  }
+  k_sell_order<<<grid_for((int64_t)n_slice * 32), kBlock, 0, h->st>>>(perm, pl, pm, plen, n_pair, sl_pl, sl_pm,
+                                                                      slw);
+  CKL();
+  pool_free(h, plen);
+  pool_free(h, pidx);
+  pool_free(h, perm);
+  pool_free(h, pkey);
+  pool_free(h, pkey_s);
   RC(excl_scan(h, slw, sl_beg, (int64_t)n_slice + 1));
   const int64_t n_sell = d2h_one(h, sl_beg + n_slice);
   uint16_t *sl_row = nullptr;
@@ -226,7 +286,7 @@ int build_half(hsde_handle *h, ShardDev &s) {
   RC(dalloc(h, &sl_val, n_sell));
   CK(cudaMemsetAsync(sl_row, 0, sizeof(uint16_t) * std::max<int64_t>(n_sell, 1), h->st));
   CK(cudaMemsetAsync(sl_val, 0, sizeof(double) * std::max<int64_t>(n_sell, 1), h->st));
-  k_fill_sell<<<grid_for(n_pair), kBlock, 0, h->st>>>(P, pl, n_pair, sl_beg, sl_row, sl_val);
+  k_fill_sell<<<grid_for(n_pair), kBlock, 0, h->st>>>(P, sl_pl, n_pair, sl_beg, sl_row, sl_val);
   CKL();
   pool_free(h, slw);
   // row-SELL tiles (A t) over the owned pairs
@@ -282,8 +342,32 @@ int build_half(hsde_handle *h, ShardDev &s) {
   CK(cudaMemsetAsync(gw + (int64_t)ntile * G, 0, sizeof(int64_t), h->st));
   k_cell_count<<<148 * 8, kBlock, 0, h->st>>>(keys_s, n_ent, cnt);
   k_widen<<<grid_for(ncell + 1), kBlock, 0, h->st>>>(cnt, cnt64, ncell + 1);
-  k_group_width<<<grid_for((int64_t)ntile * G), kBlock, 0, h->st>>>(cnt, m, ntile, G, gw);
   CKL();
+  // rows of each tile sorted by their entry count (descending, stable)
+  int *rt_row = nullptr, *rowpos = nullptr, *ridx = nullptr;
+  unsigned long long *rkey = nullptr, *rkey_s = nullptr;
+  RC(dalloc(h, &rt_row, std::max<int64_t>(ncell, 1)));
+  CK(pool_malloc(h, (void **)&rowpos, sizeof(int) * (ncell + 1)));
+  CK(pool_malloc(h, (void **)&ridx, sizeof(int) * (ncell + 1)));
+  CK(pool_malloc(h, (void **)&rkey, sizeof(unsigned long long) * (ncell + 1)));
+  CK(pool_malloc(h, (void **)&rkey_s, sizeof(unsigned long long) * (ncell + 1)));
+  k_row_keys_sort<<<grid_for(ncell), kBlock, 0, h->st>>>(cnt, m, ncell, rkey, ridx);
+  CKL();
+  {
+    int kbits = 32;
+    while ((1ll << (kbits - 32)) <= (long long)ntile) ++kbits;
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, rkey, rkey_s, ridx, rt_row, (int)ncell, 0, kbits, h->st);
+    void *tmp = nullptr;
+    CK(pool_malloc(h, &tmp, tb));
+    cub::DeviceRadixSort::SortPairs(tmp, tb, rkey, rkey_s, ridx, rt_row, (int)ncell, 0, kbits, h->st);
+    pool_free(h, tmp);
+  }
+  k_row_positions<<<grid_for(ncell), kBlock, 0, h->st>>>(cnt, rt_row, m, ntile, G, rowpos, gw);
+  CKL();
+  pool_free(h, ridx);
+  pool_free(h, rkey);
+  pool_free(h, rkey_s);
   RC(excl_scan(h, cnt64, cell_start, ncell + 1));
   RC(excl_scan(h, gw, rt_beg, (int64_t)ntile * G + 1));
   const int64_t n_rt = d2h_one(h, rt_beg + (int64_t)ntile * G);
@@ -293,9 +377,10 @@ int build_half(hsde_handle *h, ShardDev &s) {
   RC(dalloc(h, &rt_val, n_rt));
   CK(cudaMemsetAsync(rt_col, 0, sizeof(uint16_t) * std::max<int64_t>(n_rt, 1), h->st));
   CK(cudaMemsetAsync(rt_val, 0, sizeof(double) * std::max<int64_t>(n_rt, 1), h->st));
-  k_fill_rows<<<148 * 8, kBlock, 0, h->st>>>(keys_s, vals_s, n_ent, m, G, cell_start, rt_beg, rt_col,
-                                             rt_val);
+  k_fill_rows<<<148 * 8, kBlock, 0, h->st>>>(keys_s, vals_s, n_ent, m, G, cell_start, rowpos, rt_beg,
+                                             rt_col, rt_val);
   CKL();
+  pool_free(h, rowpos);
   CK(cudaStreamSynchronize(h->st));
   pool_free(h, keys_s);
   pool_free(h, vals_s);
@@ -312,6 +397,9 @@ int build_half(hsde_handle *h, ShardDev &s) {
   P.sl_beg = sl_beg;
   P.sl_row = sl_row;
   P.sl_val = sl_val;
+  P.sl_pl = sl_pl;
+  P.sl_pm = sl_pm;
+  P.rt_row = rt_row;
   P.rt_ntile = ntile;
   P.rt_G = G;
   P.rt_beg = rt_beg;
