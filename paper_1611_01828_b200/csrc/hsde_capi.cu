@@ -74,6 +74,8 @@ struct ConePlan {
   int dpmax = 0;
   size_t smem = 0;
   int per_block = 0;       // warps per CTA (warp plan)
+  double *pscratch = nullptr;  // CTA plan: d x d global scratch per CTA (second-order rebuild)
+  int64_t pstride = 0;
 };
 
 enum Mode { MODE_SINGLE = 0, MODE_EMULATED = 1, MODE_NCCL = 2 };
@@ -316,7 +318,7 @@ __global__ void k_diag_finish(double *diag, int m, int *flag) {
 int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool block,
                 const double *in, double *out, double in_scale, cudaStream_t st) {
   if (pl.count == 0) return 0;
-  ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0};
+  ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0, pl.pscratch, pl.pstride, 0};
   if (!block) {
     const int grid = (pl.count + pl.per_block - 1) / pl.per_block;
     const int thr = pl.per_block * 32;
@@ -668,6 +670,8 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
     }
     s.block_plan.smem = per_blk;
     RC(dupload(h, &s.block_plan.ids, bids.data(), bids.size()));
+    s.block_plan.pstride = (int64_t)dpb * dpb;
+    RC(dalloc(h, &s.block_plan.pscratch, (size_t)bids.size() * dpb * dpb));
     const int sm = maxsm;
     CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));

@@ -244,8 +244,8 @@ __device__ __forceinline__ void jacobi_vupdate(const Team &tm, JacobiScratch &js
 // sweeps; the full symmetric A (diagonal = eigenvalues, off-diagonal = the
 // remainder) is restored on exit.  Returns the number of sweeps performed.
 template <class Team>
-__device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
-                             bool *first_order = nullptr) {
+__device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp, int *order = nullptr,
+                             int max_order = 0) {
   double *A = js.A;
   const int lda = js.lda, half = dp / 2, noff = half * (half - 1) / 2;
   const int T = tm.size();
@@ -258,21 +258,31 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp,
   const double stop2 = norm2 * 1.925929944387236e-34;      // (2^-56 |A|_F)^2
   int sweep = 0, round = 0;
   bool pending = false;
-  // First-order exit (psd_rebuild_first_order): its error is O(off^2 / g),
-  // g the smallest |diagonal| (no eigenvalue closer to 0 can change sign while
-  // off <= g / 1000).  Exit once off^2 <= 1e-17 |A|_F g: projection error
-  // ~1e-17 |A|_F, the accuracy of a converged sweep.
-  if (first_order) *first_order = false;
-  const double fo_scale = 1e-17 * sqrt(norm2);
+  // Perturbative exits (psd_rebuild_perturbative): with g the smallest
+  // |diagonal| (no eigenvalue can change sign while off <= g / 1000), the
+  // projection of D + E by its order-k expansion around D has error
+  // O(off^(k+1) / g^k).  The sweeps stop at the first order whose bound is
+  // below 1e-15 |A|_F -- about the rounding floor of the reconstruction
+  // V diag(l+) V' itself (n eps |A|).
+  if (order) *order = 0;
+  const double tau = 1e-15 * sqrt(norm2);
   for (; sweep < kMaxSweeps; ++sweep) {
     if (!(off2 > stop2)) break;  // also stops on NaN
-    if (first_order) {
+    if (order && max_order > 0) {
       double g = CUDART_INF;
       for (int i = tm.rank; i < d; i += T) g = fmin(g, fabs(A[i * lda + i]));
       g = team_min(tm, g, js.red);
-      if (off2 <= fo_scale * g && off2 <= 1e-6 * g * g) {
-        *first_order = true;
-        break;
+      if (js.dbg && tm.rank == 0) js.dbg[63] = g / sqrt(norm2);
+      if (off2 <= 1e-6 * g * g) {
+        const double off = sqrt(off2);
+        if (off2 <= tau * g) {
+          *order = 1;
+          break;
+        }
+        if (max_order > 1 && off2 * off <= tau * g * g) {
+          *order = 2;
+          break;
+        }
       }
     }
     if (tm.rank == 0) js.flag[0] = 0;
@@ -585,12 +595,121 @@ __device__ void team_gemm_nn(const Team &tm, const double *L, int ldl, const dou
   tm.sync();
 }
 
+// out(i, j) = sum_k la(i, k) rb(k, j) over d x d (accessor operands); every
+// read completes (team barrier) before the first emit(i, j, value).
+template <int MT, class Team, class LA, class RB, class Emit>
+__device__ void team_gemm_fn(const Team &tm, int d, LA la, RB rb, Emit emit) {
+  const int nt = (d + 3) >> 2;
+  const GemmTiles<MT> g = gemm_tiles<MT>(tm, nt);
+  double acc[MT][4][4];
+#pragma unroll
+  for (int q = 0; q < MT; ++q) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[q][a][b] = 0.0;
+    if (g.on[q]) {
+      int ri[4], cj[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        ri[a] = min(g.u[q] + nt * a, d - 1);
+        cj[a] = min(g.v[q] + nt * a, d - 1);
+      }
+      for (int k = 0; k < d; ++k) {
+        double l[4], r[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          l[a] = la(ri[a], k);
+          r[a] = rb(k, cj[a]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[q][a][b] = fma(l[a], r[b], acc[q][a][b]);
+      }
+    }
+  }
+  tm.sync();
+#pragma unroll
+  for (int q = 0; q < MT; ++q)
+    if (g.on[q]) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = g.u[q] + nt * a, j = g.v[q] + nt * b;
+          if (i < d && j < d) emit(i, j, acc[q][a][b]);
+        }
+    }
+  tm.sync();
+}
+
+// Second-order projection of a nearly diagonal B = D + E (Daleckii-Krein to
+// second order, f = max(., 0), P / N = positive / non-positive diagonal):
+//   M_PP = D_P + E_PP - T1,  M_NN = -T1,
+//   M_PN = l_i G_ij + (-l_j T2_ij + l_i T3_ij) / (l_i - l_j)      (i in P, j in N)
+// with G_ij = E_ij / (l_i - l_j) on the P-N entries (0 elsewhere), E_S the
+// same-class entries of E, T1 = G |L| G, T2 = E_S G, T3 = G E_S; error
+// O(|E|^3 / g^2).  Every denominator is >= 2 g.  A holds E_S + G (its
+// diagonal in lam); M is assembled in the global scratch Mg (d x d), then
+// P = V' M V by two team GEMMs.
+template <int MT, class Team, class Emit>
+__device__ void psd_rebuild_second_order(const Team &tm, JacobiScratch &js, int d, double *Mg, Emit emit) {
+  double *A = js.A;
+  const int lda = js.lda, ldv = js.ldv;
+  double *lam = js.lam;
+  for (int i = tm.rank; i < d; i += tm.size()) lam[i] = A[i * lda + i];
+  tm.sync();
+  for (int e = tm.rank; e < d * d; e += tm.size()) {
+    const int i = e / d, j = e - i * d;
+    const double li = lam[i], lj = lam[j];
+    if (i == j) A[i * lda + j] = 0.0;
+    else if ((li > 0.0) != (lj > 0.0)) A[i * lda + j] = A[i * lda + j] / (li - lj);
+  }
+  tm.sync();
+  auto cls = [&](int i) { return lam[i] > 0.0; };
+  auto g_of = [&](int i, int k) { return cls(i) != cls(k) ? A[i * lda + k] : 0.0; };
+  auto s_of = [&](int i, int k) { return cls(i) == cls(k) ? A[i * lda + k] : 0.0; };
+  // T1 on the same-class entries
+  team_gemm_fn<MT>(
+      tm, d, g_of, [&](int k, int j) { return fabs(lam[k]) * g_of(k, j); },
+      [&](int i, int j, double t1) {
+        if (cls(i) != cls(j)) return;
+        double base = 0.0;
+        if (i == j) base = lam[i] > 0.0 ? lam[i] : 0.0;
+        else if (cls(i)) base = A[i * lda + j];
+        Mg[i * d + j] = base - t1;
+      });
+  // T2, then T3, on the P x N entries (mirrored into N x P)
+  team_gemm_fn<MT>(tm, d, s_of, g_of, [&](int i, int j, double t2) {
+    if (!cls(i) || cls(j)) return;
+    Mg[i * d + j] = lam[i] * A[i * lda + j] - lam[j] * t2 / (lam[i] - lam[j]);
+  });
+  team_gemm_fn<MT>(tm, d, g_of, s_of, [&](int i, int j, double t3) {
+    if (!cls(i) || cls(j)) return;
+    const double v = Mg[i * d + j] + lam[i] * t3 / (lam[i] - lam[j]);
+    Mg[i * d + j] = v;
+    Mg[j * d + i] = v;
+  });
+  for (int e = tm.rank; e < d * d; e += tm.size()) {
+    const int i = e / d, j = e - i * d;
+    A[i * lda + j] = Mg[i * d + j];
+  }
+  tm.sync();
+  team_gemm_nn<MT>(tm, A, lda, js.Vt, ldv, A, lda, d);  // T = M Vt
+  team_gemm_tn_sym<MT>(tm, js.Vt, ldv, A, lda, nullptr, d, d, [&](int i, int j, double v) {
+    emit(i, j, v);
+    if (i != j) emit(j, i, v);
+  });
+  tm.sync();
+}
+
 // First-order projection of a nearly diagonal B = D + E (CTA teams):
 //   P(B) = P(D) + L_D(E) + O(|E|^2 / g),  L_D(E)_ij = E_ij (l_i+ - l_j+) / (l_i - l_j)
 // (the Frechet derivative of the spectral function max(., 0); the divided
 // difference is 1 between positive, 0 between non-positive eigenvalues), g the
-// smallest |l_i|.  It is exact within same-sign pairs; jacobi_sweeps stops for
-// it only when |E|_F^2 <= 1e-17 |A|_F g and |E|_F <= g / 1000.  P = V' M V with
+// smallest |l_i|.  It is exact within same-sign pairs; jacobi_sweeps selects it
+// when |E|_F^2 <= 1e-15 |A|_F g and |E|_F <= g / 1000.  P = V' M V with
 // M = diag(l+) + L_D(E) by two team GEMMs.
 template <int MT, class Team, class Emit>
 __device__ void psd_rebuild_first_order(const Team &tm, JacobiScratch &js, int d, Emit emit) {
@@ -635,6 +754,9 @@ struct ConeArgs {
   double *out;      // PLAIN: stacked output; MINEIG: per-clique min eigenvalue [p]
   double in_scale;
   int warm;         // HOT: use / refresh the per-clique eigenvector store
+  double *pscratch; // CTA teams: d x d global scratch per CTA (second-order rebuild)
+  int64_t pstride;
+  int slot;         // this team's scratch slot
 };
 
 // Hot-path load of slot j: builds arg_s and performs the v / w_v update and
@@ -751,9 +873,10 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
     tm.sync();
   }
   // first-order exit for CTA teams whose GEMM tiles fit (not for MINEIG)
-  bool first_order = false;
+  int order = 0;
   const bool fo_ok = MODE != CONE_MINEIG && ntile * ntile <= MT * tm.size();
-  const int sw = jacobi_sweeps(tm, js, d, dp, fo_ok ? &first_order : nullptr);
+  double *Mg = ca.pscratch ? ca.pscratch + (int64_t)ca.slot * ca.pstride : nullptr;
+  const int sw = jacobi_sweeps(tm, js, d, dp, fo_ok ? &order : nullptr, fo_ok ? (Mg ? 2 : 1) : 0);
   if (MODE == CONE_HOT && tm.rank == 0 && W.sweeps) W.sweeps[k] = sw;
   // non-finite eigenvalue -> EigenFailure (symmat.py:162-163)
   double nb = 0.0;
@@ -780,7 +903,10 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
     S.w[j] += v;
   };
   auto emit_plain = [&](int a, int bcol, double v) { ca.out[off + (int64_t)a * d + bcol] = v; };
-  if (first_order) {
+  if (order == 2) {
+    if (MODE == CONE_HOT) psd_rebuild_second_order<MT>(tm, js, d, Mg, emit_hot);
+    else psd_rebuild_second_order<MT>(tm, js, d, Mg, emit_plain);
+  } else if (order == 1) {
     if (MODE == CONE_HOT) psd_rebuild_first_order<MT>(tm, js, d, emit_hot);
     else psd_rebuild_first_order<MT>(tm, js, d, emit_plain);
   } else {
@@ -800,7 +926,9 @@ __global__ void __launch_bounds__(kBlock) k_cone_warp(DevProblem P, DevState S, 
   if (gw >= ca.count) return;
   double *scratch = smem + (int64_t)wid * jacobi_scratch_doubles(ca.dpmax);
   WarpTeam tm{(int)(threadIdx.x & 31)};
-  cone_one<MODE>(tm, P, S, W, ca, ca.ids[gw], scratch);
+  ConeArgs c2 = ca;
+  c2.pscratch = nullptr;  // warp teams: first order only
+  cone_one<MODE>(tm, P, S, W, c2, ca.ids[gw], scratch);
 }
 
 // one CTA per clique (d > 32)
@@ -809,5 +937,7 @@ __global__ void __launch_bounds__(kConeBlock, 2) k_cone_block(DevProblem P, DevS
   extern __shared__ __align__(16) double smem[];
   if ((int)blockIdx.x >= ca.count) return;
   BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
-  cone_one<MODE>(tm, P, S, W, ca, ca.ids[blockIdx.x], smem);
+  ConeArgs c2 = ca;
+  c2.slot = blockIdx.x;
+  cone_one<MODE>(tm, P, S, W, c2, ca.ids[blockIdx.x], smem);
 }

@@ -19,6 +19,7 @@ for q in cliques:
         h.iterate(it - done)
         done = it
         d = h.debug_jacobi(q)
-        vals = [v for v in d[1:] if v >= 0]
-        print(q, it, "warm" if d[0] else "cold", " ".join(f"{v:.1e}" for v in vals), flush=True)
+        vals = [v for v in d[1:63] if v >= 0]
+        print(q, it, "warm" if d[0] else "cold", " ".join(f"{v:.1e}" for v in vals),
+              f" | min|lambda|/|A| {d[63]:.1e}", flush=True)
     h.close()
