@@ -644,6 +644,62 @@ __device__ void team_gemm_fn(const Team &tm, int d, LA la, RB rb, Emit emit) {
   tm.sync();
 }
 
+// fp64 tensor-core MMA (m8n8k4): D += A B, A 8 x 4 row-major, B 4 x 8.
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// CTA-team GEMM on the fp64 tensor cores: out(i, j) = sum_{k < K} la(i, k) rb(k, j)
+// for i, j < d, one 8 x 8 output tile per warp at a time (fragments: a =
+// A[lane/4][lane%4], b = B[lane%4][lane/4], d = D[lane/4][2 (lane%4) + {0,1}]).
+// emit may not write an operand.  SYM: only tiles bi <= bj, emitted to both
+// triangles (exactly symmetric).  Ends with a team barrier.
+template <bool SYM, class LA, class RB, class Emit>
+__device__ void mma_gemm(int d, int K, LA la, RB rb, Emit emit) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nt = (d + 7) >> 3, K4 = (K + 3) & ~3;
+  const int ntiles = nt * nt;
+  for (int t = w; t < ntiles; t += nw) {
+    const int bi = t / nt, bj = t - bi * nt;
+    if (SYM && bi > bj) continue;
+    const int ia = bi * 8 + (lane >> 2), jb = bj * 8 + (lane >> 2);
+    double d0 = 0.0, d1 = 0.0;
+    for (int k0 = 0; k0 < K4; k0 += 4) {
+      const int k = k0 + (lane & 3);
+      const double a = (ia < d && k < K) ? la(ia, k) : 0.0;
+      const double b = (jb < d && k < K) ? rb(k, jb) : 0.0;
+      dmma884(d0, d1, a, b);
+    }
+    const int i = bi * 8 + (lane >> 2), j = bj * 8 + 2 * (lane & 3);
+    if (i >= d) continue;
+    if (!SYM) {
+      if (j < d) emit(i, j, d0);
+      if (j + 1 < d) emit(i, j + 1, d1);
+    } else if (bi < bj) {
+      if (j < d) {
+        emit(i, j, d0);
+        emit(j, i, d0);
+      }
+      if (j + 1 < d) {
+        emit(i, j + 1, d1);
+        emit(j + 1, i, d1);
+      }
+    } else {
+      if (j < d && i <= j) {
+        emit(i, j, d0);
+        if (i != j) emit(j, i, d0);
+      }
+      if (j + 1 < d && i <= j + 1) {
+        emit(i, j + 1, d1);
+        if (i != j + 1) emit(j + 1, i, d1);
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // Second-order projection of a nearly diagonal B = D + E (Daleckii-Krein to
 // second order, f = max(., 0), P / N = positive / non-positive diagonal):
 //   M_PP = D_P + E_PP - T1,  M_NN = -T1,
@@ -739,6 +795,110 @@ __device__ void psd_rebuild_first_order(const Team &tm, JacobiScratch &js, int d
     if (i != j) emit(j, i, v);
   });
   tm.sync();
+}
+
+// ---------------------------------------------------------------------------
+// CTA teams: the dense products on the fp64 tensor cores (mma_gemm), with the
+// per-CTA global scratch Mg (d x d, L2-resident) as the intermediate so no
+// GEMM writes an operand.
+
+// B = V X V' from the previous eigenvectors (rows of Vt): T = Vt X -> Mg, B = T Vt'
+__device__ void cta_warm_start(JacobiScratch &js, int d, double *Mg) {
+  double *A = js.A, *Vt = js.Vt;
+  const int lda = js.lda, ldv = js.ldv;
+  mma_gemm<false>(
+      d, d, [&](int i, int k) { return Vt[i * ldv + k]; }, [&](int k, int j) { return A[k * lda + j]; },
+      [&](int i, int j, double v) { Mg[i * d + j] = v; });
+  mma_gemm<true>(
+      d, d, [&](int i, int k) { return Mg[i * d + k]; }, [&](int k, int j) { return Vt[j * ldv + k]; },
+      [&](int i, int j, double v) { A[i * lda + j] = v; });
+}
+
+// P = sum_{lambda > 0} lambda v v' (converged sweeps)
+template <class Emit>
+__device__ void cta_rebuild_full(const BlockTeam &tm, JacobiScratch &js, int d, Emit emit) {
+  const int r = compact_positive(tm, js, d);
+  double *W = js.A, *Vt = js.Vt;
+  const int lda = js.lda, ldv = js.ldv;
+  for (int e = tm.rank; e < r * d; e += tm.size()) {
+    const int k = e / d, i = e - k * d;
+    W[k * lda + i] = js.lam[k] * Vt[js.pos[k] * ldv + i];
+  }
+  tm.sync();
+  const int *pos = js.pos;
+  mma_gemm<true>(
+      d, r, [&](int i, int k) { return W[k * lda + i]; }, [&](int k, int j) { return Vt[pos[k] * ldv + j]; },
+      emit);
+}
+
+// P = V M V' with M = D+ + L1(E) (order 1) or + L2(E, E) (order 2), see
+// psd_rebuild_first_order / psd_rebuild_second_order
+template <class Emit>
+__device__ void cta_rebuild_perturbative(const BlockTeam &tm, JacobiScratch &js, int d, int order, double *Mg,
+                                         Emit emit) {
+  double *A = js.A, *Vt = js.Vt, *lam = js.lam;
+  const int lda = js.lda, ldv = js.ldv;
+  for (int i = tm.rank; i < d; i += tm.size()) lam[i] = A[i * lda + i];
+  tm.sync();
+  if (order == 1) {
+    for (int e = tm.rank; e < d * d; e += tm.size()) {
+      const int i = e / d, j = e - i * d;
+      const double li = lam[i], lj = lam[j];
+      double m;
+      if (i == j) {
+        m = li > 0.0 ? li : 0.0;
+      } else {
+        double dd;
+        if (li > 0.0 && lj > 0.0) dd = 1.0;
+        else if (li <= 0.0 && lj <= 0.0) dd = 0.0;
+        else dd = (fmax(li, 0.0) - fmax(lj, 0.0)) / (li - lj);
+        m = A[i * lda + j] * dd;
+      }
+      A[i * lda + j] = m;
+    }
+    tm.sync();
+  } else {
+    for (int e = tm.rank; e < d * d; e += tm.size()) {
+      const int i = e / d, j = e - i * d;
+      const double li = lam[i], lj = lam[j];
+      if (i == j) A[i * lda + j] = 0.0;
+      else if ((li > 0.0) != (lj > 0.0)) A[i * lda + j] = A[i * lda + j] / (li - lj);
+    }
+    tm.sync();
+    auto cls = [&](int i) { return lam[i] > 0.0; };
+    auto g_of = [&](int i, int k) { return cls(i) != cls(k) ? A[i * lda + k] : 0.0; };
+    auto s_of = [&](int i, int k) { return cls(i) == cls(k) ? A[i * lda + k] : 0.0; };
+    mma_gemm<false>(
+        d, d, g_of, [&](int k, int j) { return fabs(lam[k]) * g_of(k, j); },
+        [&](int i, int j, double t1) {
+          if (cls(i) != cls(j)) return;
+          double base = 0.0;
+          if (i == j) base = lam[i] > 0.0 ? lam[i] : 0.0;
+          else if (cls(i)) base = A[i * lda + j];
+          Mg[i * d + j] = base - t1;
+        });
+    mma_gemm<false>(d, d, s_of, g_of, [&](int i, int j, double t2) {
+      if (!cls(i) || cls(j)) return;
+      Mg[i * d + j] = lam[i] * A[i * lda + j] - lam[j] * t2 / (lam[i] - lam[j]);
+    });
+    mma_gemm<false>(d, d, g_of, s_of, [&](int i, int j, double t3) {
+      if (!cls(i) || cls(j)) return;
+      const double v = Mg[i * d + j] + lam[i] * t3 / (lam[i] - lam[j]);
+      Mg[i * d + j] = v;
+      Mg[j * d + i] = v;
+    });
+    for (int e = tm.rank; e < d * d; e += tm.size()) {
+      const int i = e / d, j = e - i * d;
+      A[i * lda + j] = Mg[i * d + j];
+    }
+    tm.sync();
+  }
+  // T = M Vt -> Mg, P = Vt' T
+  mma_gemm<false>(
+      d, d, [&](int i, int k) { return A[i * lda + k]; }, [&](int k, int j) { return Vt[k * ldv + j]; },
+      [&](int i, int j, double v) { Mg[i * d + j] = v; });
+  mma_gemm<true>(
+      d, d, [&](int i, int k) { return Vt[k * ldv + i]; }, [&](int k, int j) { return Mg[k * d + j]; }, emit);
 }
 
 // ---------------------------------------------------------------------------
@@ -857,7 +1017,11 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
     }
   }
   tm.sync();
-  if (warm) {
+  double *Mg = ca.pscratch ? ca.pscratch + (int64_t)ca.slot * ca.pstride : nullptr;
+  constexpr bool kCta = std::is_same<Team, BlockTeam>::value;
+  if (kCta && warm && Mg) {
+    cta_warm_start(js, d, Mg);
+  } else if (warm) {
     // B = V X V' (rows of Vt are the previous eigenvectors): T1 = Vt X, then
     // B' = Vt T1' (= B for symmetric X) with the odd-ld operand on the right
     team_gemm_nt<MT>(tm, js.Vt, ldv, A, lda, A, lda, d);
@@ -874,8 +1038,7 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   }
   // first-order exit for CTA teams whose GEMM tiles fit (not for MINEIG)
   int order = 0;
-  const bool fo_ok = MODE != CONE_MINEIG && ntile * ntile <= MT * tm.size();
-  double *Mg = ca.pscratch ? ca.pscratch + (int64_t)ca.slot * ca.pstride : nullptr;
+  const bool fo_ok = MODE != CONE_MINEIG && (Mg || ntile * ntile <= MT * tm.size());
   const int sw = jacobi_sweeps(tm, js, d, dp, fo_ok ? &order : nullptr, fo_ok ? (Mg ? 2 : 1) : 0);
   if (MODE == CONE_HOT && tm.rank == 0 && W.sweeps) W.sweeps[k] = sw;
   // non-finite eigenvalue -> EigenFailure (symmat.py:162-163)
@@ -903,6 +1066,18 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
     S.w[j] += v;
   };
   auto emit_plain = [&](int a, int bcol, double v) { ca.out[off + (int64_t)a * d + bcol] = v; };
+  if constexpr (kCta) {
+    if (Mg) {
+      if (order > 0) {
+        if (MODE == CONE_HOT) cta_rebuild_perturbative(tm, js, d, order, Mg, emit_hot);
+        else cta_rebuild_perturbative(tm, js, d, order, Mg, emit_plain);
+      } else {
+        if (MODE == CONE_HOT) cta_rebuild_full(tm, js, d, emit_hot);
+        else cta_rebuild_full(tm, js, d, emit_plain);
+      }
+      return;
+    }
+  }
   if (order == 2) {
     if (MODE == CONE_HOT) psd_rebuild_second_order<MT>(tm, js, d, Mg, emit_hot);
     else psd_rebuild_second_order<MT>(tm, js, d, Mg, emit_plain);

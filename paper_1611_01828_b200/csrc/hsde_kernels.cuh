@@ -28,6 +28,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace hsde {
 
 constexpr int kBlock = 256;          // threads per CTA for streaming kernels
