@@ -657,47 +657,52 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
 // emit may not write an operand.  SYM: only tiles bi <= bj, emitted to both
 // triangles (exactly symmetric).  Ends with a team barrier.
 template <bool SYM, class LA, class RB, class Emit>
-__device__ void mma_gemm(int d, int K, LA la, RB rb, Emit emit) {
+__device__ void mma_gemm_mn(int M, int N, int K, LA la, RB rb, Emit emit) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nt = (d + 7) >> 3, K4 = (K + 3) & ~3;
-  const int ntiles = nt * nt;
+  const int mt = (M + 7) >> 3, ntc = (N + 7) >> 3, K4 = (K + 3) & ~3;
+  const int ntiles = mt * ntc;
   for (int t = w; t < ntiles; t += nw) {
-    const int bi = t / nt, bj = t - bi * nt;
+    const int bi = t / ntc, bj = t - bi * ntc;
     if (SYM && bi > bj) continue;
     const int ia = bi * 8 + (lane >> 2), jb = bj * 8 + (lane >> 2);
     double d0 = 0.0, d1 = 0.0;
     for (int k0 = 0; k0 < K4; k0 += 4) {
       const int k = k0 + (lane & 3);
-      const double a = (ia < d && k < K) ? la(ia, k) : 0.0;
-      const double b = (jb < d && k < K) ? rb(k, jb) : 0.0;
+      const double a = (ia < M && k < K) ? la(ia, k) : 0.0;
+      const double b = (jb < N && k < K) ? rb(k, jb) : 0.0;
       dmma884(d0, d1, a, b);
     }
     const int i = bi * 8 + (lane >> 2), j = bj * 8 + 2 * (lane & 3);
-    if (i >= d) continue;
+    if (i >= M) continue;
     if (!SYM) {
-      if (j < d) emit(i, j, d0);
-      if (j + 1 < d) emit(i, j + 1, d1);
+      if (j < N) emit(i, j, d0);
+      if (j + 1 < N) emit(i, j + 1, d1);
     } else if (bi < bj) {
-      if (j < d) {
+      if (j < N) {
         emit(i, j, d0);
         emit(j, i, d0);
       }
-      if (j + 1 < d) {
+      if (j + 1 < N) {
         emit(i, j + 1, d1);
         emit(j + 1, i, d1);
       }
     } else {
-      if (j < d && i <= j) {
+      if (j < N && i <= j) {
         emit(i, j, d0);
         if (i != j) emit(j, i, d0);
       }
-      if (j + 1 < d && i <= j + 1) {
+      if (j + 1 < N && i <= j + 1) {
         emit(i, j + 1, d1);
         if (i != j + 1) emit(j + 1, i, d1);
       }
     }
   }
   __syncthreads();
+}
+
+template <bool SYM, class LA, class RB, class Emit>
+__device__ void mma_gemm(int d, int K, LA la, RB rb, Emit emit) {
+  mma_gemm_mn<SYM>(d, d, K, la, rb, emit);
 }
 
 // Second-order projection of a nearly diagonal B = D + E (Daleckii-Krein to
@@ -858,40 +863,73 @@ __device__ void cta_rebuild_perturbative(const BlockTeam &tm, JacobiScratch &js,
     }
     tm.sync();
   } else {
-    for (int e = tm.rank; e < d * d; e += tm.size()) {
-      const int i = e / d, j = e - i * d;
-      const double li = lam[i], lj = lam[j];
-      if (i == j) A[i * lda + j] = 0.0;
-      else if ((li > 0.0) != (lj > 0.0)) A[i * lda + j] = A[i * lda + j] / (li - lj);
+    // class-sorted order (positive first): pos[0, r) = P, pos[r, d) = N; the
+    // P-N entries of E become G, the same-class ones stay, all into Mg
+    int *perm = js.pos;
+    int r = 0;
+    if (tm.rank < 32) {
+      int base = 0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int i0 = 0; i0 < d; i0 += 32) {
+          const int i = i0 + tm.rank;
+          const bool pk = i < d && ((lam[i] > 0.0) == (pass == 0));
+          const unsigned mk = __ballot_sync(0xffffffffu, pk);
+          if (pk) perm[base + __popc(mk & ((1u << tm.rank) - 1u))] = i;
+          base += __popc(mk);
+          if (pass == 0 && i0 + 32 >= d && tm.rank == 0) perm[d] = base;
+        }
     }
     tm.sync();
-    auto cls = [&](int i) { return lam[i] > 0.0; };
-    auto g_of = [&](int i, int k) { return cls(i) != cls(k) ? A[i * lda + k] : 0.0; };
-    auto s_of = [&](int i, int k) { return cls(i) == cls(k) ? A[i * lda + k] : 0.0; };
-    mma_gemm<false>(
-        d, d, g_of, [&](int k, int j) { return fabs(lam[k]) * g_of(k, j); },
-        [&](int i, int j, double t1) {
-          if (cls(i) != cls(j)) return;
-          double base = 0.0;
-          if (i == j) base = lam[i] > 0.0 ? lam[i] : 0.0;
-          else if (cls(i)) base = A[i * lda + j];
-          Mg[i * d + j] = base - t1;
-        });
-    mma_gemm<false>(d, d, s_of, g_of, [&](int i, int j, double t2) {
-      if (!cls(i) || cls(j)) return;
-      Mg[i * d + j] = lam[i] * A[i * lda + j] - lam[j] * t2 / (lam[i] - lam[j]);
-    });
-    mma_gemm<false>(d, d, g_of, s_of, [&](int i, int j, double t3) {
-      if (!cls(i) || cls(j)) return;
-      const double v = Mg[i * d + j] + lam[i] * t3 / (lam[i] - lam[j]);
+    r = perm[d];
+    for (int e = tm.rank; e < d * d; e += tm.size()) {
+      const int i = e / d, j = e - i * d;
+      const int pi = perm[i], pj = perm[j];
+      double v = 0.0;
+      if (i != j) {
+        v = A[pi * lda + pj];
+        if ((i < r) != (j < r)) v /= (lam[pi] - lam[pj]);
+      }
       Mg[i * d + j] = v;
-      Mg[j * d + i] = v;
-    });
-    for (int e = tm.rank; e < d * d; e += tm.size()) {
-      const int i = e / d, j = e - i * d;
-      A[i * lda + j] = Mg[i * d + j];
     }
     tm.sync();
+    const int n = d - r;
+    // M (sorted) into A:  M_PP = D_P + E_PP - G_PN |L_N| G_NP
+    mma_gemm_mn<false>(
+        r, r, n, [&](int i, int k) { return Mg[i * d + r + k]; },
+        [&](int k, int j) { return fabs(lam[perm[r + k]]) * Mg[(r + k) * d + j]; },
+        [&](int i, int j, double t1) {
+          const double base = (i == j) ? lam[perm[i]] : Mg[i * d + j];
+          A[i * lda + j] = base - t1;
+        });
+    //                  M_NN = -G_NP L_P G_PN
+    mma_gemm_mn<false>(
+        n, n, r, [&](int i, int k) { return Mg[(r + i) * d + k]; },
+        [&](int k, int j) { return lam[perm[k]] * Mg[k * d + r + j]; },
+        [&](int i, int j, double t1) { A[(r + i) * lda + r + j] = -t1; });
+    //                  M_PN = l_i G + (-l_j E_PP G + l_i G E_NN) / (l_i - l_j)
+    mma_gemm_mn<false>(
+        r, n, r, [&](int i, int k) { return Mg[i * d + k]; }, [&](int k, int j) { return Mg[k * d + r + j]; },
+        [&](int i, int j, double t2) {
+          const double li = lam[perm[i]], lj = lam[perm[r + j]];
+          A[i * lda + r + j] = li * Mg[i * d + r + j] - lj * t2 / (li - lj);
+        });
+    mma_gemm_mn<false>(
+        r, n, n, [&](int i, int k) { return Mg[i * d + r + k]; },
+        [&](int k, int j) { return Mg[(r + k) * d + r + j]; },
+        [&](int i, int j, double t3) {
+          const double li = lam[perm[i]], lj = lam[perm[r + j]];
+          const double v = A[i * lda + r + j] + li * t3 / (li - lj);
+          A[i * lda + r + j] = v;
+          A[(r + j) * lda + i] = v;
+        });
+    // T = M Vt(perm) -> Mg, P = Vt(perm)' T
+    mma_gemm<false>(
+        d, d, [&](int i, int k) { return A[i * lda + k]; },
+        [&](int k, int j) { return Vt[perm[k] * ldv + j]; }, [&](int i, int j, double v) { Mg[i * d + j] = v; });
+    mma_gemm<true>(
+        d, d, [&](int i, int k) { return Vt[perm[k] * ldv + i]; }, [&](int k, int j) { return Mg[k * d + j]; },
+        emit);
+    return;
   }
   // T = M Vt -> Mg, P = Vt' T
   mma_gemm<false>(
