@@ -170,7 +170,8 @@ def load_traffic(name: str):
 
 
 def roofline_for(cp, prof_ms: dict, launches_per_kernel: int, peaks: dict, half: bool = True):
-    items = [(ms, name) for name, ms in prof_ms.items() if ms > 0 and kernel_units(cp, name, half)[0]]
+    items = [(ms, name) for name, ms in prof_ms.items()
+             if ms > 0 and kernel_units(cp, name, half)[0] and kernel_units(cp, name, half)[1] > 0]
     if not items:
         return None, None
     out = {}
