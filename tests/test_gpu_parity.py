@@ -385,3 +385,40 @@ def test_half_passes_off_for_nonsymmetric_columns():
 
     O.solve(bad, O.OracleSettings(max_iters=100, tol=1e-300), callback=cb)
     assert rel(u, ref["u"]) <= 1e-9
+
+
+def test_project_cone_nearly_diagonal():
+    """Blocks D + E with small E hit the perturbative exits (first / second
+    order, CTA and warp teams) before any rotation; eigh projection at 1e-13."""
+    import scipy.sparse as sp
+
+    from paper_1611_01828_b200.problem import CliqueDecomposition, DecomposedProblem
+
+    sizes = [24, 40, 80, 80, 33]
+    n = sum(sizes)
+    cl, o = [], 0
+    for d in sizes:
+        cl.append(list(range(o, o + d)))
+        o += d
+    dec = CliqueDecomposition.build(n, cl)
+    A = sp.csr_matrix(([1.0], ([0], [0])), shape=(1, n * n))
+    dp = DecomposedProblem(n=n, m=1, c=np.eye(n).ravel(), A=A, b=np.ones(1), dec=dec,
+                           block_dims=(n,))
+    _, layout = H.build_hsde(dp)
+    rng = np.random.default_rng(11)
+    u = rng.normal(size=layout.total)
+    s_in = u[layout.sl_s]
+    for k, d in enumerate(sizes):
+        lam = rng.uniform(0.5, 2.0, d) * rng.choice([-1.0, 1.0], d)
+        e = rng.normal(size=(d, d))
+        eps = [1e-9, 1e-7, 1e-7, 1e-12, 1e-6][k]
+        b = np.diag(lam) + eps * (e + e.T) / 2 * (1 - np.eye(d))
+        s_in[dec.offsets[k]: dec.offsets[k + 1]] = b.ravel()
+    u[layout.sl_s] = s_in
+    got = H.project_cone(u, layout)[layout.sl_s]
+    for k, d in enumerate(sizes):
+        o0, o1 = dec.offsets[k], dec.offsets[k + 1]
+        b = s_in[o0:o1].reshape(d, d)
+        w, v = np.linalg.eigh(0.5 * (b + b.T))
+        want = (v * np.maximum(w, 0.0)) @ v.T
+        assert rel(got[o0:o1], want.ravel()) <= 1e-13, d

@@ -138,3 +138,40 @@ def test_merit_tracker_warns(caplog):
         for k, v in [(20, 1.0), (40, 0.9), (60, 2.0), (80, 2.0), (100, 2.0), (120, 3.0)]:
             tr.record(k, v)
     assert any("fixed-point residual rose" in r.message for r in caplog.records)
+
+
+def _so_projection(lam, E):
+    """Second-order Daleckii-Krein projection of diag(lam) + E (E off-diagonal),
+    the formula of hsde_eig.cuh's cta_rebuild_perturbative (order 2)."""
+    p = lam > 0
+    diff = p[:, None] != p[None, :]
+    den = lam[:, None] - lam[None, :]
+    G = np.where(diff, E / np.where(diff, den, 1.0), 0.0)
+    ES = np.where(~diff, E, 0.0)
+    T1 = G @ (np.abs(lam)[:, None] * G)
+    T2, T3 = ES @ G, G @ ES
+    M = np.where(p[:, None] & p[None, :], ES, 0.0) - np.where(~diff, T1, 0.0)
+    M[np.diag_indices_from(M)] = np.maximum(lam, 0.0) - np.diag(T1)
+    pn = p[:, None] & ~p[None, :]
+    mpn = lam[:, None] * G + (-lam[None, :] * T2 + lam[:, None] * T3) / np.where(pn, den, 1.0)
+    M = np.where(pn, mpn, M)
+    M = np.where(pn.T, mpn.T, M)
+    return M
+
+
+def test_second_order_projection_formula():
+    """P(D + E) by the second-order expansion: error O(|E|^3), against eigh."""
+    rng = np.random.default_rng(3)
+    n = 16
+    lam = np.concatenate([rng.uniform(0.3, 2.0, 9), -rng.uniform(0.3, 2.0, 7)])
+    errs = []
+    for eps in (1e-2, 1e-3, 1e-4):
+        E = rng.normal(size=(n, n))
+        E = (E + E.T) / 2
+        np.fill_diagonal(E, 0.0)
+        E *= eps
+        w, v = np.linalg.eigh(np.diag(lam) + E)
+        exact = (v * np.maximum(w, 0.0)) @ v.T
+        errs.append(np.abs(_so_projection(lam, E) - exact).max())
+    assert errs[2] < 1e-11
+    assert errs[0] / errs[1] > 300 and errs[1] / errs[2] > 300  # cubic
