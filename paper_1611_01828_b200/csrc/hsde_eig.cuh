@@ -272,7 +272,22 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp, i
       double g = CUDART_INF;
       for (int i = tm.rank; i < d; i += T) g = fmin(g, fabs(A[i * lda + i]));
       g = team_min(tm, g, js.red);
-      if (js.dbg && tm.rank == 0) js.dbg[63] = g / sqrt(norm2);
+      if (js.dbg) {  // diagnostics: g and the cross-class (P-N) part of off(A)
+        double pn = 0.0;
+        for (int e = tm.rank; e < dp * dp; e += T) {
+          const int i = e / dp, j = e - i * dp;
+          if (j <= i || i >= d || j >= d) continue;
+          if ((A[i * lda + i] > 0.0) != (A[j * lda + j] > 0.0)) {
+            const double a = A[i * lda + j];
+            pn += 2.0 * (a * a);
+          }
+        }
+        pn = team_sum(tm, pn, js.red);
+        if (tm.rank == 0) {
+          js.dbg[63] = g / sqrt(norm2);
+          if (sweep < 20) js.dbg[40 + sweep] = sqrt(pn / norm2);
+        }
+      }
       if (off2 <= 1e-6 * g * g) {
         const double off = sqrt(off2);
         if (off2 <= tau * g) {

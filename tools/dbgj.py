@@ -19,7 +19,8 @@ for q in cliques:
         h.iterate(it - done)
         done = it
         d = h.debug_jacobi(q)
-        vals = [v for v in d[1:63] if v >= 0]
+        vals = [v for v in d[1:40] if v >= 0]
+        pn = [v for v in d[40:60] if v >= 0]
         print(q, it, "warm" if d[0] else "cold", " ".join(f"{v:.1e}" for v in vals),
-              f" | min|lambda|/|A| {d[63]:.1e}", flush=True)
+              f"| PN {' '.join(f'{v:.1e}' for v in pn)} | g {d[63]:.1e}", flush=True)
     h.close()
