@@ -1478,7 +1478,7 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
   CK(cudaStreamSynchronize(h->st));
   h->schur_diag = gv[1] == 0.0;
   for (auto &s : h->sh)
-    s.grid_schur = h->schur_diag ? grid_for(m, 64) : std::min(148 * 2, std::max(1, (m + 7) / 8));
+    s.grid_schur = h->schur_diag ? grid_for(m, 64) : std::min(148 * 4, std::max(1, (m + 7) / 8));
   const double *bsrc = descs[0].b;
   double nb2 = 0;
   for (int i = 0; i < m; ++i) nb2 += bsrc[i] * bsrc[i];

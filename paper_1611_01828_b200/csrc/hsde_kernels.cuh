@@ -321,9 +321,17 @@ __global__ void __launch_bounds__(kBlock) k_schur(DevProblem P, const double *__
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < P.m; i += warps) {
     const double *row = P.sinv + (int64_t)i * P.m;
-    double acc = 0.0;
-    for (int j = lane; j < P.m; j += 32) acc += row[j] * qs[j];
-    acc = warp_sum(acc);
+    // four independent partial sums: four row loads in flight per lane
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int j = lane;
+    for (; j + 96 < P.m; j += 128) {
+      a0 += __ldcs(row + j) * qs[j];
+      a1 += __ldcs(row + j + 32) * qs[j + 32];
+      a2 += __ldcs(row + j + 64) * qs[j + 64];
+      a3 += __ldcs(row + j + 96) * qs[j + 96];
+    }
+    for (; j < P.m; j += 32) a0 += __ldcs(row + j) * qs[j];
+    const double acc = warp_sum((a0 + a1) + (a2 + a3));
     if (lane == 0) g[i] = acc;
   }
 }
