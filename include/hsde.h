@@ -184,6 +184,24 @@ int hsde_stats(hsde_t *h, double *out);
  * subsequent iterations. */
 int hsde_debug_jacobi(hsde_t *h, int32_t clique, double *out64);
 
+/* ---- Host decomposition (no GPU needed) ------------
+ * Chordal extension + maximal cliques of one block's sparsity pattern, with
+ * the reference's orderings and tie-breaking (graphs.py:73-184, 217-220):
+ * maximum cardinality search, greedy minimum-degree fill when the pattern is
+ * not chordal (extend != 0; else HSDE_ERR_ARG = NotChordal), elimination
+ * cliques kept if maximal, cliques sorted by (min node, sorted nodes).
+ * Edges (ei[k], ej[k]) are 0-based pairs; self-loops and duplicates ignored. */
+typedef struct hsde_pattern hsde_pattern_t;
+int hsde_pattern_decompose(int32_t n, int64_t n_edges, const int32_t *ei, const int32_t *ej,
+                           int32_t extend, hsde_pattern_t **out);
+int hsde_pattern_sizes(const hsde_pattern_t *p, int64_t *n_cliques, int64_t *n_nodes, int64_t *n_fill,
+                       int32_t *was_chordal);
+/* cliques as CSR: ptr[n_cliques + 1], nodes[n_nodes] (ascending per clique) */
+int hsde_pattern_cliques(const hsde_pattern_t *p, int64_t *ptr, int32_t *nodes);
+/* fill edges (a < b) in the order the elimination added them */
+int hsde_pattern_fill(const hsde_pattern_t *p, int32_t *fi, int32_t *fj);
+void hsde_pattern_destroy(hsde_pattern_t *p);
+
 #ifdef __cplusplus
 }
 #endif

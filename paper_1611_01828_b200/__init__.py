@@ -6,6 +6,7 @@ Drop-in for the solve path of the reference package ``chordalsdp``
 hand-written CUDA kernels of ``libhsde.so`` (csrc/, C ABI in include/hsde.h).
 """
 
+from .decompose import chordal_cliques, decompose
 from .errors import EigenFailure, FactorizationFailure, TauZero
 from .problem import (CliqueDecomposition, CompressedProblem, DecomposedProblem, compress,
                       expand_to_mirror)
@@ -21,6 +22,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "CliqueDecomposition", "CompressedProblem", "DecomposedProblem", "EigenFailure",
+    "chordal_cliques", "decompose",
     "FactorizationFailure", "HsdeState", "IterationInfo", "KktCache", "ProblemStats",
     "PatternEntries", "QOperator", "Residuals", "STATUS_DUAL_INFEASIBLE", "STATUS_MAX_ITERS", "STATUS_OPTIMAL",
     "STATUS_PRIMAL_INFEASIBLE", "SolverReport", "SolverSettings", "TauZero", "Timing",

@@ -33,7 +33,8 @@ EXPORTED = (
     "hsde_get_minv_zeta", "hsde_time_iterations", "hsde_profile_iterations",
     "hsde_profile_name", "hsde_sync", "hsde_set_alpha", "hsde_stats", "hsde_create_sharded",
     "hsde_nccl_unique_id", "hsde_shard_total", "hsde_set_state_shard", "hsde_get_state_shard",
-    "hsde_debug_jacobi",
+    "hsde_debug_jacobi", "hsde_pattern_decompose", "hsde_pattern_sizes", "hsde_pattern_cliques",
+    "hsde_pattern_fill", "hsde_pattern_destroy",
 )
 HSDE_NCCL_ID_BYTES = 128
 
@@ -120,6 +121,12 @@ def load() -> C.CDLL:
         "hsde_set_state_shard": (C.c_int, [vp, C.c_int32, _dp, _dp]),
         "hsde_get_state_shard": (C.c_int, [vp, C.c_int32, _dp, _dp]),
         "hsde_debug_jacobi": (C.c_int, [vp, C.c_int32, _dp]),
+        "hsde_pattern_decompose": (C.c_int, [C.c_int32, C.c_int64, _i32p, _i32p, C.c_int32,
+                                             C.POINTER(vp)]),
+        "hsde_pattern_sizes": (C.c_int, [vp, _i64p, _i64p, _i64p, _i32p]),
+        "hsde_pattern_cliques": (C.c_int, [vp, _i64p, _i32p]),
+        "hsde_pattern_fill": (C.c_int, [vp, _i32p, _i32p]),
+        "hsde_pattern_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
