@@ -202,6 +202,22 @@ int hsde_pattern_cliques(const hsde_pattern_t *p, int64_t *ptr, int32_t *nodes);
 int hsde_pattern_fill(const hsde_pattern_t *p, int32_t *fi, int32_t *fj);
 void hsde_pattern_destroy(hsde_pattern_t *p);
 
+/* ---- SDPA sparse-format reader (no GPU needed) -----
+ * Replaces chordalsdp/sdpa.py:94-234 parse_sdpa.  text[0..len) is the file
+ * (UTF-8).  On a malformed file returns HSDE_ERR_ARG and hsde_sdpa_error()
+ * gives the reference's message, its 1-based line number and whether it is a
+ * DuplicateEntry (thread-local, valid until the next parse on this thread).
+ * Entries come back sorted by (mat, blk, i, j): mat 0 = F0, blk/i/j 0-based,
+ * i <= j (lower-triangle input normalised), explicit zeros kept. */
+typedef struct hsde_sdpa hsde_sdpa_t;
+int hsde_sdpa_parse(const char *text, int64_t len, hsde_sdpa_t **out);
+const char *hsde_sdpa_error(int64_t *line, int32_t *duplicate);
+int hsde_sdpa_sizes(const hsde_sdpa_t *p, int32_t *m, int32_t *nblocks, int64_t *n_entries);
+/* block_dims[nblocks] (signed: < 0 = diagonal block), b[m], entries[n_entries] */
+int hsde_sdpa_data(const hsde_sdpa_t *p, int32_t *block_dims, double *b, int32_t *mat, int32_t *blk,
+                   int32_t *i, int32_t *j, double *val);
+void hsde_sdpa_destroy(hsde_sdpa_t *p);
+
 #ifdef __cplusplus
 }
 #endif

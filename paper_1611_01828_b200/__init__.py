@@ -8,6 +8,7 @@ hand-written CUDA kernels of ``libhsde.so`` (csrc/, C ABI in include/hsde.h).
 
 from .decompose import chordal_cliques, decompose
 from .errors import EigenFailure, FactorizationFailure, TauZero
+from .sdpa import DuplicateEntry, ParseError, SdpProblem, SymMatrix, parse_sdpa
 from .problem import (CliqueDecomposition, CompressedProblem, DecomposedProblem, compress,
                       expand_to_mirror)
 from .report import (STATUS_DUAL_INFEASIBLE, STATUS_MAX_ITERS, STATUS_OPTIMAL,
@@ -15,14 +16,15 @@ from .report import (STATUS_DUAL_INFEASIBLE, STATUS_MAX_ITERS, STATUS_OPTIMAL,
                      SolverReport, Timing, emit_report, read_report)
 from .solver import (HsdeState, IterationInfo, KktCache, QOperator, SolverSettings,
                      VariableLayout, affine_project, build_hsde, initial_state, iterate,
-                     project_cone, recover, residuals, setup_cache, solve_decomposed,
+                     project_cone, recover, residuals, setup_cache, solve, solve_decomposed,
                      solve_inner)
 
 __version__ = "0.1.0"
 
 __all__ = [
     "CliqueDecomposition", "CompressedProblem", "DecomposedProblem", "EigenFailure",
-    "chordal_cliques", "decompose",
+    "chordal_cliques", "decompose", "DuplicateEntry", "ParseError", "SdpProblem", "SymMatrix",
+    "parse_sdpa", "solve",
     "FactorizationFailure", "HsdeState", "IterationInfo", "KktCache", "ProblemStats",
     "PatternEntries", "QOperator", "Residuals", "STATUS_DUAL_INFEASIBLE", "STATUS_MAX_ITERS", "STATUS_OPTIMAL",
     "STATUS_PRIMAL_INFEASIBLE", "SolverReport", "SolverSettings", "TauZero", "Timing",

@@ -34,7 +34,8 @@ EXPORTED = (
     "hsde_profile_name", "hsde_sync", "hsde_set_alpha", "hsde_stats", "hsde_create_sharded",
     "hsde_nccl_unique_id", "hsde_shard_total", "hsde_set_state_shard", "hsde_get_state_shard",
     "hsde_debug_jacobi", "hsde_pattern_decompose", "hsde_pattern_sizes", "hsde_pattern_cliques",
-    "hsde_pattern_fill", "hsde_pattern_destroy",
+    "hsde_pattern_fill", "hsde_pattern_destroy", "hsde_sdpa_parse", "hsde_sdpa_error",
+    "hsde_sdpa_sizes", "hsde_sdpa_data", "hsde_sdpa_destroy",
 )
 HSDE_NCCL_ID_BYTES = 128
 
@@ -127,6 +128,11 @@ def load() -> C.CDLL:
         "hsde_pattern_cliques": (C.c_int, [vp, _i64p, _i32p]),
         "hsde_pattern_fill": (C.c_int, [vp, _i32p, _i32p]),
         "hsde_pattern_destroy": (None, [vp]),
+        "hsde_sdpa_parse": (C.c_int, [C.c_char_p, C.c_int64, C.POINTER(vp)]),
+        "hsde_sdpa_error": (C.c_char_p, [_i64p, _i32p]),
+        "hsde_sdpa_sizes": (C.c_int, [vp, _i32p, _i32p, _i64p]),
+        "hsde_sdpa_data": (C.c_int, [vp, _i32p, _dp, _i32p, _i32p, _i32p, _i32p, _dp]),
+        "hsde_sdpa_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -8,9 +8,10 @@ C++ in ``libhsde.so`` (``hsde_pattern_*``) with the reference's orderings and
 tie-breaking (graphs.py:73-184, 217-220), so the cliques -- and therefore the
 slot layout and every iterate -- are identical to the reference's.
 
-Input: the reference's ``SdpProblem`` (sdpa.py:58-91) or any object with
-``m``, ``block_dims``, ``b``, ``C[blk]`` and ``A[i][blk]`` whose blocks carry
-upper-triangle ``entries`` (i, j, value).
+Input: :func:`paper_1611_01828_b200.sdpa.parse_sdpa`'s ``SdpProblem`` (flat
+``entry_table`` arrays, the fast path), the reference's ``SdpProblem``
+(sdpa.py:58-91) or any object with ``m``, ``block_dims``, ``b``, ``C[blk]``
+and ``A[i][blk]`` whose blocks carry upper-triangle ``entries`` (i, j, value).
 """
 from __future__ import annotations
 
@@ -70,17 +71,9 @@ def _entries(sym) -> np.ndarray:
     return np.asarray(ent, dtype=float).reshape(-1, 3)
 
 
-def decompose(problem, split_cones: bool = True) -> CompressedProblem:
-    """Decomposed standard form of a parsed problem, in the compressed layout
-    (decompose.py:106-176): c = -vec(F0) (OBJECTIVE_SIGN), A rows vec(F_i)
-    over both triangles, cliques of each block's extended aggregate pattern
-    (or one clique per block with ``split_cones=False``)."""
-    dims = tuple(int(d) for d in problem.block_dims)
-    sizes = [abs(d) for d in dims]
-    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-    n = int(offs[-1])
-    m = int(problem.m)
-    # entries per (matrix, block): global (row i, col j) upper triangle + value
+def _object_entries(problem, dims, offs, m):
+    """(global i, global j, value, matrix id) of every stored entry of an
+    object-view problem (``C[blk]`` / ``A[i][blk]`` with ``entries``)."""
     mats = [problem.C] + [problem.A[i] for i in range(m)]
     gi_l, gj_l, v_l, who_l = [], [], [], []
     for mid, blocks in enumerate(mats):
@@ -96,6 +89,29 @@ def decompose(problem, split_cones: bool = True) -> CompressedProblem:
     gj = np.concatenate(gj_l) if gj_l else np.zeros(0, np.int64)
     vv = np.concatenate(v_l) if v_l else np.zeros(0)
     who = np.concatenate(who_l) if who_l else np.zeros(0, np.int64)
+    return gi, gj, vv, who
+
+
+def decompose(problem, split_cones: bool = True) -> CompressedProblem:
+    """Decomposed standard form of a parsed problem, in the compressed layout
+    (decompose.py:106-176): c = -vec(F0) (OBJECTIVE_SIGN), A rows vec(F_i)
+    over both triangles, cliques of each block's extended aggregate pattern
+    (or one clique per block with ``split_cones=False``)."""
+    dims = tuple(int(d) for d in problem.block_dims)
+    sizes = [abs(d) for d in dims]
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n = int(offs[-1])
+    m = int(problem.m)
+    table = getattr(problem, "entry_table", None)
+    if table is not None:
+        # flat arrays from parse_sdpa (C++ reader): no per-entry Python objects
+        mat, blk, ii, jj, vv = table
+        gi = ii.astype(np.int64) + offs[blk]
+        gj = jj.astype(np.int64) + offs[blk]
+        vv = np.asarray(vv, dtype=float)
+        who = mat.astype(np.int64)
+    else:
+        gi, gj, vv, who = _object_entries(problem, dims, offs, m)
     # aggregate pattern (decompose.py:85-103): off-diagonal entries of F0 and
     # every F_i, explicit zeros included
     off = gi != gj

@@ -42,7 +42,7 @@ FULL_LAYOUT_MAX = 1 << 22
 __all__ = [
     "SolverSettings", "VariableLayout", "QOperator", "build_hsde", "KktCache", "setup_cache",
     "solve_inner", "affine_project", "project_cone", "HsdeState", "initial_state", "iterate",
-    "residuals", "recover", "IterationInfo", "solve_decomposed", "FactorizationFailure",
+    "residuals", "recover", "IterationInfo", "solve", "solve_decomposed", "FactorizationFailure",
     "TauZero", "EigenFailure",
 ]
 
@@ -661,6 +661,18 @@ def solve_decomposed(dp, settings: SolverSettings | None = None, iteration_callb
     report = _classify(sess, chk, k, timing)
     sess.h.close()
     return report
+
+
+def solve(problem, settings: SolverSettings | None = None, split_cones: bool = True,
+          iteration_callback=None) -> SolverReport:
+    """Decompose, embed, iterate and classify a parsed problem (solver.py:775-789):
+    host decomposition in C++ (:func:`paper_1611_01828_b200.decompose`), then
+    :func:`solve_decomposed` on the B200; decomposition time counts as setup."""
+    from .decompose import decompose
+    t0 = time.perf_counter()
+    cp = decompose(problem, split_cones=split_cones)
+    return solve_decomposed(cp, settings=settings, iteration_callback=iteration_callback,
+                            setup_elapsed=time.perf_counter() - t0)
 
 
 def recover(state: HsdeState, dp, settings: SolverSettings, iterations: int,

@@ -422,3 +422,25 @@ def test_project_cone_nearly_diagonal():
         w, v = np.linalg.eigh(0.5 * (b + b.T))
         want = (v * np.maximum(w, 0.0)) @ v.T
         assert rel(got[o0:o1], want.ravel()) <= 1e-13, d
+
+
+@pytest.mark.gpu
+def test_solve_from_sdpa_text():
+    """parse_sdpa -> solve (solver.py:775-789): C++ reader + C++ decomposition
+    + device iterations, on a max-cut SDP written as SDPA text."""
+    from paper_1611_01828_b200.synthetic import maxcut_graph
+    n = 300
+    edges = maxcut_graph(n, 11)
+    deg = np.bincount(edges.ravel(), minlength=n)
+    lines = [f"{n} = mDIM", "1 = nBLOCK", f"{n}", " ".join(["1.0"] * n)]
+    lines += [f"0 1 {i + 1} {i + 1} {0.25 * deg[i]!r}" for i in range(n) if deg[i]]
+    lines += [f"0 1 {j + 1} {i + 1} -0.25" for i, j in edges]  # lower triangle on purpose
+    lines += [f"{i + 1} 1 {i + 1} {i + 1} 1.0" for i in range(n)]
+    prob = H.parse_sdpa("\n".join(lines) + "\n")
+    st = H.SolverSettings(max_iters=4000)
+    rep = H.solve(prob, st)
+    assert rep.status == H.STATUS_OPTIMAL
+    assert abs(rep.objective_primal - rep.objective_dual) <= 1e-3 * abs(rep.objective_primal)
+    rep2 = H.solve_decomposed(H.decompose(prob), st)
+    assert rep2.iterations == rep.iterations and rep2.objective_primal == rep.objective_primal
+    assert rep.problem.n == n and rep.problem.m == n and rep.problem.p > 1
