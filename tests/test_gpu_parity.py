@@ -433,7 +433,7 @@ def test_solve_from_sdpa_text():
     edges = maxcut_graph(n, 11)
     deg = np.bincount(edges.ravel(), minlength=n)
     lines = [f"{n} = mDIM", "1 = nBLOCK", f"{n}", " ".join(["1.0"] * n)]
-    lines += [f"0 1 {i + 1} {i + 1} {0.25 * deg[i]!r}" for i in range(n) if deg[i]]
+    lines += [f"0 1 {i + 1} {i + 1} {float(0.25 * deg[i])!r}" for i in range(n) if deg[i]]
     lines += [f"0 1 {j + 1} {i + 1} -0.25" for i, j in edges]  # lower triangle on purpose
     lines += [f"{i + 1} 1 {i + 1} {i + 1} 1.0" for i in range(n)]
     prob = H.parse_sdpa("\n".join(lines) + "\n")
