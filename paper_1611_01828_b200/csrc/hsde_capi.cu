@@ -670,8 +670,8 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
     }
     s.block_plan.smem = per_blk;
     RC(dupload(h, &s.block_plan.ids, bids.data(), bids.size()));
-    s.block_plan.pstride = (int64_t)dpb * dpb;
-    RC(dalloc(h, &s.block_plan.pscratch, (size_t)bids.size() * dpb * dpb));
+    s.block_plan.pstride = 5 * (int64_t)dpb * dpb;  // class split: 5 d x d regions
+    RC(dalloc(h, &s.block_plan.pscratch, (size_t)bids.size() * s.block_plan.pstride));
     const int sm = maxsm;
     CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));

@@ -288,6 +288,10 @@ __device__ int jacobi_sweeps(const Team &tm, JacobiScratch &js, int d, int dp, i
           if (sweep < 20) js.dbg[40 + sweep] = sqrt(pn / norm2);
         }
       }
+      if (max_order > 2 && off2 <= 0.01 * g * g) {  // class split (cta_class_split)
+        *order = 3;
+        break;
+      }
       if (off2 <= 1e-6 * g * g) {
         const double off = sqrt(off2);
         if (off2 <= tau * g) {
@@ -955,6 +959,228 @@ __device__ void cta_rebuild_perturbative(const BlockTeam &tm, JacobiScratch &js,
 }
 
 // ---------------------------------------------------------------------------
+// Class-split exit (CTA teams, warm hot path): exact projection without a
+// Jacobi sweep when B = V' X V is close to diagonal.
+//
+// With the diagonal classes P (l > 0, r of them) and N (n = d - r) in sorted
+// order, the positive invariant subspace of B is span [I; X] (X: n x r), the
+// solution near 0 of the Riccati equation
+//     X L_P - L_N X = B_NP + E_NN X - X (E_PP + B_PN X)
+// (L = diagonal, E = off-diagonal within a class).  Every denominator
+// l_j - l_i (j in P, i in N) is >= 2g, g = min |l|, so the fixed-point
+// iteration contracts at about off(B) / 2g whatever the within-class
+// spacing; within-class coupling never has to be rotated away.  With
+// Z_P = [I; X] (I + X'X)^-1/2 and Z_N = [-X'; I] (I + XX')^-1/2 (exact
+// orthonormal bases of the two invariant subspaces; the inverse square roots
+// by their binomial series, |X'X| <= (off / 2g)^2),
+//     P = V'_P C V'_P',   V'_P = V Z_P,   C = Z_P' B Z_P = S_P (I + X'X) R S_P,
+// R = L_P + E_PP + B_PN X  (B [I; X] = [I; X] R), and V' = V [Z_P, Z_N] is
+// the next warm start.  No truncation: the only error is the fixed point's
+// (stopped at <= 2.5e-16) and rounding.  Taken when off(B) <= g / 10 (then no
+// eigenvalue changes sign, Weyl); otherwise, or if the iteration stalls, the
+// caller runs the sweeps.
+
+constexpr int kSplitMaxIter = 14;
+
+// one m8n8k4 output tile t of out(i, j) = sum_k la(i, k) rb(k, j) (M x N)
+template <class LA, class RB, class Emit>
+__device__ __forceinline__ void mma_tile(int t, int M, int N, int K, LA la, RB rb, Emit emit, int lane) {
+  const int ntc = (N + 7) >> 3;
+  const int bi = t / ntc, bj = t - bi * ntc;
+  const int ia = bi * 8 + (lane >> 2), jb = bj * 8 + (lane >> 2);
+  double d0 = 0.0, d1 = 0.0;
+  const int K4 = (K + 3) & ~3;
+  for (int k0 = 0; k0 < K4; k0 += 4) {
+    const int k = k0 + (lane & 3);
+    const double a = (ia < M && k < K) ? la(ia, k) : 0.0;
+    const double b = (jb < N && k < K) ? rb(k, jb) : 0.0;
+    dmma884(d0, d1, a, b);
+  }
+  const int i = bi * 8 + (lane >> 2), j = bj * 8 + 2 * (lane & 3);
+  if (i >= M) return;
+  if (j < N) emit(i, j, d0);
+  if (j + 1 < N) emit(i, j + 1, d1);
+}
+
+// two independent GEMMs in one pass (one barrier)
+template <class LA1, class RB1, class E1, class LA2, class RB2, class E2>
+__device__ void mma_gemm_dual(int M1, int N1, int K1, LA1 la1, RB1 rb1, E1 e1, int M2, int N2, int K2, LA2 la2,
+                              RB2 rb2, E2 e2) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int t1 = ((M1 + 7) >> 3) * ((N1 + 7) >> 3), t2 = ((M2 + 7) >> 3) * ((N2 + 7) >> 3);
+  for (int t = w; t < t1 + t2; t += nw) {
+    if (t < t1) mma_tile(t, M1, N1, K1, la1, rb1, e1, lane);
+    else mma_tile(t - t1, M2, N2, K2, la2, rb2, e2, lane);
+  }
+  __syncthreads();
+}
+
+// Mg: 5 d x d regions.  vst: the clique's eigenvector store (row c = basis
+// vector c).  Returns false (nothing emitted, vst and A untouched) when the
+// split does not apply; js.Vt is used as scratch either way.
+template <class Emit>
+__device__ bool cta_class_split(const BlockTeam &tm, JacobiScratch &js, int d, double *Mg, double *vst, Emit emit) {
+  double *A = js.A, *lam = js.lam;
+  const int lda = js.lda;
+  double g = CUDART_INF, o2 = 0.0;
+  for (int e = tm.rank; e < d * d; e += tm.size()) {
+    const int i = e / d, j = e - i * d;
+    const double a = A[i * lda + j];
+    if (i == j) {
+      lam[i] = a;
+      g = fmin(g, fabs(a));
+    } else {
+      o2 += a * a;
+    }
+  }
+  g = team_min(tm, g, js.red);
+  o2 = team_sum(tm, o2, js.red);
+  if (js.dbg && tm.rank == 0) js.dbg[62] = sqrt(o2) / g;
+  if (!(g > 0.0) || !(o2 <= 0.01 * g * g)) return false;  // also NaN
+  // class-sorted order: perm[0, r) = P, perm[r, d) = N
+  int *perm = js.pos;
+  if (tm.rank < 32) {
+    int base = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i0 = 0; i0 < d; i0 += 32) {
+        const int i = i0 + tm.rank;
+        const bool pk = i < d && ((lam[i] > 0.0) == (pass == 0));
+        const unsigned mk = __ballot_sync(0xffffffffu, pk);
+        if (pk) perm[base + __popc(mk & ((1u << tm.rank) - 1u))] = i;
+        base += __popc(mk);
+        if (pass == 0 && i0 + 32 >= d && tm.rank == 0) perm[d] = base;
+      }
+  }
+  tm.sync();
+  const int r = perm[d], n = d - r;
+  const int64_t dd = (int64_t)d * d;
+  double *Y = Mg, *YP = Mg + dd, *YN = YP + r * r, *SA = Mg + 2 * dd, *SB = Mg + 3 * dd, *R4 = Mg + 4 * dd;
+  double *X0 = js.Vt, *X1 = js.Vt + n * r;
+  auto bt = [&](int i, int j) { return A[perm[i] * lda + perm[j]]; };  // sorted B
+  // ---- Riccati fixed point from X1 = B_NP / Delta
+  double x2 = 0.0;
+  for (int e = tm.rank; e < n * r; e += tm.size()) {
+    const int i = e / r, j = e - i * r;
+    const double x = bt(r + i, j) / (lam[perm[j]] - lam[perm[r + i]]);
+    X0[e] = x;
+    x2 += x * x;
+  }
+  double prev = sqrt(team_sum(tm, x2, js.red));  // (barriers inside)
+  bool ok = prev == 0.0;
+  int it = 0;
+  for (; !ok && it < kSplitMaxIter; ++it) {
+    // Y = E_PP + B_PN X
+    mma_gemm_mn<false>(
+        r, r, n, [&](int i, int k) { return bt(i, r + k); }, [&](int k, int j) { return X0[k * r + j]; },
+        [&](int i, int j, double v) { Y[i * r + j] = v + (i != j ? bt(i, j) : 0.0); });
+    // X' = (B_NP + [E_NN | X] [X; -Y]) / Delta
+    double acc = 0.0;
+    mma_gemm_mn<false>(
+        n, r, d,
+        [&](int i, int k) { return k < n ? (k != i ? bt(r + i, r + k) : 0.0) : X0[i * r + (k - n)]; },
+        [&](int k, int j) { return k < n ? X0[k * r + j] : -Y[(k - n) * r + j]; },
+        [&](int i, int j, double v) {
+          const int pi = perm[r + i], pj = perm[j];
+          const double x = (A[pi * lda + pj] + v) / (lam[pj] - lam[pi]);
+          const double dx = x - X0[i * r + j];
+          acc += dx * dx;
+          X1[i * r + j] = x;
+        });
+    const double delta = sqrt(team_sum(tm, acc, js.red));
+    double *t = X0;
+    X0 = X1;
+    X1 = t;
+    const double rho = delta / prev;
+    if (delta == 0.0 || (rho < 0.5 && delta * rho <= 2.5e-16 * (1.0 - rho))) ok = true;
+    else if (!(rho < 0.5)) break;  // stalled (or NaN): let the sweeps handle it
+    prev = delta;
+  }
+  if (js.dbg && tm.rank == 0) js.dbg[60] = ok ? it : -1.0 - it;
+  if (!ok) return false;
+  // R - L_P = E_PP + B_PN X with the final X
+  mma_gemm_mn<false>(
+      r, r, n, [&](int i, int k) { return bt(i, r + k); }, [&](int k, int j) { return X0[k * r + j]; },
+      [&](int i, int j, double v) { Y[i * r + j] = v + (i != j ? bt(i, j) : 0.0); });
+  // ---- Y_P = X'X, Y_N = XX' (|Y_P|_F = |Y_N|_F sizes the series)
+  double acc = 0.0;
+  mma_gemm_dual(
+      r, r, n, [&](int i, int k) { return X0[k * r + i]; }, [&](int k, int j) { return X0[k * r + j]; },
+      [&](int i, int j, double v) {
+        YP[i * r + j] = v;
+        acc += v * v;
+      },
+      n, n, r, [&](int i, int k) { return X0[i * r + k]; }, [&](int k, int j) { return X0[j * r + k]; },
+      [&](int i, int j, double v) { YN[i * n + j] = v; });
+  const double y = sqrt(team_sum(tm, acc, js.red));
+  // (1 + y)^-1/2 = sum c_k y^k, c_k = c_{k-1} (-(2k - 1) / 2k): terms while y^k > 1e-17
+  int K = 0;
+  if (y > 0.0) {
+    double p = y;
+    while (K < 24 && p > 1e-17) {
+      ++K;
+      p *= y;
+    }
+  }
+  double cK = 1.0;
+  for (int k = 1; k <= K; ++k) cK *= -(2.0 * k - 1.0) / (2.0 * k);
+  // Horner: S = c_K I; S <- c_k I + Y S
+  double *SP = SA, *SN = SA + r * r, *TP = SB, *TN = SB + r * r;
+  for (int e = tm.rank; e < r * r + n * n; e += tm.size()) {
+    const bool inP = e < r * r;
+    const int q = inP ? e : e - r * r, m = inP ? r : n;
+    const int i = q / m, j = q - i * m;
+    SA[e] = (i == j) ? cK : 0.0;
+  }
+  tm.sync();
+  double c = cK;
+  for (int k = K - 1; k >= 0; --k) {
+    c *= -(2.0 * (k + 1)) / (2.0 * (k + 1) - 1.0);  // c_k from c_{k+1}
+    mma_gemm_dual(
+        r, r, r, [&](int i, int q) { return YP[i * r + q]; }, [&](int q, int j) { return SP[q * r + j]; },
+        [&](int i, int j, double v) { TP[i * r + j] = v + (i == j ? c : 0.0); },
+        n, n, n, [&](int i, int q) { return YN[i * n + q]; }, [&](int q, int j) { return SN[q * n + j]; },
+        [&](int i, int j, double v) { TN[i * n + j] = v + (i == j ? c : 0.0); });
+    double *t = SP;
+    SP = TP;
+    TP = t;
+    t = SN;
+    SN = TN;
+    TN = t;
+  }
+  // ---- [U | W] = V [[I, -X'], [X, I]] (sorted columns of V), into A
+  auto vh = [&](int i, int c) { return vst[perm[c] * d + i]; };
+  mma_gemm_dual(
+      d, r, n, [&](int i, int k) { return vh(i, r + k); }, [&](int k, int j) { return X0[k * r + j]; },
+      [&](int i, int j, double v) { A[i * lda + j] = vh(i, j) + v; },
+      d, n, r, [&](int i, int k) { return vh(i, k); }, [&](int k, int j) { return X0[j * r + k]; },
+      [&](int i, int j, double v) { A[i * lda + r + j] = vh(i, r + j) - v; });
+  // V' = [U S_P | W S_N] -> vst (rows 0..r-1: positive subspace)
+  mma_gemm_dual(
+      d, r, r, [&](int i, int k) { return A[i * lda + k]; }, [&](int k, int j) { return SP[k * r + j]; },
+      [&](int i, int j, double v) { vst[j * d + i] = v; },
+      d, n, n, [&](int i, int k) { return A[i * lda + r + k]; }, [&](int k, int j) { return SN[k * n + j]; },
+      [&](int i, int j, double v) { vst[(r + j) * d + i] = v; });
+  // C = S_P (I + Y_P) R S_P, R = L_P + Y
+  mma_gemm_mn<false>(
+      r, r, r, [&](int i, int k) { return YP[i * r + k] + (i == k ? 1.0 : 0.0); },
+      [&](int k, int j) { return Y[k * r + j] + (k == j ? lam[perm[j]] : 0.0); },
+      [&](int i, int j, double v) { R4[i * r + j] = v; });
+  mma_gemm_mn<false>(
+      r, r, r, [&](int i, int k) { return SP[i * r + k]; }, [&](int k, int j) { return R4[k * r + j]; },
+      [&](int i, int j, double v) { YP[i * r + j] = v; });
+  mma_gemm_mn<true>(
+      r, r, r, [&](int i, int k) { return YP[i * r + k]; }, [&](int k, int j) { return SP[k * r + j]; },
+      [&](int i, int j, double v) { R4[i * r + j] = v; });
+  // P = (V'_P C) V'_P'
+  mma_gemm_mn<false>(
+      d, r, r, [&](int i, int k) { return vst[k * d + i]; }, [&](int k, int j) { return R4[k * r + j]; },
+      [&](int i, int j, double v) { A[i * lda + j] = v; });
+  mma_gemm<true>(
+      d, r, [&](int i, int k) { return A[i * lda + k]; }, [&](int k, int j) { return vst[k * d + j]; }, emit);
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // cone kernels
 
 enum ConeMode { CONE_HOT = 0, CONE_PLAIN = 1, CONE_MINEIG = 2 };
@@ -1092,7 +1318,45 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   // first-order exit for CTA teams whose GEMM tiles fit (not for MINEIG)
   int order = 0;
   const bool fo_ok = MODE != CONE_MINEIG && (Mg || ntile * ntile <= MT * tm.size());
-  const int sw = jacobi_sweeps(tm, js, d, dp, fo_ok ? &order : nullptr, fo_ok ? (Mg ? 2 : 1) : 0);
+  // class split (CTA teams, hot path with the eigenvector store): exact exit
+  // as soon as off(B) <= g / 10, after 0 sweeps (warm) or a few (cold)
+  bool split_ok = kCta && MODE == CONE_HOT && ca.warm && Mg != nullptr;
+  int sw = 0;
+  for (;;) {
+    sw += jacobi_sweeps(tm, js, d, dp, fo_ok ? &order : nullptr, fo_ok ? (Mg ? (split_ok ? 3 : 2) : 1) : 0);
+    if constexpr (kCta) {
+      if (order == 3) {
+        // the split reads V from the store and uses js.Vt as scratch
+        for (int e = tm.rank; e < d * d; e += tm.size()) {
+          const int a = e / d, bcol = e - a * d;
+          W.vstore[off + e] = js.Vt[a * ldv + bcol];
+        }
+        tm.sync();
+        auto emit_split = [&](int a, int bcol, double v) {
+          const int64_t j = so + off + (int64_t)a * d + bcol;
+          S.u[j] = v;
+          S.w[j] += v;
+        };
+        if (cta_class_split(tm, js, d, Mg, W.vstore + off, emit_split)) {
+          if (tm.rank == 0) {
+            W.vvalid[k] = warm ? age + 1 : 1;
+            if (W.sweeps) W.sweeps[k] = sw;
+          }
+          return;
+        }
+        // stalled: restore Vt and continue sweeping without the split
+        for (int e = tm.rank; e < dp * ldv; e += tm.size()) {
+          const int i = e / ldv, j = e - i * ldv;
+          js.Vt[e] = (i < d && j < d) ? W.vstore[off + (int64_t)i * d + j] : (i == j ? 1.0 : 0.0);
+        }
+        tm.sync();
+        split_ok = false;
+        order = 0;
+        continue;
+      }
+    }
+    break;
+  }
   if (MODE == CONE_HOT && tm.rank == 0 && W.sweeps) W.sweeps[k] = sw;
   // non-finite eigenvalue -> EigenFailure (symmat.py:162-163)
   double nb = 0.0;

@@ -22,5 +22,6 @@ for q in cliques:
         vals = [v for v in d[1:40] if v >= 0]
         pn = [v for v in d[40:60] if v >= 0]
         print(q, it, "warm" if d[0] else "cold", " ".join(f"{v:.1e}" for v in vals),
-              f"| PN {' '.join(f'{v:.1e}' for v in pn)} | g {d[63]:.1e}", flush=True)
+              f"| PN {' '.join(f'{v:.1e}' for v in pn)} | g {d[63]:.1e} | split it {d[60]:.0f} off/g {d[62]:.2e}",
+              flush=True)
     h.close()
