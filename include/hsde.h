@@ -42,6 +42,7 @@ extern "C" {
                                   instead of the identity A ua = S^{-1} A t        */
 #define HSDE_FLAG_NO_FACTOR 2  /* skip the Schur factorisation (residual-only handle) */
 #define HSDE_FLAG_COLD_EIG 4   /* no warm start of the clique eigensolves             */
+#define HSDE_FLAG_NO_SPLIT 8   /* CTA cliques: no k_cone_split fast path (Jacobi only) */
 
 typedef struct hsde_problem_desc {
   int64_t n;                 /* ambient matrix order (informational)              */
@@ -175,8 +176,12 @@ const char *hsde_profile_name(int32_t slot);
 int hsde_sync(hsde_t *h);
 /* Eigensolver statistics of the last hot projection:
  * out[0] mean Jacobi sweeps per Jacobi-solved clique, out[1] max, out[2] mean
- * over d > 32, out[3] 1 if warm starts are enabled. */
-#define HSDE_STATS_LEN 4
+ * over d > 32, out[3] 1 if warm starts are enabled, out[4] / out[5] fraction of
+ * the d > 32 cliques the k_cone_split fast path finished / handed to the Jacobi
+ * kernel in the last hot projection, out[6] mean fixed-point iterations of the
+ * finished ones, out[7..9] fraction handed over because off(B) > g / 10, r > n,
+ * or the fixed point stalled. */
+#define HSDE_STATS_LEN 10
 int hsde_stats(hsde_t *h, double *out);
 /* Diagnostics: off-diagonal norm history (relative, per sweep) of the last
  * hot projection of one clique: out[0] = 1 if warm-started, out[1..] = |off|/|A|

@@ -21,7 +21,8 @@ HSDE_OK, HSDE_ERR_CUDA, HSDE_ERR_EIGEN, HSDE_ERR_FACTOR, HSDE_ERR_ARG, HSDE_ERR_
 HSDE_FLAG_EXACT_UY = 1
 HSDE_FLAG_NO_FACTOR = 2
 HSDE_FLAG_COLD_EIG = 4
-HSDE_STATS_LEN = 4
+HSDE_FLAG_NO_SPLIT = 8
+HSDE_STATS_LEN = 10
 HSDE_CHECK_LEN = 8
 HSDE_CERT_LEN = 7
 HSDE_PROFILE_SLOTS = 16
@@ -345,7 +346,10 @@ class Handle:
         out = np.empty(HSDE_STATS_LEN)
         self._rc(self._lib.hsde_stats(self._h, _ptr(out, C.c_double)))
         return {"mean_sweeps": float(out[0]), "max_sweeps": float(out[1]),
-                "mean_sweeps_large": float(out[2]), "warm_start": bool(out[3])}
+                "mean_sweeps_large": float(out[2]), "warm_start": bool(out[3]),
+                "split_done": float(out[4]), "split_handoff": float(out[5]),
+                "split_fp_iters": float(out[6]), "handoff_off": float(out[7]), "handoff_rn": float(out[8]),
+                "handoff_stall": float(out[9])}
 
     def debug_jacobi(self, clique: int = 0) -> np.ndarray:
         out = np.empty(64)

@@ -76,6 +76,7 @@ struct ConePlan {
   int per_block = 0;       // warps per CTA (warp plan)
   double *pscratch = nullptr;  // CTA plan: d x d global scratch per CTA (second-order rebuild)
   int64_t pstride = 0;
+  size_t split_smem = 0;       // CTA plan: k_cone_split (0: not launched)
 };
 
 enum Mode { MODE_SINGLE = 0, MODE_EMULATED = 1, MODE_NCCL = 2 };
@@ -140,6 +141,7 @@ struct hsde_handle {
   int gci_len = 0;
   bool factor = true;
   bool warm = true;
+  bool split = true;  // k_cone_split fast path for CTA cliques (HSDE_FLAG_NO_SPLIT off)
   bool multi() const { return mode != MODE_SINGLE; }
 };
 
@@ -318,7 +320,16 @@ __global__ void k_diag_finish(double *diag, int m, int *flag) {
 int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool block,
                 const double *in, double *out, double in_scale, cudaStream_t st) {
   if (pl.count == 0) return 0;
-  ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0, pl.pscratch, pl.pstride, 0};
+  static const int split_refresh = [] {
+    const char *e = std::getenv("HSDE_SPLIT_REFRESH");
+    return e ? std::atoi(e) : kSplitRefreshIters;
+  }();
+  static const int split_vupdate = [] {
+    const char *e = std::getenv("HSDE_SPLIT_VUPDATE");
+    return e ? std::atoi(e) : 1;
+  }();
+  ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0, pl.pscratch, pl.pstride, 0,
+              split_refresh, split_vupdate};
   if (!block) {
     const int grid = (pl.count + pl.per_block - 1) / pl.per_block;
     const int thr = pl.per_block * 32;
@@ -326,7 +337,12 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
     else if (mode == CONE_PLAIN) k_cone_warp<CONE_PLAIN><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
     else k_cone_warp<CONE_MINEIG><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
   } else {
-    if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
+    DevWork W = s.W;
+    W.cstate = nullptr;  // k_cone_block does every clique
+    if (mode == CONE_HOT && pl.split_smem && h->warm && h->split) {
+      // fast path + in-CTA Jacobi fallback (hsde_split.cuh)
+      k_cone_split<<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, s.W, ca);
+    } else if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, W, ca);
     else if (mode == CONE_PLAIN) k_cone_block<CONE_PLAIN><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
     else k_cone_block<CONE_MINEIG><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
   }
@@ -673,6 +689,12 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
     s.block_plan.pstride = 5 * (int64_t)dpb * dpb;  // class split: 5 d x d regions
     RC(dalloc(h, &s.block_plan.pscratch, (size_t)bids.size() * s.block_plan.pstride));
     const int sm = maxsm;
+    int dmax = 0;
+    for (int k : bids) dmax = std::max(dmax, s.sizes[k]);
+    if (dmax <= kSplitMaxD) {
+      s.block_plan.split_smem = std::max((size_t)split_smem_doubles(dmax) * sizeof(double), per_blk);
+      CK(cudaFuncSetAttribute(k_cone_split, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    }
     CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_MINEIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -1343,6 +1365,8 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   RC(dalloc(h, &s.W.vstore, n_d));
   RC(dalloc(h, &s.W.vvalid, std::max(p, 1)));
   RC(dalloc(h, &s.W.sweeps, std::max(p, 1)));
+  RC(dalloc(h, &s.W.cstate, std::max(p, 1)));
+  RC(dalloc(h, &s.W.xarg, std::max<int64_t>(n_d, 1)));
   RC(dalloc(h, &s.W.sepbuf, std::max(d->n_sep, 1)));
   RC(dalloc(h, &s.W.qbuf, std::max(m, 1)));
   RC(dalloc(h, &s.W.red, 8));
@@ -1351,6 +1375,7 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   CK(cudaMemset(s.W.err, 0, sizeof(int)));
   CK(cudaMemset(s.W.vvalid, 0, sizeof(int) * std::max(p, 1)));
   CK(cudaMemset(s.W.sweeps, 0, sizeof(int) * std::max(p, 1)));
+  CK(cudaMemset(s.W.cstate, 0xff, sizeof(int) * std::max(p, 1)));
   CK(cudaMemset(s.d_chk, 0, sizeof(double) * 64));
   s.grid_nc = grid_for(n_c);
   s.grid_ua = s.grid_nc;
@@ -1595,6 +1620,7 @@ int hsde_create_sharded(const hsde_problem_desc *descs, int32_t nshards, const h
   h->dev = s->device;
   h->factor = !(s->flags & HSDE_FLAG_NO_FACTOR);
   h->warm = !(s->flags & HSDE_FLAG_COLD_EIG);
+  h->split = !(s->flags & HSDE_FLAG_NO_SPLIT);
   if (cudaMallocHost(&h->h_chk, 64 * sizeof(double)) != cudaSuccess) {
     g_create_error = "cudaMallocHost failed";
     delete h;
@@ -2104,21 +2130,41 @@ int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches) 
 int hsde_stats(hsde_t *h, double *out) {
   if (!h || !out) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  double sum = 0, mx = 0, sum_big = 0, n_big = 0, n = 0;
+  double sum = 0, mx = 0, sum_big = 0, n_big = 0, n = 0, n_done = 0, n_hand = 0, n_fp = 0, n_why[3] = {0, 0, 0};
   for (auto &s : h->sh) {
-    std::vector<int> sw(std::max(s.P.p, 1));
+    std::vector<int> sw(std::max(s.P.p, 1)), cs(std::max(s.P.p, 1));
     CK(cudaMemcpyAsync(sw.data(), s.W.sweeps, sizeof(int) * sw.size(), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaMemcpyAsync(cs.data(), s.W.cstate, sizeof(int) * cs.size(), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
+    const bool split_ran = s.block_plan.split_smem && h->warm && h->split;
     for (int k = 0; k < s.P.p; ++k) {
+      const bool big = s.sizes[k] > 32;
+      const bool fast = big && split_ran && cs[k] == SPLIT_DONE;
+      if (big && split_ran) {
+        n_done += fast;
+        n_hand += cs[k] >= SPLIT_HANDOFF;
+        if (cs[k] >= SPLIT_HANDOFF && cs[k] <= SPLIT_HANDOFF + 2) ++n_why[cs[k] - SPLIT_HANDOFF];
+      }
+      if (fast) {  // no Jacobi solve; sweeps holds -(fixed-point iterations)
+        n_fp -= sw[k];
+        continue;
+      }
       sum += sw[k];
       n += 1;
       mx = std::max(mx, (double)sw[k]);
-      if (s.sizes[k] > 32) {
+      if (big) {
         sum_big += sw[k];
         n_big += 1;
       }
     }
   }
+  int nbig = 0;
+  for (auto &s : h->sh)
+    for (int k = 0; k < s.P.p; ++k) nbig += s.sizes[k] > 32;
+  out[4] = nbig ? n_done / nbig : 0.0;
+  out[5] = nbig ? n_hand / nbig : 0.0;
+  out[6] = n_done ? n_fp / n_done : 0.0;
+  for (int i = 0; i < 3; ++i) out[7 + i] = nbig ? n_why[i] / nbig : 0.0;
   out[0] = n ? sum / n : 0.0;
   out[1] = mx;
   out[2] = n_big ? sum_big / n_big : 0.0;

@@ -35,6 +35,13 @@
 
 constexpr int kWarmMaxAge = 64;
 
+// k_cone_split -> k_cone_block hand-off states (DevWork::cstate, hsde_split.cuh)
+// (SPLIT_HANDOFF + 0/1/2: off(B) > g / 10 / r > n / the fixed point stalled)
+enum SplitState { SPLIT_DONE = 0, SPLIT_UNTOUCHED = 1, SPLIT_HANDOFF = 2 };
+// vvalid bit: the fast path asks for a refreshed V (the next projection of the
+// clique runs in k_cone_block, warm, which rotates V)
+constexpr int kVRefresh = 1 << 30;
+
 struct WarpTeam {
   int rank;
   __device__ static constexpr int size() { return 32; }
@@ -1196,6 +1203,8 @@ struct ConeArgs {
   double *pscratch; // CTA teams: d x d global scratch per CTA (second-order rebuild)
   int64_t pstride;
   int slot;         // this team's scratch slot
+  int split_refresh; // k_cone_split: fixed-point iterations beyond which V is refreshed
+  int split_vupdate; // k_cone_split: rotate V onto the new invariant subspaces
 };
 
 // Hot-path load of slot j: builds arg_s and performs the v / w_v update and
@@ -1251,10 +1260,18 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   JacobiScratch js = jacobi_carve(scratch, dp);
   const int lda = js.lda, ldv = js.ldv;
   double *A = js.A;
-  const int age = (MODE == CONE_HOT && ca.warm) ? W.vvalid[k] : 0;
+  constexpr bool kCta = std::is_same<Team, BlockTeam>::value;
+  // k_cone_split ran first for CTA cliques on the hot path (hsde_split.cuh)
+  int cst = SPLIT_UNTOUCHED;
+  if (MODE == CONE_HOT && kCta && W.cstate) {
+    cst = W.cstate[k];
+    if (cst == SPLIT_DONE) return;
+  }
+  const bool handoff = cst >= SPLIT_HANDOFF;  // A <- B = Vt X Vt' from W.xarg
+  const int age = (MODE == CONE_HOT && ca.warm) ? (W.vvalid[k] & ~kVRefresh) : 0;
   constexpr int MT = TeamTiles<Team>::value;
   const int ntile = (d + 3) >> 2;
-  const bool warm = age > 0 && age < kWarmMaxAge && ntile * ntile <= MT * tm.size();
+  const bool warm = handoff || (age > 0 && age < kWarmMaxAge && ntile * ntile <= MT * tm.size());
   if (MODE == CONE_HOT && W.dbg && k == W.dbg_clique) {
     js.dbg = W.dbg;
     if (tm.rank == 0) {
@@ -1267,7 +1284,7 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   for (int e = tm.rank; e < d * d; e += tm.size()) {
     const int a = e / d, bcol = e - a * d;
     double v;
-    if (MODE == CONE_HOT) v = hot_slot_load(P, S, W, off + e, shift);
+    if (MODE == CONE_HOT) v = handoff ? W.xarg[off + e] : hot_slot_load(P, S, W, off + e, shift);
     else v = ca.in[off + e] * ca.in_scale;
     A[a * lda + bcol] = v;
     if (warm) js.Vt[a * ldv + bcol] = W.vstore[off + e];
@@ -1297,8 +1314,9 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   }
   tm.sync();
   double *Mg = ca.pscratch ? ca.pscratch + (int64_t)ca.slot * ca.pstride : nullptr;
-  constexpr bool kCta = std::is_same<Team, BlockTeam>::value;
-  if (kCta && warm && Mg) {
+  if (handoff) {
+    // B already in A
+  } else if (kCta && warm && Mg) {
     cta_warm_start(js, d, Mg);
   } else if (warm) {
     // B = V X V' (rows of Vt are the previous eigenvectors): T1 = Vt X, then

@@ -126,6 +126,8 @@ struct DevWork {
   double *qbuf;        // [m]     partial A t (all-reduced)
   double *red;         // [8]     scalar partials (all-reduced)
   int *handoff;        // [p]     1: stage-1 Jacobi handed the clique to the refinement kernel
+  int *cstate;         // [p]     k_cone_split outcome (SplitState), read by k_cone_block
+  double *xarg;        // [n_d]   k_cone_split -> k_cone_block hand-off (B = Vt X Vt')
   double *dbg;         // [64]    Jacobi off-norm history of one clique (diagnostics)
   int dbg_clique;
 };
@@ -521,6 +523,7 @@ __global__ void __launch_bounds__(kBlock) k_xupd(DevProblem P, DevState S, DevWo
 }
 
 #include "hsde_eig.cuh"
+#include "hsde_split.cuh"
 
 // ---------------------------------------------------------------------------
 // generic small kernels for the unit-level API path

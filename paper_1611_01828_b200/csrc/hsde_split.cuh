@@ -1,0 +1,746 @@
+// hsde_split.cuh -- fast path of the clique PSD projection for CTA-sized
+// cliques (32 < d <= kSplitMaxD) on the warm hot path (reference:
+// chordalsdp/symmat.py:153-165 `project_psd_batch` called from
+// solver.py:335-342; the result is the same P = Q max(Lambda, 0) Q').
+//
+// The previous iteration's eigenbasis V (rows of the per-clique store, Vt)
+// nearly diagonalises the new argument X.  With B = Vt X Vt' split by the
+// sign of its diagonal into the classes P (r entries) and N (n = d - r), in
+// class-sorted order, the positive invariant subspace of B is span Q,
+// Q = [I; Y_X] with Y_X (n x r) the solution near 0 of the Riccati equation
+//     Y_X L_P - L_N Y_X = B_NP + E_NN Y_X - Y_X (E_PP + B_PN Y_X)
+// (L = diagonal, E = off-diagonal within a class; every denominator is
+// >= 2 g, g = min |diag B|, so the fixed point contracts at about
+// off(B) / 2g).  Then B Q = Q R with R = L_P + E_PP + B_PN Y_X, and the
+// orthogonal projector onto span Q is Q G Q' with G = (I + Y_X' Y_X)^-1, so
+//     P(B) = B Q G Q' = Q (R G) Q'      and      P(X) = Ut' K Ut,
+// Ut = Vt_P + Y_X' Vt_N (r x d), K = R G (r x r).  No truncation: the only
+// errors are the fixed point's (stopped at <= 2.5e-16) and rounding.  V
+// itself is left unchanged, so it never loses orthogonality here.
+//
+// The path applies when off(B) <= g / 10 (then no eigenvalue changes sign,
+// Weyl) and r <= n; otherwise -- or when the fixed point stalls -- the kernel
+// writes B to the per-clique hand-off buffer and k_cone_block finishes the
+// clique from there (Jacobi sweeps warm-started from B and V, which also
+// refresh V).  Cliques without a valid V go to k_cone_block untouched.
+//
+// All products run on the fp64 tensor cores (mma.sync m8n8k4, DMMA) from
+// shared memory with 16 x 16 output blocks per warp (four independent
+// accumulator chains, one shared-memory load per DMMA); leading dimensions
+// are 4 (mod 16) doubles, which makes every fragment load of either
+// orientation bank-conflict free (two wavefronts per 32 lanes).  V is read
+// from the store (L2) where it is an operand.
+//
+// (included inside namespace hsde by hsde_kernels.cuh, after hsde_eig.cuh)
+
+constexpr int kSplitThreads = 384;
+constexpr int kSplitStrip = 32;  // warm-start strip width (columns of T = Vt X)
+constexpr int kSplitMaxB = 2;    // 16 x 16 blocks a warp keeps in registers
+constexpr int kSplitMaxD = 112;  // upper blocks of B: <= kSplitMaxB per warp
+constexpr int kSplitRefreshIters = 1000;  // fixed-point passes that ask for a Jacobi refresh of V
+constexpr int kLoadBatch = 4;          // hot-path slots per thread in flight
+constexpr double kSplitOff2 = 1.0 / 9.0;  // fast path while off(B)^2 <= kSplitOff2 g^2
+constexpr int kSplitMaxPasses = 24;     // fixed-point passes before handing over
+
+__host__ __device__ inline int split_ld(int c) { return ((c + 11) & ~15) + 4; }
+
+// R2 = [Y (r x ly) | S_N (n x ln), same region] [Ut (r x L)], or the strip buffer
+__host__ __device__ inline int64_t split_r2_doubles(int d) {
+  int64_t best = 2 * (int64_t)d * split_ld(kSplitStrip);  // strip buffers XS, TS
+  for (int r = 1; r <= d / 2; ++r) {
+    const int n = d - r;
+    const int64_t y = (int64_t)r * split_ld(r), sn = (int64_t)n * split_ld(n);
+    const int64_t need = (y > sn ? y : sn) + (int64_t)r * split_ld(d);
+    if (need > best) best = need;
+  }
+  return best;
+}
+
+__host__ __device__ inline int64_t split_smem_doubles(int d) {
+  // R1 | R2 | lam[d] | red[32] | ints: perm[d], pinv[d], cnt[4]
+  return (int64_t)d * split_ld(d) + split_r2_doubles(d) + d + 32 + (2 * d + 4 + 1) / 2 + 1;
+}
+
+// operand view: element (row, col) at p[row * rs + col * cs]
+struct Opd {
+  const double *p;
+  int rs, cs;
+};
+
+// One 16 x 16 output block (2 x 2 m8n8k4 tiles) of sum_{k < K} A(i, k) B(k, j)
+// accumulated into c (lane (q, kk) = (lane / 4, lane % 4) holds
+// c[a][b][e] = D(i0 + 8a + q, j0 + 8b + 2kk + e)).  Rows >= M and columns >= N
+// read a clamped valid row / column (their results are discarded by the
+// caller); k >= K is zero-filled.  BROW: B's row k is brow[k] (row gather).
+template <bool BROW = false>
+__device__ __forceinline__ void blk16(double (&c)[2][2][2], const Opd &A, const Opd &B, int i0, int j0, int M,
+                                      int N, int K, const int *brow = nullptr) {
+  const int lane = threadIdx.x & 31, q = lane >> 2, kk = lane & 3;
+  const int ia0 = min(i0 + q, M - 1), ia1 = min(i0 + 8 + q, M - 1);
+  const int jb0 = min(j0 + q, N - 1), jb1 = min(j0 + 8 + q, N - 1);
+  const double *a0 = A.p + ia0 * A.rs + kk * A.cs, *a1 = A.p + ia1 * A.rs + kk * A.cs;
+  const double *b0 = B.p + jb0 * B.cs, *b1 = B.p + jb1 * B.cs;
+  if (!BROW) {
+    b0 += kk * B.rs;
+    b1 += kk * B.rs;
+  }
+  const int sa = 4 * A.cs, sb = 4 * B.rs;
+  const int K4 = K & ~3;
+  // second tile row / column outside the output: skip its products (warp-uniform)
+  const bool ha = i0 + 8 < M, hb = j0 + 8 < N;
+  int k0 = 0;
+#pragma unroll 2
+  for (; k0 < K4; k0 += 4) {
+    double x0 = *a0, x1 = *a1, y0, y1;
+    if (BROW) {
+      const int ro = brow[k0 + kk] * B.rs;
+      y0 = b0[ro];
+      y1 = b1[ro];
+    } else {
+      y0 = *b0;
+      y1 = *b1;
+      b0 += sb;
+      b1 += sb;
+    }
+    a0 += sa;
+    a1 += sa;
+    dmma884(c[0][0][0], c[0][0][1], x0, y0);
+    if (hb) dmma884(c[0][1][0], c[0][1][1], x0, y1);
+    if (ha) dmma884(c[1][0][0], c[1][0][1], x1, y0);
+    if (ha && hb) dmma884(c[1][1][0], c[1][1][1], x1, y1);
+  }
+  if (k0 < K) {
+    double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+    if (k0 + kk < K) {
+      x0 = *a0;
+      x1 = *a1;
+      if (BROW) {
+        const int ro = brow[k0 + kk] * B.rs;
+        y0 = b0[ro];
+        y1 = b1[ro];
+      } else {
+        y0 = *b0;
+        y1 = *b1;
+      }
+    }
+    dmma884(c[0][0][0], c[0][0][1], x0, y0);
+    dmma884(c[0][1][0], c[0][1][1], x0, y1);
+    dmma884(c[1][0][0], c[1][0][1], x1, y0);
+    dmma884(c[1][1][0], c[1][1][1], x1, y1);
+  }
+}
+
+__device__ __forceinline__ void blk16_zero(double (&c)[2][2][2]) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) c[a][b][0] = c[a][b][1] = 0.0;
+}
+
+// visit the valid elements of a block: f(i, j, v)
+template <class F>
+__device__ __forceinline__ void blk16_each(const double (&c)[2][2][2], int i0, int j0, int M, int N, F f) {
+  const int lane = threadIdx.x & 31, q = lane >> 2, kk = lane & 3;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = i0 + 8 * a + q, j = j0 + 8 * b + 2 * kk + e;
+        if (i < M && j < N) f(i, j, c[a][b][e]);
+      }
+}
+
+// block t of the upper triangle (bi <= bj) of an nb x nb block grid
+__device__ __forceinline__ void upper_block(int t, int nb, int &bi, int &bj) {
+  bi = 0;
+  while (t >= nb - bi) {
+    t -= nb - bi;
+    ++bi;
+  }
+  bj = bi + t;
+}
+
+// out = A1 B1 (K1) + A2 B2 (K2) over M x N in 16 x 16 blocks, round-robin
+// over the warps.  SYM (M == N): upper blocks only, emitted to both
+// triangles from the upper values (exactly symmetric).  INPLACE: every warp
+// finishes reading before the first emit (the output may overwrite an
+// operand; at most kSplitMaxB blocks per warp).  Ends with a barrier.
+template <bool SYM, bool INPLACE, bool BROW = false, class Emit>
+__device__ void team_mm(int M, int N, const Opd &A1, const Opd &B1, int K1, const Opd &A2, const Opd &B2, int K2,
+                        Emit emit, const int *brow = nullptr) {
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int mb = (M + 15) >> 4, nb = (N + 15) >> 4;
+  const int nblk = SYM ? mb * (mb + 1) / 2 : mb * nb;
+  auto place = [&](int t, int &i0, int &j0) {
+    int bi, bj;
+    if (SYM) upper_block(t, mb, bi, bj);
+    else {
+      bi = t / nb;
+      bj = t - bi * nb;
+    }
+    i0 = bi * 16;
+    j0 = bj * 16;
+  };
+  auto out = [&](const double (&c)[2][2][2], int i0, int j0) {
+    if (SYM) {
+      blk16_each(c, i0, j0, M, N, [&](int i, int j, double v) {
+        if (i0 != j0 || i < j) {
+          emit(i, j, v);
+          emit(j, i, v);
+        } else if (i == j) {
+          emit(i, j, v);
+        }
+      });
+    } else {
+      blk16_each(c, i0, j0, M, N, emit);
+    }
+  };
+  if (INPLACE) {
+    double c[kSplitMaxB][2][2][2];
+#pragma unroll
+    for (int s = 0; s < kSplitMaxB; ++s) {
+      blk16_zero(c[s]);
+      const int t = w + s * nw;
+      if (t < nblk) {
+        int i0, j0;
+        place(t, i0, j0);
+        if (K1 > 0) blk16<BROW>(c[s], A1, B1, i0, j0, M, N, K1, brow);
+        if (K2 > 0) blk16(c[s], A2, B2, i0, j0, M, N, K2);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < kSplitMaxB; ++s) {
+      const int t = w + s * nw;
+      if (t < nblk) {
+        int i0, j0;
+        place(t, i0, j0);
+        out(c[s], i0, j0);
+      }
+    }
+  } else {
+    for (int t = w; t < nblk; t += nw) {
+      double c[2][2][2];
+      blk16_zero(c);
+      int i0, j0;
+      place(t, i0, j0);
+      if (K1 > 0) blk16<BROW>(c, A1, B1, i0, j0, M, N, K1, brow);
+      if (K2 > 0) blk16(c, A2, B2, i0, j0, M, N, K2);
+      out(c, i0, j0);
+    }
+  }
+  __syncthreads();
+}
+
+template <bool SYM, bool INPLACE, bool BROW = false, class Emit>
+__device__ __forceinline__ void team_mm1(int M, int N, const Opd &A, const Opd &B, int K, Emit emit,
+                                         const int *brow = nullptr) {
+  team_mm<SYM, INPLACE, BROW>(M, N, A, B, K, A, B, 0, emit, brow);
+}
+
+__device__ __forceinline__ double cta_sum(double v, double *red) {
+  BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
+  return team_sum(tm, v, red);
+}
+__device__ __forceinline__ double cta_min(double v, double *red) {
+  BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
+  return team_min(tm, v, red);
+}
+
+// phase timestamps of the first CTA (diagnostics: W.dbg[48 + i], clock64)
+#define SPLIT_STAMP(i)                                                                      \
+  do {                                                                                      \
+    if (W.dbg && blockIdx.x == 0 && threadIdx.x == 0) W.dbg[48 + (i)] = (double)clock64(); \
+  } while (0)
+
+// every in-place pass keeps its output blocks in registers (kSplitMaxB per warp)
+__device__ __forceinline__ bool split_fits(int r, int n, int nw) {
+  const int br = (r + 15) >> 4, bn = (n + 15) >> 4, bd = (r + n + 15) >> 4, cap = kSplitMaxB * nw;
+  return bn * br <= cap && bn * bn + br * br <= cap && bn * bd <= cap;
+}
+
+// sum over the CTA of one value per thread, after the caller's barrier has
+// made the per-warp partials (red[w], written by lane 0) visible
+__device__ __forceinline__ double red_total(const double *red, int nw) {
+  double t = 0.0;
+  for (int i = 0; i < nw; ++i) t += red[i];
+  return t;
+}
+
+// The fast path for clique k (argument load included).  Returns SPLIT_DONE,
+// or a hand-off code with B = Vt X Vt' (original order) written to W.xarg.
+__device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &W, const ConeArgs &ca, int k,
+                         double *smem) {
+  const int d = P.cl_size[k];
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int64_t off = P.cl_off[k], so = P.n_c;
+  const double shift = W.scal[S_SHIFT];
+  const double *vst = W.vstore + off;  // row c = basis vector c
+  const int L = split_ld(d);
+  double *R1 = smem, *R2 = R1 + d * L;
+  double *lam = R2 + split_r2_doubles(d), *red = lam + d;
+  int *perm = reinterpret_cast<int *>(red + 32), *pinv = perm + d, *cnt = pinv + d;
+  const int w = tid >> 5, nw = T >> 5, lane = tid & 31;
+  double *su = S.u + so + off, *sw = S.w + so + off;
+  SPLIT_STAMP(0);
+
+  // ---- argument X (hot-path slot update, solver.py:222-244, :316, :388-394),
+  //      kLoadBatch slots per thread at a time: every load of the batch is
+  //      issued before the first store (the stores may alias later loads)
+  {
+    constexpr int NB = kLoadBatch;
+    const int64_t vo = P.n_c + P.n_d + P.m;
+    const double *mzs = P.mz + P.n_c + off, *mzv = P.mz + vo + off;
+    double *vu = S.u + vo + off, *vw = S.w + vo + off;
+    for (int e0 = tid; e0 < d * d; e0 += NB * T) {
+      double us[NB], ws[NB], uv[NB], wv[NB], hu[NB], ms[NB], mv[NB];
+      int cv[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const int e = min(e0 + q * T, d * d - 1);
+        us[q] = su[e];
+        ws[q] = sw[e];
+        uv[q] = vu[e];
+        wv[q] = vw[e];
+        ms[q] = mzs[e];
+        mv[q] = mzv[e];
+        cv[q] = P.slot_cov[off + e];
+      }
+#pragma unroll
+      for (int q = 0; q < NB; ++q) hu[q] = W.ua[cv[q]];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const int e = e0 + q * T;
+        if (e >= d * d) break;
+        const double as = us[q] + ws[q], av = uv[q] + wv[q];            // a = u + w
+        const double gb = as - av;                                      // solver.py:222
+        const double ub = (gb + hu[q]) * 0.5;                           // :237-239
+        const double uvn = (ub - hu[q]) + av;                           // :242-244
+        const double us_h = relax(ub - shift * ms[q], us[q], P.alpha);  // :316, :388-390
+        const double uv_h = relax(uvn - shift * mv[q], uv[q], P.alpha);
+        const double vn = uv_h - wv[q];                                 // free block: identity
+        vu[e] = vn;
+        vw[e] = (wv[q] - uv_h) + vn;                                    // :393-394
+        sw[e] = ws[q] - us_h;                                           // completed after projection
+        const int a = e / d, b = e - a * d;
+        R1[a * L + b] = us_h - ws[q];                                   // :391
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < d * d; e += T) {  // sym = 0.5 (B + B')  (symmat.py:157)
+    const int a = e / d, b = e - a * d;
+    if (a < b) {
+      const double s = 0.5 * (R1[a * L + b] + R1[b * L + a]);
+      R1[a * L + b] = s;
+      R1[b * L + a] = s;
+    }
+  }
+  __syncthreads();
+  SPLIT_STAMP(1);
+
+  // ---- B = Vt X Vt' by column strips of T = Vt X, all from shared memory:
+  //      X -> the hand-off buffer (global, L2-resident), Vt -> R1, then per
+  //      strip J: X[:, J] -> XS, T_J = Vt X[:, J] -> TS, B += T_J Vt[:, J]'
+  //      (upper 16 x 16 blocks of B held in registers); the next strip of X
+  //      is fetched while the tensor cores work on the current one
+  const int nb = (d + 15) >> 4, nbu = nb * (nb + 1) / 2;
+  const int LS = split_ld(kSplitStrip);
+  double *XS = R2, *TS = R2 + d * LS;
+  double *xg = W.xarg + off;
+  for (int e = tid; e < d * d; e += T) {
+    const int a = e / d, b = e - a * d;
+    xg[e] = R1[a * L + b];
+  }
+  __syncthreads();
+  for (int e = tid; e < d * d; e += T) {
+    const int a = e / d, b = e - a * d;
+    R1[a * L + b] = vst[e];
+  }
+  {
+    const int s0 = min(kSplitStrip, d);
+    for (int e = tid; e < d * s0; e += T) {
+      const int a = e / s0, b = e - a * s0;
+      XS[a * LS + b] = xg[a * d + b];
+    }
+  }
+  __syncthreads();
+  double cb[kSplitMaxB][2][2][2];
+  int bi0[kSplitMaxB], bj0[kSplitMaxB];
+#pragma unroll
+  for (int s = 0; s < kSplitMaxB; ++s) {
+    blk16_zero(cb[s]);
+    const int t = w + s * nw;
+    int bi = 0, bj = 0;
+    if (t < nbu) upper_block(t, nb, bi, bj);
+    bi0[s] = bi * 16;
+    bj0[s] = bj * 16;
+  }
+  constexpr int kPf = (kSplitMaxD * kSplitStrip + kSplitThreads - 1) / kSplitThreads;
+  for (int j0 = 0; j0 < d; j0 += kSplitStrip) {
+    const int sw_ = min(kSplitStrip, d - j0), nbs = (sw_ + 15) >> 4;
+    for (int t = w; t < nb * nbs; t += nw) {
+      const int bi = t / nbs, bj = t - bi * nbs;
+      double c[2][2][2];
+      blk16_zero(c);
+      blk16(c, Opd{R1, L, 1}, Opd{XS, LS, 1}, bi * 16, bj * 16, d, sw_, d);
+      blk16_each(c, bi * 16, bj * 16, d, sw_, [&](int i, int j, double v) { TS[i * LS + j] = v; });
+    }
+    __syncthreads();
+    // next strip of X: loads issued before this strip's products, stored after
+    const int j1 = j0 + kSplitStrip, s1 = j1 < d ? min(kSplitStrip, d - j1) : 0;
+    double pf[kPf];
+#pragma unroll
+    for (int q = 0; q < kPf; ++q) {
+      const int e = tid + q * T;
+      pf[q] = 0.0;
+      if (e < d * s1) {
+        const int a = e / s1, b = e - a * s1;
+        pf[q] = xg[a * d + j1 + b];
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < kSplitMaxB; ++s)
+      if (w + s * nw < nbu) blk16(cb[s], Opd{TS, LS, 1}, Opd{R1 + j0, 1, L}, bi0[s], bj0[s], d, d, sw_);
+#pragma unroll
+    for (int q = 0; q < kPf; ++q) {
+      const int e = tid + q * T;
+      if (e < d * s1) {
+        const int a = e / s1, b = e - a * s1;
+        XS[a * LS + b] = pf[q];
+      }
+    }
+    __syncthreads();
+  }
+  SPLIT_STAMP(2);
+
+  // ---- diagonal, g = min |diag|, off(B)^2 (upper values, mirrored)
+  double o2 = 0.0;
+#pragma unroll
+  for (int s = 0; s < kSplitMaxB; ++s)
+    if (w + s * nw < nbu)
+      blk16_each(cb[s], bi0[s], bj0[s], d, d, [&](int i, int j, double v) {
+        if (i == j) lam[i] = v;
+        else if (i < j) o2 += 2.0 * v * v;
+      });
+  __syncthreads();
+  double g = CUDART_INF;
+  for (int i = tid; i < d; i += T) g = fmin(g, fabs(lam[i]));
+  g = cta_min(g, red);
+  o2 = cta_sum(o2, red);
+  // class-sorted order: perm[0, r) = P (diag > 0), perm[r, d) = N
+  if (tid < 32) {
+    int base = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i0 = 0; i0 < d; i0 += 32) {
+        const int i = i0 + tid;
+        const bool pk = i < d && ((lam[i] > 0.0) == (pass == 0));
+        const unsigned mk = __ballot_sync(0xffffffffu, pk);
+        if (pk) {
+          const int pos = base + __popc(mk & ((1u << tid) - 1u));
+          perm[pos] = i;
+          pinv[i] = pos;
+        }
+        base += __popc(mk);
+        if (pass == 0 && i0 + 32 >= d && tid == 0) cnt[0] = base;
+      }
+  }
+  __syncthreads();
+  const int r = cnt[0], n = d - r;
+  // off(B) < g keeps the inertia (Weyl: |E|_2 <= |E|_F < min |diag|); the
+  // fixed point contracts at about off / 2g, so a looser bound only costs passes
+  const bool applies = g > 0.0 && o2 <= kSplitOff2 * g * g && r <= n &&  // also false on NaN
+                       split_fits(r, n, nw);
+  if (!applies) {
+    // hand B (original order) to the Jacobi path
+    double *xb = W.xarg + off;
+#pragma unroll
+    for (int s = 0; s < kSplitMaxB; ++s)
+      if (w + s * nw < nbu)
+        blk16_each(cb[s], bi0[s], bj0[s], d, d, [&](int i, int j, double v) {
+          if (i <= j) {
+            xb[i * d + j] = v;
+            xb[j * d + i] = v;
+          }
+        });
+    return r > n ? SPLIT_HANDOFF + 1 : SPLIT_HANDOFF;  // reason: r > n / off(B) > g / 10
+  }
+  // sorted B with a zero diagonal into R1 (X is dead), sorted diagonal into lam
+  const double lsv = tid < d ? lam[perm[tid]] : 0.0;
+#pragma unroll
+  for (int s = 0; s < kSplitMaxB; ++s)
+    if (w + s * nw < nbu)
+      blk16_each(cb[s], bi0[s], bj0[s], d, d, [&](int i, int j, double v) {
+        const int pi = pinv[i], pj = pinv[j];
+        if (i < j) {
+          R1[pi * L + pj] = v;
+          R1[pj * L + pi] = v;
+        } else if (i == j) {
+          R1[pi * L + pi] = 0.0;
+        }
+      });
+  __syncthreads();
+  if (tid < d) lam[tid] = lsv;
+  __syncthreads();
+  SPLIT_STAMP(3);
+
+  if (r == 0) {  // no eigenvalue > 0: P = 0 (w_s holds ws - us_h already)
+    for (int e = tid; e < d * d; e += T) su[e] = 0.0;
+    return SPLIT_DONE;
+  }
+
+  // ---- Riccati fixed point, Y_X in the N-P block of R1 (B_NP = B_PN').
+  // One product pass per iteration: the quadratic term uses the previous
+  // iterate (lagged), X_{k+1} = (B_NP + E_NN X_k + X_k Yn_{k-1}) / Delta with
+  // Yn_k = -(E_PP + B_PN X_k) formed in the same pass (same fixed point; the
+  // lag adds ~ |X| off / 2g to the contraction factor).
+  const Opd EPP{R1, L, 1}, BPN{R1 + r, L, 1}, ENN{R1 + r * L + r, L, 1}, XX{R1 + r * L, L, 1};
+  const int ly = split_ld(r);
+  const int ln = split_ld(n);
+  const int snoff = max(r * ly, n * ln);
+  double *Ybuf[2] = {R2, R2 + r * ly};  // (the second overlaps S_N / Ut, formed later)
+  double *Ut = R2 + snoff;
+  double x2 = 0.0;
+  for (int e = tid; e < n * r; e += T) {
+    const int i = e / r, j = e - i * r;
+    const double x = R1[(r + i) * L + j] / (lam[j] - lam[r + i]);
+    R1[(r + i) * L + j] = x;
+    x2 += x * x;
+  }
+  __syncthreads();
+  // Yn_0 = -(E_PP + B_PN X_0)
+  team_mm1<false, false>(r, r, BPN, XX, n, [&](int i, int j, double v) { Ybuf[0][i * ly + j] = -(v + R1[i * L + j]); });
+  double prev = sqrt(cta_sum(x2, red));
+  bool ok = prev == 0.0;
+  int it = 0, yb = 0;
+  const int mb = (n + 15) >> 4, nbr = (r + 15) >> 4, nx = mb * nbr, ny = nbr * nbr;
+  for (; !ok && it < kSplitMaxPasses; ++it) {
+    // pass: X blocks staged in registers (in place), Yn_{k} blocks emitted to the other buffer
+    double c[kSplitMaxB][2][2][2];
+    const double *Yc = Ybuf[yb];
+    double *Yo = Ybuf[yb ^ 1];
+#pragma unroll
+    for (int s = 0; s < kSplitMaxB; ++s) {
+      blk16_zero(c[s]);
+      const int t = w + s * nw;
+      if (t < nx) {
+        const int bi = t / nbr, bj = t - bi * nbr;
+        blk16(c[s], ENN, XX, bi * 16, bj * 16, n, r, n);
+        blk16(c[s], XX, Opd{Yc, ly, 1}, bi * 16, bj * 16, n, r, r);
+      }
+    }
+    for (int t = ((w - nx) % nw + nw) % nw; t < ny; t += nw) {  // round robin after the X blocks
+      const int bi = t / nbr, bj = t - bi * nbr;
+      double cy[2][2][2];
+      blk16_zero(cy);
+      blk16(cy, BPN, XX, bi * 16, bj * 16, r, r, n);
+      blk16_each(cy, bi * 16, bj * 16, r, r, [&](int i, int j, double v) { Yo[i * ly + j] = -(v + R1[i * L + j]); });
+    }
+    __syncthreads();
+    double acc = 0.0;
+#pragma unroll
+    for (int s = 0; s < kSplitMaxB; ++s) {
+      const int t = w + s * nw;
+      if (t < nx) {
+        const int bi = t / nbr, bj = t - bi * nbr;
+        blk16_each(c[s], bi * 16, bj * 16, n, r, [&](int i, int j, double v) {
+          const double x = (R1[j * L + r + i] + v) / (lam[j] - lam[r + i]);
+          const double dx = x - R1[(r + i) * L + j];
+          acc += dx * dx;
+          R1[(r + i) * L + j] = x;
+        });
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) red[w] = acc;
+    __syncthreads();
+    const double delta = sqrt(red_total(red, nw));
+    yb ^= 1;
+    const double rho = delta / prev;
+    if (delta == 0.0 || (rho < 0.5 && delta * rho <= 2.5e-16 * (1.0 - rho))) ok = true;
+    else if (!(rho < 0.5)) break;  // stalled (or NaN)
+    prev = delta;
+    __syncthreads();  // red is rewritten by the next pass
+  }
+  if (!ok) {
+    // hand B back (original order): N-P block from B_PN', diagonal from lam
+    double *xb = W.xarg + off;
+    for (int e = tid; e < d * d; e += T) {
+      const int i = e / d, j = e - i * d;
+      const int pi = pinv[i], pj = pinv[j];
+      double v;
+      if (pi == pj) v = lam[pi];
+      else if (pi >= r && pj < r) v = R1[pj * L + pi];
+      else v = R1[pi * L + pj];
+      xb[e] = v;
+    }
+    return SPLIT_HANDOFF + 2;  // reason: stalled
+  }
+  SPLIT_STAMP(4);
+  if (W.dbg && blockIdx.x == 0 && tid == 0) W.dbg[47] = it;
+  // ---- one pass over the final X:  Y = E_PP + B_PN X (R = L_P + Y) -> Yb,
+  //      Y_P = X' X -> YPt (Ut's region, temporary), Y_N = X X' -> E_NN block
+  const bool vup = ca.split_vupdate != 0;
+  const int nbn = mb;
+  double *Yb = Ybuf[0], *YPt = Ut, *EX = R2;  // EX: n x ln (S_N, after Y is dead)
+  double y2 = 0.0;
+  {
+    const int nyu = nbr * (nbr + 1) / 2, nyn = vup ? nbn * (nbn + 1) / 2 : 0;
+    for (int t = w; t < ny + nyu + nyn; t += nw) {
+      double cy[2][2][2];
+      blk16_zero(cy);
+      if (t < ny) {
+        const int bi = t / nbr, bj = t - bi * nbr;
+        blk16(cy, BPN, XX, bi * 16, bj * 16, r, r, n);
+        blk16_each(cy, bi * 16, bj * 16, r, r, [&](int i, int j, double v) { Yb[i * ly + j] = v + R1[i * L + j]; });
+      } else if (t < ny + nyu) {
+        int bi, bj;
+        upper_block(t - ny, nbr, bi, bj);
+        blk16(cy, Opd{R1 + r * L, 1, L}, XX, bi * 16, bj * 16, r, r, n);
+        blk16_each(cy, bi * 16, bj * 16, r, r, [&](int i, int j, double v) {
+          if (bi != bj || i < j) {
+            YPt[i * ly + j] = v;
+            YPt[j * ly + i] = v;
+            y2 += 2.0 * v * v;
+          } else if (i == j) {
+            YPt[i * ly + i] = v;
+            y2 += v * v;
+          }
+        });
+      } else {
+        int bi, bj;
+        upper_block(t - ny - nyu, nbn, bi, bj);
+        blk16(cy, XX, Opd{R1 + r * L, 1, L}, bi * 16, bj * 16, n, n, r);
+        double *YN = R1 + r * L + r;
+        blk16_each(cy, bi * 16, bj * 16, n, n, [&](int i, int j, double v) {
+          if (bi != bj || i < j) {
+            YN[i * L + j] = v;
+            YN[j * L + i] = v;
+          } else if (i == j) {
+            YN[i * L + i] = v;
+          }
+        });
+      }
+    }
+  }
+  y2 = warp_sum(y2);
+  if (lane == 0) red[w] = y2;
+  __syncthreads();
+  const double y = sqrt(red_total(red, nw));
+  int nt = 0;  // series terms: y^(nt+1) <= 1e-17
+  for (double p = y; nt < 40 && p > 1e-17; p *= y) ++nt;
+  double *Kb = R1 + r;  // K = R G in the (dead) B_PN block
+  // K <- R - K Y_P from K = R (error y^(nt+1))
+  for (int e = tid; e < r * r; e += T) {
+    const int i = e / r, j = e - i * r;
+    Kb[i * L + j] = Yb[i * ly + j] + (i == j ? lam[i] : 0.0);
+  }
+  __syncthreads();
+  for (int t = 0; t < nt; ++t)
+    team_mm1<false, true>(r, r, Opd{Kb, L, 1}, Opd{YPt, ly, 1}, r, [&](int i, int j, double v) {
+      Kb[i * L + j] = (Yb[i * ly + j] + (i == j ? lam[i] : 0.0)) - v;
+    });
+  if (vup) {
+    // S_P = (I + Y_P)^-1/2 -> E_PP block, S_N = (I + Y_N)^-1/2 -> EX (Y is
+    // dead): binomial series sum_k c_k Y^k, c_k = c_{k-1} (-(2k - 1) / 2k),
+    // by Horner in place
+    double *SP = R1, *SN = EX;
+    const double *YN = R1 + r * L + r;
+    double cK = 1.0;
+    for (int q = 1; q <= nt; ++q) cK *= -(2.0 * q - 1.0) / (2.0 * q);
+    for (int e = tid; e < r * r + n * n; e += T) {
+      if (e < r * r) {
+        const int i = e / r, j = e - i * r;
+        SP[i * L + j] = i == j ? cK : 0.0;
+      } else {
+        const int q = e - r * r, i = q / n, j = q - i * n;
+        SN[i * ln + j] = i == j ? cK : 0.0;
+      }
+    }
+    __syncthreads();
+    double c = cK;
+    const int nsp = nbr * nbr;
+    for (int q = nt - 1; q >= 0; --q) {
+      c *= -(2.0 * (q + 1)) / (2.0 * (q + 1) - 1.0);  // c_q from c_{q+1}
+      double cc[kSplitMaxB][2][2][2];
+#pragma unroll
+      for (int s2 = 0; s2 < kSplitMaxB; ++s2) {
+        blk16_zero(cc[s2]);
+        const int t = w + s2 * nw;
+        if (t < nsp) {
+          const int bi = t / nbr, bj = t - bi * nbr;
+          blk16(cc[s2], Opd{YPt, ly, 1}, Opd{SP, L, 1}, bi * 16, bj * 16, r, r, r);
+        } else if (t < nsp + nbn * nbn) {
+          const int bi = (t - nsp) / nbn, bj = (t - nsp) - bi * nbn;
+          blk16(cc[s2], Opd{YN, L, 1}, Opd{SN, ln, 1}, bi * 16, bj * 16, n, n, n);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int s2 = 0; s2 < kSplitMaxB; ++s2) {
+        const int t = w + s2 * nw;
+        if (t < nsp) {
+          const int bi = t / nbr, bj = t - bi * nbr;
+          blk16_each(cc[s2], bi * 16, bj * 16, r, r,
+                     [&](int i, int j, double v) { SP[i * L + j] = v + (i == j ? c : 0.0); });
+        } else if (t < nsp + nbn * nbn) {
+          const int bi = (t - nsp) / nbn, bj = (t - nsp) - bi * nbn;
+          blk16_each(cc[s2], bi * 16, bj * 16, n, n,
+                     [&](int i, int j, double v) { SN[i * ln + j] = v + (i == j ? c : 0.0); });
+        }
+      }
+      __syncthreads();
+    }
+  }
+  SPLIT_STAMP(5);
+  // Ut = Vt_P + Y_X' Vt_N  (r x d; rows of V gathered through perm) -> R2
+  team_mm1<false, false, true>(
+      r, d, Opd{R1 + r * L, 1, L}, Opd{vst, d, 1}, n,
+      [&](int i, int j, double v) { Ut[i * L + j] = v + vst[perm[i] * d + j]; }, perm + r);
+  double *Tt = R1 + r * L;  // rows r.. of R1
+  if (vup) {
+    // Wt = Vt_N - Y_X Vt_P (n x d) in place over rows r.. of R1 (Y_X, Y_N dead after)
+    team_mm1<false, true, true>(
+        n, d, XX, Opd{vst, d, 1}, r,
+        [&](int i, int j, double v) { Tt[i * L + j] = vst[perm[r + i] * d + j] - v; }, perm);
+    // V' = [S_P Ut; S_N Wt] -> the store (rows 0..r-1: positive subspace)
+    double *vw = W.vstore + off;
+    team_mm1<false, false>(r, d, Opd{R1, L, 1}, Opd{Ut, L, 1}, r, [&](int i, int j, double v) { vw[i * d + j] = v; });
+    team_mm1<false, false>(n, d, Opd{EX, ln, 1}, Opd{Tt, L, 1}, n,
+                           [&](int i, int j, double v) { vw[(r + i) * d + j] = v; });
+  }
+  SPLIT_STAMP(6);
+  // Tt = K Ut (r x d) -> rows r.. of R1
+  team_mm1<false, false>(r, d, Opd{Kb, L, 1}, Opd{Ut, L, 1}, r, [&](int i, int j, double v) { Tt[i * L + j] = v; });
+  SPLIT_STAMP(7);
+  // P = Ut' Tt  (d x d, symmetric) -> u_s; then w_s = (ws - us_h) + P
+  // (solver.py:391-394) in a coalesced pass
+  team_mm1<true, false>(d, d, Opd{Ut, 1, L}, Opd{Tt, L, 1}, r, [&](int i, int j, double v) { su[i * d + j] = v; });
+  for (int e = tid; e < d * d; e += T) sw[e] += su[e];
+  SPLIT_STAMP(8);
+  if (tid == 0 && W.sweeps) W.sweeps[k] = -it;  // (stats: fixed-point iterations)
+  if (tid == 0 && it > ca.split_refresh) W.vvalid[k] |= kVRefresh;
+  return SPLIT_DONE;
+}
+
+// One CTA per CTA-sized clique on the hot path: the fast path when the
+// clique has a valid eigenbasis, otherwise -- or when the fast path hands
+// over -- the Jacobi path (cone_one) in the same CTA.
+__global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
+  extern __shared__ __align__(16) double smem[];
+  if ((int)blockIdx.x >= ca.count) return;
+  const int k = ca.ids[blockIdx.x];
+  const int d = P.cl_size[k];
+  const int vv = W.vvalid[k];
+  ConeArgs c2 = ca;
+  c2.slot = blockIdx.x;
+  int st = SPLIT_UNTOUCHED;
+  if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d > 32) st = split_one(P, S, W, c2, k, smem);
+  if (threadIdx.x == 0) W.cstate[k] = st;
+  if (st == SPLIT_DONE) return;
+  __syncthreads();  // cstate and the hand-off B are visible to the whole CTA
+  BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
+  cone_one<CONE_HOT>(tm, P, S, W, c2, k, smem);
+}
