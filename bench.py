@@ -137,11 +137,16 @@ def kernel_units(cp, name: str, half: bool = True):
         return "bytes", 48 * Nc
     if name == "k_schur":
         return "bytes", 8 * (m * m if not cp_schur_diag(cp) else m)
-    if name == "k_cone_block":
+    if name == "k_cone_cta":  # k_cone_split (warm) / k_cone_block: 11 d^3 per clique
         return "flops", float((11 * big.astype(np.float64) ** 3).sum())
     if name == "k_cone_warp":
         return "flops", float((11 * small.astype(np.float64) ** 3).sum())
     return None, 0.0
+
+
+# profile slot -> the kernels it times (hot path, warm starts on)
+KERNELS = {"k_cone_cta": "k_cone_split", "k_ua": "k_ua_half",
+           "k_spmv_seg": "k_pair_sum + k_spmv_half + k_rowsum_tiles"}
 
 
 def cp_schur_diag(cp) -> bool:
@@ -185,9 +190,12 @@ def roofline_for(cp, prof_ms: dict, launches_per_kernel: int, peaks: dict, half:
                          "frac": ach / peak, "traffic": load_traffic(name),
                          "algorithmic_per_launch": amount, "avg_launch_ms": t * 1e3}
         else:
+            # fp64 products run on the tensor cores (DMMA m8n8k4); the peak is the
+            # measured cuBLAS DGEMM rate (profiles/fp64_peaks.json), the fp64
+            # tensor-core ceiling of this part
             peak = peaks.get("fp64_tflops")
             ach = amount / t / 1e12
-            out[name] = {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+            out[name] = {"bound": "tensor", "precision": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                          "frac": (ach / peak) if peak else None, "traffic": load_traffic(name),
                          "algorithmic_per_launch": amount, "avg_launch_ms": t * 1e3}
     dominant = max(items)[1]
@@ -343,7 +351,7 @@ def run_ours(args):
             "eig_stats": eig_stats,
         }
         if roofs:
-            line["roofline"] = dict(roofs[dominant], kernel=dominant)
+            line["roofline"] = dict(roofs[dominant], kernel=KERNELS.get(dominant, dominant))
             line["roofline_all"] = roofs
     # --- e2e: public API on host data, default to-tolerance solve ------------------
     if not args.no_e2e:

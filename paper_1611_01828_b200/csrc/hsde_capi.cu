@@ -66,7 +66,7 @@ enum ProfSlot {
 };
 const char *kProfNames[HSDE_PROFILE_SLOTS] = {
     "k_prep_ry", "k_rhs", "k_spmv_seg", "k_schur", "k_ua", "k_scalars", "k_cone_warp",
-    "k_cone_block", "k_xupd", "allreduce", "", "", "", "", "", ""};
+    "k_cone_cta", "k_xupd", "allreduce", "", "", "", "", "", ""};
 
 struct ConePlan {
   int *ids = nullptr;

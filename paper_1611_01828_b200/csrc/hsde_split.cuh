@@ -255,6 +255,11 @@ __device__ __forceinline__ double cta_min(double v, double *red) {
     if (W.dbg && blockIdx.x == 0 && threadIdx.x == 0) W.dbg[48 + (i)] = (double)clock64(); \
   } while (0)
 
+// floor(e / m) for 0 <= e < 2^21 and 1 <= m <= 4096 from inv = 1.0f / m: the
+// exact quotient of e + 1/2 sits >= 1/(2m) from an integer, far above the
+// float rounding (no integer division in the element loops)
+__device__ __forceinline__ int qdiv(int e, float inv) { return (int)(((float)e + 0.5f) * inv); }
+
 // every in-place pass keeps its output blocks in registers (kSplitMaxB per warp)
 __device__ __forceinline__ bool split_fits(int r, int n, int nw) {
   const int br = (r + 15) >> 4, bn = (n + 15) >> 4, bd = (r + n + 15) >> 4, cap = kSplitMaxB * nw;
@@ -283,6 +288,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   double *lam = R2 + split_r2_doubles(d), *red = lam + d;
   int *perm = reinterpret_cast<int *>(red + 32), *pinv = perm + d, *cnt = pinv + d;
   const int w = tid >> 5, nw = T >> 5, lane = tid & 31;
+  const float invd = 1.0f / d;
   double *su = S.u + so + off, *sw = S.w + so + off;
   SPLIT_STAMP(0);
 
@@ -324,14 +330,14 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
         vu[e] = vn;
         vw[e] = (wv[q] - uv_h) + vn;                                    // :393-394
         sw[e] = ws[q] - us_h;                                           // completed after projection
-        const int a = e / d, b = e - a * d;
+        const int a = qdiv(e, invd), b = e - a * d;
         R1[a * L + b] = us_h - ws[q];                                   // :391
       }
     }
   }
   __syncthreads();
   for (int e = tid; e < d * d; e += T) {  // sym = 0.5 (B + B')  (symmat.py:157)
-    const int a = e / d, b = e - a * d;
+    const int a = qdiv(e, invd), b = e - a * d;
     if (a < b) {
       const double s = 0.5 * (R1[a * L + b] + R1[b * L + a]);
       R1[a * L + b] = s;
@@ -351,18 +357,18 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   double *XS = R2, *TS = R2 + d * LS;
   double *xg = W.xarg + off;
   for (int e = tid; e < d * d; e += T) {
-    const int a = e / d, b = e - a * d;
+    const int a = qdiv(e, invd), b = e - a * d;
     xg[e] = R1[a * L + b];
   }
   __syncthreads();
   for (int e = tid; e < d * d; e += T) {
-    const int a = e / d, b = e - a * d;
+    const int a = qdiv(e, invd), b = e - a * d;
     R1[a * L + b] = vst[e];
   }
   {
     const int s0 = min(kSplitStrip, d);
     for (int e = tid; e < d * s0; e += T) {
-      const int a = e / s0, b = e - a * s0;
+      const int a = qdiv(e, 1.0f / s0), b = e - a * s0;
       XS[a * LS + b] = xg[a * d + b];
     }
   }
@@ -382,7 +388,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   for (int j0 = 0; j0 < d; j0 += kSplitStrip) {
     const int sw_ = min(kSplitStrip, d - j0), nbs = (sw_ + 15) >> 4;
     for (int t = w; t < nb * nbs; t += nw) {
-      const int bi = t / nbs, bj = t - bi * nbs;
+      const int bi = qdiv(t, 1.0f / nbs), bj = t - bi * nbs;
       double c[2][2][2];
       blk16_zero(c);
       blk16(c, Opd{R1, L, 1}, Opd{XS, LS, 1}, bi * 16, bj * 16, d, sw_, d);
@@ -391,13 +397,14 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     __syncthreads();
     // next strip of X: loads issued before this strip's products, stored after
     const int j1 = j0 + kSplitStrip, s1 = j1 < d ? min(kSplitStrip, d - j1) : 0;
+    const float inv1 = 1.0f / max(s1, 1);
     double pf[kPf];
 #pragma unroll
     for (int q = 0; q < kPf; ++q) {
       const int e = tid + q * T;
       pf[q] = 0.0;
       if (e < d * s1) {
-        const int a = e / s1, b = e - a * s1;
+        const int a = qdiv(e, inv1), b = e - a * s1;
         pf[q] = xg[a * d + j1 + b];
       }
     }
@@ -408,7 +415,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     for (int q = 0; q < kPf; ++q) {
       const int e = tid + q * T;
       if (e < d * s1) {
-        const int a = e / s1, b = e - a * s1;
+        const int a = qdiv(e, inv1), b = e - a * s1;
         XS[a * LS + b] = pf[q];
       }
     }
@@ -449,6 +456,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   }
   __syncthreads();
   const int r = cnt[0], n = d - r;
+  const float invr = 1.0f / max(r, 1), invn = 1.0f / max(n, 1);
   // off(B) < g keeps the inertia (Weyl: |E|_2 <= |E|_F < min |diag|); the
   // fixed point contracts at about off / 2g, so a looser bound only costs passes
   const bool applies = g > 0.0 && o2 <= kSplitOff2 * g * g && r <= n &&  // also false on NaN
@@ -504,7 +512,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   double *Ut = R2 + snoff;
   double x2 = 0.0;
   for (int e = tid; e < n * r; e += T) {
-    const int i = e / r, j = e - i * r;
+    const int i = qdiv(e, invr), j = e - i * r;
     const double x = R1[(r + i) * L + j] / (lam[j] - lam[r + i]);
     R1[(r + i) * L + j] = x;
     x2 += x * x;
@@ -516,6 +524,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   bool ok = prev == 0.0;
   int it = 0, yb = 0;
   const int mb = (n + 15) >> 4, nbr = (r + 15) >> 4, nx = mb * nbr, ny = nbr * nbr;
+  const float invbr = 1.0f / nbr, invbn = 1.0f / mb, invbd = 1.0f / ((d + 15) >> 4);
   for (; !ok && it < kSplitMaxPasses; ++it) {
     // pass: X blocks staged in registers (in place), Yn_{k} blocks emitted to the other buffer
     double c[kSplitMaxB][2][2][2];
@@ -526,13 +535,16 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
       blk16_zero(c[s]);
       const int t = w + s * nw;
       if (t < nx) {
-        const int bi = t / nbr, bj = t - bi * nbr;
+        const int bi = qdiv(t, invbr), bj = t - bi * nbr;
         blk16(c[s], ENN, XX, bi * 16, bj * 16, n, r, n);
         blk16(c[s], XX, Opd{Yc, ly, 1}, bi * 16, bj * 16, n, r, r);
       }
     }
-    for (int t = ((w - nx) % nw + nw) % nw; t < ny; t += nw) {  // round robin after the X blocks
-      const int bi = t / nbr, bj = t - bi * nbr;
+    // the quadratic term moves ~|X| off / 2g per pass (well below the linear
+    // contraction): refresh Yn on odd passes only (lag <= 2; Ybuf[0] = Yn(X_0))
+    const bool newy = (it & 1) != 0;
+    for (int t = ((w - nx) % nw + nw) % nw; newy && t < ny; t += nw) {  // round robin after the X blocks
+      const int bi = qdiv(t, invbr), bj = t - bi * nbr;
       double cy[2][2][2];
       blk16_zero(cy);
       blk16(cy, BPN, XX, bi * 16, bj * 16, r, r, n);
@@ -544,7 +556,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     for (int s = 0; s < kSplitMaxB; ++s) {
       const int t = w + s * nw;
       if (t < nx) {
-        const int bi = t / nbr, bj = t - bi * nbr;
+        const int bi = qdiv(t, invbr), bj = t - bi * nbr;
         blk16_each(c[s], bi * 16, bj * 16, n, r, [&](int i, int j, double v) {
           const double x = (R1[j * L + r + i] + v) / (lam[j] - lam[r + i]);
           const double dx = x - R1[(r + i) * L + j];
@@ -557,7 +569,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     if (lane == 0) red[w] = acc;
     __syncthreads();
     const double delta = sqrt(red_total(red, nw));
-    yb ^= 1;
+    if (newy) yb ^= 1;
     const double rho = delta / prev;
     if (delta == 0.0 || (rho < 0.5 && delta * rho <= 2.5e-16 * (1.0 - rho))) ok = true;
     else if (!(rho < 0.5)) break;  // stalled (or NaN)
@@ -568,7 +580,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     // hand B back (original order): N-P block from B_PN', diagonal from lam
     double *xb = W.xarg + off;
     for (int e = tid; e < d * d; e += T) {
-      const int i = e / d, j = e - i * d;
+      const int i = qdiv(e, invd), j = e - i * d;
       const int pi = pinv[i], pj = pinv[j];
       double v;
       if (pi == pj) v = lam[pi];
@@ -592,7 +604,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
       double cy[2][2][2];
       blk16_zero(cy);
       if (t < ny) {
-        const int bi = t / nbr, bj = t - bi * nbr;
+        const int bi = qdiv(t, invbr), bj = t - bi * nbr;
         blk16(cy, BPN, XX, bi * 16, bj * 16, r, r, n);
         blk16_each(cy, bi * 16, bj * 16, r, r, [&](int i, int j, double v) { Yb[i * ly + j] = v + R1[i * L + j]; });
       } else if (t < ny + nyu) {
@@ -634,7 +646,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   double *Kb = R1 + r;  // K = R G in the (dead) B_PN block
   // K <- R - K Y_P from K = R (error y^(nt+1))
   for (int e = tid; e < r * r; e += T) {
-    const int i = e / r, j = e - i * r;
+    const int i = qdiv(e, invr), j = e - i * r;
     Kb[i * L + j] = Yb[i * ly + j] + (i == j ? lam[i] : 0.0);
   }
   __syncthreads();
@@ -652,10 +664,10 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     for (int q = 1; q <= nt; ++q) cK *= -(2.0 * q - 1.0) / (2.0 * q);
     for (int e = tid; e < r * r + n * n; e += T) {
       if (e < r * r) {
-        const int i = e / r, j = e - i * r;
+        const int i = qdiv(e, invr), j = e - i * r;
         SP[i * L + j] = i == j ? cK : 0.0;
       } else {
-        const int q = e - r * r, i = q / n, j = q - i * n;
+        const int q = e - r * r, i = qdiv(q, invn), j = q - i * n;
         SN[i * ln + j] = i == j ? cK : 0.0;
       }
     }
@@ -670,10 +682,10 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
         blk16_zero(cc[s2]);
         const int t = w + s2 * nw;
         if (t < nsp) {
-          const int bi = t / nbr, bj = t - bi * nbr;
+          const int bi = qdiv(t, invbr), bj = t - bi * nbr;
           blk16(cc[s2], Opd{YPt, ly, 1}, Opd{SP, L, 1}, bi * 16, bj * 16, r, r, r);
         } else if (t < nsp + nbn * nbn) {
-          const int bi = (t - nsp) / nbn, bj = (t - nsp) - bi * nbn;
+          const int bi = qdiv(t - nsp, invbn), bj = (t - nsp) - bi * nbn;
           blk16(cc[s2], Opd{YN, L, 1}, Opd{SN, ln, 1}, bi * 16, bj * 16, n, n, n);
         }
       }
@@ -682,11 +694,11 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
       for (int s2 = 0; s2 < kSplitMaxB; ++s2) {
         const int t = w + s2 * nw;
         if (t < nsp) {
-          const int bi = t / nbr, bj = t - bi * nbr;
+          const int bi = qdiv(t, invbr), bj = t - bi * nbr;
           blk16_each(cc[s2], bi * 16, bj * 16, r, r,
                      [&](int i, int j, double v) { SP[i * L + j] = v + (i == j ? c : 0.0); });
         } else if (t < nsp + nbn * nbn) {
-          const int bi = (t - nsp) / nbn, bj = (t - nsp) - bi * nbn;
+          const int bi = qdiv(t - nsp, invbn), bj = (t - nsp) - bi * nbn;
           blk16_each(cc[s2], bi * 16, bj * 16, n, n,
                      [&](int i, int j, double v) { SN[i * ln + j] = v + (i == j ? c : 0.0); });
         }
@@ -695,30 +707,79 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     }
   }
   SPLIT_STAMP(5);
-  // Ut = Vt_P + Y_X' Vt_N  (r x d; rows of V gathered through perm) -> R2
-  team_mm1<false, false, true>(
-      r, d, Opd{R1 + r * L, 1, L}, Opd{vst, d, 1}, n,
-      [&](int i, int j, double v) { Ut[i * L + j] = v + vst[perm[i] * d + j]; }, perm + r);
   double *Tt = R1 + r * L;  // rows r.. of R1
+  const int nbd = (d + 15) >> 4, nut = nbr * nbd, nwt = vup ? nbn * nbd : 0;
+  {
+    // one pass: Ut = Vt_P + Y_X' Vt_N (r x d) -> R2, and (vup) Wt = Vt_N - Y_X Vt_P
+    // (n x d) in place over rows r.. of R1 (staged; Y_X, Y_N are dead after);
+    // rows of V gathered through perm
+    double cw[kSplitMaxB][2][2][2];
+#pragma unroll
+    for (int s2 = 0; s2 < kSplitMaxB; ++s2) {
+      blk16_zero(cw[s2]);
+      const int t = w + s2 * nw;
+      if (t < nwt) {
+        const int bi = qdiv(t, invbd), bj = t - bi * nbd;
+        blk16<true>(cw[s2], XX, Opd{vst, d, 1}, bi * 16, bj * 16, n, d, r, perm);
+      }
+    }
+    for (int t = ((w - nwt) % nw + nw) % nw; t < nut; t += nw) {
+      const int bi = qdiv(t, invbd), bj = t - bi * nbd;
+      double cu[2][2][2];
+      blk16_zero(cu);
+      blk16<true>(cu, Opd{R1 + r * L, 1, L}, Opd{vst, d, 1}, bi * 16, bj * 16, r, d, n, perm + r);
+      blk16_each(cu, bi * 16, bj * 16, r, d, [&](int i, int j, double v) { Ut[i * L + j] = v + vst[perm[i] * d + j]; });
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s2 = 0; s2 < kSplitMaxB; ++s2) {
+      const int t = w + s2 * nw;
+      if (t < nwt) {
+        const int bi = qdiv(t, invbd), bj = t - bi * nbd;
+        blk16_each(cw[s2], bi * 16, bj * 16, n, d,
+                   [&](int i, int j, double v) { Tt[i * L + j] = vst[perm[r + i] * d + j] - v; });
+      }
+    }
+    __syncthreads();
+  }
   if (vup) {
-    // Wt = Vt_N - Y_X Vt_P (n x d) in place over rows r.. of R1 (Y_X, Y_N dead after)
-    team_mm1<false, true, true>(
-        n, d, XX, Opd{vst, d, 1}, r,
-        [&](int i, int j, double v) { Tt[i * L + j] = vst[perm[r + i] * d + j] - v; }, perm);
-    // V' = [S_P Ut; S_N Wt] -> the store (rows 0..r-1: positive subspace)
+    // V' = [S_P Ut; S_N Wt] -> the store (rows 0..r-1: positive subspace), one pass
     double *vw = W.vstore + off;
-    team_mm1<false, false>(r, d, Opd{R1, L, 1}, Opd{Ut, L, 1}, r, [&](int i, int j, double v) { vw[i * d + j] = v; });
-    team_mm1<false, false>(n, d, Opd{EX, ln, 1}, Opd{Tt, L, 1}, n,
-                           [&](int i, int j, double v) { vw[(r + i) * d + j] = v; });
+    const int nvn = nbn * nbd;
+    for (int t = w; t < nut + nvn; t += nw) {
+      double cv[2][2][2];
+      blk16_zero(cv);
+      if (t < nut) {
+        const int bi = qdiv(t, invbd), bj = t - bi * nbd;
+        blk16(cv, Opd{R1, L, 1}, Opd{Ut, L, 1}, bi * 16, bj * 16, r, d, r);
+        blk16_each(cv, bi * 16, bj * 16, r, d, [&](int i, int j, double v) { vw[i * d + j] = v; });
+      } else {
+        const int bi = qdiv(t - nut, invbd), bj = (t - nut) - bi * nbd;
+        blk16(cv, Opd{EX, ln, 1}, Opd{Tt, L, 1}, bi * 16, bj * 16, n, d, n);
+        blk16_each(cv, bi * 16, bj * 16, n, d, [&](int i, int j, double v) { vw[(r + i) * d + j] = v; });
+      }
+    }
+    __syncthreads();
   }
   SPLIT_STAMP(6);
-  // Tt = K Ut (r x d) -> rows r.. of R1
+  // Tt = K Ut (r x d) -> rows r.. of R1 (Wt is dead)
   team_mm1<false, false>(r, d, Opd{Kb, L, 1}, Opd{Ut, L, 1}, r, [&](int i, int j, double v) { Tt[i * L + j] = v; });
   SPLIT_STAMP(7);
   // P = Ut' Tt  (d x d, symmetric) -> u_s; then w_s = (ws - us_h) + P
   // (solver.py:391-394) in a coalesced pass
   team_mm1<true, false>(d, d, Opd{Ut, 1, L}, Opd{Tt, L, 1}, r, [&](int i, int j, double v) { su[i * d + j] = v; });
-  for (int e = tid; e < d * d; e += T) sw[e] += su[e];
+  for (int e0 = tid; e0 < d * d; e0 += 4 * T) {  // (batched: the stores may alias later loads)
+    double a4[4], b4[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = min(e0 + q * T, d * d - 1);
+      a4[q] = sw[e];
+      b4[q] = su[e];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (e0 + q * T < d * d) sw[e0 + q * T] = a4[q] + b4[q];
+  }
   SPLIT_STAMP(8);
   if (tid == 0 && W.sweeps) W.sweeps[k] = -it;  // (stats: fixed-point iterations)
   if (tid == 0 && it > ca.split_refresh) W.vvalid[k] |= kVRefresh;
