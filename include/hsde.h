@@ -180,8 +180,9 @@ int hsde_sync(hsde_t *h);
  * the d > 32 cliques the k_cone_split fast path finished / handed to the Jacobi
  * kernel in the last hot projection, out[6] mean fixed-point iterations of the
  * finished ones, out[7..9] fraction handed over because off(B) > g / 10, r > n,
- * or the fixed point stalled. */
-#define HSDE_STATS_LEN 10
+ * or the fixed point stalled, out[10] fraction finished by the fast path after
+ * Jacobi sweeps refreshed the basis. */
+#define HSDE_STATS_LEN 11
 int hsde_stats(hsde_t *h, double *out);
 /* Diagnostics: off-diagonal norm history (relative, per sweep) of the last
  * hot projection of one clique: out[0] = 1 if warm-started, out[1..] = |off|/|A|

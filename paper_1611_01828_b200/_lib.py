@@ -22,7 +22,7 @@ HSDE_FLAG_EXACT_UY = 1
 HSDE_FLAG_NO_FACTOR = 2
 HSDE_FLAG_COLD_EIG = 4
 HSDE_FLAG_NO_SPLIT = 8
-HSDE_STATS_LEN = 10
+HSDE_STATS_LEN = 11
 HSDE_CHECK_LEN = 8
 HSDE_CERT_LEN = 7
 HSDE_PROFILE_SLOTS = 16
@@ -349,7 +349,7 @@ class Handle:
                 "mean_sweeps_large": float(out[2]), "warm_start": bool(out[3]),
                 "split_done": float(out[4]), "split_handoff": float(out[5]),
                 "split_fp_iters": float(out[6]), "handoff_off": float(out[7]), "handoff_rn": float(out[8]),
-                "handoff_stall": float(out[9])}
+                "handoff_stall": float(out[9]), "split_resumed": float(out[10])}
 
     def debug_jacobi(self, clique: int = 0) -> np.ndarray:
         out = np.empty(64)

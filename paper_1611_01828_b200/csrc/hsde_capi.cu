@@ -123,7 +123,7 @@ struct hsde_handle {
   // parallel branches for the independent cone launches (size classes, shards)
   static constexpr int kAux = 4;
   cudaStream_t aux[kAux] = {};
-  cudaEvent_t ev_fork = nullptr, ev_join[kAux] = {};
+  cudaEvent_t ev_fork = nullptr, ev_xjoin = nullptr, ev_join[kAux] = {};
   hsde_settings set{};
   hsde_info_t info{};
   std::vector<void *> bufs;
@@ -329,7 +329,7 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
     return e ? std::atoi(e) : 1;
   }();
   ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0, pl.pscratch, pl.pstride, 0,
-              split_refresh, split_vupdate};
+              split_refresh, split_vupdate, 0};
   if (!block) {
     const int grid = (pl.count + pl.per_block - 1) / pl.per_block;
     const int thr = pl.per_block * 32;
@@ -340,7 +340,8 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
     DevWork W = s.W;
     W.cstate = nullptr;  // k_cone_block does every clique
     if (mode == CONE_HOT && pl.split_smem && h->warm && h->split) {
-      // fast path + in-CTA Jacobi fallback (hsde_split.cuh)
+      // fast path, Jacobi path in the same CTA for cliques without a basis
+      // and for hand-overs (hsde_split.cuh)
       k_cone_split<<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, s.W, ca);
     } else if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, W, ca);
     else if (mode == CONE_PLAIN) k_cone_block<CONE_PLAIN><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
@@ -545,6 +546,8 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
   // cone projections: the plans (size classes, shards) are independent, so
   // they run as parallel branches (fork / join on events; captured as graph
   // edges) -- except under the per-phase profile, which keeps them in order
+  // The x update (k_xupd) touches only the x segment, the cones only s / v:
+  // under graph capture it is one more parallel branch.
   struct ConeJob {
     ShardDev *s;
     const ConePlan *pl;
@@ -560,6 +563,24 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
   for (int g = 0; g < G; ++g)
     if (h->sh[g].block_plan.count) jobs.push_back({&h->sh[g], &h->sh[g].block_plan, true});
   nl += (int)jobs.size();
+  auto launch_xupd = [&](cudaStream_t xs) -> int {
+    for (int g = 0; g < G; ++g) {
+      ShardDev &s = h->sh[g];
+      k_xupd<<<s.grid_nc, kBlock, 0, xs>>>(s.P, s.S, s.W);
+      CKL();
+      ++nl;
+    }
+    return 0;
+  };
+  const bool branch_x = !ev && !jobs.empty();
+  if (branch_x) {
+    // fork: k_xupd on its own branch, the cone jobs as below
+    CK(cudaEventRecord(h->ev_fork, st));
+    cudaStream_t xs = h->aux[hsde_handle::kAux - 1];
+    CK(cudaStreamWaitEvent(xs, h->ev_fork, 0));
+    RC(launch_xupd(xs));
+    CK(cudaEventRecord(h->ev_xjoin, xs));
+  }
   if (ev || jobs.size() <= 1) {
     if (n_warp_jobs == 0) mark(PS_CONE_WARP);
     for (size_t j = 0; j < jobs.size(); ++j) {
@@ -570,25 +591,21 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
     CK(cudaEventRecord(h->ev_fork, st));
     // the largest job (CTA plan if any, else the last warp class) stays on st
     for (size_t j = 0; j + 1 < jobs.size(); ++j) {
-      cudaStream_t a = h->aux[j % hsde_handle::kAux];
+      cudaStream_t a = h->aux[j % (hsde_handle::kAux - 1)];
       CK(cudaStreamWaitEvent(a, h->ev_fork, 0));
       RC(launch_cone(h, *jobs[j].s, CONE_HOT, *jobs[j].pl, jobs[j].block, nullptr, nullptr, 1.0, a));
     }
     RC(launch_cone(h, *jobs.back().s, CONE_HOT, *jobs.back().pl, jobs.back().block, nullptr, nullptr, 1.0,
                    st));
-    for (size_t j = 0; j + 1 < jobs.size() && j < (size_t)hsde_handle::kAux; ++j) {
+    for (size_t j = 0; j + 1 < jobs.size() && j < (size_t)hsde_handle::kAux - 1; ++j) {
       CK(cudaEventRecord(h->ev_join[j], h->aux[j]));
       CK(cudaStreamWaitEvent(st, h->ev_join[j], 0));
     }
     mark(PS_CONE_WARP);
   }
   mark(PS_CONE_BLOCK);
-  for (int g = 0; g < G; ++g) {
-    ShardDev &s = h->sh[g];
-    k_xupd<<<s.grid_nc, kBlock, 0, st>>>(s.P, s.S, s.W);
-    CKL();
-    ++nl;
-  }
+  if (branch_x) CK(cudaStreamWaitEvent(st, h->ev_xjoin, 0));
+  else RC(launch_xupd(st));
   mark(PS_XUPD);
   if (launches) *launches += nl;
   return 0;
@@ -1445,7 +1462,8 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
       return HSDE_ERR_CUDA;
     }
   }
-  if (cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+  if (cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_xjoin, cudaEventDisableTiming) != cudaSuccess) {
     h->err = "event create failed";
     return HSDE_ERR_CUDA;
   }
@@ -1655,6 +1673,7 @@ void hsde_destroy(hsde_t *h) {
     if (h->ev_join[a]) cudaEventDestroy(h->ev_join[a]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_xjoin) cudaEventDestroy(h->ev_xjoin);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
 }
@@ -2130,7 +2149,7 @@ int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches) 
 int hsde_stats(hsde_t *h, double *out) {
   if (!h || !out) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  double sum = 0, mx = 0, sum_big = 0, n_big = 0, n = 0, n_done = 0, n_hand = 0, n_fp = 0, n_why[3] = {0, 0, 0};
+  double sum = 0, mx = 0, sum_big = 0, n_big = 0, n = 0, n_done = 0, n_hand = 0, n_fp = 0, n_res = 0, n_why[3] = {0, 0, 0};
   for (auto &s : h->sh) {
     std::vector<int> sw(std::max(s.P.p, 1)), cs(std::max(s.P.p, 1));
     CK(cudaMemcpyAsync(sw.data(), s.W.sweeps, sizeof(int) * sw.size(), cudaMemcpyDeviceToHost, h->st));
@@ -2139,11 +2158,16 @@ int hsde_stats(hsde_t *h, double *out) {
     const bool split_ran = s.block_plan.split_smem && h->warm && h->split;
     for (int k = 0; k < s.P.p; ++k) {
       const bool big = s.sizes[k] > 32;
-      const bool fast = big && split_ran && cs[k] == SPLIT_DONE;
+      // final states: 0 fast path, 16 fast path after Jacobi sweeps (resumed),
+      // 33 Jacobi (no basis), 34..36 Jacobi after a hand-over (reason + 34)
+      const bool resumed = big && split_ran && cs[k] == SPLIT_DONE + 16;
+      const bool fast = big && split_ran && (cs[k] == SPLIT_DONE || resumed);
+      n_res += resumed;
       if (big && split_ran) {
         n_done += fast;
-        n_hand += cs[k] >= SPLIT_HANDOFF;
-        if (cs[k] >= SPLIT_HANDOFF && cs[k] <= SPLIT_HANDOFF + 2) ++n_why[cs[k] - SPLIT_HANDOFF];
+        const int why = cs[k] - (SPLIT_DONE + 32 + SPLIT_HANDOFF);
+        n_hand += why >= 0 && why <= 2;
+        if (why >= 0 && why <= 2) ++n_why[why];
       }
       if (fast) {  // no Jacobi solve; sweeps holds -(fixed-point iterations)
         n_fp -= sw[k];
@@ -2165,6 +2189,7 @@ int hsde_stats(hsde_t *h, double *out) {
   out[5] = nbig ? n_hand / nbig : 0.0;
   out[6] = n_done ? n_fp / n_done : 0.0;
   for (int i = 0; i < 3; ++i) out[7 + i] = nbig ? n_why[i] / nbig : 0.0;
+  out[10] = nbig ? n_res / nbig : 0.0;
   out[0] = n ? sum / n : 0.0;
   out[1] = mx;
   out[2] = n_big ? sum_big / n_big : 0.0;
@@ -2178,6 +2203,7 @@ int hsde_debug_jacobi(hsde_t *h, int32_t clique, double *out64) {
   ShardDev &s = h->sh[0];
   CK(cudaStreamSynchronize(h->st));
   CK(cudaMemcpy(out64, s.W.dbg, 64 * sizeof(double), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(s.W.dbg + 23, 0, sizeof(double)));  // k_cone_split hand-over record counter
   if (clique != s.W.dbg_clique) {
     s.W.dbg_clique = clique;
     if (h->factor) RC(rebuild_graphs(h));

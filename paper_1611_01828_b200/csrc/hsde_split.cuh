@@ -277,7 +277,7 @@ __device__ __forceinline__ double red_total(const double *red, int nw) {
 // The fast path for clique k (argument load included).  Returns SPLIT_DONE,
 // or a hand-off code with B = Vt X Vt' (original order) written to W.xarg.
 __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &W, const ConeArgs &ca, int k,
-                         double *smem) {
+                         double *smem, bool resume) {
   const int d = P.cl_size[k];
   const int tid = threadIdx.x, T = blockDim.x;
   const int64_t off = P.cl_off[k], so = P.n_c;
@@ -292,61 +292,63 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   double *su = S.u + so + off, *sw = S.w + so + off;
   SPLIT_STAMP(0);
 
+  if (!resume) {
   // ---- argument X (hot-path slot update, solver.py:222-244, :316, :388-394),
-  //      kLoadBatch slots per thread at a time: every load of the batch is
-  //      issued before the first store (the stores may alias later loads)
-  {
-    constexpr int NB = kLoadBatch;
-    const int64_t vo = P.n_c + P.n_d + P.m;
-    const double *mzs = P.mz + P.n_c + off, *mzv = P.mz + vo + off;
-    double *vu = S.u + vo + off, *vw = S.w + vo + off;
-    for (int e0 = tid; e0 < d * d; e0 += NB * T) {
-      double us[NB], ws[NB], uv[NB], wv[NB], hu[NB], ms[NB], mv[NB];
-      int cv[NB];
-#pragma unroll
-      for (int q = 0; q < NB; ++q) {
-        const int e = min(e0 + q * T, d * d - 1);
-        us[q] = su[e];
-        ws[q] = sw[e];
-        uv[q] = vu[e];
-        wv[q] = vw[e];
-        ms[q] = mzs[e];
-        mv[q] = mzv[e];
-        cv[q] = P.slot_cov[off + e];
-      }
-#pragma unroll
-      for (int q = 0; q < NB; ++q) hu[q] = W.ua[cv[q]];
-#pragma unroll
-      for (int q = 0; q < NB; ++q) {
-        const int e = e0 + q * T;
-        if (e >= d * d) break;
-        const double as = us[q] + ws[q], av = uv[q] + wv[q];            // a = u + w
-        const double gb = as - av;                                      // solver.py:222
-        const double ub = (gb + hu[q]) * 0.5;                           // :237-239
-        const double uvn = (ub - hu[q]) + av;                           // :242-244
-        const double us_h = relax(ub - shift * ms[q], us[q], P.alpha);  // :316, :388-390
-        const double uv_h = relax(uvn - shift * mv[q], uv[q], P.alpha);
-        const double vn = uv_h - wv[q];                                 // free block: identity
-        vu[e] = vn;
-        vw[e] = (wv[q] - uv_h) + vn;                                    // :393-394
-        sw[e] = ws[q] - us_h;                                           // completed after projection
-        const int a = qdiv(e, invd), b = e - a * d;
-        R1[a * L + b] = us_h - ws[q];                                   // :391
+    //      kLoadBatch slots per thread at a time: every load of the batch is
+    //      issued before the first store (the stores may alias later loads)
+    {
+      constexpr int NB = kLoadBatch;
+      const int64_t vo = P.n_c + P.n_d + P.m;
+      const double *mzs = P.mz + P.n_c + off, *mzv = P.mz + vo + off;
+      double *vu = S.u + vo + off, *vw = S.w + vo + off;
+      for (int e0 = tid; e0 < d * d; e0 += NB * T) {
+        double us[NB], ws[NB], uv[NB], wv[NB], hu[NB], ms[NB], mv[NB];
+        int cv[NB];
+  #pragma unroll
+        for (int q = 0; q < NB; ++q) {
+          const int e = min(e0 + q * T, d * d - 1);
+          us[q] = su[e];
+          ws[q] = sw[e];
+          uv[q] = vu[e];
+          wv[q] = vw[e];
+          ms[q] = mzs[e];
+          mv[q] = mzv[e];
+          cv[q] = P.slot_cov[off + e];
+        }
+  #pragma unroll
+        for (int q = 0; q < NB; ++q) hu[q] = W.ua[cv[q]];
+  #pragma unroll
+        for (int q = 0; q < NB; ++q) {
+          const int e = e0 + q * T;
+          if (e >= d * d) break;
+          const double as = us[q] + ws[q], av = uv[q] + wv[q];            // a = u + w
+          const double gb = as - av;                                      // solver.py:222
+          const double ub = (gb + hu[q]) * 0.5;                           // :237-239
+          const double uvn = (ub - hu[q]) + av;                           // :242-244
+          const double us_h = relax(ub - shift * ms[q], us[q], P.alpha);  // :316, :388-390
+          const double uv_h = relax(uvn - shift * mv[q], uv[q], P.alpha);
+          const double vn = uv_h - wv[q];                                 // free block: identity
+          vu[e] = vn;
+          vw[e] = (wv[q] - uv_h) + vn;                                    // :393-394
+          sw[e] = ws[q] - us_h;                                           // completed after projection
+          const int a = qdiv(e, invd), b = e - a * d;
+          R1[a * L + b] = us_h - ws[q];                                   // :391
+        }
       }
     }
-  }
-  __syncthreads();
-  for (int e = tid; e < d * d; e += T) {  // sym = 0.5 (B + B')  (symmat.py:157)
-    const int a = qdiv(e, invd), b = e - a * d;
-    if (a < b) {
-      const double s = 0.5 * (R1[a * L + b] + R1[b * L + a]);
-      R1[a * L + b] = s;
-      R1[b * L + a] = s;
+    __syncthreads();
+    for (int e = tid; e < d * d; e += T) {  // sym = 0.5 (B + B')  (symmat.py:157)
+      const int a = qdiv(e, invd), b = e - a * d;
+      if (a < b) {
+        const double s = 0.5 * (R1[a * L + b] + R1[b * L + a]);
+        R1[a * L + b] = s;
+        R1[b * L + a] = s;
+      }
     }
+    __syncthreads();
+    SPLIT_STAMP(1);
+  
   }
-  __syncthreads();
-  SPLIT_STAMP(1);
-
   // ---- B = Vt X Vt' by column strips of T = Vt X, all from shared memory:
   //      X -> the hand-off buffer (global, L2-resident), Vt -> R1, then per
   //      strip J: X[:, J] -> XS, T_J = Vt X[:, J] -> TS, B += T_J Vt[:, J]'
@@ -356,6 +358,34 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   const int LS = split_ld(kSplitStrip);
   double *XS = R2, *TS = R2 + d * LS;
   double *xg = W.xarg + off;
+  double cb[kSplitMaxB][2][2][2];
+  int bi0[kSplitMaxB], bj0[kSplitMaxB];
+#pragma unroll
+  for (int s = 0; s < kSplitMaxB; ++s) {
+    blk16_zero(cb[s]);
+    const int t = w + s * nw;
+    int bi = 0, bj = 0;
+    if (t < nbu) upper_block(t, nb, bi, bj);
+    bi0[s] = bi * 16;
+    bj0[s] = bj * 16;
+  }
+  if (resume) {
+    // B handed back by the Jacobi path (basis refreshed, V in the store)
+#pragma unroll
+    for (int s = 0; s < kSplitMaxB; ++s)
+      if (w + s * nw < nbu) {
+        const int q = lane >> 2, kk = lane & 3;
+#pragma unroll
+        for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+          for (int b2 = 0; b2 < 2; ++b2)
+#pragma unroll
+            for (int e2 = 0; e2 < 2; ++e2) {
+              const int i = min(bi0[s] + 8 * a2 + q, d - 1), j = min(bj0[s] + 8 * b2 + 2 * kk + e2, d - 1);
+              cb[s][a2][b2][e2] = xg[i * d + j];
+            }
+      }
+  } else {
   for (int e = tid; e < d * d; e += T) {
     const int a = qdiv(e, invd), b = e - a * d;
     xg[e] = R1[a * L + b];
@@ -373,17 +403,6 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     }
   }
   __syncthreads();
-  double cb[kSplitMaxB][2][2][2];
-  int bi0[kSplitMaxB], bj0[kSplitMaxB];
-#pragma unroll
-  for (int s = 0; s < kSplitMaxB; ++s) {
-    blk16_zero(cb[s]);
-    const int t = w + s * nw;
-    int bi = 0, bj = 0;
-    if (t < nbu) upper_block(t, nb, bi, bj);
-    bi0[s] = bi * 16;
-    bj0[s] = bj * 16;
-  }
   constexpr int kPf = (kSplitMaxD * kSplitStrip + kSplitThreads - 1) / kSplitThreads;
   for (int j0 = 0; j0 < d; j0 += kSplitStrip) {
     const int sw_ = min(kSplitStrip, d - j0), nbs = (sw_ + 15) >> 4;
@@ -421,6 +440,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     }
     __syncthreads();
   }
+  }  // !resume
   SPLIT_STAMP(2);
 
   // ---- diagonal, g = min |diag|, off(B)^2 (upper values, mirrored)
@@ -461,6 +481,16 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   // fixed point contracts at about off / 2g, so a looser bound only costs passes
   const bool applies = g > 0.0 && o2 <= kSplitOff2 * g * g && r <= n &&  // also false on NaN
                        split_fits(r, n, nw);
+  if (!applies && W.dbg && tid == 0) {  // diagnostics: (g, off, |diag|_max) of up to 8 hand-overs
+    const unsigned long long c = atomicAdd(reinterpret_cast<unsigned long long *>(W.dbg + 23), 1ull);
+    double mx = 0.0;
+    for (int i = 0; i < d; ++i) mx = fmax(mx, fabs(lam[i]));
+    if (c < 8) {
+      W.dbg[24 + 3 * c] = g;
+      W.dbg[25 + 3 * c] = sqrt(o2);
+      W.dbg[26 + 3 * c] = mx;
+    }
+  }
   if (!applies) {
     // hand B (original order) to the Jacobi path
     double *xb = W.xarg + off;
@@ -787,8 +817,9 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
 }
 
 // One CTA per CTA-sized clique on the hot path: the fast path when the
-// clique has a valid eigenbasis, otherwise -- or when the fast path hands
-// over -- the Jacobi path (cone_one) in the same CTA.
+// clique has a valid eigenbasis; otherwise -- or when the fast path hands
+// over -- the Jacobi path (cone_one) in the same CTA, so a hand-over overlaps
+// the other cliques instead of serialising behind them.
 __global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
   extern __shared__ __align__(16) double smem[];
   if ((int)blockIdx.x >= ca.count) return;
@@ -798,10 +829,11 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, D
   ConeArgs c2 = ca;
   c2.slot = blockIdx.x;
   int st = SPLIT_UNTOUCHED;
-  if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d > 32) st = split_one(P, S, W, c2, k, smem);
+  if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d > 32) st = split_one(P, S, W, c2, k, smem, false);
   if (threadIdx.x == 0) W.cstate[k] = st;
   if (st == SPLIT_DONE) return;
   __syncthreads();  // cstate and the hand-off B are visible to the whole CTA
   BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
   cone_one<CONE_HOT>(tm, P, S, W, c2, k, smem);
+  if (threadIdx.x == 0) W.cstate[k] = SPLIT_DONE + 32 + st;  // (stats: finished by the Jacobi path)
 }

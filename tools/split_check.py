@@ -27,11 +27,18 @@ for name, flags in (("split", 0), ("jacobi", _lib.HSDE_FLAG_NO_SPLIT)):
     done = 0
     while done < a.iters:
         step = min(20, a.iters - done)
-        h.iterate(step)
+        ms_chunk = h.time_iterations(step) / step
         done += step
         st = h.stats()
-        hist.append((done, round(st["split_done"], 3), round(st["split_fp_iters"], 2), round(st["handoff_off"], 3),
-                     round(st["handoff_rn"], 3), round(st["handoff_stall"], 3), round(st["mean_sweeps_large"], 2)))
+        if name == "split":
+            dbg = h.debug_jacobi(0)
+            nh = int(np.frombuffer(dbg[23:24].tobytes(), dtype=np.uint64)[0])
+            if nh:
+                print("   handovers at", done, nh, [tuple(round(float(x), 5) for x in dbg[24 + 3 * i:27 + 3 * i]) for i in range(min(nh, 8))], flush=True)
+            dbg[23] = 0.0
+            h.clear_debug() if hasattr(h, "clear_debug") else None
+        hist.append((done, round(ms_chunk, 3), round(st["split_done"], 3), round(st["split_fp_iters"], 2), round(st["handoff_off"], 3),
+                     round(st["handoff_rn"], 3), round(st["handoff_stall"], 3), round(st["split_resumed"], 3), round(st["mean_sweeps_large"], 2)))
     h.sync()
     u, w = h.get_state()
     res[name] = (u, w)
@@ -43,7 +50,7 @@ for name, flags in (("split", 0), ("jacobi", _lib.HSDE_FLAG_NO_SPLIT)):
     st_ = dbg[48:57]
     if name == "split":
         print("  phase cycles:", [int(st_[i + 1] - st_[i]) for i in range(8)], "fp iters", dbg[47], flush=True)
-    print("  (iter, done, fp_iters, h_off, h_rn, h_stall, sweeps_large):", hist, flush=True)
+    print("  (iter, ms/it, done, fp_iters, h_off, h_rn, h_stall, resumed, sweeps_large):", hist, flush=True)
     h.close()
 du = np.linalg.norm(res["split"][0] - res["jacobi"][0]) / np.linalg.norm(res["jacobi"][0])
 dw = np.linalg.norm(res["split"][1] - res["jacobi"][1]) / np.linalg.norm(res["jacobi"][1])
