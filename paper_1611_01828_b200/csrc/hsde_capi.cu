@@ -342,7 +342,9 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
     if (mode == CONE_HOT && pl.split_smem && h->warm && h->split) {
       // fast path, Jacobi path in the same CTA for cliques without a basis
       // and for hand-overs (hsde_split.cuh)
-      k_cone_split<<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, s.W, ca);
+      ConeArgs co = ca;
+      co.ids = s.W.corder;  // scheduled by k_scalars (s.W.cta_ids)
+      k_cone_split<<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, s.W, co);
     } else if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, W, ca);
     else if (mode == CONE_PLAIN) k_cone_block<CONE_PLAIN><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
     else k_cone_block<CONE_MINEIG><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
@@ -710,6 +712,8 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
     for (int k : bids) dmax = std::max(dmax, s.sizes[k]);
     if (dmax <= kSplitMaxD) {
       s.block_plan.split_smem = std::max((size_t)split_smem_doubles(dmax) * sizeof(double), per_blk);
+      s.W.cta_ids = s.block_plan.ids;  // k_scalars schedules them for k_cone_split
+      s.W.cta_n = s.block_plan.count;
       CK(cudaFuncSetAttribute(k_cone_split, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     }
     CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -1383,6 +1387,8 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   RC(dalloc(h, &s.W.vvalid, std::max(p, 1)));
   RC(dalloc(h, &s.W.sweeps, std::max(p, 1)));
   RC(dalloc(h, &s.W.cstate, std::max(p, 1)));
+  RC(dalloc(h, &s.W.ckey, std::max(p, 1)));
+  RC(dalloc(h, &s.W.corder, std::max(p, 1)));
   RC(dalloc(h, &s.W.xarg, std::max<int64_t>(n_d, 1)));
   RC(dalloc(h, &s.W.sepbuf, std::max(d->n_sep, 1)));
   RC(dalloc(h, &s.W.qbuf, std::max(m, 1)));
@@ -1393,6 +1399,7 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   CK(cudaMemset(s.W.vvalid, 0, sizeof(int) * std::max(p, 1)));
   CK(cudaMemset(s.W.sweeps, 0, sizeof(int) * std::max(p, 1)));
   CK(cudaMemset(s.W.cstate, 0xff, sizeof(int) * std::max(p, 1)));
+  CK(cudaMemset(s.W.ckey, 0, sizeof(int) * std::max(p, 1)));
   CK(cudaMemset(s.d_chk, 0, sizeof(double) * 64));
   s.grid_nc = grid_for(n_c);
   s.grid_ua = s.grid_nc;

@@ -127,6 +127,10 @@ struct DevWork {
   double *red;         // [8]     scalar partials (all-reduced)
   int *handoff;        // [p]     1: stage-1 Jacobi handed the clique to the refinement kernel
   int *cstate;         // [p]     k_cone_split outcome (SplitState), read by k_cone_block
+  int *ckey;           // [p]     predicted cost of the clique's next projection (schedule key)
+  int *corder;         // [p]     CTA-plan clique ids, refresh candidates first (k_scalars)
+  const int *cta_ids;  // CTA-plan clique ids (plan order) to be scheduled into corder, or null
+  int cta_n;
   double *xarg;        // [n_d]   k_cone_split -> k_cone_block hand-off (B = Vt X Vt')
   double *dbg;         // [64]    Jacobi off-norm history of one clique (diagnostics)
   int dbg_clique;
@@ -464,6 +468,14 @@ __global__ void __launch_bounds__(1024) k_scalars(DevProblem P, DevState S, DevW
   __shared__ double sh[32];
   __shared__ double bc[4];
   const int64_t yo = P.n_c + P.n_d;
+  // k_cone_split schedule (hsde_split.cuh): ids and keys loaded first, the
+  // partition done at the end (their latency hides behind the sums)
+  const bool sched = W.cta_ids != nullptr;
+  int my_id = 0, my_key = 0;
+  if (sched && (int)threadIdx.x < W.cta_n) {
+    my_id = W.cta_ids[threadIdx.x];
+    my_key = W.ckey[my_id];
+  }
   double a = 0.0;
   if (!cua_red)
     for (int i = threadIdx.x; i < nparts; i += blockDim.x) a += W.part[i];
@@ -506,6 +518,51 @@ __global__ void __launch_bounds__(1024) k_scalars(DevProblem P, DevState S, DevW
     S.u[yo + i] = yn;
     S.w[yo + i] = wn;
     W.ry[i] = (yn + wn) + atau_next * P.b[i];
+  }
+  if (sched) {
+    // the cliques with key 1 (likely to need a Jacobi refresh) first, plan order
+    // otherwise: a stable partition by ballots, blockDim.x ids per chunk
+    __shared__ int cnt[32];
+    int base1 = 0, base0 = 0;
+    const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5, nwq = blockDim.x >> 5;
+    if (W.cta_n > (int)blockDim.x) {  // multi-chunk plans: count the key-1 ids first
+      int n1 = 0;
+      for (int i = threadIdx.x; i < W.cta_n; i += blockDim.x) n1 += W.ckey[W.cta_ids[i]] != 0;
+      base0 = (int)block_sum((double)n1, sh);
+      if (threadIdx.x == 0) bc[2] = base0;
+      __syncthreads();
+      base0 = (int)bc[2];
+    }
+    for (int c0 = 0; c0 < W.cta_n; c0 += blockDim.x) {
+      const int i = c0 + threadIdx.x;
+      const bool in = i < W.cta_n;
+      int id = my_id, key = my_key;
+      if (c0 > 0 && in) {
+        id = W.cta_ids[i];
+        key = W.ckey[id];
+      }
+      const bool k1 = in && key != 0;
+      const unsigned b1 = __ballot_sync(0xffffffffu, k1), b0 = __ballot_sync(0xffffffffu, in && !k1);
+      if (lane == 0) cnt[wq] = __popc(b1) | (__popc(b0) << 16);
+      __syncthreads();
+      int p1 = 0, p0 = 0, t1 = 0, t0 = 0;
+      for (int q = 0; q < nwq; ++q) {
+        const int c1 = cnt[q] & 0xffff, c0n = cnt[q] >> 16;
+        if (q < wq) {
+          p1 += c1;
+          p0 += c0n;
+        }
+        t1 += c1;
+        t0 += c0n;
+      }
+      if (W.cta_n <= (int)blockDim.x) base0 = t1;  // single chunk: the key-1 count is t1
+      const unsigned below = (1u << lane) - 1u;
+      if (k1) W.corder[base1 + p1 + __popc(b1 & below)] = id;
+      else if (in) W.corder[base0 + p0 + __popc(b0 & below)] = id;
+      base1 += t1;
+      base0 += t0;
+      __syncthreads();
+    }
   }
 }
 

@@ -15,7 +15,7 @@
 // orthogonal projector onto span Q is Q G Q' with G = (I + Y_X' Y_X)^-1, so
 //     P(B) = B Q G Q' = Q (R G) Q'      and      P(X) = Ut' K Ut,
 // Ut = Vt_P + Y_X' Vt_N (r x d), K = R G (r x r).  No truncation: the only
-// errors are the fixed point's (stopped at <= 2.5e-16) and rounding.  V
+// errors are the fixed point's (stopped at <= kSplitTol) and rounding.  V
 // itself is left unchanged, so it never loses orthogonality here.
 //
 // The path applies when off(B) <= g / 10 (then no eigenvalue changes sign,
@@ -41,6 +41,10 @@ constexpr int kSplitRefreshIters = 1000;  // fixed-point passes that ask for a J
 constexpr int kLoadBatch = 4;          // hot-path slots per thread in flight
 constexpr double kSplitOff2 = 1.0 / 9.0;  // fast path while off(B)^2 <= kSplitOff2 g^2
 constexpr int kSplitMaxPasses = 24;     // fixed-point passes before handing over
+// fixed-point stop: estimated error of Y <= kSplitTol.  Y is dimensionless
+// (subspace coordinates): an error e moves P by ~ e |B|, below the rounding of
+// the d-term products themselves (~ d eps |B| = 1.8e-14 |B| at d = 80)
+constexpr double kSplitTol = 1e-15;
 
 __host__ __device__ inline int split_ld(int c) { return ((c + 11) & ~15) + 4; }
 
@@ -290,6 +294,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   const int w = tid >> 5, nw = T >> 5, lane = tid & 31;
   const float invd = 1.0f / d;
   double *su = S.u + so + off, *sw = S.w + so + off;
+  bool refreshed = false;  // (stats) Jacobi sweeps refreshed the basis in this call
   SPLIT_STAMP(0);
 
   if (!resume) {
@@ -444,19 +449,79 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   SPLIT_STAMP(2);
 
   // ---- diagonal, g = min |diag|, off(B)^2 (upper values, mirrored)
-  double o2 = 0.0;
+  double o2, g;
+  auto measure = [&]() {
+    o2 = 0.0;
 #pragma unroll
-  for (int s = 0; s < kSplitMaxB; ++s)
-    if (w + s * nw < nbu)
-      blk16_each(cb[s], bi0[s], bj0[s], d, d, [&](int i, int j, double v) {
-        if (i == j) lam[i] = v;
-        else if (i < j) o2 += 2.0 * v * v;
-      });
-  __syncthreads();
-  double g = CUDART_INF;
-  for (int i = tid; i < d; i += T) g = fmin(g, fabs(lam[i]));
-  g = cta_min(g, red);
-  o2 = cta_sum(o2, red);
+    for (int s = 0; s < kSplitMaxB; ++s)
+      if (w + s * nw < nbu)
+        blk16_each(cb[s], bi0[s], bj0[s], d, d, [&](int i, int j, double v) {
+          if (i == j) lam[i] = v;
+          else if (i < j) o2 += 2.0 * v * v;
+        });
+    __syncthreads();
+    g = CUDART_INF;
+    for (int i = tid; i < d; i += T) g = fmin(g, fabs(lam[i]));
+    g = cta_min(g, red);
+    o2 = cta_sum(o2, red);
+  };
+  measure();
+  if (!(o2 <= kSplitOff2 * g * g) && g > 0.0 && o2 < CUDART_INF) {
+    // Refresh: the within-class drift of the kept basis made the split
+    // inapplicable.  Jacobi sweeps on B, warm from V (hsde_eig.cuh), in this
+    // CTA until the class-split point; then the split goes on with the
+    // rotated B and V.  (B is in registers, X and V in global memory: the
+    // Jacobi scratch may overwrite the whole shared-memory area.)
+    const int dp = d + (d & 1);
+    BlockTeam tm{tid, T};
+    JacobiScratch js = jacobi_carve(smem, dp);
+#pragma unroll
+    for (int s = 0; s < kSplitMaxB; ++s)
+      if (w + s * nw < nbu)
+        blk16_each(cb[s], bi0[s], bj0[s], d, d, [&](int i, int j, double v) {
+          if (i <= j) {
+            js.A[i * js.lda + j] = v;
+            js.A[j * js.lda + i] = v;
+          }
+        });
+    for (int e = tid; e < dp * js.ldv; e += T) {
+      const int i = e / js.ldv, j = e - i * js.ldv;
+      js.Vt[e] = (i < d && j < d) ? vst[i * d + j] : (i == j ? 1.0 : 0.0);
+    }
+    if (d & 1)
+      for (int e = tid; e < dp; e += T) {
+        js.A[d * js.lda + e] = 0.0;
+        js.A[e * js.lda + d] = 0.0;
+      }
+    jacobi_prepare(tm, js, dp, false);
+    __syncthreads();
+    int order = 0;
+    jacobi_sweeps(tm, js, d, dp, &order, 3);
+    double *vw = W.vstore + off;
+    for (int e = tid; e < d * d; e += T) {
+      const int a = qdiv(e, invd), b = e - a * d;
+      vw[e] = js.Vt[a * js.ldv + b];
+    }
+    {
+      const int q = lane >> 2, kk = lane & 3;
+#pragma unroll
+      for (int s = 0; s < kSplitMaxB; ++s)
+        if (w + s * nw < nbu)
+#pragma unroll
+          for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+            for (int b2 = 0; b2 < 2; ++b2)
+#pragma unroll
+              for (int e2 = 0; e2 < 2; ++e2) {
+                const int i = min(bi0[s] + 8 * a2 + q, d - 1), j = min(bj0[s] + 8 * b2 + 2 * kk + e2, d - 1);
+                cb[s][a2][b2][e2] = js.A[i * js.lda + j];
+              }
+    }
+    __syncthreads();  // the scratch overlaps lam / red / perm
+    if (tid == 0 && W.sweeps) W.sweeps[k] = 0;
+    measure();
+    refreshed = true;
+  }
   // class-sorted order: perm[0, r) = P (diag > 0), perm[r, d) = N
   if (tid < 32) {
     int base = 0;
@@ -525,6 +590,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   SPLIT_STAMP(3);
 
   if (r == 0) {  // no eigenvalue > 0: P = 0 (w_s holds ws - us_h already)
+    if (tid == 0) W.ckey[k] = 0;
     for (int e = tid; e < d * d; e += T) su[e] = 0.0;
     return SPLIT_DONE;
   }
@@ -601,7 +667,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     const double delta = sqrt(red_total(red, nw));
     if (newy) yb ^= 1;
     const double rho = delta / prev;
-    if (delta == 0.0 || (rho < 0.5 && delta * rho <= 2.5e-16 * (1.0 - rho))) ok = true;
+    if (delta == 0.0 || (rho < 0.5 && delta * rho <= kSplitTol * (1.0 - rho))) ok = true;
     else if (!(rho < 0.5)) break;  // stalled (or NaN)
     prev = delta;
     __syncthreads();  // red is rewritten by the next pass
@@ -812,6 +878,10 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   }
   SPLIT_STAMP(8);
   if (tid == 0 && W.sweeps) W.sweeps[k] = -it;  // (stats: fixed-point iterations)
+  // schedule key for the next iteration: passes, plus a refresh risk when off(B)
+  // is already near the applicability bound
+  if (tid == 0) W.ckey[k] = o2 > 0.5 * kSplitOff2 * g * g ? 1 : 0;
+  if (refreshed) return SPLIT_DONE + 16;  // (stats: after a Jacobi refresh)
   if (tid == 0 && it > ca.split_refresh) W.vvalid[k] |= kVRefresh;
   return SPLIT_DONE;
 }
@@ -831,9 +901,12 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, D
   int st = SPLIT_UNTOUCHED;
   if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d > 32) st = split_one(P, S, W, c2, k, smem, false);
   if (threadIdx.x == 0) W.cstate[k] = st;
-  if (st == SPLIT_DONE) return;
+  if (st == SPLIT_DONE || st == SPLIT_DONE + 16) return;
   __syncthreads();  // cstate and the hand-off B are visible to the whole CTA
   BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
   cone_one<CONE_HOT>(tm, P, S, W, c2, k, smem);
-  if (threadIdx.x == 0) W.cstate[k] = SPLIT_DONE + 32 + st;  // (stats: finished by the Jacobi path)
+  if (threadIdx.x == 0) {
+    W.cstate[k] = SPLIT_DONE + 32 + st;  // (stats: finished by the Jacobi path)
+    W.ckey[k] = 1;                        // schedule first next time
+  }
 }
