@@ -380,12 +380,35 @@ __global__ void k_pair_sum(DevProblem P, const double *__restrict__ t, double *_
 
 // q0 partials: part[r * ntile + tile] = sum over the tile's owned pairs of
 // A_r,pair x_pair; the tile's pair values are staged in shared memory.
+// PAIRS: x_pair = t_l + t_mirror formed while staging (no separate pair-sum pass)
+template <bool PAIRS>
 __global__ void __launch_bounds__(kBlock) k_spmv_half(DevProblem P, const double *__restrict__ xq,
                                                        double *__restrict__ part) {
   __shared__ double xs[kRowTile];
   const int tile = blockIdx.x / kRowTileSplit, rr = blockIdx.x - tile * kRowTileSplit;
   const int q0 = tile * kRowTile, wn = min(kRowTile, P.n_pair - q0);
-  for (int i = threadIdx.x; i < wn; i += blockDim.x) xs[i] = xq[q0 + i];
+  if (PAIRS) {
+    for (int i0 = threadIdx.x; i0 < wn; i0 += 4 * blockDim.x) {  // 4 pairs in flight per thread
+      int l[4], mm[4];
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = min(i0 + u * (int)blockDim.x, wn - 1);
+        l[u] = P.pair_l[q0 + i];
+        mm[u] = P.pair_m[q0 + i];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = xq[l[u]];
+        b[u] = mm[u] != l[u] ? xq[mm[u]] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u * (int)blockDim.x < wn) xs[i0 + u * blockDim.x] = a[u] + b[u];
+    }
+  } else {
+    for (int i = threadIdx.x; i < wn; i += blockDim.x) xs[i] = xq[q0 + i];
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int G = P.rt_G;
