@@ -287,6 +287,12 @@ class Handle:
                                                 _ptr(w, C.c_double)))
         return u, w
 
+    def get_u(self, shard: int = 0):
+        """u alone (the report needs no w)."""
+        u = np.empty(self.totals[shard])
+        self._rc(self._lib.hsde_get_state_shard(self._h, shard, _ptr(u, C.c_double), None))
+        return u
+
     def set_state_shard(self, shard: int, u, w):
         u = self._vec(u, self.totals[shard])
         w = self._vec(w, self.totals[shard])

@@ -31,7 +31,9 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/hsde.h"
@@ -209,9 +211,60 @@ int dalloc(hsde_handle *h, T **p, size_t n) {
   return 0;
 }
 
+// Large host->device copies from pageable memory (the caller's arrays: A
+// alone is 0.46 GB for config 4) go through two pinned staging buffers: the
+// host copy of a chunk is split over threads while the DMA engine moves the
+// previous chunk (pageable cudaMemcpy runs at ~11 GB/s on this host).
+constexpr size_t kStagedMin = 16u << 20;
+constexpr size_t kStageChunk = 32u << 20;
+
+int h2d_staged(hsde_handle *h, void *dst, const void *src, size_t bytes) {
+  static std::mutex mu;
+  static char *pin[2] = {nullptr, nullptr};
+  static cudaEvent_t done[2] = {nullptr, nullptr};
+  static cudaStream_t cs = nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pin[0]) {
+    for (int b = 0; b < 2; ++b)
+      if (cudaHostAlloc((void **)&pin[b], kStageChunk, cudaHostAllocDefault) != cudaSuccess ||
+          cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming) != cudaSuccess) {
+        pin[0] = pin[1] = nullptr;
+        cudaGetLastError();
+        cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);  // no pinned memory
+        if (e != cudaSuccess) {
+          h->err = std::string("cudaMemcpy H2D: ") + cudaGetErrorString(e);
+          return HSDE_ERR_CUDA;
+        }
+        return 0;
+      }
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  }
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const char *s8 = static_cast<const char *>(src);
+  char *d8 = static_cast<char *>(dst);
+  bool used[2] = {false, false};
+  for (size_t off = 0, c = 0; off < bytes; off += kStageChunk, ++c) {
+    const int b = (int)(c & 1);
+    const size_t len = std::min(kStageChunk, bytes - off);
+    if (used[b]) CK(cudaEventSynchronize(done[b]));  // its previous DMA has finished
+    const size_t per = (len + hw - 1) / hw;
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < hw && t * per < len; ++t)
+      th.emplace_back([=] { std::memcpy(pin[b] + t * per, s8 + off + t * per, std::min(per, len - t * per)); });
+    std::memcpy(pin[b], s8 + off, std::min(per, len));
+    for (auto &x : th) x.join();
+    CK(cudaMemcpyAsync(d8 + off, pin[b], len, cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(done[b], cs));
+    used[b] = true;
+  }
+  CK(cudaStreamSynchronize(cs));
+  return 0;
+}
+
 template <class T>
 int dupload(hsde_handle *h, T **p, const T *src, size_t n) {
   RC(dalloc(h, p, n));
+  if (n * sizeof(T) >= kStagedMin) return h2d_staged(h, *p, src, n * sizeof(T));
   if (n) {
     cudaError_t e = cudaMemcpy(*p, src, n * sizeof(T), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
@@ -1445,10 +1498,14 @@ int set_data(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d, double sc,
   s.P.b = b_d;
   const double consts[4] = {sb, sc, 1.0, 0.0};
   RC(dupload(h, &s.d_consts, consts, 4));
-  std::vector<double> z(s.P.total - 1, 0.0);  // zeta (solver.py:264)
-  for (int c = 0; c < n_c; ++c) z[c] = cint[c];
-  for (int i = 0; i < m; ++i) z[n_c + n_d + i] = -bint[i];
-  RC(dupload(h, &s.d_zeta, z.data(), z.size()));
+  // zeta = (c, 0, -b, 0) (solver.py:264): zero on the device, two segments copied
+  RC(dalloc(h, &s.d_zeta, (size_t)(s.P.total - 1)));
+  CK(cudaMemsetAsync(s.d_zeta, 0, sizeof(double) * (size_t)(s.P.total - 1), h->st));
+  std::vector<double> nb(m);
+  for (int i = 0; i < m; ++i) nb[i] = -bint[i];
+  CK(cudaMemcpyAsync(s.d_zeta, c_d, sizeof(double) * n_c, cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaMemcpyAsync(s.d_zeta + n_c + n_d, nb.data(), sizeof(double) * m, cudaMemcpyHostToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
   return 0;
 }
 
@@ -1544,14 +1601,14 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
   tick("set_data");
   // norms of the iterated data (residual denominators, solver.py:417-423)
   {
-    double nci = 0;
-    for (auto &s : h->sh) {
-      std::vector<double> cc(s.P.n_c);
-      CK(cudaMemcpy(cc.data(), s.P.c, sizeof(double) * s.P.n_c, cudaMemcpyDeviceToHost));
-      std::vector<unsigned char> ow(s.P.n_c, 1);
-      if (s.P.owned) CK(cudaMemcpy(ow.data(), s.P.owned, s.P.n_c, cudaMemcpyDeviceToHost));
-      for (int c = 0; c < s.P.n_c; ++c)
-        if (ow[c]) nci += cc[c] * cc[c];
+    double nci = 0;  // |c|^2 of the iterated (scaled) c over the owners, on the host
+    for (int g = 0; g < nshards; ++g) {
+      const hsde_problem_desc &dg = descs[g];
+      for (int c = 0; c < dg.n_c; ++c) {
+        if (dg.owned && !dg.owned[c]) continue;
+        const double ci = sc == 1.0 ? dg.c[c] : sc * dg.c[c];
+        nci += ci * ci;
+      }
     }
     double *red = h->sh[0].W.red;
     for (auto &s : h->sh) CK(cudaMemset(s.W.red, 0, sizeof(double)));

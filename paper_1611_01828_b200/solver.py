@@ -497,16 +497,15 @@ class _Session:
         return HsdeState(self.mapper.up(u), self.mapper.up(w))
 
     def unscaled(self):
-        """Compressed unscaled iterate (solver.py:668-687)."""
-        u, w = self.raw_state()
+        """Compressed unscaled u (solver.py:668-687; the report reads u only)."""
+        u = self.h.get_u() if self.shards is None else self.raw_state()[0]
         cp = self.cp
         if self.sigma_c != 1.0 or self.sigma_b != 1.0:
-            for vec in (u, w):
-                vec[cp.sl_x] /= self.sigma_b
-                vec[cp.sl_s] /= self.sigma_b
-                vec[cp.sl_y] /= self.sigma_c
-                vec[cp.sl_v] /= self.sigma_c
-        return u, w
+            u[cp.sl_x] /= self.sigma_b
+            u[cp.sl_s] /= self.sigma_b
+            u[cp.sl_y] /= self.sigma_c
+            u[cp.sl_v] /= self.sigma_c
+        return u
 
 
 def _pattern_index(cp: CompressedProblem, dp):
@@ -522,9 +521,16 @@ def _pattern_index(cp: CompressedProblem, dp):
     else:
         edges = np.asarray(sorted(dp.aggregate.edges), dtype=np.int64).reshape(-1, 2)
     diag = np.arange(n, dtype=np.int64)
-    pairs = np.concatenate([np.asarray(edges, dtype=np.int64).reshape(-1, 2),
-                            np.stack([diag, diag], axis=1)])
-    code = np.unique(pairs[:, 0] * n + pairs[:, 1])
+    edges = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+    ecode = edges[:, 0] * n + edges[:, 1]
+    dcode = diag * (n + 1)
+    if ecode.size and bool(np.all(ecode[1:] > ecode[:-1])):
+        # sorted, unique edge codes (the usual case): merge the diagonal in O(N)
+        at = np.searchsorted(ecode, dcode)
+        present = ecode[np.minimum(at, ecode.size - 1)] == dcode
+        code = np.insert(ecode, at[~present], dcode[~present])
+    else:
+        code = np.unique(np.concatenate([ecode, dcode]))
     gi, gj = code // n, code % n
     flat = gj * n + gi
     pos = np.searchsorted(cp.covered, flat)
@@ -563,7 +569,7 @@ def _classify(sess: _Session, chk: np.ndarray, iterations: int, timing: Timing) 
     tau, kappa = float(chk[3]), float(chk[4])
     if tau > st.infeas_tau_tol:
         res = Residuals(primal=float(chk[0]), dual=float(chk[1]), gap=float(chk[2]))
-        u, _ = sess.unscaled()
+        u = sess.unscaled()
         xt = u[cp.sl_x] / tau
         yt = u[cp.sl_y] / tau
         vt = u[cp.sl_v] / tau
@@ -585,7 +591,7 @@ def _classify(sess: _Session, chk: np.ndarray, iterations: int, timing: Timing) 
         cert = sess.h.certificate()
         status = _cert_decision(cert, st.tol)
         if status is not None:
-            u, _ = sess.unscaled()
+            u = sess.unscaled()
             if status == STATUS_DUAL_INFEASIBLE:
                 by = float(cert[0])
                 yt, vt = u[cp.sl_y] / by, u[cp.sl_v] / by
