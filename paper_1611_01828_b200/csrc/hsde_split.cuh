@@ -45,6 +45,8 @@ constexpr int kSplitMaxPasses = 24;     // fixed-point passes before handing ove
 // (subspace coordinates): an error e moves P by ~ e |B|, below the rounding of
 // the d-term products themselves (~ d eps |B| = 1.8e-14 |B| at d = 80)
 constexpr double kSplitTol = 1e-15;
+// schedule key: off(B)^2 above kSplitKey2 of the bound marks a refresh candidate
+constexpr double kSplitKey2 = 0.25;
 
 __host__ __device__ inline int split_ld(int c) { return ((c + 11) & ~15) + 4; }
 
@@ -880,7 +882,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   if (tid == 0 && W.sweeps) W.sweeps[k] = -it;  // (stats: fixed-point iterations)
   // schedule key for the next iteration: passes, plus a refresh risk when off(B)
   // is already near the applicability bound
-  if (tid == 0) W.ckey[k] = o2 > 0.5 * kSplitOff2 * g * g ? 1 : 0;
+  if (tid == 0) W.ckey[k] = o2 > kSplitKey2 * kSplitOff2 * g * g ? 1 : 0;
   if (refreshed) return SPLIT_DONE + 16;  // (stats: after a Jacobi refresh)
   if (tid == 0 && it > ca.split_refresh) W.vvalid[k] |= kVRefresh;
   return SPLIT_DONE;
