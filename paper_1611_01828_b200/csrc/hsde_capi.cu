@@ -382,7 +382,7 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
     return e ? std::atoi(e) : 1;
   }();
   ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0, pl.pscratch, pl.pstride, 0,
-              split_refresh, split_vupdate, 0};
+              split_refresh, split_vupdate};
   if (!block) {
     const int grid = (pl.count + pl.per_block - 1) / pl.per_block;
     const int thr = pl.per_block * 32;

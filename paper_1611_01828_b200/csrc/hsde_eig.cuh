@@ -37,8 +37,7 @@ constexpr int kWarmMaxAge = 64;
 
 // k_cone_split -> k_cone_block hand-off states (DevWork::cstate, hsde_split.cuh)
 // (SPLIT_HANDOFF + 0/1/2: off(B) > g / 10 / r > n / the fixed point stalled)
-// SPLIT_EXPORTED: the Jacobi path refreshed V and handed B back (W.xarg)
-enum SplitState { SPLIT_DONE = 0, SPLIT_UNTOUCHED = 1, SPLIT_HANDOFF = 2, SPLIT_EXPORTED = 8 };
+enum SplitState { SPLIT_DONE = 0, SPLIT_UNTOUCHED = 1, SPLIT_HANDOFF = 2 };
 // vvalid bit: the fast path asks for a refreshed V (the next projection of the
 // clique runs in k_cone_block, warm, which rotates V)
 constexpr int kVRefresh = 1 << 30;
@@ -1206,7 +1205,6 @@ struct ConeArgs {
   int slot;         // this team's scratch slot
   int split_refresh; // k_cone_split: fixed-point iterations beyond which V is refreshed
   int split_vupdate; // k_cone_split: rotate V onto the new invariant subspaces
-  int split_export;  // CTA Jacobi path: stop at the class-split point and export B
 };
 
 // Hot-path load of slot j: builds arg_s and performs the v / w_v update and
@@ -1267,8 +1265,8 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   int cst = SPLIT_UNTOUCHED;
   if (MODE == CONE_HOT && kCta && W.cstate) {
     cst = W.cstate[k];
-    // finished by the fast path (also after a resume), or waiting for it
-    if (cst == SPLIT_DONE || cst >= SPLIT_DONE + 16 || cst == SPLIT_EXPORTED) return;
+    // finished by the fast path (also after a refresh, SPLIT_DONE + 16) or here
+    if (cst == SPLIT_DONE || cst >= SPLIT_DONE + 16) return;
   }
   const bool handoff = cst >= SPLIT_HANDOFF;  // A <- B = Vt X Vt' from W.xarg
   const int age = (MODE == CONE_HOT && ca.warm) ? (W.vvalid[k] & ~kVRefresh) : 0;
@@ -1353,19 +1351,6 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
           W.vstore[off + e] = js.Vt[a * ldv + bcol];
         }
         tm.sync();
-        if (ca.split_export) {
-          // hand B (= A, off(A) <= g / 10 in the refreshed basis) back to the
-          // k_cone_split fast path (hsde_split.cuh)
-          for (int e = tm.rank; e < d * d; e += tm.size()) {
-            const int a = e / d, bcol = e - a * d;
-            W.xarg[off + e] = A[a * lda + bcol];
-          }
-          if (tm.rank == 0) {
-            W.cstate[k] = SPLIT_EXPORTED;
-            if (W.sweeps) W.sweeps[k] = sw;
-          }
-          return;
-        }
         auto emit_split = [&](int a, int bcol, double v) {
           const int64_t j = so + off + (int64_t)a * d + bcol;
           S.u[j] = v;
@@ -1469,7 +1454,7 @@ __global__ void __launch_bounds__(kConeBlock, 2) k_cone_block(DevProblem P, DevS
   const int cst = (MODE == CONE_HOT && W.cstate) ? W.cstate[k] : -1;
   cone_one<MODE>(tm, P, S, W, c2, k, smem);
   // after k_cone_split: mark the cliques finished here (32 + the state they came in with)
-  if (MODE == CONE_HOT && W.cstate && threadIdx.x == 0 && (cst == SPLIT_UNTOUCHED ||
-      (cst >= SPLIT_HANDOFF && cst <= SPLIT_HANDOFF + 2)) && W.cstate[k] != SPLIT_EXPORTED)
+  if (MODE == CONE_HOT && W.cstate && threadIdx.x == 0 &&
+      (cst == SPLIT_UNTOUCHED || (cst >= SPLIT_HANDOFF && cst <= SPLIT_HANDOFF + 2)))
     W.cstate[k] = SPLIT_DONE + 32 + cst;
 }

@@ -45,6 +45,7 @@ constexpr int kSplitMaxPasses = 24;     // fixed-point passes before handing ove
 // (subspace coordinates): an error e moves P by ~ e |B|, below the rounding of
 // the d-term products themselves (~ d eps |B| = 1.8e-14 |B| at d = 80)
 constexpr double kSplitTol = 1e-15;
+constexpr double kSplitStall = 0.8;  // pass-to-pass ratio taken as a stall
 // schedule key: off(B)^2 above kSplitKey2 of the bound marks a refresh candidate
 constexpr double kSplitKey2 = 0.25;
 
@@ -283,7 +284,7 @@ __device__ __forceinline__ double red_total(const double *red, int nw) {
 // The fast path for clique k (argument load included).  Returns SPLIT_DONE,
 // or a hand-off code with B = Vt X Vt' (original order) written to W.xarg.
 __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &W, const ConeArgs &ca, int k,
-                         double *smem, bool resume) {
+                         double *smem) {
   const int d = P.cl_size[k];
   const int tid = threadIdx.x, T = blockDim.x;
   const int64_t off = P.cl_off[k], so = P.n_c;
@@ -299,7 +300,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   bool refreshed = false;  // (stats) Jacobi sweeps refreshed the basis in this call
   SPLIT_STAMP(0);
 
-  if (!resume) {
+  {
   // ---- argument X (hot-path slot update, solver.py:222-244, :316, :388-394),
     //      kLoadBatch slots per thread at a time: every load of the batch is
     //      issued before the first store (the stores may alias later loads)
@@ -376,23 +377,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     bi0[s] = bi * 16;
     bj0[s] = bj * 16;
   }
-  if (resume) {
-    // B handed back by the Jacobi path (basis refreshed, V in the store)
-#pragma unroll
-    for (int s = 0; s < kSplitMaxB; ++s)
-      if (w + s * nw < nbu) {
-        const int q = lane >> 2, kk = lane & 3;
-#pragma unroll
-        for (int a2 = 0; a2 < 2; ++a2)
-#pragma unroll
-          for (int b2 = 0; b2 < 2; ++b2)
-#pragma unroll
-            for (int e2 = 0; e2 < 2; ++e2) {
-              const int i = min(bi0[s] + 8 * a2 + q, d - 1), j = min(bj0[s] + 8 * b2 + 2 * kk + e2, d - 1);
-              cb[s][a2][b2][e2] = xg[i * d + j];
-            }
-      }
-  } else {
+  {
   for (int e = tid; e < d * d; e += T) {
     const int a = qdiv(e, invd), b = e - a * d;
     xg[e] = R1[a * L + b];
@@ -447,7 +432,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     }
     __syncthreads();
   }
-  }  // !resume
+  }
   SPLIT_STAMP(2);
 
   // ---- diagonal, g = min |diag|, off(B)^2 (upper values, mirrored)
@@ -669,8 +654,11 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     const double delta = sqrt(red_total(red, nw));
     if (newy) yb ^= 1;
     const double rho = delta / prev;
-    if (delta == 0.0 || (rho < 0.5 && delta * rho <= kSplitTol * (1.0 - rho))) ok = true;
-    else if (!(rho < 0.5)) break;  // stalled (or NaN)
+    // converged: the estimated remaining error delta rho / (1 - rho) is below the
+    // tolerance, or the increment itself is at the rounding level; stalled: no
+    // contraction (or NaN) -- the pass budget bounds slow contraction
+    if (delta <= 0.1 * kSplitTol || (rho < kSplitStall && delta * rho <= kSplitTol * (1.0 - rho))) ok = true;
+    else if (!(rho < kSplitStall)) break;
     prev = delta;
     __syncthreads();  // red is rewritten by the next pass
   }
@@ -901,7 +889,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, D
   ConeArgs c2 = ca;
   c2.slot = blockIdx.x;
   int st = SPLIT_UNTOUCHED;
-  if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d > 32) st = split_one(P, S, W, c2, k, smem, false);
+  if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d > 32) st = split_one(P, S, W, c2, k, smem);
   if (threadIdx.x == 0) W.cstate[k] = st;
   if (st == SPLIT_DONE || st == SPLIT_DONE + 16) return;
   __syncthreads();  // cstate and the hand-off B are visible to the whole CTA

@@ -1,0 +1,25 @@
+"""Per-iteration graph time and fast-path statistics of the first iterations.
+
+    python tools/early_iters.py [--config 4] [--iters 40]
+"""
+import argparse
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from paper_1611_01828_b200 import _lib  # noqa: E402
+from paper_1611_01828_b200.synthetic import make_config  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=4)
+ap.add_argument("--iters", type=int, default=40)
+a = ap.parse_args()
+h = _lib.Handle(make_config(a.config))
+for i in range(a.iters):
+    ms = h.time_iterations(1)
+    st = h.stats()
+    print(i + 1, round(ms, 3), {k: round(v, 3) for k, v in st.items() if k in (
+        "mean_sweeps_large", "split_done", "split_fp_iters", "split_resumed", "handoff_off", "handoff_stall")},
+        flush=True)
+h.close()
