@@ -41,6 +41,8 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 using namespace hsde;
 
@@ -1238,6 +1240,82 @@ int build_csc_device(hsde_handle *h, int m, int n_c, int64_t nnz, const int64_t 
   return 0;
 }
 
+// Cover lists on the device (the host loop took ~18 ms on config 4's 2.56M
+// slots): cov_slot = slots sorted by covered coordinate, ascending slot within
+// a coordinate (stable radix sort: bincount order, graphs.py:228), cov_ptr
+// from the integer counts, p_inv = 1 / (1 + D/2) (solver.py:250) unless the
+// global cover counts are given, and the heavy coordinates (> kHeavy slots)
+// in ascending order.
+__global__ void k_cov_finish(const unsigned long long *cnt, int n_c, int *cov_ptr, const double *cover_counts,
+                             double *p_inv, unsigned char *heavy_flag) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= n_c; c += gridDim.x * blockDim.x) {
+    cov_ptr[c] = (int)cnt[c];
+    if (c == n_c) continue;
+    const int k = (int)(cnt[c + 1] - cnt[c]);
+    const double D = cover_counts ? cover_counts[c] : (double)k;
+    p_inv[c] = 1.0 / (1.0 + 0.5 * D);
+    heavy_flag[c] = k > kHeavy;
+  }
+}
+
+int build_covers_device(hsde_handle *h, int n_c, int64_t n_d, const int *slot_cov, const double *cover_counts_d,
+                        int **cov_ptr, int **cov_slot, double **p_inv, int **heavy, int *n_heavy) {
+  RC(dalloc(h, cov_ptr, n_c + 1));
+  RC(dalloc(h, cov_slot, std::max<int64_t>(n_d, 1)));
+  RC(dalloc(h, p_inv, std::max(n_c, 1)));
+  unsigned long long *cnt = nullptr;
+  unsigned char *flag = nullptr;
+  int *idx = nullptr, *keys_out = nullptr, *hv = nullptr, *nsel = nullptr;
+  void *tmp = nullptr;
+  CK(pool_malloc(h, (void **)&cnt, sizeof(unsigned long long) * (n_c + 1)));
+  CK(pool_malloc(h, (void **)&flag, std::max(n_c, 1)));
+  CK(pool_malloc(h, (void **)&hv, sizeof(int) * std::max(n_c, 1)));
+  CK(pool_malloc(h, (void **)&nsel, sizeof(int)));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (n_c + 1), h->st));
+  const int g = 148 * 8;
+  if (n_d > 0) {
+    if (n_d > INT32_MAX) {
+      h->err = "more than 2^31 clique slots are not supported";
+      return HSDE_ERR_ARG;
+    }
+    k_col_count<<<g, kBlock, 0, h->st>>>(slot_cov, n_d, cnt);
+    CKL();
+  }
+  size_t tb = 0, tb2 = 0, tb3 = 0;
+  int end_bit = 1;
+  while ((1ll << end_bit) < (long long)n_c) ++end_bit;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, cnt, cnt, n_c + 1, h->st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb2, slot_cov, keys_out, idx, *cov_slot, (int)n_d, 0, end_bit, h->st);
+  cub::DeviceSelect::Flagged(nullptr, tb3, cub::CountingInputIterator<int>(0), flag, hv, nsel, n_c, h->st);
+  CK(pool_malloc(h, (void **)&tmp, std::max(tb, std::max(tb2, tb3))));
+  CK(pool_malloc(h, (void **)&idx, sizeof(int) * std::max<int64_t>(n_d, 1)));
+  CK(pool_malloc(h, (void **)&keys_out, sizeof(int) * std::max<int64_t>(n_d, 1)));
+  cub::DeviceScan::InclusiveSum(tmp, tb, cnt, cnt, n_c + 1, h->st);
+  if (n_d > 0) {
+    k_iota<<<g, kBlock, 0, h->st>>>(idx, n_d);
+    CKL();
+    cub::DeviceRadixSort::SortPairs(tmp, tb2, slot_cov, keys_out, idx, *cov_slot, (int)n_d, 0, end_bit, h->st);
+  }
+  k_cov_finish<<<grid_for(n_c + 1), kBlock, 0, h->st>>>(cnt, n_c, *cov_ptr, cover_counts_d, *p_inv, flag);
+  CKL();
+  cub::DeviceSelect::Flagged(tmp, tb3, cub::CountingInputIterator<int>(0), flag, hv, nsel, n_c, h->st);
+  int nh = 0;
+  CK(cudaMemcpyAsync(&nh, nsel, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  RC(dalloc(h, heavy, std::max(nh, 1)));
+  if (nh) CK(cudaMemcpyAsync(*heavy, hv, sizeof(int) * nh, cudaMemcpyDeviceToDevice, h->st));
+  *n_heavy = nh;
+  CK(cudaStreamSynchronize(h->st));
+  pool_free(h, tmp);
+  pool_free(h, idx);
+  pool_free(h, keys_out);
+  pool_free(h, cnt);
+  pool_free(h, flag);
+  pool_free(h, hv);
+  pool_free(h, nsel);
+  return 0;
+}
+
 #include "hsde_setup_half.cuh"
 
 int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
@@ -1327,22 +1405,8 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   }
   row_seg[m] = (int)seg_row.size();
   tick("  host CSR+segments");
-  // cover lists (stable by slot) and cover counts D
-  std::vector<int> cov_ptr(n_c + 1, 0), cov_slot(n_d);
-  for (int64_t j = 0; j < n_d; ++j) cov_ptr[d->slot_cov[j] + 1]++;
-  for (int c = 0; c < n_c; ++c) cov_ptr[c + 1] += cov_ptr[c];
-  {
-    std::vector<int> pos(cov_ptr.begin(), cov_ptr.end() - 1);
-    for (int64_t j = 0; j < n_d; ++j) cov_slot[pos[d->slot_cov[j]]++] = (int)j;
-  }
-  std::vector<int> heavy;
-  for (int c = 0; c < n_c; ++c)
-    if (cov_ptr[c + 1] - cov_ptr[c] > kHeavy) heavy.push_back(c);
-  std::vector<double> p_inv(n_c);
-  for (int c = 0; c < n_c; ++c) {
-    const double D = d->cover_counts ? d->cover_counts[c] : (double)(cov_ptr[c + 1] - cov_ptr[c]);
-    p_inv[c] = 1.0 / (1.0 + 0.5 * D);  // solver.py:250 (global cover counts)
-  }
+  // cover lists, cover counts D, P^{-1} and the heavy coordinates: on the device
+  // (build_covers_device) after slot_cov is uploaded
   std::vector<int> sep_of;
   if (d->n_sep > 0) {
     sep_of.assign(n_c, -1);
@@ -1375,15 +1439,21 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   RC(dupload(h, &seg_row_d, seg_row.data(), seg_row.size()));
   RC(dupload(h, &seg_beg_d, seg_beg.data(), seg_beg.size()));
   RC(dupload(h, &row_seg_d, row_seg.data(), m + 1));
-  RC(dupload(h, &cov_ptr_d, cov_ptr.data(), n_c + 1));
-  RC(dupload(h, &cov_slot_d, cov_slot.data(), n_d));
   RC(dupload(h, &slot_cov_d, d->slot_cov, n_d));
+  int n_heavy = 0;
+  {
+    double *cc_d = nullptr;  // global cover counts (sharded runs), temporary
+    if (d->cover_counts) {
+      CK(pool_malloc(h, (void **)&cc_d, sizeof(double) * std::max(n_c, 1)));
+      CK(cudaMemcpy(cc_d, d->cover_counts, sizeof(double) * n_c, cudaMemcpyHostToDevice));
+    }
+    RC(build_covers_device(h, n_c, n_d, slot_cov_d, cc_d, &cov_ptr_d, &cov_slot_d, &pinv_d, &heavy_d, &n_heavy));
+    if (cc_d) pool_free(h, cc_d);
+  }
   RC(dupload(h, &cl_off, d->clique_offsets, p + 1));
   RC(dupload(h, &cl_size, d->clique_sizes, p));
-  RC(dupload(h, &pinv_d, p_inv.data(), n_c));
   RC(dupload(h, &s.d_c_orig, d->c, n_c));
   RC(dupload(h, &s.d_b_orig, d->b, m));
-  RC(dupload(h, &heavy_d, heavy.data(), heavy.size()));
   if (d->owned) {
     RC(dupload(h, &owned_d, owned.data(), n_c));
     P.owned = owned_d;
@@ -1412,7 +1482,7 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   P.cl_size = cl_size;
   P.p_inv = pinv_d;
   P.heavy = heavy_d;
-  P.n_heavy = (int)heavy.size();
+  P.n_heavy = n_heavy;
   tick("  uploads");
   RC(build_half(h, s));
   tick("  half-pass layouts");
