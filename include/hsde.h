@@ -207,6 +207,11 @@ int hsde_pattern_cliques(const hsde_pattern_t *p, int64_t *ptr, int32_t *nodes);
 /* fill edges (a < b) in the order the elimination added them */
 int hsde_pattern_fill(const hsde_pattern_t *p, int32_t *fi, int32_t *fj);
 void hsde_pattern_destroy(hsde_pattern_t *p);
+/* pos[q] = first i with covered[i] >= col[q] * n + row[q] (covered sorted): the
+ * report's lookup of the pattern entries in the covered layout
+ * (solver.py:443-452; replaces np.searchsorted), O(nq + n_covered), host only. */
+int hsde_pattern_positions(const int64_t *covered, int64_t n_covered, int64_t n, const int64_t *row,
+                           const int64_t *col, int64_t nq, int64_t *pos);
 
 /* ---- SDPA sparse-format reader (no GPU needed) -----
  * Replaces chordalsdp/sdpa.py:94-234 parse_sdpa.  text[0..len) is the file

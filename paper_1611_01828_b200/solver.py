@@ -533,7 +533,7 @@ def _pattern_index(cp: CompressedProblem, dp):
         code = np.unique(np.concatenate([ecode, dcode]))
     gi, gj = code // n, code % n
     flat = gj * n + gi
-    pos = np.searchsorted(cp.covered, flat)
+    pos = _lib.pattern_positions(cp.covered, n, gi, gj)  # = np.searchsorted(cp.covered, flat)
     pos_c = np.minimum(pos, max(cp.N_c - 1, 0))
     hit = (pos < cp.N_c) & (cp.covered[pos_c] == flat) if cp.N_c else np.zeros(flat.size, bool)
     dims = np.abs(np.asarray(cp.block_dims or (n,), dtype=np.int64))
