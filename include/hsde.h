@@ -207,11 +207,14 @@ int hsde_pattern_cliques(const hsde_pattern_t *p, int64_t *ptr, int32_t *nodes);
 /* fill edges (a < b) in the order the elimination added them */
 int hsde_pattern_fill(const hsde_pattern_t *p, int32_t *fi, int32_t *fj);
 void hsde_pattern_destroy(hsde_pattern_t *p);
-/* pos[q] = first i with covered[i] >= col[q] * n + row[q] (covered sorted): the
- * report's lookup of the pattern entries in the covered layout
- * (solver.py:443-452; replaces np.searchsorted), O(nq + n_covered), host only. */
-int hsde_pattern_positions(const int64_t *covered, int64_t n_covered, int64_t n, const int64_t *row,
-                           const int64_t *col, int64_t nq, int64_t *pos);
+/* The report's pattern index (solver.py:443-452 on the compressed layout): for the
+ * sorted codes gi * n + gj of the aggregate pattern plus the diagonal, the 1-based
+ * block and block-local (i, j), the position of the flat id gj * n + gi in the
+ * sorted `covered` (clamped) and whether it is there.  Replaces np.searchsorted and
+ * friends in the report; O(nq + n_covered), host only. */
+int hsde_pattern_index(const int64_t *covered, int64_t n_covered, int64_t n, const int64_t *code, int64_t nq,
+                       const int64_t *starts, int32_t nblocks, int64_t *block, int64_t *li, int64_t *lj,
+                       int64_t *pos_c, uint8_t *hit);
 
 /* ---- SDPA sparse-format reader (no GPU needed) -----
  * Replaces chordalsdp/sdpa.py:94-234 parse_sdpa.  text[0..len) is the file

@@ -36,7 +36,7 @@ EXPORTED = (
     "hsde_nccl_unique_id", "hsde_shard_total", "hsde_set_state_shard", "hsde_get_state_shard",
     "hsde_debug_jacobi", "hsde_pattern_decompose", "hsde_pattern_sizes", "hsde_pattern_cliques",
     "hsde_pattern_fill", "hsde_pattern_destroy", "hsde_sdpa_parse", "hsde_sdpa_error",
-    "hsde_sdpa_sizes", "hsde_sdpa_data", "hsde_sdpa_destroy", "hsde_pattern_positions",
+    "hsde_sdpa_sizes", "hsde_sdpa_data", "hsde_sdpa_destroy", "hsde_pattern_index",
 )
 HSDE_NCCL_ID_BYTES = 128
 
@@ -134,7 +134,8 @@ def load() -> C.CDLL:
         "hsde_sdpa_sizes": (C.c_int, [vp, _i32p, _i32p, _i64p]),
         "hsde_sdpa_data": (C.c_int, [vp, _i32p, _dp, _i32p, _i32p, _i32p, _i32p, _dp]),
         "hsde_sdpa_destroy": (None, [vp]),
-        "hsde_pattern_positions": (C.c_int, [_i64p, C.c_int64, C.c_int64, _i64p, _i64p, C.c_int64, _i64p]),
+        "hsde_pattern_index": (C.c_int, [_i64p, C.c_int64, C.c_int64, _i64p, C.c_int64, _i64p, C.c_int32,
+                                         _i64p, _i64p, _i64p, _i64p, C.POINTER(C.c_uint8)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -408,14 +409,16 @@ def default_device() -> int:
     return int(os.environ.get("HSDE_DEVICE", os.environ.get("LOCAL_RANK", "0")))
 
 
-def pattern_positions(covered: np.ndarray, n: int, row: np.ndarray, col: np.ndarray) -> np.ndarray:
-    """np.searchsorted(covered, col * n + row) in O(len(row) + len(covered)) (library, host)."""
+def pattern_index(covered: np.ndarray, n: int, code: np.ndarray, starts: np.ndarray):
+    """(block, i, j, pos_c, hit) of the report's pattern rows (library, host; O(N))."""
     cov = np.ascontiguousarray(covered, dtype=np.int64)
-    r = np.ascontiguousarray(row, dtype=np.int64)
-    c = np.ascontiguousarray(col, dtype=np.int64)
-    out = np.empty(r.size, dtype=np.int64)
-    rc = load().hsde_pattern_positions(_ptr(cov, C.c_int64), cov.size, int(n), _ptr(r, C.c_int64),
-                                       _ptr(c, C.c_int64), r.size, _ptr(out, C.c_int64))
+    cd = np.ascontiguousarray(code, dtype=np.int64)
+    st = np.ascontiguousarray(starts, dtype=np.int64)
+    outs = [np.empty(cd.size, dtype=np.int64) for _ in range(4)]
+    hit = np.empty(cd.size, dtype=np.uint8)
+    rc = load().hsde_pattern_index(_ptr(cov, C.c_int64), cov.size, int(n), _ptr(cd, C.c_int64), cd.size,
+                                   _ptr(st, C.c_int64), st.size - 1, *[_ptr(o, C.c_int64) for o in outs],
+                                   _ptr(hit, C.c_uint8))
     if rc:
-        raise ValueError("hsde_pattern_positions: bad arguments")
-    return out
+        raise ValueError("hsde_pattern_index: bad arguments")
+    return outs[0], outs[1], outs[2], outs[3], hit.view(bool)

@@ -304,39 +304,53 @@ int hsde_pattern_fill(const hsde_pattern_t *p, int32_t *fi, int32_t *fj) {
 
 void hsde_pattern_destroy(hsde_pattern_t *p) { delete p; }
 
-// pos[q] = first index i with covered[i] >= col[q] * n + row[q] (np.searchsorted,
-// side="left", on the column-major flat id), covered sorted: the report's
-// lookup of the pattern entries in the covered layout (solver.py:443-452
-// restated on the compressed layout).  O(nq + n_covered): the needles are
+// The report's pattern index (solver.py:443-452 restated on the compressed
+// layout): for the sorted codes gi * n + gj of the aggregate pattern plus the
+// diagonal, the block (1-based), the block-local (i, j) (1-based), and where
+// the column-major flat id gj * n + gi sits in the sorted `covered` (pos_c,
+// clamped) and whether it is there (hit).  O(nq + n_covered): the lookups are
 // bucketed by column (stable), the column ranges of `covered` found in one
-// pass, and each column merged with a forward pointer (a binary search where a
-// column's rows do not ascend).
-int hsde_pattern_positions(const int64_t *covered, int64_t n_covered, int64_t n, const int64_t *row,
-                           const int64_t *col, int64_t nq, int64_t *pos) {
-  if (n < 0 || n_covered < 0 || nq < 0 || (n_covered && !covered) || (nq && (!row || !col || !pos)))
+// pass, and each column merged with a forward pointer (a binary search where
+// a column's rows do not ascend).  starts[0..nblocks] are the block offsets.
+int hsde_pattern_index(const int64_t *covered, int64_t n_covered, int64_t n, const int64_t *code, int64_t nq,
+                       const int64_t *starts, int32_t nblocks, int64_t *block, int64_t *li, int64_t *lj,
+                       int64_t *pos_c, uint8_t *hit) {
+  if (n <= 0 || n_covered < 0 || nq < 0 || nblocks < 1 || !starts || (n_covered && !covered) ||
+      (nq && (!code || !block || !li || !lj || !pos_c || !hit)))
     return HSDE_ERR_ARG;
-  for (int64_t q = 0; q < nq; ++q)
-    if (col[q] < 0 || col[q] >= n || row[q] < 0 || row[q] >= n) return HSDE_ERR_ARG;
   std::vector<int64_t> cstart(n + 1), cnt(n + 1, 0), order(nq);
+  for (int64_t q = 0; q < nq; ++q) {
+    if (code[q] < 0 || code[q] >= n * n) return HSDE_ERR_ARG;
+    ++cnt[code[q] % n + 1];
+  }
   for (int64_t c = 0, i = 0; c <= n; ++c) {  // first covered index of column c
     while (i < n_covered && covered[i] < c * n) ++i;
     cstart[c] = i;
   }
-  for (int64_t q = 0; q < nq; ++q) ++cnt[col[q] + 1];
   for (int64_t c = 0; c < n; ++c) cnt[c + 1] += cnt[c];
   {
     std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
-    for (int64_t q = 0; q < nq; ++q) order[fill[col[q]]++] = q;
+    for (int64_t q = 0; q < nq; ++q) order[fill[code[q] % n]++] = q;
   }
+  auto block_of = [&](int64_t x) {
+    return (int64_t)(std::upper_bound(starts, starts + nblocks + 1, x) - starts) - 1;
+  };
   for (int64_t c = 0; c < n; ++c) {
     int64_t i = cstart[c], prev = -1;
     const int64_t end = cstart[c + 1];
+    const int64_t bc = block_of(c);
     for (int64_t t = cnt[c]; t < cnt[c + 1]; ++t) {
-      const int64_t q = order[t], key = c * n + row[q];
-      if (row[q] < prev) i = std::lower_bound(covered + cstart[c], covered + end, key) - covered;
+      const int64_t q = order[t], r = code[q] / n, key = c * n + r;  // (gi, gj) = (r, c)
+      if (r < prev) i = std::lower_bound(covered + cstart[c], covered + end, key) - covered;
       while (i < end && covered[i] < key) ++i;
-      pos[q] = i;
-      prev = row[q];
+      prev = r;
+      const int64_t pc = std::min(i, std::max<int64_t>(n_covered - 1, 0));
+      pos_c[q] = pc;
+      hit[q] = i < n_covered && covered[pc] == key;
+      const int64_t br = block_of(r);
+      block[q] = br + 1;
+      li[q] = r - starts[br] + 1;
+      lj[q] = c - starts[bc] + 1;
     }
   }
   return HSDE_OK;

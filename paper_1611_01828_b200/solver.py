@@ -531,16 +531,11 @@ def _pattern_index(cp: CompressedProblem, dp):
         code = np.insert(ecode, at[~present], dcode[~present])
     else:
         code = np.unique(np.concatenate([ecode, dcode]))
-    gi, gj = code // n, code % n
-    flat = gj * n + gi
-    pos = _lib.pattern_positions(cp.covered, n, gi, gj)  # = np.searchsorted(cp.covered, flat)
-    pos_c = np.minimum(pos, max(cp.N_c - 1, 0))
-    hit = (pos < cp.N_c) & (cp.covered[pos_c] == flat) if cp.N_c else np.zeros(flat.size, bool)
     dims = np.abs(np.asarray(cp.block_dims or (n,), dtype=np.int64))
     starts = np.concatenate([[0], np.cumsum(dims)])
-    bi = np.searchsorted(starts, gi, side="right") - 1
-    bj = np.searchsorted(starts, gj, side="right") - 1
-    out = (bi + 1, gi - starts[bi] + 1, gj - starts[bj] + 1, pos_c, hit)
+    # block, block-local (i, j), and the covered position of the flat id
+    # gj * n + gi (= np.searchsorted(cp.covered, gj * n + gi)), in the library
+    out = _lib.pattern_index(cp.covered, n, code, starts)
     cp._cache[key] = out
     return out
 

@@ -73,3 +73,30 @@ def test_decompose_matches_reference_compressed(golden_dir):
         assert np.array_equal(cp.sizes, z[pre + "clique_sizes"]), t
         assert np.array_equal(cp.slot_cov, z[pre + "slot_cov"]), t
         assert np.array_equal(cp.aggregate_edges, z[pre + "aggregate_edges"]), t
+
+
+def test_report_pattern_index_matches_numpy(golden_dir):
+    """The library's pattern index (hsde_pattern_index) equals the numpy
+    restatement of solver.py:443-452 on the reference's multi-block problems."""
+    from paper_1611_01828_b200 import solver as S
+
+    z = np.load(golden_dir / "decompose.npz")
+    for t in range(int(z["n_problems"])):
+        cp = decompose(_problem(z, f"p{t}_"))
+        n = cp.n
+        edges = cp.aggregate_edges if cp.aggregate_edges is not None else np.zeros((0, 2), np.int64)
+        diag = np.arange(n, dtype=np.int64)
+        pairs = np.concatenate([np.asarray(edges, dtype=np.int64).reshape(-1, 2), np.stack([diag, diag], 1)])
+        code = np.unique(pairs[:, 0] * n + pairs[:, 1])
+        gi, gj = code // n, code % n
+        flat = gj * n + gi
+        pos = np.searchsorted(cp.covered, flat)
+        pos_c = np.minimum(pos, max(cp.N_c - 1, 0))
+        hit = (pos < cp.N_c) & (cp.covered[pos_c] == flat)
+        starts = np.concatenate([[0], np.cumsum(np.abs(np.asarray(cp.block_dims or (n,))))])
+        bi = np.searchsorted(starts, gi, side="right") - 1
+        bj = np.searchsorted(starts, gj, side="right") - 1
+        want = (bi + 1, gi - starts[bi] + 1, gj - starts[bj] + 1, pos_c, hit)
+        got = S._pattern_index(cp, cp)
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b), t
