@@ -241,7 +241,7 @@ int h2d_staged(hsde_handle *h, void *dst, const void *src, size_t bytes) {
       }
     CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   }
-  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   const char *s8 = static_cast<const char *>(src);
   char *d8 = static_cast<char *>(dst);
   bool used[2] = {false, false};
