@@ -358,21 +358,34 @@ def run_ours(args):
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        t0 = time.perf_counter()
-        # a fresh NCCL unique id per communicator
-        rep = H.solve_decomposed(cp, H.SolverSettings(device=dev),
-                                 comm=init_comm() if comm is not None else None)
-        wall = time.perf_counter() - t0
+        # three complete solves (each: H2D + setup + solve + report); the median
+        # wall is reported (the host-side setup varies run to run), all three listed
+        walls, reps = [], []
+        for _ in range(3):
+            cp._cache.pop("pattern_index", None)  # each solve builds its report from scratch
+            if dist:
+                dist.barrier()
+            t0 = time.perf_counter()
+            # a fresh NCCL unique id per communicator
+            reps.append(H.solve_decomposed(cp, H.SolverSettings(device=dev),
+                                           comm=init_comm() if comm is not None else None))
+            walls.append(time.perf_counter() - t0)
+        mid = int(np.argsort(walls)[1])
+        rep, wall = reps[mid], walls[mid]
     if rank == 0 and not args.no_e2e:
-        nbytes = (cp.A.data.nbytes + cp.A.indices.nbytes // 2 + 8 * (cp.m + 1) + 8 * cp.N_c
+        # host -> device: A (CSR: fp64 values, int32 columns, int64 row pointers), c, b,
+        # clique offsets / sizes, slot -> covered map; device -> host: the checks and u
+        nbytes = (cp.A.data.nbytes + 4 * cp.A.nnz + 8 * (cp.m + 1) + 8 * cp.N_c
                   + 8 * cp.m + 8 * (cp.p + 1) + 4 * cp.p + 4 * cp.n_d)
         checks = (rep.iterations + 19) // 20
-        d2h = checks * 8 * 16 + 8 * 2 * (cp.total)
+        d2h = checks * 8 * 16 + 8 * cp.total
         line["e2e"] = {"value": rep.iterations / wall, "unit": "iterations/s",
                        "h2d_bytes_per_step": int(nbytes / max(rep.iterations, 1)),
                        "d2h_bytes_per_step": int(d2h / max(rep.iterations, 1)),
+                       "walls_s": [round(x, 4) for x in walls],
                        "what": "solve_decomposed(CompressedProblem on host, default settings) "
-                               "wall clock: H2D + device setup + solve to 1e-4 + report"}
+                               "wall clock, median of 3 solves: H2D + device setup + solve to "
+                               "1e-4 + report"}
         line["time_to_tol"] = {"status": rep.status, "iterations": rep.iterations,
                                "iterations_s": rep.timing.iterations_s,
                                "setup_s": rep.timing.setup_s, "wall_s": wall,
