@@ -1657,7 +1657,8 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
   CK(cudaStreamSynchronize(h->st));
   h->schur_diag = gv[1] == 0.0;
   for (auto &s : h->sh)
-    s.grid_schur = h->schur_diag ? grid_for(m, 64) : std::min(148 * 4, std::max(1, (m + 7) / 8));
+    s.grid_schur = h->schur_diag ? grid_for(m, 64)
+                                 : std::min(148 * 8, std::max(1, (m + 1) / ((kBlock / 32) / kSchurSplit)));
   const double *bsrc = descs[0].b;
   double nb2 = 0;
   for (int i = 0; i < m; ++i) nb2 += bsrc[i] * bsrc[i];

@@ -303,6 +303,8 @@ __global__ void __launch_bounds__(kBlock) k_spmv_seg(DevProblem P, const double 
 // g = S^{-1} (q0 - rho_y).  Every CTA rebuilds q0 - rho_y from the segment
 // partials (ordered) into shared memory, then one warp per output row of the
 // symmetric inverse.
+constexpr int kSchurSplit = 4;  // warps per row of the dense S^-1 apply
+
 __global__ void __launch_bounds__(kBlock) k_schur(DevProblem P, const double *__restrict__ qseg,
                                                    const double *__restrict__ qfull,
                                                    const double *__restrict__ ry,
@@ -323,22 +325,40 @@ __global__ void __launch_bounds__(kBlock) k_schur(DevProblem P, const double *__
       g[i] = qs[i] * P.sinv[i];
     return;
   }
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < P.m; i += warps) {
-    const double *row = P.sinv + (int64_t)i * P.m;
-    // four independent partial sums: four row loads in flight per lane
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int j = lane;
-    for (; j + 96 < P.m; j += 128) {
-      a0 += __ldcs(row + j) * qs[j];
-      a1 += __ldcs(row + j + 32) * qs[j + 32];
-      a2 += __ldcs(row + j + 64) * qs[j + 64];
-      a3 += __ldcs(row + j + 96) * qs[j + 96];
+  // kSchurSplit warps per row (contiguous column segments), rows in pairs per
+  // CTA: enough warps in flight for a latency-bound m x m apply; partials
+  // summed in fixed order
+  __shared__ double part[kBlock / 32];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int rows_per_cta = (kBlock / 32) / kSchurSplit, seg = wq % kSchurSplit;
+  const int seg_len = (P.m + kSchurSplit - 1) / kSchurSplit;
+  const int j0 = seg * seg_len, j1 = min(P.m, j0 + seg_len);
+  for (int base = blockIdx.x * rows_per_cta; base < P.m; base += gridDim.x * rows_per_cta) {
+    const int i = base + wq / kSchurSplit;
+    double a[4] = {0.0, 0.0, 0.0, 0.0};
+    if (i < P.m) {
+      // S^-1 (m^2 doubles) is read with cached loads: it stays in L2 across
+      // iterations while the A passes stream with evict-first loads
+      const double *row = P.sinv + (int64_t)i * P.m;
+      int j = j0 + lane;
+      for (; j + 96 < j1; j += 128) {
+        double r4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) r4[u] = __ldg(row + j + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] += r4[u] * qs[j + 32 * u];
+      }
+      for (; j < j1; j += 32) a[0] += __ldg(row + j) * qs[j];
     }
-    for (; j < P.m; j += 32) a0 += __ldcs(row + j) * qs[j];
-    const double acc = warp_sum((a0 + a1) + (a2 + a3));
-    if (lane == 0) g[i] = acc;
+    const double acc = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
+    if (lane == 0) part[wq] = acc;
+    __syncthreads();
+    if (seg == 0 && lane == 0 && i < P.m) {
+      double t = 0.0;
+      for (int q = 0; q < kSchurSplit; ++q) t += part[wq + q];
+      g[i] = t;
+    }
+    __syncthreads();
   }
 }
 
