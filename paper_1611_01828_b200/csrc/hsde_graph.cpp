@@ -308,50 +308,43 @@ void hsde_pattern_destroy(hsde_pattern_t *p) { delete p; }
 // layout): for the sorted codes gi * n + gj of the aggregate pattern plus the
 // diagonal, the block (1-based), the block-local (i, j) (1-based), and where
 // the column-major flat id gj * n + gi sits in the sorted `covered` (pos_c,
-// clamped) and whether it is there (hit).  O(nq + n_covered): the lookups are
-// bucketed by column (stable), the column ranges of `covered` found in one
-// pass, and each column merged with a forward pointer (a binary search where
-// a column's rows do not ascend).  starts[0..nblocks] are the block offsets.
+// clamped) and whether it is there (hit).  One pass in code order: the row gi
+// never decreases, so within every column gj the looked-up keys ascend and a
+// per-column pointer into `covered` only moves forward -- O(nq + n_covered),
+// sequential output.  starts[0..nblocks] are the block offsets.
 int hsde_pattern_index(const int64_t *covered, int64_t n_covered, int64_t n, const int64_t *code, int64_t nq,
                        const int64_t *starts, int32_t nblocks, int64_t *block, int64_t *li, int64_t *lj,
                        int64_t *pos_c, uint8_t *hit) {
   if (n <= 0 || n_covered < 0 || nq < 0 || nblocks < 1 || !starts || (n_covered && !covered) ||
       (nq && (!code || !block || !li || !lj || !pos_c || !hit)))
     return HSDE_ERR_ARG;
-  std::vector<int64_t> cstart(n + 1), cnt(n + 1, 0), order(nq);
-  for (int64_t q = 0; q < nq; ++q) {
-    if (code[q] < 0 || code[q] >= n * n) return HSDE_ERR_ARG;
-    ++cnt[code[q] % n + 1];
-  }
+  for (int64_t q = 0; q < nq; ++q)
+    if (code[q] < 0 || code[q] >= n * n || (q && code[q] <= code[q - 1])) return HSDE_ERR_ARG;  // sorted, unique
+  std::vector<int64_t> ptr(n + 1), cblock(n);
   for (int64_t c = 0, i = 0; c <= n; ++c) {  // first covered index of column c
     while (i < n_covered && covered[i] < c * n) ++i;
-    cstart[c] = i;
+    ptr[c] = i;
   }
-  for (int64_t c = 0; c < n; ++c) cnt[c + 1] += cnt[c];
-  {
-    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
-    for (int64_t q = 0; q < nq; ++q) order[fill[code[q] % n]++] = q;
+  const std::vector<int64_t> cend(ptr.begin() + 1, ptr.end());
+  for (int64_t c = 0, b = 0; c < n; ++c) {  // block of every column / row index
+    while (b + 1 < nblocks && starts[b + 1] <= c) ++b;
+    cblock[c] = b;
   }
-  auto block_of = [&](int64_t x) {
-    return (int64_t)(std::upper_bound(starts, starts + nblocks + 1, x) - starts) - 1;
-  };
-  for (int64_t c = 0; c < n; ++c) {
-    int64_t i = cstart[c], prev = -1;
-    const int64_t end = cstart[c + 1];
-    const int64_t bc = block_of(c);
-    for (int64_t t = cnt[c]; t < cnt[c + 1]; ++t) {
-      const int64_t q = order[t], r = code[q] / n, key = c * n + r;  // (gi, gj) = (r, c)
-      if (r < prev) i = std::lower_bound(covered + cstart[c], covered + end, key) - covered;
-      while (i < end && covered[i] < key) ++i;
-      prev = r;
-      const int64_t pc = std::min(i, std::max<int64_t>(n_covered - 1, 0));
-      pos_c[q] = pc;
-      hit[q] = i < n_covered && covered[pc] == key;
-      const int64_t br = block_of(r);
-      block[q] = br + 1;
-      li[q] = r - starts[br] + 1;
-      lj[q] = c - starts[bc] + 1;
-    }
+  int64_t r = 0;
+  for (int64_t q = 0; q < nq; ++q) {
+    while (code[q] >= (r + 1) * n) ++r;
+    const int64_t c = code[q] - r * n, key = c * n + r;  // (gi, gj) = (r, c)
+    int64_t i = ptr[c];
+    const int64_t end = cend[c];
+    while (i < end && covered[i] < key) ++i;
+    ptr[c] = i;
+    const int64_t pc = std::min(i, std::max<int64_t>(n_covered - 1, 0));
+    pos_c[q] = pc;
+    hit[q] = i < n_covered && covered[pc] == key;
+    const int64_t br = cblock[r], bc = cblock[c];
+    block[q] = br + 1;
+    li[q] = r - starts[br] + 1;
+    lj[q] = c - starts[bc] + 1;
   }
   return HSDE_OK;
 }
