@@ -132,6 +132,11 @@ int hsde_info(const hsde_t *h, hsde_info_t *out);
 /* State of the ADMM loop in the normalised problem (solver.py:358-363). */
 int hsde_set_state(hsde_t *h, const double *u, const double *w);
 int hsde_get_state(hsde_t *h, double *u, double *w);
+/* The report's vectors (solver.py:575-585, single shard): x = u_x and y = u_y in
+ * the normalised units (n_c, m; the caller unscales), and hv = H' vt with
+ * vt = (u_v / sigma_c) / tau summed per covered coordinate in ascending slot order
+ * (the reference's unscale + np.bincount, graphs.py:251).  Null outputs are skipped. */
+int hsde_report_vectors(hsde_t *h, double tau, double *x, double *y, double *hv);
 int hsde_reset_state(hsde_t *h);               /* initial_state (solver.py:366-372) */
 /* Change the over-relaxation alpha of subsequent iterations (iterate takes the
  * settings per call, solver.py:375-380); rebuilds the iteration graphs. */

@@ -36,7 +36,7 @@ EXPORTED = (
     "hsde_nccl_unique_id", "hsde_shard_total", "hsde_set_state_shard", "hsde_get_state_shard",
     "hsde_debug_jacobi", "hsde_pattern_decompose", "hsde_pattern_sizes", "hsde_pattern_cliques",
     "hsde_pattern_fill", "hsde_pattern_destroy", "hsde_sdpa_parse", "hsde_sdpa_error",
-    "hsde_sdpa_sizes", "hsde_sdpa_data", "hsde_sdpa_destroy", "hsde_pattern_index",
+    "hsde_sdpa_sizes", "hsde_sdpa_data", "hsde_sdpa_destroy", "hsde_pattern_index", "hsde_report_vectors",
 )
 HSDE_NCCL_ID_BYTES = 128
 
@@ -134,6 +134,7 @@ def load() -> C.CDLL:
         "hsde_sdpa_sizes": (C.c_int, [vp, _i32p, _i32p, _i64p]),
         "hsde_sdpa_data": (C.c_int, [vp, _i32p, _dp, _i32p, _i32p, _i32p, _i32p, _dp]),
         "hsde_sdpa_destroy": (None, [vp]),
+        "hsde_report_vectors": (C.c_int, [vp, C.c_double, _dp, _dp, _dp]),
         "hsde_pattern_index": (C.c_int, [_i64p, C.c_int64, C.c_int64, _i64p, C.c_int64, _i64p, C.c_int32,
                                          _i64p, _i64p, _i64p, _i64p, C.POINTER(C.c_uint8)]),
     }
@@ -288,6 +289,15 @@ class Handle:
         self._rc(self._lib.hsde_get_state_shard(self._h, shard, _ptr(u, C.c_double),
                                                 _ptr(w, C.c_double)))
         return u, w
+
+    def report_vectors(self, tau: float):
+        """(u_x, u_y, H'((u_v / sigma_c) / tau)) for the report (single shard)."""
+        x = np.empty(self.cp.N_c)
+        y = np.empty(self.cp.m)
+        hv = np.empty(self.cp.N_c)
+        self._rc(self._lib.hsde_report_vectors(self._h, float(tau), _ptr(x, C.c_double),
+                                               _ptr(y, C.c_double), _ptr(hv, C.c_double)))
+        return x, y, hv
 
     def get_u(self, shard: int = 0):
         """u alone (the report needs no w)."""

@@ -1852,6 +1852,37 @@ int hsde_get_state_shard(hsde_t *h, int32_t g, double *u, double *w) {
   return HSDE_OK;
 }
 
+// H' vt with vt = (u_v / sigma_c) / tau, one thread per covered coordinate
+// summing its slots in ascending order: the reference's unscale, divide and
+// np.bincount (solver.py:668-687, 575-585; graphs.py:251) in the same order
+__global__ void k_report_hv(DevProblem P, const double *u, double sc, double tau, double *hv) {
+  const int64_t vo = P.n_c + P.n_d + P.m;
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < P.n_c; l += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int e = P.cov_ptr[l]; e < P.cov_ptr[l + 1]; ++e) {
+      const double v = sc == 1.0 ? u[vo + P.cov_slot[e]] : u[vo + P.cov_slot[e]] / sc;
+      acc += v / tau;
+    }
+    hv[l] = acc;
+  }
+}
+
+int hsde_report_vectors(hsde_t *h, double tau, double *x, double *y, double *hv) {
+  if (!h || h->sh.size() != 1 || !(tau > 0.0)) return HSDE_ERR_ARG;
+  cudaSetDevice(h->dev);
+  ShardDev &s = h->sh[0];
+  const DevProblem &P = s.P;
+  if (x) CK(cudaMemcpyAsync(x, s.S.u, sizeof(double) * P.n_c, cudaMemcpyDeviceToHost, h->st));
+  if (y) CK(cudaMemcpyAsync(y, s.S.u + P.n_c + P.n_d, sizeof(double) * P.m, cudaMemcpyDeviceToHost, h->st));
+  if (hv) {
+    k_report_hv<<<grid_for(P.n_c), kBlock, 0, h->st>>>(P, s.S.u, h->info.sigma_c, tau, s.d_hv);
+    CKL();
+    CK(cudaMemcpyAsync(hv, s.d_hv, sizeof(double) * P.n_c, cudaMemcpyDeviceToHost, h->st));
+  }
+  CK(cudaStreamSynchronize(h->st));
+  return HSDE_OK;
+}
+
 int hsde_set_state(hsde_t *h, const double *u, const double *w) {
   return hsde_set_state_shard(h, 0, u, w);
 }

@@ -564,17 +564,28 @@ def _classify(sess: _Session, chk: np.ndarray, iterations: int, timing: Timing) 
     tau, kappa = float(chk[3]), float(chk[4])
     if tau > st.infeas_tau_tol:
         res = Residuals(primal=float(chk[0]), dual=float(chk[1]), gap=float(chk[2]))
-        u = sess.unscaled()
-        xt = u[cp.sl_x] / tau
-        yt = u[cp.sl_y] / tau
-        vt = u[cp.sl_v] / tau
+        hvt = None
+        if sess.shards is None:
+            # x, y and H' vt straight from the device (no full-state copy, no host bincount)
+            ux, uy, hvt = sess.h.report_vectors(tau)
+            if sess.sigma_b != 1.0:
+                ux /= sess.sigma_b
+            if sess.sigma_c != 1.0:
+                uy /= sess.sigma_c
+            xt, yt = ux / tau, uy / tau
+        else:
+            u = sess.unscaled()
+            xt = u[cp.sl_x] / tau
+            yt = u[cp.sl_y] / tau
         obj_p = sign * float(cp.c @ xt)
         obj_d = sign * float(cp.b @ yt)
         if res.max() <= st.tol:
+            if hvt is None:
+                hvt = cp.scatter(u[cp.sl_v] / tau)
             solution = {
                 "x_entries": _pattern_entries(cp, dp, xt),
                 "y": [float(t) for t in yt],
-                "z_entries": _pattern_entries(cp, dp, cp.scatter(vt)),
+                "z_entries": _pattern_entries(cp, dp, hvt),
             }
             return SolverReport(status=STATUS_OPTIMAL, objective_primal=obj_p,
                                 objective_dual=obj_d, iterations=iterations, residuals=res,

@@ -466,3 +466,24 @@ def test_split_fast_path_matches_jacobi_path():
     assert stats[0]["split_done"] >= 0.9
     assert 1 <= stats[0]["split_fp_iters"] <= 24
     assert stats[1]["split_done"] == 0.0
+
+
+def test_report_vectors_match_host_path():
+    """The report's device vectors (u_x, u_y and H' vt summed in slot order,
+    hsde_report_vectors) equal the host restatement (unscale, divide,
+    np.bincount: solver.py:668-687, graphs.py:251) bit for bit."""
+    from paper_1611_01828_b200 import _lib
+
+    cp = make_config(2)
+    h = _lib.Handle(cp)
+    h.iterate(60)
+    u, _ = h.get_state()
+    tau = float(u[-1])
+    x, y, hv = h.report_vectors(tau)
+    h.close()
+    assert np.array_equal(x, u[cp.sl_x])
+    assert np.array_equal(y, u[cp.sl_y])
+    v = u[cp.sl_v]
+    if h.sigma_c != 1.0:
+        v = v / h.sigma_c
+    assert np.array_equal(hv, cp.scatter(v / tau))
