@@ -918,6 +918,17 @@ int schur_partial_dense(hsde_handle *h, ShardDev &s) {
   return rc;
 }
 
+// One cuSOLVER handle per device for the process: creating one costs up to a
+// few hundred ms (module load), which every solve_decomposed call would pay.
+cusolverDnHandle_t solver_handle(int dev) {
+  static std::mutex mu;
+  static cusolverDnHandle_t hs[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!hs[dev] && cusolverDnCreate(&hs[dev]) != CUSOLVER_STATUS_SUCCESS) hs[dev] = nullptr;
+  return hs[dev];
+}
+
 // reduced S (in the shard's d_schur) -> S^{-1} (cuSOLVER Cholesky, potrs on I)
 int schur_factor(hsde_handle *h, ShardDev &s) {
   SetupTimer tick;
@@ -936,8 +947,10 @@ int schur_factor(hsde_handle *h, ShardDev &s) {
              " reduced system failed: non-finite entries";
     return HSDE_ERR_FACTOR;
   }
-  cusolverDnHandle_t cs;
-  if (cusolverDnCreate(&cs) != CUSOLVER_STATUS_SUCCESS) {
+  static std::mutex cs_mu;  // the shared handle is used by one setup at a time
+  std::lock_guard<std::mutex> cs_lock(cs_mu);
+  cusolverDnHandle_t cs = solver_handle(h->dev);
+  if (!cs) {
     h->err = "cusolverDnCreate failed";
     return HSDE_ERR_CUDA;
   }
@@ -956,7 +969,6 @@ int schur_factor(hsde_handle *h, ShardDev &s) {
   if (info != 0) {
     pool_free(h, work);
     pool_free(h, dinfo);
-    cusolverDnDestroy(cs);
     h->err = "Cholesky of the " + std::to_string(m) + " x " + std::to_string(m) +
              " reduced system failed: leading minor " + std::to_string(info) + " not positive";
     return HSDE_ERR_FACTOR;
@@ -969,7 +981,6 @@ int schur_factor(hsde_handle *h, ShardDev &s) {
   CK(cudaStreamSynchronize(h->st));
   pool_free(h, work);
   pool_free(h, dinfo);
-  cusolverDnDestroy(cs);
   k_symmetrize<<<grid_for((int64_t)m * m), kBlock, 0, h->st>>>(X, m, S);  // S^{-1}, symmetric
   CKL();
   tick("    potrf+potrs");
