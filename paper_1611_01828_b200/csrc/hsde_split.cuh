@@ -649,9 +649,10 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
       }
     }
     acc = warp_sum(acc);
-    if (lane == 0) red[w] = acc;
+    double *rb = red + 16 * (it & 1);  // alternating halves: no barrier before the next pass writes
+    if (lane == 0) rb[w] = acc;
     __syncthreads();
-    const double delta = sqrt(red_total(red, nw));
+    const double delta = sqrt(red_total(rb, nw));
     if (newy) yb ^= 1;
     const double rho = delta / prev;
     // converged: the estimated remaining error delta rho / (1 - rho) is below the
@@ -660,8 +661,8 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     if (delta <= 0.1 * kSplitTol || (rho < kSplitStall && delta * rho <= kSplitTol * (1.0 - rho))) ok = true;
     else if (!(rho < kSplitStall)) break;
     prev = delta;
-    __syncthreads();  // red is rewritten by the next pass
   }
+  __syncthreads();  // every warp has read the last pass's partials
   if (!ok) {
     // hand B back (original order): N-P block from B_PN', diagonal from lam
     double *xb = W.xarg + off;
