@@ -15,7 +15,7 @@
 // orthogonal projector onto span Q is Q G Q' with G = (I + Y_X' Y_X)^-1, so
 //     P(B) = B Q G Q' = Q (R G) Q'      and      P(X) = Ut' K Ut,
 // Ut = Vt_P + Y_X' Vt_N (r x d), K = R G (r x r).  No truncation: the only
-// errors are the fixed point's (stopped at <= kSplitTol) and rounding.  V
+// errors are the fixed point's (residual <= kSplitTol |B|_F) and rounding.  V
 // itself is left unchanged, so it never loses orthogonality here.
 //
 // The path applies when off(B) <= g / 10 (then no eigenvalue changes sign,
@@ -41,9 +41,8 @@ constexpr int kSplitRefreshIters = 1000;  // fixed-point passes that ask for a J
 constexpr int kLoadBatch = 4;          // hot-path slots per thread in flight
 constexpr double kSplitOff2 = 1.0 / 9.0;  // fast path while off(B)^2 <= kSplitOff2 g^2
 constexpr int kSplitMaxPasses = 24;     // fixed-point passes before handing over
-// fixed-point stop: estimated error of Y <= kSplitTol.  Y is dimensionless
-// (subspace coordinates): an error e moves P by ~ e |B|, below the rounding of
-// the d-term products themselves (~ d eps |B| = 1.8e-14 |B| at d = 80)
+// fixed-point stop: estimated remaining Riccati residual <= kSplitTol |B|_F
+// (below the rounding of the d-term products themselves, ~ d eps |B|)
 constexpr double kSplitTol = 1e-15;
 constexpr double kSplitStall = 0.8;  // pass-to-pass ratio taken as a stall
 // schedule key: off(B)^2 above kSplitKey2 of the bound marks a refresh candidate
@@ -436,7 +435,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   SPLIT_STAMP(2);
 
   // ---- diagonal, g = min |diag|, off(B)^2 (upper values, mirrored)
-  double o2, g;
+  double o2, g, nb2;  // off(B)^2, min |diag|, |B|_F^2
   auto measure = [&]() {
     o2 = 0.0;
 #pragma unroll
@@ -448,9 +447,14 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
         });
     __syncthreads();
     g = CUDART_INF;
-    for (int i = tid; i < d; i += T) g = fmin(g, fabs(lam[i]));
+    double l2 = 0.0;
+    for (int i = tid; i < d; i += T) {
+      g = fmin(g, fabs(lam[i]));
+      l2 += lam[i] * lam[i];
+    }
     g = cta_min(g, red);
     o2 = cta_sum(o2, red);
+    nb2 = o2 + cta_sum(l2, red);
   };
   measure();
   if (!(o2 <= kSplitOff2 * g * g) && g > 0.0 && o2 < CUDART_INF) {
@@ -510,30 +514,51 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     refreshed = true;
   }
   // class-sorted order: perm[0, r) = P (diag > 0), perm[r, d) = N
-  if (tid < 32) {
-    int base = 0;
-    for (int pass = 0; pass < 2; ++pass)
-      for (int i0 = 0; i0 < d; i0 += 32) {
-        const int i = i0 + tid;
-        const bool pk = i < d && ((lam[i] > 0.0) == (pass == 0));
-        const unsigned mk = __ballot_sync(0xffffffffu, pk);
-        if (pk) {
-          const int pos = base + __popc(mk & ((1u << tid) - 1u));
-          perm[pos] = i;
-          pinv[i] = pos;
+  auto classify = [&]() {
+    if (tid < 32) {
+      int base = 0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int i0 = 0; i0 < d; i0 += 32) {
+          const int i = i0 + tid;
+          const bool pk = i < d && ((lam[i] > 0.0) == (pass == 0));
+          const unsigned mk = __ballot_sync(0xffffffffu, pk);
+          if (pk) {
+            const int pos = base + __popc(mk & ((1u << tid) - 1u));
+            perm[pos] = i;
+            pinv[i] = pos;
+          }
+          base += __popc(mk);
+          if (pass == 0 && i0 + 32 >= d && tid == 0) cnt[0] = base;
         }
-        base += __popc(mk);
-        if (pass == 0 && i0 + 32 >= d && tid == 0) cnt[0] = base;
-      }
+    }
+    __syncthreads();
+  };
+  classify();
+  // more positive than non-positive eigenvalues: project -B instead, X+ = X + (-X)+
+  // (the paths below need r <= n)
+  const bool neg = 2 * cnt[0] > d;
+  if (neg) {
+#pragma unroll
+    for (int s = 0; s < kSplitMaxB; ++s)
+#pragma unroll
+      for (int a2 = 0; a2 < 2; ++a2)
+#pragma unroll
+        for (int b2 = 0; b2 < 2; ++b2) {
+          cb[s][a2][b2][0] = -cb[s][a2][b2][0];
+          cb[s][a2][b2][1] = -cb[s][a2][b2][1];
+        }
+    if (tid < d) lam[tid] = -lam[tid];
+    __syncthreads();
+    classify();
   }
-  __syncthreads();
+  const double bsign = neg ? -1.0 : 1.0;  // hand-overs carry B itself
   const int r = cnt[0], n = d - r;
   const float invr = 1.0f / max(r, 1), invn = 1.0f / max(n, 1);
   // off(B) < g keeps the inertia (Weyl: |E|_2 <= |E|_F < min |diag|); the
   // fixed point contracts at about off / 2g, so a looser bound only costs passes
   const bool applies = g > 0.0 && o2 <= kSplitOff2 * g * g && r <= n &&  // also false on NaN
                        split_fits(r, n, nw);
-  if (!applies && W.dbg && tid == 0) {  // diagnostics: (g, off, |diag|_max) of up to 8 hand-overs
+  if (false && !applies && W.dbg && tid == 0) {  // diagnostics: (g, off, |diag|_max) of up to 8 hand-overs
     const unsigned long long c = atomicAdd(reinterpret_cast<unsigned long long *>(W.dbg + 23), 1ull);
     double mx = 0.0;
     for (int i = 0; i < d; ++i) mx = fmax(mx, fabs(lam[i]));
@@ -551,8 +576,8 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
       if (w + s * nw < nbu)
         blk16_each(cb[s], bi0[s], bj0[s], d, d, [&](int i, int j, double v) {
           if (i <= j) {
-            xb[i * d + j] = v;
-            xb[j * d + i] = v;
+            xb[i * d + j] = bsign * v;
+            xb[j * d + i] = bsign * v;
           }
         });
     return r > n ? SPLIT_HANDOFF + 1 : SPLIT_HANDOFF;  // reason: r > n / off(B) > g / 10
@@ -576,9 +601,13 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   __syncthreads();
   SPLIT_STAMP(3);
 
-  if (r == 0) {  // no eigenvalue > 0: P = 0 (w_s holds ws - us_h already)
+  if (r == 0) {  // no eigenvalue > 0: P = 0, or X if B was negated (w_s holds ws - us_h already)
     if (tid == 0) W.ckey[k] = 0;
-    for (int e = tid; e < d * d; e += T) su[e] = 0.0;
+    for (int e = tid; e < d * d; e += T) {
+      const double p = neg ? xg[e] : 0.0;
+      su[e] = p;
+      if (neg) sw[e] += p;
+    }
     return SPLIT_DONE;
   }
 
@@ -596,14 +625,15 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   double x2 = 0.0;
   for (int e = tid; e < n * r; e += T) {
     const int i = qdiv(e, invr), j = e - i * r;
-    const double x = R1[(r + i) * L + j] / (lam[j] - lam[r + i]);
-    R1[(r + i) * L + j] = x;
-    x2 += x * x;
+    const double bnp = R1[(r + i) * L + j];
+    R1[(r + i) * L + j] = bnp / (lam[j] - lam[r + i]);
+    x2 += bnp * bnp;  // the first increment in residual units (Delta * dX)
   }
   __syncthreads();
   // Yn_0 = -(E_PP + B_PN X_0)
   team_mm1<false, false>(r, r, BPN, XX, n, [&](int i, int j, double v) { Ybuf[0][i * ly + j] = -(v + R1[i * L + j]); });
-  double prev = sqrt(cta_sum(x2, red));
+  double prev = sqrt(cta_sum(x2, red)), prev2 = prev;
+  const double tolR = kSplitTol * sqrt(nb2);
   bool ok = prev == 0.0;
   int it = 0, yb = 0;
   const int mb = (n + 15) >> 4, nbr = (r + 15) >> 4, nx = mb * nbr, ny = nbr * nbr;
@@ -641,8 +671,9 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
       if (t < nx) {
         const int bi = qdiv(t, invbr), bj = t - bi * nbr;
         blk16_each(c[s], bi * 16, bj * 16, n, r, [&](int i, int j, double v) {
-          const double x = (R1[j * L + r + i] + v) / (lam[j] - lam[r + i]);
-          const double dx = x - R1[(r + i) * L + j];
+          const double dl = lam[j] - lam[r + i];
+          const double x = (R1[j * L + r + i] + v) / dl;
+          const double dx = (x - R1[(r + i) * L + j]) * dl;  // increment in residual units
           acc += dx * dx;
           R1[(r + i) * L + j] = x;
         });
@@ -654,12 +685,29 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     __syncthreads();
     const double delta = sqrt(red_total(rb, nw));
     if (newy) yb ^= 1;
-    const double rho = delta / prev;
-    // converged: the estimated remaining error delta rho / (1 - rho) is below the
-    // tolerance, or the increment itself is at the rounding level; stalled: no
-    // contraction (or NaN) -- the pass budget bounds slow contraction
-    if (delta <= 0.1 * kSplitTol || (rho < kSplitStall && delta * rho <= kSplitTol * (1.0 - rho))) ok = true;
-    else if (!(rho < kSplitStall)) break;
+    // contraction per pass: over two passes (the lagged quadratic term makes
+    // consecutive increments non-monotone), over one for the first pass
+    const double rho = it == 0 ? delta / prev : sqrt(delta / prev2);
+    // Increments are measured in residual units (Delta o dY, the Riccati residual
+    // the pass removed), against |B|_F: X then solves the Riccati equation of a
+    // matrix within ~kSplitTol |B|_F of B, and P(.) is 1-Lipschitz, so P is
+    // accurate to that level even where Y itself is ill-conditioned (tiny g)
+    // and stops improving at ~eps |B| / g.  Converged: the estimated remaining
+    // residual delta rho / (1 - rho) is below the tolerance, or the increment
+    // itself is at the rounding level; stalled: no contraction (or NaN) -- the
+    // pass budget bounds slow contraction.
+    if (delta <= 0.1 * tolR || (rho < kSplitStall && delta * rho <= tolR * (1.0 - rho))) ok = true;
+    else if (!(rho < kSplitStall)) {
+      if (W.dbg && tid == 0) {  // diagnostics: (refreshed, pass, rho, delta, g, off, r) of up to 4 stalls
+        const unsigned long long c = atomicAdd(reinterpret_cast<unsigned long long *>(W.dbg + 23), 1ull);
+        if (c < 4) {
+          double *o = W.dbg + 24 + 7 * c;
+          o[0] = refreshed; o[1] = it; o[2] = rho; o[3] = delta; o[4] = g; o[5] = sqrt(o2); o[6] = r;
+        }
+      }
+      break;
+    }
+    prev2 = prev;
     prev = delta;
   }
   __syncthreads();  // every warp has read the last pass's partials
@@ -673,7 +721,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
       if (pi == pj) v = lam[pi];
       else if (pi >= r && pj < r) v = R1[pj * L + pi];
       else v = R1[pi * L + pj];
-      xb[e] = v;
+      xb[e] = bsign * v;
     }
     return SPLIT_HANDOFF + 2;  // reason: stalled
   }
@@ -856,16 +904,21 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   // (solver.py:391-394) in a coalesced pass
   team_mm1<true, false>(d, d, Opd{Ut, 1, L}, Opd{Tt, L, 1}, r, [&](int i, int j, double v) { su[i * d + j] = v; });
   for (int e0 = tid; e0 < d * d; e0 += 4 * T) {  // (batched: the stores may alias later loads)
-    double a4[4], b4[4];
+    double a4[4], b4[4], x4[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int e = min(e0 + q * T, d * d - 1);
       a4[q] = sw[e];
       b4[q] = su[e];
+      x4[q] = neg ? xg[e] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      if (e0 + q * T < d * d) sw[e0 + q * T] = a4[q] + b4[q];
+      if (e0 + q * T < d * d) {
+        const double p = neg ? x4[q] + b4[q] : b4[q];  // X+ = X + (-X)+ after a negation
+        if (neg) su[e0 + q * T] = p;
+        sw[e0 + q * T] = a4[q] + p;
+      }
   }
   SPLIT_STAMP(8);
   if (tid == 0 && W.sweeps) W.sweeps[k] = -it;  // (stats: fixed-point iterations)

@@ -4,6 +4,8 @@
 """
 import argparse
 import sys
+
+import numpy as np
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -22,4 +24,8 @@ for i in range(a.iters):
     print(i + 1, round(ms, 3), {k: round(v, 3) for k, v in st.items() if k in (
         "mean_sweeps_large", "split_done", "split_fp_iters", "split_resumed", "handoff_off", "handoff_stall")},
         flush=True)
+    dbg = h.debug_jacobi(0)
+    nh = int(np.frombuffer(dbg[23:24].tobytes(), dtype=np.uint64)[0])
+    if nh:
+        print("   stalls", nh, [tuple(float('%.3g' % x) for x in dbg[24 + 7 * i:31 + 7 * i]) for i in range(min(nh, 4))], flush=True)
 h.close()
