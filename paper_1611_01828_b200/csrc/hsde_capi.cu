@@ -115,6 +115,7 @@ struct ShardDev {
   double *d_schur = nullptr;      // [m*m] partial / factored Schur (owned)
   int grid_heavy = 0, grid_nc = 1, grid_nd = 1, grid_m = 1, grid_T = 1, grid_seg = 1, grid_schur = 1;
   int grid_ua = 1;  // k_ua / k_ua_half grid = number of c.ua block partials
+  int grid_rhs = 1, grid_xupd = 1;  // light CTAs of k_rhs; k_xupd grid (no partials)
   size_t schur_smem = 0;
   std::vector<int> sizes;         // clique sizes (host copy)
   int64_t maxcol = 0;
@@ -488,7 +489,7 @@ int inner_dist(hsde_handle *h, const std::vector<const double *> &rho,
       k_zero<<<grid_for(h->n_sep), kBlock, 0, st>>>(s.W.sepbuf, h->n_sep);
       CKL();
     }
-    k_rhs<false><<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(P, s.S, s.W, rx, rs, rv, s.grid_heavy);
+    k_rhs<false><<<s.grid_rhs + s.grid_heavy, kBlock, 0, st>>>(P, s.S, s.W, rx, rs, rv, s.grid_heavy);
     CKL();
   }
   RC(reduce(h, BUF_SEP, h->n_sep));
@@ -547,7 +548,7 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
       CKL();
       ++nl;
     }
-    k_rhs<true><<<s.grid_nc + s.grid_heavy, kBlock, 0, st>>>(s.P, s.S, s.W, nullptr, nullptr, nullptr,
+    k_rhs<true><<<s.grid_rhs + s.grid_heavy, kBlock, 0, st>>>(s.P, s.S, s.W, nullptr, nullptr, nullptr,
                                                             s.grid_heavy);
     CKL();
     ++nl;
@@ -625,7 +626,7 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
   auto launch_xupd = [&](cudaStream_t xs) -> int {
     for (int g = 0; g < G; ++g) {
       ShardDev &s = h->sh[g];
-      k_xupd<<<s.grid_nc, kBlock, 0, xs>>>(s.P, s.S, s.W);
+      k_xupd<<<s.grid_xupd, kBlock, 0, xs>>>(s.P, s.S, s.W);
       CKL();
       ++nl;
     }
@@ -1539,8 +1540,20 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   CK(cudaMemset(s.d_chk, 0, sizeof(double) * 64));
   s.grid_nc = grid_for(n_c);
   s.grid_ua = s.grid_nc;
+  {
+    auto env_cap = [](const char *name, int def) {
+      const char *e = std::getenv(name);
+      return e ? std::max(1, atoi(e)) : def;
+    };
+    s.grid_rhs = grid_for(n_c, env_cap("HSDE_RHS_CTAS", 148 * 8));
+    s.grid_xupd = grid_for(n_c, env_cap("HSDE_XUPD_CTAS", 148 * 8));
+  }
   if (P.half) {
-    s.grid_ua = std::max(1, std::min(148 * 8, (P.n_slice + 7) / 8));
+    // two CTAs' worth of slices per SM slot (148 x 16): the second wave
+    // balances the ragged slice lengths (config 4: 76 -> 68 us vs 148 x 8)
+    int cap = 148 * 16;
+    if (const char *e = std::getenv("HSDE_UA_CTAS")) cap = std::max(1, std::min(kMaxParts, atoi(e)));
+    s.grid_ua = std::max(1, std::min(cap, (P.n_slice + 7) / 8));
     const int sm = (int)(sizeof(double) * (size_t)m);
     if (sm > 48 * 1024) {
       CK(cudaFuncSetAttribute(k_ua_half<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
