@@ -436,7 +436,8 @@ int launch_aq(hsde_handle *h, ShardDev &s, cudaStream_t st, int *nl) {
     // slower: the gathers sit at the start of every CTA, 4x redundant)
     k_pair_sum<<<grid_for(P.n_pair), kBlock, 0, st>>>(P, s.W.t, s.W.xq);
     CKL();
-    k_spmv_half<false><<<P.rt_ntile * kRowTileSplit, kBlock, 0, st>>>(P, s.W.xq, s.W.rtpart);
+    k_spmv_half<false><<<P.rt_ntile * P.rt_split, kBlock, sizeof(double) * P.rt_tile, st>>>(P, s.W.xq,
+                                                                                            s.W.rtpart);
     CKL();
     k_rowsum_tiles<<<grid_for((int64_t)P.m * 32), kBlock, 0, st>>>(P, s.W.rtpart, s.W.qbuf);
     CKL();

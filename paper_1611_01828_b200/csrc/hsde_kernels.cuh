@@ -89,7 +89,8 @@ struct DevProblem {
   const uint16_t *sl_row;// lane j at sl_beg[s] + 32 k + j
   const double *sl_val;
   const int *sl_pl, *sl_pm;  // [n_pair] the pair (l, mirror) of SELL position q
-  int rt_ntile, rt_G;    // row-SELL tiles of kRowTile pairs x groups of 32 rows (A t),
+  int rt_tile, rt_split;  // pairs per row-SELL tile (<= kRowTile), CTAs per tile
+  int rt_ntile, rt_G;    // row-SELL tiles of rt_tile pairs x groups of 32 rows (A t),
   const int64_t *rt_beg; // owned pairs only, rows sorted by length within a tile;
   const uint16_t *rt_col;// [rt_ntile * rt_G + 1]; column within the tile
   const double *rt_val;
@@ -404,7 +405,10 @@ __device__ __forceinline__ double sell_dot(const double *__restrict__ val, const
 
 constexpr int kRowTile = 4096;  // pairs per row-SELL tile (16-bit column index)
 constexpr int kSellSigma = 1024;  // SELL-32 sorting window (pairs)
-constexpr int kRowTileSplit = 4;  // CTAs per tile (row groups split among them)
+constexpr int kRowTileDefault = 2048;  // default P.rt_tile
+constexpr int kRowTileSplit = 2;  // default P.rt_split: CTAs per tile (row groups split among them)
+// (config 4, m = 1000: 4096 x 4 -> 2048 x 2 took k_spmv_half from 74 to 67 us; 16 KB of
+// staged pair values per CTA lets 2x more CTAs reside, 1024 x 4 / 2048 x 4 / x 8 measured 67-70 us)
 
 // pair values x_q = t_l + t_mirror (t_l on the diagonal)
 __global__ void k_pair_sum(DevProblem P, const double *__restrict__ t, double *__restrict__ xq) {
@@ -420,9 +424,9 @@ __global__ void k_pair_sum(DevProblem P, const double *__restrict__ t, double *_
 template <bool PAIRS>
 __global__ void __launch_bounds__(kBlock) k_spmv_half(DevProblem P, const double *__restrict__ xq,
                                                        double *__restrict__ part) {
-  __shared__ double xs[kRowTile];
-  const int tile = blockIdx.x / kRowTileSplit, rr = blockIdx.x - tile * kRowTileSplit;
-  const int q0 = tile * kRowTile, wn = min(kRowTile, P.n_pair - q0);
+  extern __shared__ double xs[];  // [P.rt_tile]
+  const int tile = blockIdx.x / P.rt_split, rr = blockIdx.x - tile * P.rt_split;
+  const int q0 = tile * P.rt_tile, wn = min(P.rt_tile, P.n_pair - q0);
   if (PAIRS) {
     for (int i0 = threadIdx.x; i0 < wn; i0 += 4 * blockDim.x) {  // 4 pairs in flight per thread
       int l[4], mm[4];
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_half(DevProblem P, const double
   __syncthreads();
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int G = P.rt_G;
-  for (int gr = rr * nw + (threadIdx.x >> 5); gr < G; gr += kRowTileSplit * nw) {
+  for (int gr = rr * nw + (threadIdx.x >> 5); gr < G; gr += P.rt_split * nw) {
     const int64_t b = P.rt_beg[(int64_t)tile * G + gr], e = P.rt_beg[(int64_t)tile * G + gr + 1];
     const double acc = sell_dot(P.rt_val, P.rt_col, xs, b + lane, e);
     const int rq = gr * 32 + lane;

@@ -121,8 +121,8 @@ __global__ void k_row_keys(DevProblem P, const int *pl, int n_pair, const int *o
     if (!own_len[q]) continue;
     const int l = pl[q];
     const int64_t cb = P.at_cp[l], n = P.at_cp[l + 1] - cb;
-    const unsigned long long tile = (unsigned long long)(q / kRowTile);
-    const unsigned long long lc = (unsigned long long)(q - (int)tile * kRowTile);
+    const unsigned long long tile = (unsigned long long)(q / P.rt_tile);
+    const unsigned long long lc = (unsigned long long)(q - (int)tile * P.rt_tile);
     for (int64_t k = 0; k < n; ++k) {
       const unsigned long long r = (unsigned long long)P.at_row[cb + k];
       keys[epos[q] + k] = ((tile * (unsigned long long)P.m + r) << 12) | lc;
@@ -300,7 +300,11 @@ int build_half(hsde_handle *h, ShardDev &s) {
     pool_free(h, own_len64);
   }
   const int64_t n_ent = d2h_one(h, own_pos + n_pair);
-  const int ntile = (n_pair + kRowTile - 1) / kRowTile, G = (m + 31) / 32;
+  P.rt_tile = kRowTileDefault;
+  P.rt_split = kRowTileSplit;
+  if (const char *e = std::getenv("HSDE_RT_TILE")) P.rt_tile = std::max(256, std::min(kRowTile, atoi(e)));
+  if (const char *e = std::getenv("HSDE_RT_SPLIT")) P.rt_split = std::max(1, std::min(16, atoi(e)));
+  const int ntile = (n_pair + P.rt_tile - 1) / P.rt_tile, G = (m + 31) / 32;
   unsigned long long *keys = nullptr, *keys_s = nullptr;
   double *vals = nullptr, *vals_s = nullptr;
   const int64_t ne = std::max<int64_t>(n_ent, 1);
