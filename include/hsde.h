@@ -43,6 +43,7 @@ extern "C" {
 #define HSDE_FLAG_NO_FACTOR 2  /* skip the Schur factorisation (residual-only handle) */
 #define HSDE_FLAG_COLD_EIG 4   /* no warm start of the clique eigensolves             */
 #define HSDE_FLAG_NO_SPLIT 8   /* CTA cliques: no k_cone_split fast path (Jacobi only) */
+#define HSDE_FLAG_JACOBI 16    /* CTA cliques: Jacobi instead of the tridiagonal cold path */
 
 typedef struct hsde_problem_desc {
   int64_t n;                 /* ambient matrix order (informational)              */
@@ -186,8 +187,11 @@ int hsde_sync(hsde_t *h);
  * kernel in the last hot projection, out[6] mean fixed-point iterations of the
  * finished ones, out[7..9] fraction handed over because off(B) > g / 10, r > n,
  * or the fixed point stalled, out[10] fraction finished by the fast path after
- * Jacobi sweeps refreshed the basis. */
-#define HSDE_STATS_LEN 11
+ * Jacobi sweeps refreshed the basis, out[11] fraction handed to the cold path
+ * because the kept basis needed a refresh (off(B) > g / 3), out[12] fraction
+ * finished by the tridiagonal cold path (any reason), out[13] fraction the
+ * cold path handed to the Jacobi path (close eigenvalues). */
+#define HSDE_STATS_LEN 14
 int hsde_stats(hsde_t *h, double *out);
 /* Diagnostics: off-diagonal norm history (relative, per sweep) of the last
  * hot projection of one clique: out[0] = 1 if warm-started, out[1..] = |off|/|A|

@@ -22,7 +22,8 @@ HSDE_FLAG_EXACT_UY = 1
 HSDE_FLAG_NO_FACTOR = 2
 HSDE_FLAG_COLD_EIG = 4
 HSDE_FLAG_NO_SPLIT = 8
-HSDE_STATS_LEN = 11
+HSDE_FLAG_JACOBI = 16
+HSDE_STATS_LEN = 14
 HSDE_CHECK_LEN = 8
 HSDE_CERT_LEN = 7
 HSDE_PROFILE_SLOTS = 16
@@ -367,7 +368,8 @@ class Handle:
                 "mean_sweeps_large": float(out[2]), "warm_start": bool(out[3]),
                 "split_done": float(out[4]), "split_handoff": float(out[5]),
                 "split_fp_iters": float(out[6]), "handoff_off": float(out[7]), "handoff_rn": float(out[8]),
-                "handoff_stall": float(out[9]), "split_resumed": float(out[10])}
+                "handoff_stall": float(out[9]), "split_resumed": float(out[10]),
+                "handoff_refresh": float(out[11]), "cold_done": float(out[12]), "cold_failed": float(out[13])}
 
     def debug_jacobi(self, clique: int = 0) -> np.ndarray:
         out = np.empty(64)

@@ -81,10 +81,17 @@ struct ConePlan {
   double *pscratch = nullptr;  // CTA plan: d x d global scratch per CTA (second-order rebuild)
   int64_t pstride = 0;
   size_t split_smem = 0;       // CTA plan: k_cone_split (0: not launched)
+  int cold_cv = 0;             // CTA plan: tridiagonal cold path variant (0: Jacobi)
+  size_t cold_smem = 0;
+  int *cfail = nullptr;        // [count] cold-path failures (follow-up Jacobi launch)
 };
 
 enum Mode { MODE_SINGLE = 0, MODE_EMULATED = 1, MODE_NCCL = 2 };
 enum Buf { BUF_SEP = 0, BUF_Q, BUF_RED, BUF_CHK, BUF_SCHUR, BUF_MINEIG, BUF_COUNT };
+
+__global__ void k_set_i32(int *p, int n, int v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
+}
 
 // sum (or min) the G shard buffers element-wise, result written back to all
 __global__ void k_reduce_ptrs(double *const *ptrs, int G, int64_t n, int64_t off, int op_min) {
@@ -147,6 +154,7 @@ struct hsde_handle {
   bool factor = true;
   bool warm = true;
   bool split = true;  // k_cone_split fast path for CTA cliques (HSDE_FLAG_NO_SPLIT off)
+  bool jacobi = false;  // HSDE_FLAG_JACOBI: no tridiagonal cold path
   bool multi() const { return mode != MODE_SINGLE; }
 };
 
@@ -373,8 +381,11 @@ __global__ void k_diag_finish(double *diag, int m, int *flag) {
 }
 
 // cone launches (one shard)
+// part (CTA plan with the fast path and the cold path): 0 both, serially;
+// 1 the fast path only; 2 the cold path and its Jacobi fallback only (1 and 2
+// run concurrently on disjoint cliques: W.ccur, set by k_scalars)
 int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool block,
-                const double *in, double *out, double in_scale, cudaStream_t st) {
+                const double *in, double *out, double in_scale, cudaStream_t st, int part = 0) {
   if (pl.count == 0) return 0;
   static const int split_refresh = [] {
     const char *e = std::getenv("HSDE_SPLIT_REFRESH");
@@ -392,19 +403,46 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
     if (mode == CONE_HOT) k_cone_warp<CONE_HOT><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
     else if (mode == CONE_PLAIN) k_cone_warp<CONE_PLAIN><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
     else k_cone_warp<CONE_MINEIG><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
-  } else {
-    DevWork W = s.W;
-    W.cstate = nullptr;  // k_cone_block does every clique
-    if (mode == CONE_HOT && pl.split_smem && h->warm && h->split) {
-      // fast path, Jacobi path in the same CTA for cliques without a basis
-      // and for hand-overs (hsde_split.cuh)
-      ConeArgs co = ca;
-      co.ids = s.W.corder;  // scheduled by k_scalars (s.W.cta_ids)
-      k_cone_split<<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, s.W, co);
-    } else if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, W, ca);
-    else if (mode == CONE_PLAIN) k_cone_block<CONE_PLAIN><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
-    else k_cone_block<CONE_MINEIG><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, s.W, ca);
+    CKL();
+    return 0;
   }
+  DevWork W = s.W;
+  W.cstate = nullptr;  // k_cone_block does every clique (of its list)
+  const int cv = h->jacobi ? 0 : pl.cold_cv;
+  ca.cfail = pl.cfail;
+  const bool split = mode == CONE_HOT && pl.split_smem && h->warm && h->split;
+  if (split && part != 2) {
+    // fast path (hsde_split.cuh) on the cliques with a usable basis; its
+    // hand-overs finish on the Jacobi path in the same CTA
+    ConeArgs co = ca;
+    co.ids = s.W.corder;  // scheduled by k_scalars (s.W.cta_ids)
+    DevWork Ws = s.W;
+    if (!cv) Ws.ccur = Ws.cnext = nullptr;  // (Jacobi variant: every clique)
+    k_cone_split<false><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, Ws, co);
+    CKL();
+    if (!cv || part == 1) return 0;
+  }
+  if (cv && !(mode == CONE_HOT && !split && !h->split)) {
+    // tridiagonal cold path (hsde_cold.cuh), then its failures on the Jacobi path
+    DevWork Wc = s.W;
+    if (!split) Wc.ccur = Wc.cnext = Wc.cstate = nullptr;  // every clique
+    auto go = [&](auto kern) { kern<<<pl.count, kColdThreads, pl.cold_smem, st>>>(s.P, s.S, Wc, ca); };
+    if (mode == CONE_HOT) {
+      if (cv == 1) go(k_cone_cold<CONE_HOT, 20, 3, 3>);
+      else go(k_cone_cold<CONE_HOT, 24, 3, 2>);
+    } else if (mode == CONE_PLAIN) {
+      if (cv == 1) go(k_cone_cold<CONE_PLAIN, 20, 3, 3>);
+      else go(k_cone_cold<CONE_PLAIN, 24, 3, 2>);
+    } else {
+      if (cv == 1) go(k_cone_cold<CONE_MINEIG, 20, 3, 3>);
+      else go(k_cone_cold<CONE_MINEIG, 24, 3, 2>);
+    }
+    CKL();
+    ca.fail_only = 1;
+  }
+  if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, W, ca);
+  else if (mode == CONE_PLAIN) k_cone_block<CONE_PLAIN><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, W, ca);
+  else k_cone_block<CONE_MINEIG><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, W, ca);
   CKL();
   return 0;
 }
@@ -613,16 +651,26 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
     ShardDev *s;
     const ConePlan *pl;
     bool block;
+    int part;
   };
   std::vector<ConeJob> jobs;
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
     for (const ConePlan &wp : s.warp_plans)
-      if (wp.count) jobs.push_back({&s, &wp, false});
+      if (wp.count) jobs.push_back({&s, &wp, false, 0});
   }
   const size_t n_warp_jobs = jobs.size();
-  for (int g = 0; g < G; ++g)
-    if (h->sh[g].block_plan.count) jobs.push_back({&h->sh[g], &h->sh[g].block_plan, true});
+  for (int g = 0; g < G; ++g) {
+    const ConePlan &bp = h->sh[g].block_plan;
+    if (!bp.count) continue;
+    const bool two = bp.split_smem && h->warm && h->split && bp.cold_cv && !h->jacobi;
+    if (two && !ev) {  // fast path and cold path on disjoint cliques, concurrently
+      jobs.push_back({&h->sh[g], &bp, true, 2});
+      jobs.push_back({&h->sh[g], &bp, true, 1});
+    } else {
+      jobs.push_back({&h->sh[g], &bp, true, 0});
+    }
+  }
   nl += (int)jobs.size();
   auto launch_xupd = [&](cudaStream_t xs) -> int {
     for (int g = 0; g < G; ++g) {
@@ -645,7 +693,7 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
   if (ev || jobs.size() <= 1) {
     if (n_warp_jobs == 0) mark(PS_CONE_WARP);
     for (size_t j = 0; j < jobs.size(); ++j) {
-      RC(launch_cone(h, *jobs[j].s, CONE_HOT, *jobs[j].pl, jobs[j].block, nullptr, nullptr, 1.0, st));
+      RC(launch_cone(h, *jobs[j].s, CONE_HOT, *jobs[j].pl, jobs[j].block, nullptr, nullptr, 1.0, st, jobs[j].part));
       if (j + 1 == n_warp_jobs) mark(PS_CONE_WARP);
     }
   } else {
@@ -654,10 +702,10 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
     for (size_t j = 0; j + 1 < jobs.size(); ++j) {
       cudaStream_t a = h->aux[j % (hsde_handle::kAux - 1)];
       CK(cudaStreamWaitEvent(a, h->ev_fork, 0));
-      RC(launch_cone(h, *jobs[j].s, CONE_HOT, *jobs[j].pl, jobs[j].block, nullptr, nullptr, 1.0, a));
+      RC(launch_cone(h, *jobs[j].s, CONE_HOT, *jobs[j].pl, jobs[j].block, nullptr, nullptr, 1.0, a, jobs[j].part));
     }
     RC(launch_cone(h, *jobs.back().s, CONE_HOT, *jobs.back().pl, jobs.back().block, nullptr, nullptr, 1.0,
-                   st));
+                   st, jobs.back().part));
     for (size_t j = 0; j + 1 < jobs.size() && j < (size_t)hsde_handle::kAux - 1; ++j) {
       CK(cudaEventRecord(h->ev_join[j], h->aux[j]));
       CK(cudaStreamWaitEvent(st, h->ev_join[j], 0));
@@ -769,11 +817,27 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
     const int sm = maxsm;
     int dmax = 0;
     for (int k : bids) dmax = std::max(dmax, s.sizes[k]);
+    // cold path variant: capacity d <= 84 / 96 (larger cliques of the plan
+    // are flagged to the Jacobi launch that follows)
+    int dmin = 1 << 30;
+    for (int k : bids) dmin = std::min(dmin, s.sizes[k]);
+    s.block_plan.cold_cv = dmin > kColdMaxD ? 0 : dmax <= 80 ? 1 : 2;
+    if (s.block_plan.cold_cv) {
+      s.block_plan.cold_smem = (size_t)cold_smem_doubles(std::min(dmax, kColdMaxD)) * sizeof(double);
+      RC(dalloc(h, &s.block_plan.cfail, bids.size()));
+      CK(cudaMemset(s.block_plan.cfail, 0, sizeof(int) * bids.size()));
+      CK(cudaFuncSetAttribute(k_cone_cold<CONE_HOT, 20, 3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_cone_cold<CONE_PLAIN, 20, 3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_cone_cold<CONE_MINEIG, 20, 3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_cone_cold<CONE_HOT, 24, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_cone_cold<CONE_PLAIN, 24, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_cone_cold<CONE_MINEIG, 24, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    }
     if (dmax <= kSplitMaxD) {
       s.block_plan.split_smem = std::max((size_t)split_smem_doubles(dmax) * sizeof(double), per_blk);
       s.W.cta_ids = s.block_plan.ids;  // k_scalars schedules them for k_cone_split
       s.W.cta_n = s.block_plan.count;
-      CK(cudaFuncSetAttribute(k_cone_split, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_cone_split<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     }
     CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -1085,6 +1149,7 @@ int init_state(hsde_handle *h) {
     CK(cudaMemcpyAsync(s.d_prev_u, s.S.u, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
     CK(cudaMemcpyAsync(s.d_prev_w, s.S.w, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
     CK(cudaMemsetAsync(s.W.vvalid, 0, sizeof(int) * std::max(s.P.p, 1), h->st));
+    k_set_i32<<<1, 256, 0, h->st>>>(s.W.cnext, std::max(s.P.p, 1), 1);  // no basis: cold path first
     CK(cudaStreamSynchronize(h->st));
   }
   return 0;
@@ -1523,6 +1588,8 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   RC(dalloc(h, &s.d_mineig, std::max(p, 1)));
   RC(dalloc(h, &s.W.vstore, n_d));
   RC(dalloc(h, &s.W.vvalid, std::max(p, 1)));
+  RC(dalloc(h, &s.W.ccur, std::max(p, 1)));
+  RC(dalloc(h, &s.W.cnext, std::max(p, 1)));
   RC(dalloc(h, &s.W.sweeps, std::max(p, 1)));
   RC(dalloc(h, &s.W.cstate, std::max(p, 1)));
   RC(dalloc(h, &s.W.ckey, std::max(p, 1)));
@@ -1535,6 +1602,9 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   s.W.dbg_clique = 0;
   CK(cudaMemset(s.W.err, 0, sizeof(int)));
   CK(cudaMemset(s.W.vvalid, 0, sizeof(int) * std::max(p, 1)));
+  k_set_i32<<<1, 256>>>(s.W.ccur, std::max(p, 1), 1);
+  k_set_i32<<<1, 256>>>(s.W.cnext, std::max(p, 1), 1);
+  CK(cudaDeviceSynchronize());
   CK(cudaMemset(s.W.sweeps, 0, sizeof(int) * std::max(p, 1)));
   CK(cudaMemset(s.W.cstate, 0xff, sizeof(int) * std::max(p, 1)));
   CK(cudaMemset(s.W.ckey, 0, sizeof(int) * std::max(p, 1)));
@@ -1801,6 +1871,7 @@ int hsde_create_sharded(const hsde_problem_desc *descs, int32_t nshards, const h
   h->factor = !(s->flags & HSDE_FLAG_NO_FACTOR);
   h->warm = !(s->flags & HSDE_FLAG_COLD_EIG);
   h->split = !(s->flags & HSDE_FLAG_NO_SPLIT);
+  h->jacobi = (s->flags & HSDE_FLAG_JACOBI) != 0;
   if (cudaMallocHost(&h->h_chk, 64 * sizeof(double)) != cudaSuccess) {
     g_create_error = "cudaMallocHost failed";
     delete h;
@@ -1862,6 +1933,7 @@ int hsde_set_state_shard(hsde_t *h, int32_t g, const double *u, const double *w)
   CK(cudaMemcpyAsync(s.d_prev_u, s.S.u, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
   CK(cudaMemcpyAsync(s.d_prev_w, s.S.w, sizeof(double) * T, cudaMemcpyDeviceToDevice, h->st));
   CK(cudaMemsetAsync(s.W.vvalid, 0, sizeof(int) * std::max(s.P.p, 1), h->st));
+    k_set_i32<<<1, 256, 0, h->st>>>(s.W.cnext, std::max(s.P.p, 1), 1);  // no basis: cold path first
   CK(cudaStreamSynchronize(h->st));
   return HSDE_OK;
 }
@@ -2342,28 +2414,39 @@ int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches) 
 int hsde_stats(hsde_t *h, double *out) {
   if (!h || !out) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  double sum = 0, mx = 0, sum_big = 0, n_big = 0, n = 0, n_done = 0, n_hand = 0, n_fp = 0, n_res = 0, n_why[3] = {0, 0, 0};
+  double sum = 0, mx = 0, sum_big = 0, n_big = 0, n = 0, n_done = 0, n_hand = 0, n_fp = 0, n_res = 0,
+         n_why[4] = {0, 0, 0, 0}, n_cold = 0, n_fail = 0;
   for (auto &s : h->sh) {
     std::vector<int> sw(std::max(s.P.p, 1)), cs(std::max(s.P.p, 1));
+    std::vector<int> cf(std::max(s.block_plan.count, 1), 0);
     CK(cudaMemcpyAsync(sw.data(), s.W.sweeps, sizeof(int) * sw.size(), cudaMemcpyDeviceToHost, h->st));
     CK(cudaMemcpyAsync(cs.data(), s.W.cstate, sizeof(int) * cs.size(), cudaMemcpyDeviceToHost, h->st));
+    if (s.block_plan.cfail)
+      CK(cudaMemcpyAsync(cf.data(), s.block_plan.cfail, sizeof(int) * s.block_plan.count, cudaMemcpyDeviceToHost,
+                         h->st));
     CK(cudaStreamSynchronize(h->st));
     const bool split_ran = s.block_plan.split_smem && h->warm && h->split;
+    const bool cold_ran = s.block_plan.cold_cv && !h->jacobi;
+    for (int i = 0; i < s.block_plan.count; ++i) n_fail += cf[i] != 0;
     for (int k = 0; k < s.P.p; ++k) {
       const bool big = s.sizes[k] > 32;
       // final states: 0 fast path, 16 fast path after Jacobi sweeps (resumed),
-      // 33 Jacobi (no basis), 34..36 Jacobi after a hand-over (reason + 34)
+      // 33 cold / Jacobi path (no basis), 34..37 after a hand-over (reason + 34)
       const bool resumed = big && split_ran && cs[k] == SPLIT_DONE + 16;
       const bool fast = big && split_ran && (cs[k] == SPLIT_DONE || resumed);
       n_res += resumed;
       if (big && split_ran) {
         n_done += fast;
         const int why = cs[k] - (SPLIT_DONE + 32 + SPLIT_HANDOFF);
-        n_hand += why >= 0 && why <= 2;
-        if (why >= 0 && why <= 2) ++n_why[why];
+        n_hand += why >= 0 && why <= 3;
+        if (why >= 0 && why <= 3) ++n_why[why];
       }
       if (fast) {  // no Jacobi solve; sweeps holds -(fixed-point iterations)
         n_fp -= sw[k];
+        continue;
+      }
+      if (big && cold_ran) {
+        n_cold += 1;
         continue;
       }
       sum += sw[k];
@@ -2383,6 +2466,9 @@ int hsde_stats(hsde_t *h, double *out) {
   out[6] = n_done ? n_fp / n_done : 0.0;
   for (int i = 0; i < 3; ++i) out[7 + i] = nbig ? n_why[i] / nbig : 0.0;
   out[10] = nbig ? n_res / nbig : 0.0;
+  out[11] = nbig ? n_why[3] / nbig : 0.0;
+  out[12] = nbig ? (n_cold - n_fail) / nbig : 0.0;
+  out[13] = nbig ? n_fail / nbig : 0.0;
   out[0] = n ? sum / n : 0.0;
   out[1] = mx;
   out[2] = n_big ? sum_big / n_big : 0.0;

@@ -1205,6 +1205,9 @@ struct ConeArgs {
   int slot;         // this team's scratch slot
   int split_refresh; // k_cone_split: fixed-point iterations beyond which V is refreshed
   int split_vupdate; // k_cone_split: rotate V onto the new invariant subspaces
+  int *cfail;        // cold path (hsde_cold.cuh): [count] 1 = handed to the Jacobi path
+  int fail_only;     // k_cone_block: only the slots flagged in cfail (HOT: raw X in W.xarg)
+  int cold;          // k_cone_split: hand-overs go to the cold path (X kept in W.xarg)
 };
 
 // Hot-path load of slot j: builds arg_s and performs the v / w_v update and
@@ -1268,11 +1271,12 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
     // finished by the fast path (also after a refresh, SPLIT_DONE + 16) or here
     if (cst == SPLIT_DONE || cst >= SPLIT_DONE + 16) return;
   }
-  const bool handoff = cst >= SPLIT_HANDOFF;  // A <- B = Vt X Vt' from W.xarg
+  const bool xcold = MODE == CONE_HOT && ca.fail_only;  // cold-path failure: raw X in W.xarg
+  const bool handoff = !xcold && cst >= SPLIT_HANDOFF;  // A <- B = Vt X Vt' from W.xarg
   const int age = (MODE == CONE_HOT && ca.warm) ? (W.vvalid[k] & ~kVRefresh) : 0;
   constexpr int MT = TeamTiles<Team>::value;
   const int ntile = (d + 3) >> 2;
-  const bool warm = handoff || (age > 0 && age < kWarmMaxAge && ntile * ntile <= MT * tm.size());
+  const bool warm = handoff || (!xcold && age > 0 && age < kWarmMaxAge && ntile * ntile <= MT * tm.size());
   if (MODE == CONE_HOT && W.dbg && k == W.dbg_clique) {
     js.dbg = W.dbg;
     if (tm.rank == 0) {
@@ -1285,7 +1289,7 @@ __device__ void cone_one(const Team &tm, const DevProblem &P, const DevState &S,
   for (int e = tm.rank; e < d * d; e += tm.size()) {
     const int a = e / d, bcol = e - a * d;
     double v;
-    if (MODE == CONE_HOT) v = handoff ? W.xarg[off + e] : hot_slot_load(P, S, W, off + e, shift);
+    if (MODE == CONE_HOT) v = (handoff || xcold) ? W.xarg[off + e] : hot_slot_load(P, S, W, off + e, shift);
     else v = ca.in[off + e] * ca.in_scale;
     A[a * lda + bcol] = v;
     if (warm) js.Vt[a * ldv + bcol] = W.vstore[off + e];
@@ -1447,6 +1451,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kConeBlock, 2) k_cone_block(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
   extern __shared__ __align__(16) double smem[];
   if ((int)blockIdx.x >= ca.count) return;
+  if (ca.fail_only && !ca.cfail[blockIdx.x]) return;  // after the cold path: its failures only
   BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
   ConeArgs c2 = ca;
   c2.slot = blockIdx.x;

@@ -132,7 +132,8 @@ struct DevWork {
   int *corder;         // [p]     CTA-plan clique ids, refresh candidates first (k_scalars)
   const int *cta_ids;  // CTA-plan clique ids (plan order) to be scheduled into corder, or null
   int cta_n;
-  double *xarg;        // [n_d]   k_cone_split -> k_cone_block hand-off (B = Vt X Vt')
+  double *xarg;        // [n_d]   k_cone_split -> k_cone_block hand-off (B = Vt X Vt'); cold path: raw X
+  int *ccur, *cnext;   // [p]     CTA cliques: 1 = cold path this / next iteration (k_scalars copies next -> cur)
   double *dbg;         // [64]    Jacobi off-norm history of one clique (diagnostics)
   int dbg_clique;
 };
@@ -567,6 +568,11 @@ __global__ void __launch_bounds__(1024) k_scalars(DevProblem P, DevState S, DevW
     S.w[yo + i] = wn;
     W.ry[i] = (yn + wn) + atau_next * P.b[i];
   }
+  if (sched && W.ccur)  // this iteration's split / cold decision (hsde_cold.cuh)
+    for (int i = threadIdx.x; i < W.cta_n; i += blockDim.x) {
+      const int id = W.cta_ids[i];
+      W.ccur[id] = W.cnext[id];
+    }
   if (sched) {
     // the cliques with key 1 (likely to need a Jacobi refresh) first, plan order
     // otherwise: a stable partition by ballots, blockDim.x ids per chunk
@@ -629,6 +635,7 @@ __global__ void __launch_bounds__(kBlock) k_xupd(DevProblem P, DevState S, DevWo
 
 #include "hsde_eig.cuh"
 #include "hsde_split.cuh"
+#include "hsde_cold.cuh"
 
 // ---------------------------------------------------------------------------
 // generic small kernels for the unit-level API path

@@ -36,7 +36,11 @@
 constexpr int kSplitThreads = 384;
 constexpr int kSplitStrip = 32;  // warm-start strip width (columns of T = Vt X)
 constexpr int kSplitMaxB = 2;    // 16 x 16 blocks a warp keeps in registers
-constexpr int kSplitMaxD = 112;  // upper blocks of B: <= kSplitMaxB per warp
+constexpr int kSplitMaxD = 96;   // upper blocks of B: <= kSplitMaxB per warp
+// B's upper 16 x 16 blocks live in registers during the warm start: all of
+// them must be owned by some warp (nb = 6 -> 21 blocks <= 2 x 12)
+static_assert(((kSplitMaxD + 15) / 16) * ((kSplitMaxD + 15) / 16 + 1) / 2 <= kSplitMaxB * (kSplitThreads / 32),
+              "kSplitMaxD: B's upper blocks exceed the warps' register blocks");
 constexpr int kSplitRefreshIters = 1000;  // fixed-point passes that ask for a Jacobi refresh of V
 constexpr int kLoadBatch = 4;          // hot-path slots per thread in flight
 constexpr double kSplitOff2 = 1.0 / 9.0;  // fast path while off(B)^2 <= kSplitOff2 g^2
@@ -457,9 +461,15 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     nb2 = o2 + cta_sum(l2, red);
   };
   measure();
+  if (!(o2 <= kSplitOff2 * g * g) && g > 0.0 && o2 < CUDART_INF && ca.cold) {
+    // the within-class drift of the kept basis made the split inapplicable:
+    // the cold path (hsde_cold.cuh) re-diagonalises X (still in xg) in this CTA
+    return SPLIT_HANDOFF + 3;
+  }
   if (!(o2 <= kSplitOff2 * g * g) && g > 0.0 && o2 < CUDART_INF) {
-    // Refresh: the within-class drift of the kept basis made the split
-    // inapplicable.  Jacobi sweeps on B, warm from V (hsde_eig.cuh), in this
+    // far above the bound (off(B) > 0.6 g): the cold path next iteration
+    if (tid == 0 && W.cnext) W.cnext[k] = o2 > 0.36 * g * g ? 1 : 0;
+    // (Jacobi variant) Jacobi sweeps on B, warm from V (hsde_eig.cuh), in this
     // CTA until the class-split point; then the split goes on with the
     // rotated B and V.  (B is in registers, X and V in global memory: the
     // Jacobi scratch may overwrite the whole shared-memory area.)
@@ -558,16 +568,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   // fixed point contracts at about off / 2g, so a looser bound only costs passes
   const bool applies = g > 0.0 && o2 <= kSplitOff2 * g * g && r <= n &&  // also false on NaN
                        split_fits(r, n, nw);
-  if (false && !applies && W.dbg && tid == 0) {  // diagnostics: (g, off, |diag|_max) of up to 8 hand-overs
-    const unsigned long long c = atomicAdd(reinterpret_cast<unsigned long long *>(W.dbg + 23), 1ull);
-    double mx = 0.0;
-    for (int i = 0; i < d; ++i) mx = fmax(mx, fabs(lam[i]));
-    if (c < 8) {
-      W.dbg[24 + 3 * c] = g;
-      W.dbg[25 + 3 * c] = sqrt(o2);
-      W.dbg[26 + 3 * c] = mx;
-    }
-  }
+  if (!applies && ca.cold) return SPLIT_HANDOFF + 1;  // X stays in xg for the cold path
   if (!applies) {
     // hand B (original order) to the Jacobi path
     double *xb = W.xarg + off;
@@ -711,6 +712,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     prev = delta;
   }
   __syncthreads();  // every warp has read the last pass's partials
+  if (!ok && ca.cold) return SPLIT_HANDOFF + 2;  // stalled: X stays in xg for the cold path
   if (!ok) {
     // hand B back (original order): N-P block from B_PN', diagonal from lam
     double *xb = W.xarg + off;
@@ -922,6 +924,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   }
   SPLIT_STAMP(8);
   if (tid == 0 && W.sweeps) W.sweeps[k] = -it;  // (stats: fixed-point iterations)
+  if (tid == 0 && W.cnext && !refreshed) W.cnext[k] = 0;
   // schedule key for the next iteration: passes, plus a refresh risk when off(B)
   // is already near the applicability bound
   if (tid == 0) W.ckey[k] = o2 > kSplitKey2 * kSplitOff2 * g * g ? 1 : 0;
@@ -930,27 +933,4 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   return SPLIT_DONE;
 }
 
-// One CTA per CTA-sized clique on the hot path: the fast path when the
-// clique has a valid eigenbasis; otherwise -- or when the fast path hands
-// over -- the Jacobi path (cone_one) in the same CTA, so a hand-over overlaps
-// the other cliques instead of serialising behind them.
-__global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
-  extern __shared__ __align__(16) double smem[];
-  if ((int)blockIdx.x >= ca.count) return;
-  const int k = ca.ids[blockIdx.x];
-  const int d = P.cl_size[k];
-  const int vv = W.vvalid[k];
-  ConeArgs c2 = ca;
-  c2.slot = blockIdx.x;
-  int st = SPLIT_UNTOUCHED;
-  if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d > 32) st = split_one(P, S, W, c2, k, smem);
-  if (threadIdx.x == 0) W.cstate[k] = st;
-  if (st == SPLIT_DONE || st == SPLIT_DONE + 16) return;
-  __syncthreads();  // cstate and the hand-off B are visible to the whole CTA
-  BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
-  cone_one<CONE_HOT>(tm, P, S, W, c2, k, smem);
-  if (threadIdx.x == 0) {
-    W.cstate[k] = SPLIT_DONE + 32 + st;  // (stats: finished by the Jacobi path)
-    W.ckey[k] = 1;                        // schedule first next time
-  }
-}
+// (k_cone_split, the kernel around split_one, is in hsde_cold.cuh: its hand-overs run the cold path)

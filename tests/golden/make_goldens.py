@@ -1,6 +1,6 @@
 """Generate golden fixtures by running the LIVE reference (build container only).
 
-    python tests/golden/make_goldens.py first toys cfg0 cfg1 cfg2 [cfg3] [cfg4]
+    python tests/golden/make_goldens.py first toys cfg0 cfg1 cfg2 [cfg3] [cfg4] [cfg4long]
 
 Imports ``chordalsdp`` from /root/reference/pkg/src (read-only, never copied)
 and writes ``tests/golden/*.npz``.  The GPU box never runs this; it only reads
@@ -15,8 +15,16 @@ the committed fixtures.  Sections:
 * ``cfgK``  -- BASELINE config K (paper_1611_01828_b200.synthetic) solved by
   the reference: iterate at a fixed iteration count (500; config 4: 40) with
   tol=1e-300, the per-check log, and the default-settings to-tolerance report.
-  Small configs store the full compressed state; large ones a summary
-  (segment norms + 4096 seeded sample entries).
+  Configs 0-3 store the full compressed state (w only on its nonzero z/kappa
+  segments); config 4 a summary (segment norms + 4096 seeded sample entries).
+  The to-tolerance report's solution entries (x_entries / z_entries, solver.py:
+  553-556) or certificate entry lists (solver.py:472-503) are stored too.
+* ``cfg4long`` -- config 4 iterated by the reference to a fixed 200 iterations
+  (tol=1e-300): summaries at iterations 100 and 200 plus the check log (SURVEY
+  section 7.1's long pin; about an hour of CPU).
+
+Every config fixture records ``gen_hash``: a SHA-256 over the generated
+problem's arrays, so a generator change is detected by the tests.
 """
 from __future__ import annotations
 
@@ -40,7 +48,7 @@ from chordalsdp import solver as R  # noqa: E402
 from paper_1611_01828_b200.problem import expand_to_mirror  # noqa: E402
 from paper_1611_01828_b200.synthetic import make_config  # noqa: E402
 
-FULL_STATE_MAX = 60_000  # store the whole compressed state below this length
+FULL_STATE_MAX = 600_000  # store the whole compressed state below this length
 N_SAMPLES = 4096
 
 
@@ -50,6 +58,21 @@ def to_reference(cp):
     dec = RCD.build(cp.n, [list(map(int, c)) for c in cp.cliques], pat)
     return RDP(n=cp.n, m=cp.m, c=mir.c, A=mir.A, b=cp.b.copy(), dec=dec,
                aggregate=pat, block_dims=(cp.n,))
+
+
+def gen_hash(cp) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for arr in (cp.covered, cp.A.indptr, cp.A.indices, cp.A.data, cp.c, cp.b,
+                cp.sizes, np.concatenate([np.asarray(c) for c in cp.cliques])):
+        a = np.ascontiguousarray(arr)
+        h.update(str(a.dtype).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def entries_array(rows) -> np.ndarray:
+    return np.array(rows, dtype=np.float64).reshape(-1, 4)
 
 
 def sample_index(total: int) -> np.ndarray:
@@ -63,7 +86,11 @@ def state_summary(cp, u, w, prefix):
     for name, vec in (("u", u), ("w", w)):
         out[f"{prefix}{name}_norms"] = np.array([np.linalg.norm(vec[sl]) for sl in segs.values()]
                                                 + [vec[-1]])
-        if cp.total <= FULL_STATE_MAX:
+        if cp.total <= FULL_STATE_MAX and name == "w":
+            # the x / y / v parts of w are exactly 0
+            out[f"{prefix}w_z"] = vec[cp.sl_s]
+            out[f"{prefix}w_kappa"] = np.float64(vec[-1])
+        elif cp.total <= FULL_STATE_MAX:
             out[f"{prefix}{name}"] = vec
         else:
             idx = sample_index(cp.total)
@@ -146,7 +173,7 @@ def section_cfg(idx: int):
     dp = to_reference(cp)
     print(f"cfg{idx}: built reference problem in {time.time() - t:.1f}s")
     fixed = 40 if idx == 4 else 500
-    out = {"fixed_iters": np.int64(fixed)}
+    out = {"fixed_iters": np.int64(fixed), "gen_hash": np.array(gen_hash(cp))}
     log = []
 
     def cb(info):
@@ -191,9 +218,41 @@ def section_cfg(idx: int):
         out["cert_min_eig"] = np.float64(cert["min_block_eigenvalue"])
         if "y" in cert:
             out["cert_y"] = np.array(cert["y"])
+        for key in ("slack_entries", "ray_entries"):
+            if key in cert:
+                out[f"cert_{key}"] = entries_array(cert[key])
+    if rep.solution is not None:
+        out["sol_x_entries"] = entries_array(rep.solution["x_entries"])
+        out["sol_z_entries"] = entries_array(rep.solution["z_entries"])
+        out["sol_y"] = np.array(rep.solution["y"], dtype=np.float64)
     np.savez_compressed(HERE / f"cfg{idx}_reference.npz", **out)
     print(f"cfg{idx}: {rep.status} it={rep.iterations} obj={out['tol_obj']} "
           f"tol run {time.time() - t:.1f}s")
+
+
+def section_cfg4long(fixed: int = 200, mid: int = 100):
+    cp = make_config(4)
+    t = time.time()
+    dp = to_reference(cp)
+    print(f"cfg4long: built reference problem in {time.time() - t:.1f}s", flush=True)
+    out = {"fixed_iters": np.int64(fixed), "mid_iters": np.int64(mid),
+           "gen_hash": np.array(gen_hash(cp))}
+    log = []
+
+    def cb(info):
+        log.append((info.iteration, info.pres, info.dres, info.gap, info.tau, info.kappa))
+        print(f"cfg4long: check {log[-1]} at {time.time() - t:.0f}s", flush=True)
+        if info.iteration in (mid, fixed):
+            pre = "fixed_" if info.iteration == fixed else "mid_"
+            out.update(state_summary(cp, cp.compress_vector(info.state.u),
+                                     cp.compress_vector(info.state.w_dual), pre))
+
+    t = time.time()
+    R.solve_decomposed(dp, R.SolverSettings(max_iters=fixed, tol=1e-300), iteration_callback=cb)
+    out["fixed_log"] = np.array(log)
+    out["fixed_wall_s"] = np.float64(time.time() - t)
+    np.savez_compressed(HERE / "cfg4_long_reference.npz", **out)
+    print(f"cfg4long: {fixed} iterations in {time.time() - t:.1f}s")
 
 
 if __name__ == "__main__":
@@ -202,6 +261,8 @@ if __name__ == "__main__":
             section_first()
         elif arg == "toys":
             section_toys()
+        elif arg == "cfg4long":
+            section_cfg4long()
         elif arg.startswith("cfg"):
             section_cfg(int(arg[3:]))
         else:

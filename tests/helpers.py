@@ -66,3 +66,32 @@ def dense_inner(dp) -> np.ndarray:
 def rel(a, b) -> float:
     a, b = np.asarray(a, float), np.asarray(b, float)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def fixture_state(z, cp, prefix: str = "fixed_"):
+    """Full compressed (u, w) of a config fixture (tests/golden/make_goldens.py),
+    or None when the fixture holds only samples.  w is stored on its nonzero
+    segments (z and kappa); its x / y / v parts are exactly 0."""
+    if prefix + "u" not in z.files:
+        return None
+    u = np.asarray(z[prefix + "u"], float)
+    if prefix + "w" in z.files:
+        return u, np.asarray(z[prefix + "w"], float)
+    w = np.zeros_like(u)
+    w[cp.sl_s] = z[prefix + "w_z"]
+    w[-1] = float(z[prefix + "w_kappa"])
+    return u, w
+
+
+def gen_hash(cp) -> str:
+    """SHA-256 over a generated problem's arrays (the same digest
+    tests/golden/make_goldens.py records as ``gen_hash``)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for arr in (cp.covered, cp.A.indptr, cp.A.indices, cp.A.data, cp.c, cp.b,
+                cp.sizes, np.concatenate([np.asarray(c) for c in cp.cliques])):
+        a = np.ascontiguousarray(arr)
+        h.update(str(a.dtype).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()

@@ -208,18 +208,21 @@ def _fixed_run(cfg, iters):
     return cp, states, np.array(logs)
 
 
-def _compare_state(z, cp, u, w, tol):
-    if "fixed_u" in z.files:
-        assert rel(u, z["fixed_u"]) <= tol
-        assert rel(w, z["fixed_w"]) <= tol
+def _compare_state(z, cp, u, w, tol, prefix="fixed_"):
+    from helpers import fixture_state
+
+    full = fixture_state(z, cp, prefix)
+    if full is not None:
+        assert rel(u, full[0]) <= tol
+        assert rel(w, full[1]) <= tol
         return
     # large configs: 4096 seeded sample entries + per-segment norms
     for name, vec in (("u", u), ("w", w)):
-        idx, val = z[f"fixed_{name}_idx"], z[f"fixed_{name}_val"]
+        idx, val = z[f"{prefix}{name}_idx"], z[f"{prefix}{name}_val"]
         assert rel(vec[idx], val) <= tol, name
         norms = np.array([np.linalg.norm(vec[sl]) for sl in (cp.sl_x, cp.sl_s, cp.sl_y, cp.sl_v)]
                          + [vec[-1]])
-        ref = z[f"fixed_{name}_norms"]
+        ref = z[f"{prefix}{name}_norms"]
         scale = np.linalg.norm(ref)
         assert np.all(np.abs(norms - ref) <= tol * scale), (name, norms, ref)
 
@@ -487,3 +490,72 @@ def test_report_vectors_match_host_path():
     if h.sigma_c != 1.0:
         v = v / h.sigma_c
     assert np.array_equal(hv, cp.scatter(v / tau))
+
+
+def _entries(pe):
+    return np.column_stack([pe.block, pe.i, pe.j, pe.value]).astype(float)
+
+
+def _compare_entries(got, ref, tol):
+    assert got.shape == ref.shape
+    assert np.array_equal(got[:, :3], ref[:, :3])  # block, i, j: same pattern rows, same order
+    scale = np.linalg.norm(ref[:, 3])
+    assert np.linalg.norm(got[:, 3] - ref[:, 3]) <= tol * max(scale, 1e-300)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+def test_report_entries_match_reference(golden_dir, cfg):
+    """Solution entries x_entries / z_entries / y (solver.py:553-556) and the
+    certificate's entry list (solver.py:472-503) against the reference report
+    of the same to-tolerance solve: identical [block, i, j] rows, values within
+    1e-6 relative (the final iterates agree to ~1e-10)."""
+    z = np.load(golden_dir / f"cfg{cfg}_reference.npz")
+    rep = H.solve_decomposed(make_config(cfg), H.SolverSettings())
+    assert rep.status == str(z["tol_status"])
+    if "sol_x_entries" in z.files:
+        _compare_entries(_entries(rep.solution["x_entries"]), z["sol_x_entries"], 1e-6)
+        _compare_entries(_entries(rep.solution["z_entries"]), z["sol_z_entries"], 1e-6)
+        assert rel(np.array(rep.solution["y"]), z["sol_y"]) <= 1e-6
+    else:
+        assert "cert_slack_entries" in z.files or "cert_ray_entries" in z.files
+        key = "slack_entries" if "cert_slack_entries" in z.files else "ray_entries"
+        _compare_entries(_entries(rep.certificate[key]), z[f"cert_{key}"], 1e-6)
+
+
+def test_recover_matches_solve_report(golden_dir):
+    """recover (solver.py:608-617) on the final iterate of an un-normalised
+    solve gives the same status, objectives and solution entries as the solve."""
+    cp = make_config(0)
+    st = H.SolverSettings(normalize=False)
+    last = {}
+
+    def cb(info):
+        last["state"] = info.state
+
+    rep = H.solve_decomposed(cp, st, iteration_callback=cb)
+    s = last["state"]
+    rec = H.recover(H.HsdeState(s.u.copy(), s.w_dual.copy()), cp, st, rep.iterations, rep.timing)
+    assert rec.status == rep.status == "Optimal"
+    assert rec.iterations == rep.iterations
+    assert abs(rec.objective_primal - rep.objective_primal) <= 1e-12 * abs(rep.objective_primal)
+    assert abs(rec.objective_dual - rep.objective_dual) <= 1e-12 * abs(rep.objective_dual)
+    _compare_entries(_entries(rec.solution["x_entries"]), _entries(rep.solution["x_entries"]), 1e-12)
+    _compare_entries(_entries(rec.solution["z_entries"]), _entries(rep.solution["z_entries"]), 1e-12)
+
+
+@pytest.mark.parametrize("at", ["mid", "fixed"])
+def test_config4_long_pin(golden_dir, at):
+    """Config 4 iterated 100 / 200 iterations (tol = 1e-300) against the
+    reference's own iterates (tests/golden/cfg4_long_reference.npz, ~50 min of
+    reference CPU time): 4096 seeded entries + segment norms within 1e-8."""
+    path = golden_dir / "cfg4_long_reference.npz"
+    if not path.exists():
+        pytest.skip("cfg4_long_reference.npz not generated")
+    z = np.load(path)
+    from helpers import gen_hash
+
+    cp = make_config(4)
+    assert gen_hash(cp) == str(z["gen_hash"])
+    iters = int(z[f"{at}_iters"])
+    _, st, logs = _fixed_run(4, iters)
+    _compare_state(z, cp, st["u"], st["w"], 1e-8, prefix=f"{at}_")

@@ -81,9 +81,12 @@ def test_config_fixed_iterations_match_reference(golden_dir, cfg):
         states[k] = (u.copy(), w.copy())
 
     O.solve(cp, O.OracleSettings(max_iters=500, tol=1e-300), callback=cb)
+    from helpers import fixture_state
+
     u, w = states[500]
-    assert rel(u, z["fixed_u"]) <= 1e-8
-    assert rel(w, z["fixed_w"]) <= 1e-8
+    ru, rw = fixture_state(z, cp)
+    assert rel(u, ru) <= 1e-8
+    assert rel(w, rw) <= 1e-8
 
 
 @pytest.mark.parametrize("cfg", [0, 1])
