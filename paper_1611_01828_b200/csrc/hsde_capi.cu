@@ -381,9 +381,11 @@ __global__ void k_diag_finish(double *diag, int m, int *flag) {
 }
 
 // cone launches (one shard)
-// part (CTA plan with the fast path and the cold path): 0 both, serially;
-// 1 the fast path only; 2 the cold path and its Jacobi fallback only (1 and 2
-// run concurrently on disjoint cliques: W.ccur, set by k_scalars)
+// part (CTA plan with the fast path and the cold path): 0 everything,
+// serially; 1 the fast path; 2 the cold path on the predicted cliques
+// (W.ccur, set by k_scalars; 1 and 2 run concurrently on disjoint cliques);
+// 3 the cold path on the fast path's hand-overs, then the Jacobi fallback
+// (after 1 and 2)
 int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool block,
                 const double *in, double *out, double in_scale, cudaStream_t st, int part = 0) {
   if (pl.count == 0) return 0;
@@ -411,22 +413,8 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
   const int cv = h->jacobi ? 0 : pl.cold_cv;
   ca.cfail = pl.cfail;
   const bool split = mode == CONE_HOT && pl.split_smem && h->warm && h->split;
-  if (split && part != 2) {
-    // fast path (hsde_split.cuh) on the cliques with a usable basis; its
-    // hand-overs finish on the Jacobi path in the same CTA
-    ConeArgs co = ca;
-    co.ids = s.W.corder;  // scheduled by k_scalars (s.W.cta_ids)
-    DevWork Ws = s.W;
-    if (!cv) Ws.ccur = Ws.cnext = nullptr;  // (Jacobi variant: every clique)
-    k_cone_split<false><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, Ws, co);
-    CKL();
-    if (!cv || part == 1) return 0;
-  }
-  if (cv && !(mode == CONE_HOT && !split && !h->split)) {
-    // tridiagonal cold path (hsde_cold.cuh), then its failures on the Jacobi path
-    DevWork Wc = s.W;
-    if (!split) Wc.ccur = Wc.cnext = Wc.cstate = nullptr;  // every clique
-    auto go = [&](auto kern) { kern<<<pl.count, kColdThreads, pl.cold_smem, st>>>(s.P, s.S, Wc, ca); };
+  auto cold = [&](const DevWork &Wc, const ConeArgs &a) {
+    auto go = [&](auto kern) { kern<<<pl.count, kColdThreads, pl.cold_smem, st>>>(s.P, s.S, Wc, a); };
     if (mode == CONE_HOT) {
       if (cv == 1) go(k_cone_cold<CONE_HOT, 20, 3, 3>);
       else go(k_cone_cold<CONE_HOT, 24, 3, 2>);
@@ -437,7 +425,42 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
       if (cv == 1) go(k_cone_cold<CONE_MINEIG, 20, 3, 3>);
       else go(k_cone_cold<CONE_MINEIG, 24, 3, 2>);
     }
-    CKL();
+    return cudaGetLastError();
+  };
+  if (split) {
+    if (!cv) {  // (Jacobi variant) every clique, hand-overs on the Jacobi path in the same CTA
+      ConeArgs co = ca;
+      co.ids = s.W.corder;
+      DevWork Ws = s.W;
+      Ws.ccur = Ws.cnext = nullptr;
+      k_cone_split<false><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, Ws, co);
+      CKL();
+      return 0;
+    }
+    if (part == 0 || part == 1) {  // fast path (hsde_split.cuh), scheduled by k_scalars
+      ConeArgs co = ca;
+      co.ids = s.W.corder;
+      k_cone_split<true><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, s.W, co);
+      CKL();
+    }
+    if (part == 0 || part == 2) {  // cold path on the predicted cliques
+      ConeArgs c0 = ca;
+      c0.cold_pass = 0;
+      if (cold(s.W, c0) != cudaSuccess) CKL();
+    }
+    if (part == 0 || part == 3) {  // cold path on the hand-overs, then the fallback
+      ConeArgs c1 = ca;
+      c1.cold_pass = 1;
+      if (cold(s.W, c1) != cudaSuccess) CKL();
+      ca.fail_only = 1;
+    } else {
+      return 0;
+    }
+  } else if (cv && !(mode == CONE_HOT && !h->split)) {
+    // tridiagonal cold path on every clique, then its failures on the Jacobi path
+    DevWork Wc = s.W;
+    Wc.ccur = Wc.cnext = Wc.cstate = nullptr;
+    if (cold(Wc, ca) != cudaSuccess) CKL();
     ca.fail_only = 1;
   }
   if (mode == CONE_HOT) k_cone_block<CONE_HOT><<<pl.count, kConeBlock, pl.smem, st>>>(s.P, s.S, W, ca);
@@ -654,6 +677,7 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
     int part;
   };
   std::vector<ConeJob> jobs;
+  std::vector<int> tails;  // shards whose CTA plan needs the hand-over pass after the join
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
     for (const ConePlan &wp : s.warp_plans)
@@ -664,9 +688,10 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
     const ConePlan &bp = h->sh[g].block_plan;
     if (!bp.count) continue;
     const bool two = bp.split_smem && h->warm && h->split && bp.cold_cv && !h->jacobi;
-    if (two && !ev) {  // fast path and cold path on disjoint cliques, concurrently
+    if (two && !ev) {  // fast path and cold path on disjoint cliques, concurrently (part 3 after the join)
       jobs.push_back({&h->sh[g], &bp, true, 2});
       jobs.push_back({&h->sh[g], &bp, true, 1});
+      tails.push_back(g);
     } else {
       jobs.push_back({&h->sh[g], &bp, true, 0});
     }
@@ -712,6 +737,9 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
     }
     mark(PS_CONE_WARP);
   }
+  for (int g : tails)
+    RC(launch_cone(h, h->sh[g], CONE_HOT, h->sh[g].block_plan, true, nullptr, nullptr, 1.0, st, 3));
+  nl += 2 * (int)tails.size();
   mark(PS_CONE_BLOCK);
   if (branch_x) CK(cudaStreamWaitEvent(st, h->ev_xjoin, 0));
   else RC(launch_xupd(st));
@@ -838,6 +866,7 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
       s.W.cta_ids = s.block_plan.ids;  // k_scalars schedules them for k_cone_split
       s.W.cta_n = s.block_plan.count;
       CK(cudaFuncSetAttribute(k_cone_split<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_cone_split<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     }
     CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));

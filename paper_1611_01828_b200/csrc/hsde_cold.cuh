@@ -737,15 +737,17 @@ __device__ int cold_one(const DevProblem &P, const DevState &S, const DevWork &W
     __syncthreads();
     return COLD_OK;
   }
-  if (MODE == CONE_HOT && W.cnext) {
+  if (MODE == CONE_HOT && W.cnext && !xin) {
     // next iteration on the fast path when it would apply with margin:
-    // off(B) <= |X_next - X|_F, predicted by |X - X_prev|_F, against 0.3 min |lam|
-    // (the fast path's g; hsde_split.cuh applies at off(B) <= g / 3)
+    // off(B) <= |X_next - X|_F, predicted by |X - X_prev|_F, against min |lam|
+    // (the fast path's g; hsde_split.cuh applies at off(B) <= 0.45 g)
     dx2 = cta_sum(dx2, cs.misc);
     double g = CUDART_INF;
     for (int i = 0; i < d; ++i) g = fmin(g, fabs(cs.lam[i]));
     const bool prev = (W.vvalid[k] & ~kVRefresh) > 0;
-    if (tid == 0) W.cnext[k] = (prev && dx2 <= 0.09 * g * g) ? 0 : 1;
+    // (measured on config 4: off(B) / |X - X_prev|_F ~ 0.3 - 0.5, so |dX| <= 0.6 g
+    // predicts off(B) <~ 0.3 g, inside the fast path's 0.45 g)
+    if (tid == 0) W.cnext[k] = (prev && dx2 <= 0.36 * g * g) ? 0 : 1;  // |dX| <= 0.6 g
   }
   if (MODE == CONE_HOT) {
     double *su = S.u + so + off, *sw = S.w + so + off;
@@ -785,19 +787,26 @@ __global__ void __launch_bounds__(kColdThreads, MINB) k_cone_cold(DevProblem P, 
   const int k = ca.ids[blockIdx.x];
   const int d = P.cl_size[k];
   int cst = SPLIT_UNTOUCHED;
-  if (MODE == CONE_HOT && W.ccur && !W.ccur[k]) {  // on the warm path this iteration (k_cone_split)
-    if (threadIdx.x == 0 && ca.cfail) ca.cfail[blockIdx.x] = 0;
-    return;
+  bool xin = false;
+  if (MODE == CONE_HOT && W.ccur) {
+    if (ca.cold_pass == 0 && !W.ccur[k]) {  // on the warm path this iteration (k_cone_split)
+      if (threadIdx.x == 0 && ca.cfail) ca.cfail[blockIdx.x] = 0;
+      return;
+    }
+    if (ca.cold_pass == 1) {  // after k_cone_split: its hand-overs (X in W.xarg)
+      cst = W.cstate[k];
+      if (W.ccur[k] || cst < SPLIT_HANDOFF || cst > SPLIT_HANDOFF + 3) return;
+      xin = true;
+    }
   }
   ConeArgs c2 = ca;
   c2.slot = blockIdx.x;
   const bool fits = d <= 32 * MR && d <= kColdNW * MC;
-  const bool xin = false;
   int st = COLD_FAIL;
   if (fits) {
     st = cold_one<MODE, MC, MR>(P, S, W, c2, k, smem, xin);
   } else if (MODE == CONE_HOT && !xin) {
-    // the Jacobi fallback reads X from W.xarg: do the slot update here
+    // the Jacobi fallback reads raw X from W.xarg: do the slot update here
     const double shift = W.scal[S_SHIFT];
     const int64_t off = P.cl_off[k];
     for (int e = threadIdx.x; e < d * d; e += blockDim.x) W.xarg[off + e] = hot_slot_load(P, S, W, off + e, shift);
@@ -806,6 +815,7 @@ __global__ void __launch_bounds__(kColdThreads, MINB) k_cone_cold(DevProblem P, 
     if (ca.cfail) ca.cfail[blockIdx.x] = st == COLD_FAIL ? 1 : 0;
     if (MODE == CONE_HOT && W.cstate) W.cstate[k] = SPLIT_DONE + 32 + cst;  // (stats: finished here)
     if (MODE == CONE_HOT && W.ckey) W.ckey[k] = 1;
+    if (MODE == CONE_HOT && xin && W.cnext) W.cnext[k] = 1;  // a hand-over: cold next time too
   }
 }
 
@@ -827,8 +837,10 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, D
   int st = SPLIT_UNTOUCHED;
   if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d > 32) st = split_one(P, S, W, c2, k, smem);
   if (threadIdx.x == 0) W.cstate[k] = st;
-  if (COLD || st == SPLIT_DONE || st == SPLIT_DONE + 16) return;
-  if (threadIdx.x == 0 && W.cnext && st != SPLIT_UNTOUCHED) W.cnext[k] = 1;  // stalled: cold next
+  if (st == SPLIT_DONE || st == SPLIT_DONE + 16) return;
+  if (threadIdx.x == 0 && W.cnext && st != SPLIT_UNTOUCHED) W.cnext[k] = 1;  // handed over: cold next
+  if (COLD && st != SPLIT_UNTOUCHED) return;  // k_cone_cold (cold_pass 1) finishes it from W.xarg
+
   __syncthreads();  // cstate and the hand-off B are visible to the whole CTA
   BlockTeam tm{(int)threadIdx.x, (int)blockDim.x};
   cone_one<CONE_HOT>(tm, P, S, W, c2, k, smem);

@@ -1208,6 +1208,7 @@ struct ConeArgs {
   int *cfail;        // cold path (hsde_cold.cuh): [count] 1 = handed to the Jacobi path
   int fail_only;     // k_cone_block: only the slots flagged in cfail (HOT: raw X in W.xarg)
   int cold;          // k_cone_split: hand-overs go to the cold path (X kept in W.xarg)
+  int cold_pass;     // k_cone_cold after k_cone_split: 0 the predicted cliques (W.ccur), 1 its hand-overs
 };
 
 // Hot-path load of slot j: builds arg_s and performs the v / w_v update and

@@ -43,7 +43,7 @@ static_assert(((kSplitMaxD + 15) / 16) * ((kSplitMaxD + 15) / 16 + 1) / 2 <= kSp
               "kSplitMaxD: B's upper blocks exceed the warps' register blocks");
 constexpr int kSplitRefreshIters = 1000;  // fixed-point passes that ask for a Jacobi refresh of V
 constexpr int kLoadBatch = 4;          // hot-path slots per thread in flight
-constexpr double kSplitOff2 = 1.0 / 9.0;  // fast path while off(B)^2 <= kSplitOff2 g^2
+constexpr double kSplitOff2 = 0.2;  // fast path while off(B)^2 <= kSplitOff2 g^2 (off < 0.45 g: Weyl keeps the inertia)
 constexpr int kSplitMaxPasses = 24;     // fixed-point passes before handing over
 // fixed-point stop: estimated remaining Riccati residual <= kSplitTol |B|_F
 // (below the rounding of the d-term products themselves, ~ d eps |B|)
@@ -461,9 +461,10 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     nb2 = o2 + cta_sum(l2, red);
   };
   measure();
-  if (!(o2 <= kSplitOff2 * g * g) && g > 0.0 && o2 < CUDART_INF && ca.cold) {
-    // the within-class drift of the kept basis made the split inapplicable:
-    // the cold path (hsde_cold.cuh) re-diagonalises X (still in xg) in this CTA
+  if (!(o2 <= kSplitOff2 * g * g) && g > 0.0 && o2 < CUDART_INF && ca.cold && o2 > 0.36 * g * g) {
+    // the kept basis is far from diagonalising X (off(B) > 0.6 g): the cold path
+    // (hsde_cold.cuh) re-diagonalises X (still in xg); closer to the bound a
+    // warm Jacobi refresh in this CTA is cheaper (below)
     return SPLIT_HANDOFF + 3;
   }
   if (!(o2 <= kSplitOff2 * g * g) && g > 0.0 && o2 < CUDART_INF) {
@@ -924,7 +925,9 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   }
   SPLIT_STAMP(8);
   if (tid == 0 && W.sweeps) W.sweeps[k] = -it;  // (stats: fixed-point iterations)
-  if (tid == 0 && W.cnext && !refreshed) W.cnext[k] = 0;
+  // next iteration: the cold path when this basis was already near the bound
+  // (off(B) > 0.35 g: the drift of a kept basis grows), else the fast path
+  if (tid == 0 && W.cnext && !refreshed) W.cnext[k] = o2 > 0.1225 * g * g ? 1 : 0;
   // schedule key for the next iteration: passes, plus a refresh risk when off(B)
   // is already near the applicability bound
   if (tid == 0) W.ckey[k] = o2 > kSplitKey2 * kSplitOff2 * g * g ? 1 : 0;

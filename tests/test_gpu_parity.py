@@ -559,3 +559,30 @@ def test_config4_long_pin(golden_dir, at):
     iters = int(z[f"{at}_iters"])
     _, st, logs = _fixed_run(4, iters)
     _compare_state(z, cp, st["u"], st["w"], 1e-8, prefix=f"{at}_")
+
+
+@pytest.mark.parametrize("d,h", [(57, 40), (71, 40), (40, 40)])
+def test_large_cliques_hot_path(d, h):
+    """Cliques of order 97 and 111 (above the fast path's and the cold path's
+    register tiles: the Jacobi path) and 80 (fast + cold path) through 80 hot
+    iterations against the CPU oracle at 1e-8 (orders 97-112)."""
+    from oracle import hsde_oracle as O
+    from paper_1611_01828_b200.synthetic import block_arrow
+
+    cp = block_arrow(3, d, h, 30, 0.05, 11, f"arrow_{d}_{h}")
+    assert int(cp.sizes.max()) == d + h
+    got = {}
+
+    def cb(info):
+        if info.iteration == 80:
+            got["u"] = info.state.u.copy()
+
+    H.solve_decomposed(cp, H.SolverSettings(max_iters=80, tol=1e-300), iteration_callback=cb)
+    ref = {}
+
+    def ocb(k, p, dd, g, tau, kap, u, w):
+        if k == 80:
+            ref["u"] = u.copy()
+
+    O.solve(cp, O.OracleSettings(max_iters=80, tol=1e-300), callback=ocb)
+    assert rel(got["u"], ref["u"]) <= 1e-8

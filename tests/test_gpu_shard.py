@@ -78,3 +78,46 @@ def test_nccl_path_single_rank():
                        comm=comm)
     assert rel(got["u"], a["u"]) <= 1e-12
     assert np.allclose(np.array(logs)[:, 1:4], la[:, 1:4], rtol=1e-9)
+
+
+@pytest.fixture(scope="module")
+def cfg4_single():
+    """Config 4 (the BENCH workload), 40 iterations on the single-shard path."""
+    cp = make_config(4)
+    a, la = _run(cp, 40)
+    return cp, a, la
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_config4_emulated_shards(cfg4_single, G):
+    """Config 4 cut into G clique shards (G = 8: 50 cliques per shard), the
+    shards emulated on this device with the NCCL path's reduction points:
+    iterates within 1e-10 of the single-shard path after 40 iterations, and
+    every shard keeps the symmetric half passes (the arrow-head mirror pairs
+    are owned by one rank, so no pair is split across shards)."""
+    from paper_1611_01828_b200 import _lib
+    from paper_1611_01828_b200.shard import make_shards
+
+    cp, a, la = cfg4_single
+    shards = make_shards(cp, G)
+    h = _lib.Handle(cp, shards=shards)
+    try:
+        assert h.n_shards == G
+        assert h.half_passes
+    finally:
+        h.close()
+    b, lb = _run(cp, 40, shards=G)
+    assert rel(b["u"], a["u"]) <= 1e-10
+    assert rel(b["w"], a["w"]) <= 1e-10
+    assert np.allclose(lb[:, 1:4], la[:, 1:4], rtol=1e-7)
+
+
+def test_config4_emulated_shards_to_tolerance(golden_dir):
+    """Config 4 on 8 emulated shards to tolerance: the reference's status,
+    iteration count (+-2) and primal objective (1e-6)."""
+    z = np.load(golden_dir / "cfg4_reference.npz")
+    rep = H.solve_decomposed(make_config(4), H.SolverSettings(), shards=8)
+    assert rep.status == str(z["tol_status"])
+    assert abs(rep.iterations - int(z["tol_iters"])) <= 2
+    ref = z["tol_obj"]
+    assert abs(rep.objective_primal - ref[0]) <= 1e-6 * abs(ref[0])

@@ -104,3 +104,14 @@ def test_config_to_tolerance_matches_reference(golden_dir, cfg):
         ref = z["tol_obj"]
         assert abs(out["objective_primal"] - ref[0]) <= 1e-6 * abs(ref[0])
         assert abs(out["objective_dual"] - ref[1]) <= 1e-6 * abs(ref[1])
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+def test_generator_hash_matches_fixture(golden_dir, cfg):
+    """The synthetic generator still produces the problems the reference
+    fixtures were computed on (tests/golden/make_goldens.py gen_hash)."""
+    from helpers import gen_hash
+    from paper_1611_01828_b200.synthetic import make_config
+
+    z = np.load(golden_dir / f"cfg{cfg}_reference.npz")
+    assert gen_hash(make_config(cfg)) == str(z["gen_hash"])
