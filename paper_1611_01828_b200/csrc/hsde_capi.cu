@@ -84,6 +84,8 @@ struct ConePlan {
   int cold_cv = 0;             // CTA plan: tridiagonal cold path variant (0: Jacobi)
   size_t cold_smem = 0;
   int *cfail = nullptr;        // [count] cold-path failures (follow-up Jacobi launch)
+  int wper_block = 0;          // warp plan, cold path: warps per CTA and shared memory
+  size_t wsmem = 0;
 };
 
 enum Mode { MODE_SINGLE = 0, MODE_EMULATED = 1, MODE_NCCL = 2 };
@@ -402,6 +404,19 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
   if (!block) {
     const int grid = (pl.count + pl.per_block - 1) / pl.per_block;
     const int thr = pl.per_block * 32;
+    if (!h->jacobi && pl.cfail && mode != CONE_HOT) {
+      // warp cold path (hsde_cold.cuh), then its failures on the warp Jacobi
+      // path.  (Not on the hot path: warm-started warp Jacobi is faster there,
+      // e.g. config 1: 33 vs 77 us per projection; measured, tools/small_profile.py)
+      ca.cfail = pl.cfail;
+      const int wg = (pl.count + pl.wper_block - 1) / pl.wper_block;
+      const int wt = pl.wper_block * 32;
+      if (mode == CONE_HOT) k_cone_wcold<CONE_HOT><<<wg, wt, pl.wsmem, st>>>(s.P, s.S, s.W, ca);
+      else if (mode == CONE_PLAIN) k_cone_wcold<CONE_PLAIN><<<wg, wt, pl.wsmem, st>>>(s.P, s.S, s.W, ca);
+      else k_cone_wcold<CONE_MINEIG><<<wg, wt, pl.wsmem, st>>>(s.P, s.S, s.W, ca);
+      CKL();
+      ca.fail_only = 1;
+    }
     if (mode == CONE_HOT) k_cone_warp<CONE_HOT><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
     else if (mode == CONE_PLAIN) k_cone_warp<CONE_PLAIN><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
     else k_cone_warp<CONE_MINEIG><<<grid, thr, pl.smem, st>>>(s.P, s.S, s.W, ca);
@@ -800,10 +815,14 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
   std::vector<int> wids[3], bids;
   const int wcap[3] = {8, 16, 32};
   int dpb = 2;
+  // few cliques (less than two per SM): CTA teams for every clique of order
+  // >= 8 -- the fast / cold paths cut the projection latency that a warp team
+  // cannot hide (config 0: 20 cliques of order 20)
+  const bool few = p <= 296;
   for (int k = 0; k < p; ++k) {
     const int d = sizes[k];
     const int dp = d + (d & 1);
-    if (d <= 32) {
+    if (d <= 32 && !(few && d >= 8)) {
       wids[dp <= 8 ? 0 : dp <= 16 ? 1 : 2].push_back(k);
     } else {
       bids.push_back(k);
@@ -823,12 +842,22 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
     pl.per_block = pb;
     pl.smem = per_warp * pb;
     if (!wids[c].empty()) RC(dupload(h, &pl.ids, wids[c].data(), wids[c].size()));
+    // warp cold path: 8 warps per CTA for the small classes, 4 for d <= 32
+    pl.wper_block = wcap[c] <= 16 ? 8 : 4;
+    pl.wsmem = (size_t)wcold_scratch_doubles(wcap[c]) * sizeof(double) * pl.wper_block;
+    if (!wids[c].empty()) {
+      RC(dalloc(h, &pl.cfail, wids[c].size()));
+      CK(cudaMemset(pl.cfail, 0, sizeof(int) * wids[c].size()));
+    }
   }
   {
     const int sm = maxsm;  // attribute is per kernel, shared by every shard / handle
     CK(cudaFuncSetAttribute(k_cone_warp<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_warp<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_warp<CONE_MINEIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute(k_cone_wcold<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute(k_cone_wcold<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    CK(cudaFuncSetAttribute(k_cone_wcold<CONE_MINEIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   }
   s.block_plan.count = (int)bids.size();
   s.block_plan.dpmax = dpb;

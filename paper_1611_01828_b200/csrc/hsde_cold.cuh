@@ -753,12 +753,9 @@ __device__ int cold_one(const DevProblem &P, const DevState &S, const DevWork &W
     double *su = S.u + so + off, *sw = S.w + so + off;
     auto xat = [&](int a, int b) { return 0.5 * (xg[a * d + b] + xg[b * d + a]); };
     cold_finish(
-        d, cs, W.vstore + off, g2, xat,
-        [&](int a, int b, double v) {
-          su[a * d + b] = v;
-          sw[a * d + b] += v;  // w_s = (w_s - us_h) + P (solver.py:391-394)
-        },
-        W.dbg);
+        d, cs, W.vstore + off, g2, xat, [&](int a, int b, double v) { su[a * d + b] = v; }, W.dbg);
+    __syncthreads();
+    for (int e = tid; e < d * d; e += T) sw[e] += su[e];  // w_s = (w_s - us_h) + P (solver.py:391-394)
     if (tid == 0) {
       W.vvalid[k] = 1;
       if (W.sweeps) W.sweeps[k] = 0;
@@ -835,7 +832,7 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, D
   c2.cold = COLD;
   if (W.ccur && W.ccur[k]) return;  // this iteration on the cold path (k_cone_cold, concurrent)
   int st = SPLIT_UNTOUCHED;
-  if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d > 32) st = split_one(P, S, W, c2, k, smem);
+  if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d >= 8) st = split_one(P, S, W, c2, k, smem);
   if (threadIdx.x == 0) W.cstate[k] = st;
   if (st == SPLIT_DONE || st == SPLIT_DONE + 16) return;
   if (threadIdx.x == 0 && W.cnext && st != SPLIT_UNTOUCHED) W.cnext[k] = 1;  // handed over: cold next
@@ -848,4 +845,331 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, D
     W.cstate[k] = SPLIT_DONE + 32 + st;  // (stats: finished by the Jacobi path)
     W.ckey[k] = 1;                        // schedule first next time
   }
+}
+
+// ===========================================================================
+// Warp-sized cliques (d <= 32): the same cold eigensolver run by one warp per
+// clique, the matrix in the warp's shared-memory slice (lane i owns row i;
+// no CTA barriers, __syncwarp only).  Replaces the warp Jacobi sweeps on the
+// hot path of the many-small-clique configurations.
+
+__host__ __device__ inline int wcold_ld(int dp) { return dp | 1; }
+__host__ __device__ inline int64_t wcold_scratch_doubles(int dp) {
+  const int ld = wcold_ld(dp);
+  const int64_t n = (int64_t)dp * ld + ((int64_t)dp * (dp - 1) / 2 + 2) + 2 * 32 + 6 * 32 + 8 + (3 * 32 + 2) / 2 + 2;
+  return (n + 1) & ~int64_t(1);
+}
+
+struct WColdSmem {
+  double *Z, *Hv, *vb, *wb, *dg, *es, *e2, *taus, *lam, *lamu, *misc;
+  int *rank, *bs, *be, *flag;
+  int ld;
+};
+
+__device__ inline WColdSmem wcold_carve(double *base, int dp) {
+  WColdSmem c;
+  c.ld = wcold_ld(dp);
+  c.Z = base;
+  c.Hv = c.Z + (int64_t)dp * c.ld;
+  c.vb = c.Hv + ((int64_t)dp * (dp - 1) / 2 + 2);
+  c.wb = c.vb + 32;
+  c.dg = c.wb + 32;
+  c.es = c.dg + 32;
+  c.e2 = c.es + 32;
+  c.taus = c.e2 + 32;
+  c.lam = c.taus + 32;
+  c.lamu = c.lam + 32;
+  c.misc = c.lamu + 32;
+  c.rank = reinterpret_cast<int *>(c.misc + 8);
+  c.bs = c.rank + 32;
+  c.be = c.bs + 32;
+  c.flag = c.be + 32;
+  return c;
+}
+
+__device__ __forceinline__ double warp_allmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_allmin(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// eigendecomposition of the symmetric X in Z (rows / columns < d <= 32):
+// COLD_OK with lam ascending (unscaled) and, unless values_only, Z = V
+__device__ int wcold_eig(int d, const WColdSmem &c, bool values_only) {
+  const int l = threadIdx.x & 31, ld = c.ld;
+  // ---- Householder tridiagonalisation (dsytd2 order), lane i owns row i
+  for (int s = 0; s + 2 < d; ++s) {
+    const double x = l < d ? c.Z[l * ld + s] : 0.0;
+    const double sig = warp_allsum((l > s + 1 && l < d) ? x * x : 0.0);
+    const double x0 = __shfl_sync(0xffffffffu, x, (s + 1) & 31), dss = __shfl_sync(0xffffffffu, x, s & 31);
+    double tau = 0.0, beta = x0, scal = 0.0;
+    if (sig > 0.0) {
+      const double n2 = fma(x0, x0, sig), rn = rsqrt(n2), nx = n2 * rn;
+      beta = -copysign(nx, x0);
+      tau = fma(fabs(x0), rn, 1.0);
+      scal = copysign(__drcp_rn(fabs(x0) + nx), x0);
+    }
+    const double v = l == s + 1 ? 1.0 : ((l > s + 1 && l < d) ? x * scal : 0.0);
+    c.vb[l] = v;
+    if (l > s && l < d) c.Hv[cold_hoff(s, d) + (l - s - 1)] = v;
+    if (l == 0) {
+      c.dg[s] = dss;
+      c.es[s] = beta;
+      c.taus[s] = tau;
+    }
+    __syncwarp();
+    double p = 0.0;
+    if (l > s && l < d)
+      for (int k = s + 1; k < d; ++k) p = fma(c.Z[l * ld + k], c.vb[k], p);
+    p *= tau;
+    const double K = -0.5 * tau * warp_allsum(p * v);
+    const double wv = fma(K, v, p);
+    c.wb[l] = wv;
+    __syncwarp();
+    if (l > s && l < d)
+      for (int k = s + 1; k < d; ++k) c.Z[l * ld + k] = fma(-v, c.wb[k], fma(-wv, c.vb[k], c.Z[l * ld + k]));
+    __syncwarp();
+  }
+  if (l == 0) {
+    if (d >= 2) {
+      c.dg[d - 2] = c.Z[(d - 2) * ld + d - 2];
+      c.es[d - 2] = c.Z[(d - 1) * ld + d - 2];
+    }
+    c.dg[d - 1] = c.Z[(d - 1) * ld + d - 1];
+  }
+  __syncwarp();
+  // ---- scale T, split, blocks
+  double gl = CUDART_INF, gh = -CUDART_INF;
+  if (l < d) {
+    const double el = l > 0 ? fabs(c.es[l - 1]) : 0.0, er = l + 1 < d ? fabs(c.es[l]) : 0.0;
+    gl = c.dg[l] - el - er;
+    gh = c.dg[l] + el + er;
+  }
+  gl = warp_allmin(gl);
+  gh = warp_allmax(gh);
+  const double tn = fmax(fabs(gl), fabs(gh));
+  if (!(tn < CUDART_INF)) return COLD_FAIL + 1;  // non-finite
+  double sc = 1.0;
+  if (tn > 0.0) {
+    int ex;
+    frexp(tn, &ex);
+    sc = ldexp(1.0, -ex);
+  }
+  __syncwarp();
+  if (l < d) {
+    c.dg[l] *= sc;
+    if (l + 1 < d) {
+      const double e = c.es[l] * sc;
+      c.es[l] = fabs(e) <= 0x1p-52 ? 0.0 : e;
+      c.e2[l] = c.es[l] * c.es[l];
+    }
+  }
+  __syncwarp();
+  if (l < d) {
+    int b0 = l, b1 = l;
+    while (b0 > 0 && c.es[b0 - 1] != 0.0) --b0;
+    while (b1 < d - 1 && c.es[b1] != 0.0) ++b1;
+    c.bs[l] = b0;
+    c.be[l] = b1;
+  }
+  __syncwarp();
+  // ---- bisection (multisection: g lanes per eigenvalue)
+  {
+    int g = 1;
+    while (2 * g * d <= 32) g *= 2;
+    const double lo0 = gl * sc - 0x1p-40, hi0 = gh * sc + 0x1p-40;
+    const int rounds = (int)ceilf(54.0f / log2f((float)(g + 1)));
+    const double ig = 1.0 / (g + 1);
+    const int j = min(l / g, d - 1), q = l - (l / g) * g;
+    const int b0 = c.bs[j], b1 = c.be[j], jj = j - b0;
+    double lo = lo0, hi = hi0;
+    for (int rd = 0; rd < rounds; ++rd) {
+      const double xx = fma(hi - lo, (q + 1) * ig, lo);
+      const int cnt = sturm_count(c.dg, c.e2, b0, b1, xx);
+      double lc = cnt <= jj ? xx : -CUDART_INF, hc = cnt > jj ? xx : CUDART_INF;
+      for (int o = g >> 1; o > 0; o >>= 1) {
+        lc = fmax(lc, __shfl_xor_sync(0xffffffffu, lc, o));
+        hc = fmin(hc, __shfl_xor_sync(0xffffffffu, hc, o));
+      }
+      lo = fmax(lo, lc);
+      hi = fmin(hi, hc);
+    }
+    if (q == 0 && l < g * d) c.lamu[j] = 0.5 * (lo + hi);
+  }
+  __syncwarp();
+  int bad = 0;
+  if (l < d) {
+    const double lj = c.lamu[l];
+    int rk = 0;
+    for (int i = 0; i < d; ++i) {
+      const double li = c.lamu[i];
+      rk += (li < lj) || (li == lj && i < l);
+    }
+    c.rank[l] = rk;
+    c.lam[rk] = lj / sc;
+    if (l > c.bs[l] && !(lj - c.lamu[l - 1] > 0x1p-40)) bad = 1;
+    if (!(fabs(lj) < CUDART_INF)) bad = 2;
+  }
+  bad = __reduce_max_sync(0xffffffffu, bad);
+  __syncwarp();
+  if (bad) return COLD_FAIL + (bad == 2);
+  if (values_only) return COLD_OK;
+  // ---- eigenvectors of T into the sorted columns of Z (the reduced matrix is dead)
+  if (l < d && !twisted_vector(c.dg, c.es, c.bs[l], c.be[l], c.lamu[l], c.Z + c.rank[l], ld, d)) bad = 1;
+  bad = __reduce_max_sync(0xffffffffu, bad);
+  __syncwarp();
+  if (bad) return COLD_FAIL;
+  // ---- back transformation, lane j owns column j
+  if (l < d)
+    for (int s = d - 3; s >= 0; --s) {
+      const double tau = c.taus[s];
+      if (tau == 0.0) continue;
+      const double *hv = c.Hv + cold_hoff(s, d) - (s + 1);
+      double t = 0.0;
+      for (int i = s + 1; i < d; ++i) t = fma(hv[i], c.Z[i * ld + l], t);
+      t *= tau;
+      for (int i = s + 1; i < d; ++i) c.Z[i * ld + l] = fma(-t, hv[i], c.Z[i * ld + l]);
+    }
+  __syncwarp();
+  return COLD_OK;
+}
+
+// one warp per clique; failures flagged in ca.cfail[warp slot] for the warp
+// Jacobi launch that follows (k_cone_warp with ca.fail_only)
+template <int MODE>
+__device__ int wcold_one(const DevProblem &P, const DevState &S, const DevWork &W, const ConeArgs &ca, int k,
+                         double *scratch) {
+  const int d = P.cl_size[k];
+  const int l = threadIdx.x & 31;
+  const int64_t off = P.cl_off[k], so = P.n_c;
+  if (d == 1) {  // np.maximum(b, 0.0)
+    if (l == 0) {
+      const double a = MODE == CONE_HOT ? hot_slot_load(P, S, W, off, W.scal[S_SHIFT]) : ca.in[off] * ca.in_scale;
+      const double pr = (a != a) ? a : (a > 0.0 ? a : 0.0);
+      if (MODE == CONE_HOT) {
+        S.u[so + off] = pr;
+        S.w[so + off] += pr;
+      } else if (MODE == CONE_PLAIN) {
+        ca.out[off] = pr;
+      } else {
+        ca.out[k] = a;
+      }
+    }
+    return COLD_OK;
+  }
+  const WColdSmem c = wcold_carve(scratch, ca.dpmax);
+  const int ld = c.ld;
+  double *xg = W.xarg + off;
+  if (MODE == CONE_HOT) {
+    const double shift = W.scal[S_SHIFT];
+    for (int e = l; e < d * d; e += 32) {
+      const int a = e / d, b = e - a * d;
+      const double x = hot_slot_load(P, S, W, off + e, shift);
+      c.Z[a * ld + b] = x;
+      xg[e] = x;
+    }
+  } else {
+    for (int e = l; e < d * d; e += 32) {
+      const int a = e / d, b = e - a * d;
+      c.Z[a * ld + b] = ca.in[off + e] * ca.in_scale;
+    }
+  }
+  __syncwarp();
+  for (int e = l; e < d * d; e += 32) {  // sym = 0.5 (B + B')  (symmat.py:157)
+    const int a = e / d, b = e - a * d;
+    if (a < b) {
+      const double s = 0.5 * (c.Z[a * ld + b] + c.Z[b * ld + a]);
+      c.Z[a * ld + b] = s;
+      c.Z[b * ld + a] = s;
+    }
+  }
+  __syncwarp();
+  const int st = wcold_eig(d, c, MODE == CONE_MINEIG);
+  if (st == COLD_FAIL + 1) {  // non-finite eigenvalue: EigenFailure (symmat.py:162-163)
+    if (l == 0) atomicOr(W.err, 1);
+    return COLD_OK;
+  }
+  if (st != COLD_OK) return COLD_FAIL;
+  if (MODE == CONE_MINEIG) {
+    if (l == 0) ca.out[k] = c.lam[0];
+    return COLD_OK;
+  }
+  // ---- one Newton-Schulz step when V'V departs from I (lane j: column j)
+  {
+    double gcol[32];
+    double dev = 0.0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      double g = 0.0;
+      if (q < d && l < d)
+        for (int i = 0; i < d; ++i) g = fma(c.Z[i * ld + l], c.Z[i * ld + q], g);
+      gcol[q] = g;
+      if (q < d && l < d) dev = fmax(dev, fabs(g - (q == l ? 1.0 : 0.0)));
+    }
+    dev = warp_allmax(dev);
+    if (dev > 0x1p-46)
+      for (int i = 0; i < d; ++i) {  // row by row: every lane reads row i, then writes its entry
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          if (q < d) acc = fma(c.Z[i * ld + q], gcol[q], acc);
+        const double vn = l < d ? fma(-0.5, acc, 1.5 * c.Z[i * ld + l]) : 0.0;
+        __syncwarp();
+        if (l < d) c.Z[i * ld + l] = vn;
+        __syncwarp();
+      }
+  }
+  // ---- P = W W' (W = V_C sqrt |lam_C|, the smaller class C) or X + W W'
+  int r = 0;
+  for (int i = 0; i < d; ++i) r += c.lam[i] > 0.0;
+  const bool pos = r <= d - r;
+  const int c0 = pos ? d - r : 0, K = pos ? r : d - r;
+  if (l >= c0 && l < c0 + K) {
+    const double f = sqrt(fabs(c.lam[l]));
+    for (int i = 0; i < d; ++i) c.Z[i * ld + l] *= f;
+  }
+  __syncwarp();
+  double wrow[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) wrow[q] = (l < d && q < K) ? c.Z[l * ld + c0 + q] : 0.0;
+  double *su = S.u + so + off, *sw = S.w + so + off;
+  for (int i = 0; i < d; ++i) {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (q < K) acc = fma(c.Z[i * ld + c0 + q], wrow[q], acc);
+    if (l < d) {
+      double pv = acc;
+      if (!pos) {
+        const double xa = MODE == CONE_HOT ? 0.5 * (xg[i * d + l] + xg[l * d + i])
+                                           : 0.5 * (ca.in[off + i * d + l] + ca.in[off + l * d + i]) * ca.in_scale;
+        pv += xa;
+      }
+      if (MODE == CONE_HOT) {
+        su[i * d + l] = pv;
+        sw[i * d + l] += pv;  // w_s = (w_s - us_h) + P (solver.py:391-394)
+      } else {
+        ca.out[off + i * d + l] = pv;
+      }
+    }
+  }
+  if (MODE == CONE_HOT && l == 0 && W.sweeps) W.sweeps[k] = 0;
+  return COLD_OK;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_cone_wcold(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
+  extern __shared__ __align__(16) double smem[];
+  const int wid = threadIdx.x >> 5;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + wid;
+  if (gw >= ca.count) return;
+  double *scratch = smem + (int64_t)wid * wcold_scratch_doubles(ca.dpmax);
+  const int k = ca.ids[gw];
+  const int st = P.cl_size[k] <= 32 ? wcold_one<MODE>(P, S, W, ca, k, scratch) : COLD_FAIL;
+  if ((threadIdx.x & 31) == 0 && ca.cfail) ca.cfail[gw] = st == COLD_FAIL ? 1 : 0;
 }

@@ -1440,6 +1440,7 @@ __global__ void __launch_bounds__(kBlock) k_cone_warp(DevProblem P, DevState S, 
   const int wid = threadIdx.x >> 5;
   const int gw = blockIdx.x * (blockDim.x >> 5) + wid;
   if (gw >= ca.count) return;
+  if (ca.fail_only && !ca.cfail[gw]) return;  // after the warp cold path: its failures only
   double *scratch = smem + (int64_t)wid * jacobi_scratch_doubles(ca.dpmax);
   WarpTeam tm{(int)(threadIdx.x & 31)};
   ConeArgs c2 = ca;
