@@ -149,6 +149,31 @@ KERNELS = {"k_cone_cta": "k_cone_split", "k_ua": "k_ua_half",
            "k_spmv_seg": "k_pair_sum + k_spmv_half + k_rowsum_tiles"}
 
 
+def config_dict(cp, cfg: int, world: int) -> dict:
+    """The `config` object of both arms (identical keys and values)."""
+    from paper_1611_01828_b200.synthetic import CONFIG_NAMES, config_stats
+
+    return {"workload": CONFIG_NAMES[cfg], **config_stats(cp),
+            "parallelism": "single GPU" if world == 1 else
+            f"clique shards x{world} (NCCL all-reduce: separators, A t, c.ua)",
+            "l2": "no flush: per-iteration working set > 126 MB L2 (A in SELL layouts ~0.53 GB + state ~0.11 GB)"}
+
+
+def host_info() -> dict:
+    """CPU model and core counts of this host (lscpu), for the CPU baselines."""
+    out = {"os_cpu_count": os.cpu_count()}
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in txt.splitlines():
+            k, _, v = line.partition(":")
+            k, v = k.strip(), v.strip()
+            if k in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU(s)"):
+                out[k] = v
+    except Exception:
+        pass
+    return out
+
+
 def cp_schur_diag(cp) -> bool:
     counts = np.bincount(cp.A.indices, minlength=cp.N_c)
     return bool(counts.max(initial=0) <= 1)
@@ -207,15 +232,27 @@ def roofline_for(cp, prof_ms: dict, launches_per_kernel: int, peaks: dict, half:
 
 
 def cpu_sample(cp, budget_s: float, max_iters: int | None = None, warmup: int = 0,
-               warm_budget_s: float = 30.0):
+               warm_budget_s: float = 30.0, blas_threads: int | None = None):
     """Time the oracle port on this host: setup, up to `warmup` untimed
     iterations (within warm_budget_s), then iterations until max_iters or
-    budget_s of loop time."""
+    budget_s of loop time.  blas_threads: limit the BLAS pool (threadpoolctl;
+    BASELINE.md section 3 asks for all cores and OPENBLAS_NUM_THREADS=1)."""
+    import contextlib
+
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+    except Exception:
+        threadpool_info = threadpool_limits = None
+    ctx = (threadpool_limits(limits=blas_threads) if (blas_threads and threadpool_limits)
+           else contextlib.nullcontext())
+    with ctx:
+        return _cpu_sample(cp, budget_s, max_iters, warmup, warm_budget_s, threadpool_info)
+
+
+def _cpu_sample(cp, budget_s, max_iters, warmup, warm_budget_s, threadpool_info):
     from oracle import hsde_oracle as O
 
     try:
-        from threadpoolctl import threadpool_info
-
         threads = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
     except Exception:
         threads = os.cpu_count() or 1
@@ -263,8 +300,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": s["iterations"], "warmup": s["warmup"],
         "ms_per_step": 1e3 * s["loop_s"] / s["iterations"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_NAMES[args.config], **config_stats(cp),
-                   "l2": "working set > L2 (A alone 0.92 GB in CSR+CSC)"},
+        "config": config_dict(cp, args.config, 1),
+        "host": host_info(),
         "cpu_baseline": {"value": s["rate"], "unit": "iterations/s", "cores": s["threads"],
                          "kind": "port",
                          "sample": f"{s['iterations']} timed iterations of config {args.config} "
@@ -340,11 +377,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_local / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator of BASELINE config; SURVEY 8d RNG order)",
-            "config": {"workload": CONFIG_NAMES[args.config], **config_stats(cp),
-                       "parallelism": "single GPU" if world == 1 else
-                       f"clique shards x{world} (NCCL all-reduce: separators, A t, c.ua)",
-                       "l2": "no flush: per-iteration working set (A in SELL layouts ~0.53 GB + state ~0.11 GB) > 126 MB L2",
-                       "half_passes": half},
+            "config": config_dict(cp, args.config, world),
+            "layout": {"half_passes": half},
             "clocks": clocks,
             "gpu_launches": int(round(gpu_launches_per_iter * args.steps)) + 1,
             "kernel_ms_per_iteration": {k: v / prof_iters for k, v in prof.items() if v > 0},
@@ -391,6 +425,23 @@ def run_ours(args):
                                "setup_s": rep.timing.setup_s, "wall_s": wall,
                                "objective_primal": rep.objective_primal,
                                "objective_dual": rep.objective_dual}
+        # the rate of the real workload: the default solve's loop, iterations 1..40
+        line["to_tol_iterations_per_s"] = rep.iterations / rep.timing.iterations_s
+    if rank == 0 and world == 1 and not args.no_e2e and not args.no_extras:
+        # the same call on the reference's own input layout (x dense over n^2, A over
+        # n^2 columns): compress (problem.compress) runs inside solve_decomposed
+        from paper_1611_01828_b200.problem import expand_to_mirror
+
+        dpr = expand_to_mirror(cp)
+        t0 = time.perf_counter()
+        repr_ = H.solve_decomposed(dpr, H.SolverSettings(device=dev))
+        wall_r = time.perf_counter() - t0
+        del dpr
+        line["e2e_reference_layout"] = {
+            "value": repr_.iterations / wall_r, "unit": "iterations/s", "wall_s": wall_r,
+            "status": repr_.status, "iterations": repr_.iterations,
+            "what": "solve_decomposed(DecomposedProblem in the reference layout: dense c over n^2, "
+                    "A over n^2 columns): compress + H2D + setup + solve + report"}
     # --- other configs (small, latency-bound): iterations/s ----------------------------
     if rank == 0 and world == 1 and not args.no_extras:
         extra = {}
@@ -414,12 +465,18 @@ def run_ours(args):
         line["other_configs"] = extra
     # --- CPU baseline (rank 0, N=1 only) ----------------------------------------------
     if rank == 0 and world == 1 and not args.no_cpu:
-        s = cpu_sample(cp, float(os.environ.get("HSDE_CPU_BUDGET_S", "20")))
+        budget = float(os.environ.get("HSDE_CPU_BUDGET_S", "12"))
+        s = cpu_sample(cp, budget)
+        s1 = cpu_sample(cp, budget, blas_threads=1)
         line["cpu_baseline"] = {
             "value": s["rate"], "unit": "iterations/s", "cores": s["threads"], "kind": "port",
             "sample": f"{s['iterations']} iterations of config {args.config} from the zero start "
                       f"({s['loop_s']:.1f}s loop after {s['setup_s']:.1f}s setup), "
-                      "oracle/hsde_oracle.py numpy+scipy"}
+                      "oracle/hsde_oracle.py numpy+scipy, BLAS on all host threads",
+            "single_thread": {"value": s1["rate"], "cores": 1,
+                              "sample": f"{s1['iterations']} iterations, {s1['loop_s']:.1f}s loop, "
+                                        "BLAS limited to 1 thread (threadpoolctl)"},
+            "host": host_info()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

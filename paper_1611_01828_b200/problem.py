@@ -277,14 +277,27 @@ def compress(dp, full: bool = False) -> CompressedProblem:
     c_full = np.asarray(dp.c, dtype=float)
     if full:
         covered = np.arange(n2, dtype=np.int64)
+        pos, slot_cov = A.indices.astype(np.int64), gi.astype(np.int32)
+    elif 0 < n2 < 2 ** 31:
+        # O(n^2) byte mask + int32 rank map instead of sorting the ~nnz(A)
+        # column ids (config 4: 42M ids, 6.8 s -> ~1.5 s)
+        mark = c_full != 0.0
+        mark[gi] = True
+        mark[A.indices] = True
+        covered = np.flatnonzero(mark)
+        rank = np.cumsum(mark, dtype=np.int32)
+        rank -= 1
+        pos = rank[A.indices]
+        slot_cov = rank[gi]
+        del mark, rank
     else:
         parts = [gi, A.indices.astype(np.int64), np.flatnonzero(c_full)]
         covered = np.unique(np.concatenate(parts)) if n2 else np.zeros(0, np.int64)
-    pos = np.searchsorted(covered, A.indices.astype(np.int64))
+        pos = np.searchsorted(covered, A.indices.astype(np.int64))
+        slot_cov = np.searchsorted(covered, gi).astype(np.int32)
     Ac = sp.csr_matrix((A.data.copy(), pos.astype(np.int64), A.indptr.copy()),
                        shape=(m, covered.shape[0]))
     Ac.sort_indices()
-    slot_cov = np.searchsorted(covered, gi).astype(np.int32)
     cliques = tuple(np.asarray(c, dtype=np.int64) for c in dp.dec.cliques)
     sizes = np.asarray(dp.dec.sizes, dtype=np.int64)
     offsets = np.asarray(dp.dec.offsets, dtype=np.int64)
