@@ -586,3 +586,74 @@ def test_large_cliques_hot_path(d, h):
 
     O.solve(cp, O.OracleSettings(max_iters=80, tol=1e-300), callback=ocb)
     assert rel(got["u"], ref["u"]) <= 1e-8
+
+
+def test_cold_path_matches_jacobi_path():
+    """Config 4's first 30 iterations -- all cliques on the tridiagonal cold
+    path (hsde_cold.cuh), then the fast path -- against the Jacobi-only
+    eigensolver (HSDE_FLAG_JACOBI): same iterate to 1e-10."""
+    from paper_1611_01828_b200 import _lib
+
+    cp = make_config(4)
+    st = []
+    for flags in (0, _lib.HSDE_FLAG_JACOBI):
+        h = _lib.Handle(cp, flags=flags)
+        h.iterate(30)
+        st.append(h.get_state())
+        if flags == 0:
+            stats = h.stats()
+        h.close()
+    assert rel(st[0][0], st[1][0]) <= 1e-10
+    assert rel(st[0][1], st[1][1]) <= 1e-10
+    assert stats["cold_failed"] == 0.0
+
+
+def _adversarial_blocks(rng, d):
+    q, _ = np.linalg.qr(rng.normal(size=(d, d)))
+    lam = np.ones(d)
+    lam[: d // 3] = -2.0
+    x = rng.normal(size=d)
+    tight = np.concatenate([1 + 1e-9 * rng.normal(size=d // 2), -1 + 1e-9 * rng.normal(size=d - d // 2)])
+    near0 = np.linspace(-1, 1, d)
+    near0[d // 2: d // 2 + 5] = 1e-13 * np.arange(5)
+    return {
+        "two_values": (q * lam) @ q.T, "identity": np.eye(d), "zero": np.zeros((d, d)),
+        "diag": np.diag(rng.normal(size=d)), "rank1": np.outer(x, x) - 0.5 * np.eye(d),
+        "tight_clusters": (q * tight) @ q.T, "near_zero_cluster": (q * near0) @ q.T,
+        "graded": (q * np.logspace(-12, 0, d) * np.sign(rng.normal(size=d))) @ q.T,
+    }
+
+
+@pytest.mark.parametrize("kind", ["two_values", "identity", "zero", "diag", "rank1", "tight_clusters",
+                                  "near_zero_cluster", "graded"])
+def test_project_cone_adversarial_spectra(kind):
+    """The cold eigensolver (warp d <= 32, CTA d <= 96, Jacobi beyond) on
+    repeated, clustered, zero and graded spectra: 1e-12 of numpy's eigh
+    projection (symmat.py:153-165)."""
+    import scipy.sparse as sp
+
+    from paper_1611_01828_b200.problem import CliqueDecomposition, DecomposedProblem
+
+    sizes = [5, 16, 29, 33, 64, 80, 96, 111]
+    n = sum(sizes)
+    cl, o = [], 0
+    for d in sizes:
+        cl.append(list(range(o, o + d)))
+        o += d
+    dec = CliqueDecomposition.build(n, cl)
+    A = sp.csr_matrix(([1.0], ([0], [0])), shape=(1, n * n))
+    dp = DecomposedProblem(n=n, m=1, c=np.eye(n).ravel(), A=A, b=np.ones(1), dec=dec, block_dims=(n,))
+    _, layout = H.build_hsde(dp)
+    rng = np.random.default_rng(17)
+    u = rng.normal(size=layout.total)
+    s_in = u[layout.sl_s].copy()
+    for k, d in enumerate(sizes):
+        s_in[dec.offsets[k]:dec.offsets[k + 1]] = _adversarial_blocks(rng, d)[kind].ravel()
+    u[layout.sl_s] = s_in
+    got = H.project_cone(u, layout)[layout.sl_s]
+    for k, d in enumerate(sizes):
+        o0, o1 = dec.offsets[k], dec.offsets[k + 1]
+        b = s_in[o0:o1].reshape(d, d)
+        w, v = np.linalg.eigh(0.5 * (b + b.T))
+        want = ((v * np.maximum(w, 0.0)) @ v.T).ravel()
+        assert np.linalg.norm(got[o0:o1] - want) <= 1e-12 * max(np.linalg.norm(b), 1e-300), (kind, d)
