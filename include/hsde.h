@@ -196,7 +196,8 @@ int hsde_stats(hsde_t *h, double *out);
 /* Diagnostics: off-diagonal norm history (relative, per sweep) of the last
  * hot projection of one clique: out[0] = 1 if warm-started, out[1..] = |off|/|A|
  * after each sweep (-1 past the last).  `clique` selects the clique traced by
- * subsequent iterations. */
+ * subsequent iterations.  The diagnostics buffer exists only when the handle
+ * was created with HSDE_DEBUG=1 in the environment; otherwise HSDE_ERR_ARG. */
 int hsde_debug_jacobi(hsde_t *h, int32_t clique, double *out64);
 
 /* ---- Host decomposition (no GPU needed) ------------

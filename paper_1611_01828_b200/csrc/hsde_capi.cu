@@ -231,12 +231,21 @@ int dalloc(hsde_handle *h, T **p, size_t n) {
 constexpr size_t kStagedMin = 16u << 20;
 constexpr size_t kStageChunk = 32u << 20;
 
+// (staging state per device: the copy stream and events belong to the device
+// that was current when they were created)
+struct StageState {
+  char *pin[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  cudaStream_t cs = nullptr;
+};
+
 int h2d_staged(hsde_handle *h, void *dst, const void *src, size_t bytes) {
   static std::mutex mu;
-  static char *pin[2] = {nullptr, nullptr};
-  static cudaEvent_t done[2] = {nullptr, nullptr};
-  static cudaStream_t cs = nullptr;
+  static StageState states[64];
   std::lock_guard<std::mutex> lock(mu);
+  StageState &S = states[(h->dev >= 0 && h->dev < 64) ? h->dev : 0];
+  char **pin = S.pin;
+  cudaEvent_t *done = S.done;
   if (!pin[0]) {
     for (int b = 0; b < 2; ++b)
       if (cudaHostAlloc((void **)&pin[b], kStageChunk, cudaHostAllocDefault) != cudaSuccess ||
@@ -250,8 +259,9 @@ int h2d_staged(hsde_handle *h, void *dst, const void *src, size_t bytes) {
         }
         return 0;
       }
-    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&S.cs, cudaStreamNonBlocking));
   }
+  cudaStream_t cs = S.cs;
   const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
   const char *s8 = static_cast<const char *>(src);
   char *d8 = static_cast<char *>(dst);
@@ -1656,7 +1666,10 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   RC(dalloc(h, &s.W.sepbuf, std::max(d->n_sep, 1)));
   RC(dalloc(h, &s.W.qbuf, std::max(m, 1)));
   RC(dalloc(h, &s.W.red, 8));
-  RC(dalloc(h, &s.W.dbg, 64));
+  // diagnostics buffer (Jacobi history, phase stamps): only under HSDE_DEBUG=1,
+  // so production iterations carry no diagnostic stores
+  s.W.dbg = nullptr;
+  if (const char *e = std::getenv("HSDE_DEBUG"); e && std::atoi(e)) RC(dalloc(h, &s.W.dbg, 64));
   s.W.dbg_clique = 0;
   CK(cudaMemset(s.W.err, 0, sizeof(int)));
   CK(cudaMemset(s.W.vvalid, 0, sizeof(int) * std::max(p, 1)));
@@ -2538,6 +2551,10 @@ int hsde_debug_jacobi(hsde_t *h, int32_t clique, double *out64) {
   if (!h || !out64) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
   ShardDev &s = h->sh[0];
+  if (!s.W.dbg) {
+    h->err = "hsde_debug_jacobi: diagnostics are off (create the handle with HSDE_DEBUG=1 in the environment)";
+    return HSDE_ERR_ARG;
+  }
   CK(cudaStreamSynchronize(h->st));
   CK(cudaMemcpy(out64, s.W.dbg, 64 * sizeof(double), cudaMemcpyDeviceToHost));
   CK(cudaMemset(s.W.dbg + 23, 0, sizeof(double)));  // k_cone_split hand-over record counter

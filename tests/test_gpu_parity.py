@@ -615,7 +615,8 @@ def _adversarial_blocks(rng, d):
     x = rng.normal(size=d)
     tight = np.concatenate([1 + 1e-9 * rng.normal(size=d // 2), -1 + 1e-9 * rng.normal(size=d - d // 2)])
     near0 = np.linspace(-1, 1, d)
-    near0[d // 2: d // 2 + 5] = 1e-13 * np.arange(5)
+    nz = min(5, d - d // 2)
+    near0[d // 2: d // 2 + nz] = 1e-13 * np.arange(nz)
     return {
         "two_values": (q * lam) @ q.T, "identity": np.eye(d), "zero": np.zeros((d, d)),
         "diag": np.diag(rng.normal(size=d)), "rank1": np.outer(x, x) - 0.5 * np.eye(d),

@@ -1,3 +1,6 @@
+import os
+
+os.environ.setdefault("HSDE_DEBUG", "1")  # diagnostics buffer (hsde_debug_jacobi)
 import sys
 sys.path.insert(0, "/root/repo")
 import numpy as np

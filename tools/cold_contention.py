@@ -3,6 +3,9 @@ block-arrow problems with 148 / 296 / 444 cliques of order 80.
 
     python tools/cold_contention.py
 """
+import os
+
+os.environ.setdefault("HSDE_DEBUG", "1")  # diagnostics buffer (hsde_debug_jacobi)
 import sys
 from pathlib import Path
 

@@ -4,6 +4,9 @@ mode, all 400 cliques cold) and after hot iterations 1..3.
 
     python tools/cold_phases.py
 """
+import os
+
+os.environ.setdefault("HSDE_DEBUG", "1")  # diagnostics buffer (hsde_debug_jacobi)
 import sys
 import time
 from pathlib import Path

@@ -1,5 +1,8 @@
 """Jacobi off-norm history (relative to |A|_F) per sweep for a few cliques, at a
 few iteration counts.  python tools/dbgj.py [config] [clique ...]"""
+import os
+
+os.environ.setdefault("HSDE_DEBUG", "1")  # diagnostics buffer (hsde_debug_jacobi)
 import sys
 
 import numpy as np

@@ -2,6 +2,9 @@
 
     python tools/early_iters.py [--config 4] [--iters 40]
 """
+import os
+
+os.environ.setdefault("HSDE_DEBUG", "1")  # diagnostics buffer (hsde_debug_jacobi)
 import argparse
 import sys
 

@@ -2,6 +2,9 @@
 
     python tools/split_check.py [--config 4] [--iters 200]
 """
+import os
+
+os.environ.setdefault("HSDE_DEBUG", "1")  # diagnostics buffer (hsde_debug_jacobi)
 import argparse
 import sys
 import time
