@@ -145,7 +145,8 @@ def kernel_units(cp, name: str, half: bool = True):
 
 
 # profile slot -> the kernels it times (hot path, warm starts on)
-KERNELS = {"k_cone_cta": "k_cone_split", "k_ua": "k_ua_half",
+KERNELS = {"k_cone_cta": "CTA cone launches: k_cone_cold (cold path, young bases) + k_cone_split (warm fast path)",
+           "k_ua": "k_ua_half",
            "k_spmv_seg": "k_pair_sum + k_spmv_half + k_rowsum_tiles"}
 
 
@@ -325,6 +326,11 @@ def run_ours(args):
     from paper_1611_01828_b200.synthetic import make_config, config_stats, CONFIG_NAMES
 
     dev = local if world > 1 else 0
+    if world > 1:
+        # communicator lines (ranks, transports, NVLS) on stderr, so a multi-GPU run
+        # shows its N ranks
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     torch.cuda.set_device(dev)
     dist = None
     comm = None
@@ -361,14 +367,33 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_local = float(t.item())
     value = args.steps / t_local  # iterations/s of the whole (sharded) problem
-    # --- roofline: per-kernel CUDA events over a few eager iterations ------------
-    prof_iters = 5
-    prof, launches = h.profile_iterations(prof_iters)
-    eig_stats = h.stats()
+    # --- roofline: per-kernel CUDA events over eager iterations -------------------
+    # (a) the SAME window as `value`: a second handle replays the warm-up, then
+    #     iterations W+1 .. W+K run eagerly with events around every kernel
+    #     (one event set per iteration, one sync at the end);
+    # (b) steady state: the first handle goes on to iteration >= 220, then 20
+    #     profiled iterations (every clique on the warm fast path).
+    if comm is None:
+        h2 = _lib.Handle(cp, device=dev)
+    else:
+        h2 = _lib.Handle(cp, shards=[shards[rank]], comm=init_comm(), device=dev)
+    h2.iterate(args.warmup)
+    h2.sync()
+    prof_iters = args.steps
+    prof, launches = h2.profile_iterations(prof_iters)
+    eig_stats = h2.stats()
+    h2.close()
     gpu_launches_per_iter = (launches - 1) / prof_iters
     peaks = load_peaks()
     half = h.half_passes
     dominant, roofs = roofline_for(cp, prof, prof_iters, peaks, half)
+    done = args.warmup + args.steps
+    if done < 220:
+        h.iterate(220 - done)
+        h.sync()
+    steady_iters = 20
+    prof_s, _ = h.profile_iterations(steady_iters)
+    _, roofs_s = roofline_for(cp, prof_s, steady_iters, peaks, half)
     h.close()
     line = None
     if rank == 0:
@@ -385,8 +410,15 @@ def run_ours(args):
             "eig_stats": eig_stats,
         }
         if roofs:
-            line["roofline"] = dict(roofs[dominant], kernel=KERNELS.get(dominant, dominant))
+            line["roofline"] = dict(roofs[dominant], kernel=KERNELS.get(dominant, dominant),
+                                    window=f"iterations {args.warmup + 1}..{args.warmup + args.steps} "
+                                           "(the window `value` times)")
             line["roofline_all"] = roofs
+        if roofs_s:
+            line["roofline_steady_state"] = {
+                "window": f"iterations {max(done, 220) + 1}..{max(done, 220) + steady_iters}",
+                "kernel_ms_per_iteration": {k: v / steady_iters for k, v in prof_s.items() if v > 0},
+                "kernels": roofs_s}
     # --- e2e: public API on host data, default to-tolerance solve ------------------
     if not args.no_e2e:
         torch.cuda.synchronize()

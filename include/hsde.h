@@ -200,6 +200,25 @@ int hsde_stats(hsde_t *h, double *out);
  * was created with HSDE_DEBUG=1 in the environment; otherwise HSDE_ERR_ARG. */
 int hsde_debug_jacobi(hsde_t *h, int32_t clique, double *out64);
 
+/* ---- Covered layout of a reference-layout problem (host, no GPU needed) ----
+ * problem.compress: the reference's DecomposedProblem keeps x over all n^2
+ * coordinates (chordalsdp/decompose.py:40-79: dense c, A over n^2 columns,
+ * graphs.py:228 gather_index); the device iterates on the covered ones
+ * (clique-selected + support of A's columns + support of c).  build marks them
+ * in a bit mask (multi-threaded) and returns their number; fill writes the
+ * ascending covered ids, c on them, the rank of every column id of A (pos, the
+ * compressed CSR's column indices: order-preserving) and of every gather index
+ * (slot_cov).  Column ids as int32 or int64 (the other pointer null).
+ * HSDE_ERR_ARG on an id outside [0, n2) or more than 2^31 - 1 covered ids. */
+typedef struct hsde_cover hsde_cover_t;
+int hsde_cover_build(int64_t n2, const double *c_full, const int64_t *gather_index, int64_t n_gather,
+                     const int32_t *a_col32, const int64_t *a_col64, int64_t nnz, hsde_cover_t **out,
+                     int64_t *n_cov);
+int hsde_cover_fill(const hsde_cover_t *cv, const double *c_full, const int64_t *gather_index, int64_t n_gather,
+                    const int32_t *a_col32, const int64_t *a_col64, int64_t nnz, int64_t *covered,
+                    double *c_cov, int32_t *pos, int32_t *slot_cov);
+void hsde_cover_destroy(hsde_cover_t *cv);
+
 /* ---- Host decomposition (no GPU needed) ------------
  * Chordal extension + maximal cliques of one block's sparsity pattern, with
  * the reference's orderings and tie-breaking (graphs.py:73-184, 217-220):

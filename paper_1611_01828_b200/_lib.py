@@ -38,6 +38,7 @@ EXPORTED = (
     "hsde_debug_jacobi", "hsde_pattern_decompose", "hsde_pattern_sizes", "hsde_pattern_cliques",
     "hsde_pattern_fill", "hsde_pattern_destroy", "hsde_sdpa_parse", "hsde_sdpa_error",
     "hsde_sdpa_sizes", "hsde_sdpa_data", "hsde_sdpa_destroy", "hsde_pattern_index", "hsde_report_vectors",
+    "hsde_cover_build", "hsde_cover_fill", "hsde_cover_destroy",
 )
 HSDE_NCCL_ID_BYTES = 128
 
@@ -136,6 +137,11 @@ def load() -> C.CDLL:
         "hsde_sdpa_data": (C.c_int, [vp, _i32p, _dp, _i32p, _i32p, _i32p, _i32p, _dp]),
         "hsde_sdpa_destroy": (None, [vp]),
         "hsde_report_vectors": (C.c_int, [vp, C.c_double, _dp, _dp, _dp]),
+        "hsde_cover_build": (C.c_int, [C.c_int64, _dp, _i64p, C.c_int64, _i32p, _i64p, C.c_int64,
+                                       C.POINTER(vp), _i64p]),
+        "hsde_cover_fill": (C.c_int, [vp, _dp, _i64p, C.c_int64, _i32p, _i64p, C.c_int64, _i64p, _dp,
+                                      _i32p, _i32p]),
+        "hsde_cover_destroy": (None, [vp]),
         "hsde_pattern_index": (C.c_int, [_i64p, C.c_int64, C.c_int64, _i64p, C.c_int64, _i64p, C.c_int32,
                                          _i64p, _i64p, _i64p, _i64p, C.POINTER(C.c_uint8)]),
     }
@@ -419,6 +425,39 @@ def device_count() -> int:
 
 def default_device() -> int:
     return int(os.environ.get("HSDE_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+
+
+def cover_layout(n2: int, c_full: np.ndarray, gather_index: np.ndarray, a_col: np.ndarray):
+    """(covered, c on covered, rank of A's column ids, rank of the gather index) of a
+    reference-layout problem (library, host threads; hsde_cover_*)."""
+    lib = load()
+    cf = np.ascontiguousarray(c_full, dtype=np.float64)
+    gi = np.ascontiguousarray(gather_index, dtype=np.int64)
+    col = np.ascontiguousarray(a_col)
+    if col.dtype == np.int32:
+        c32, c64 = _ptr(col, C.c_int32), None
+    else:
+        col = np.ascontiguousarray(col, dtype=np.int64)
+        c32, c64 = None, _ptr(col, C.c_int64)
+    h = C.c_void_p()
+    ncov = C.c_int64()
+    rc = lib.hsde_cover_build(int(n2), _ptr(cf, C.c_double), _ptr(gi, C.c_int64), gi.size, c32, c64, col.size,
+                              C.byref(h), C.byref(ncov))
+    if rc:
+        raise ValueError("hsde_cover_build: a coordinate id outside [0, n^2)")
+    try:
+        covered = np.empty(ncov.value, dtype=np.int64)
+        c_cov = np.empty(ncov.value, dtype=np.float64)
+        pos = np.empty(col.size, dtype=np.int32)
+        slot_cov = np.empty(gi.size, dtype=np.int32)
+        rc = lib.hsde_cover_fill(h, _ptr(cf, C.c_double), _ptr(gi, C.c_int64), gi.size, c32, c64, col.size,
+                                 _ptr(covered, C.c_int64), _ptr(c_cov, C.c_double), _ptr(pos, C.c_int32),
+                                 _ptr(slot_cov, C.c_int32))
+        if rc:
+            raise ValueError("hsde_cover_fill: bad arguments")
+    finally:
+        lib.hsde_cover_destroy(h)
+    return covered, c_cov, pos, slot_cov
 
 
 def pattern_index(covered: np.ndarray, n: int, code: np.ndarray, starts: np.ndarray):

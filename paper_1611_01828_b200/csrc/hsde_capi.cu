@@ -133,6 +133,7 @@ struct ShardDev {
 
 struct hsde_handle {
   int dev = 0;
+  int n_sm = 148;  // multiprocessors of the device
   cudaStream_t st = nullptr;
   // parallel branches for the independent cone launches (size classes, shards)
   static constexpr int kAux = 4;
@@ -409,6 +410,10 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
     const char *e = std::getenv("HSDE_SPLIT_VUPDATE");
     return e ? std::atoi(e) : 1;
   }();
+  static const int split_prefetch = [] {
+    const char *e = std::getenv("HSDE_SPLIT_PREFETCH");
+    return e ? std::atoi(e) : 1;
+  }();
   ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0, pl.pscratch, pl.pstride, 0,
               split_refresh, split_vupdate};
   if (!block) {
@@ -465,6 +470,7 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
     if (part == 0 || part == 1) {  // fast path (hsde_split.cuh), scheduled by k_scalars
       ConeArgs co = ca;
       co.ids = s.W.corder;
+      co.pf_ahead = split_prefetch ? 2 * h->n_sm : 0;  // two CTAs per SM resident
       k_cone_split<true><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, s.W, co);
       CKL();
     }
@@ -1757,6 +1763,7 @@ int create_impl(const hsde_problem_desc *descs, int nshards, const hsde_settings
     return HSDE_ERR_CUDA;
   }
   retain_pool(h->dev);
+  if (int n = 0; cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, h->dev) == cudaSuccess && n > 0) h->n_sm = n;
   for (int a = 0; a < hsde_handle::kAux; ++a) {
     if (cudaStreamCreateWithFlags(&h->aux[a], cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_join[a], cudaEventDisableTiming) != cudaSuccess) {
@@ -2457,7 +2464,10 @@ int hsde_time_iterations(hsde_t *h, int32_t k, float *ms) {
 int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches) {
   if (!h || !ms || k < 1) return HSDE_ERR_ARG;
   cudaSetDevice(h->dev);
-  cudaEvent_t ev[PS_COUNT + 1];
+  // one event set per iteration, one synchronisation at the end: the host
+  // runs ahead of the device, so the intervals hold kernel time and not the
+  // launch latency an idle device would add after a per-iteration sync
+  std::vector<cudaEvent_t> ev((size_t)k * (PS_COUNT + 1));
   for (auto &e : ev) CK(cudaEventCreate(&e));
   for (int i = 0; i < HSDE_PROFILE_SLOTS; ++i) ms[i] = 0.f;
   int nl = 0;
@@ -2468,12 +2478,13 @@ int hsde_profile_iterations(hsde_t *h, int32_t k, float *ms, int32_t *launches) 
   }
   const int order[] = {PS_COUNT, PS_RHS, PS_SPMV, PS_SCHUR, PS_UA, PS_COMM, PS_SCALARS,
                        PS_CONE_WARP, PS_CONE_BLOCK, PS_XUPD};
+  for (int it = 0; it < k; ++it) RC(launch_iteration(h, ev.data() + (size_t)it * (PS_COUNT + 1), &nl));
+  CK(cudaStreamSynchronize(h->st));
   for (int it = 0; it < k; ++it) {
-    RC(launch_iteration(h, ev, &nl));
-    CK(cudaEventSynchronize(ev[PS_XUPD]));
+    cudaEvent_t *e = ev.data() + (size_t)it * (PS_COUNT + 1);
     for (int q = 1; q < 10; ++q) {
       float t = 0.f;
-      CK(cudaEventElapsedTime(&t, ev[order[q - 1]], ev[order[q]]));
+      CK(cudaEventElapsedTime(&t, e[order[q - 1]], e[order[q]]));
       ms[order[q]] += t;
     }
   }

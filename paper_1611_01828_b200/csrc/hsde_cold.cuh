@@ -39,6 +39,8 @@ constexpr int kColdNW = 4;
 constexpr int kColdThreads = kColdNW * 32;
 constexpr int kColdMaxD = 96;
 constexpr int kColdNB = 8;  // reflectors per compact-WY block
+constexpr int kColdLoadBatch = 4;  // hot-path slots per thread in flight (128 threads per CTA)
+constexpr int kColdSturmPts = 1;  // bracket points per thread and bisection round (independent Sturm chains)
 
 enum ColdStatus { COLD_OK = 0, COLD_FAIL = 1 };
 
@@ -331,6 +333,55 @@ __device__ __forceinline__ int sturm_count(const double *da, const double *e2, i
   return c;
 }
 
+// NP Sturm counts of the same block at once (independent recurrences
+// interleaved: the bisection rounds are latency chains of one DFMA per step,
+// so NP points per thread cost about one)
+template <int NP>
+__device__ __forceinline__ void sturm_count_n(const double *da, const double *e2, int bs, int be,
+                                              const double (&x)[NP], int (&c)[NP]) {
+  double pp[NP], pc[NP];
+  const double a0 = da[bs];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    pp[p] = 1.0;
+    pc[p] = a0 - x[p];
+    c[p] = sgn_bit(pc[p]);
+  }
+  int k = bs + 1;
+  for (; k + 7 <= be; k += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double ak = da[k + u], ek = e2[k + u - 1];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const double pn = fma(ak - x[p], pc[p], -ek * pp[p]);
+        c[p] += sgn_bit(pn) ^ sgn_bit(pc[p]);
+        pp[p] = pc[p];
+        pc[p] = pn;
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int ex = (__double2hiint(pc[p]) >> 20) & 0x7ff;  // biased exponent (integer pipe)
+      if (ex > 1023 + 300 || (ex < 1023 - 300 && ex > 0)) {
+        const double f = ex > 1023 ? 0x1p-300 : 0x1p300;
+        pc[p] *= f;
+        pp[p] *= f;
+      }
+    }
+  }
+  for (; k <= be; ++k) {
+    const double ak = da[k], ek = e2[k - 1];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const double pn = fma(ak - x[p], pc[p], -ek * pp[p]);
+      c[p] += sgn_bit(pn) ^ sgn_bit(pc[p]);
+      pp[p] = pc[p];
+      pc[p] = pn;
+    }
+  }
+}
+
 // 3. twisted-factorisation eigenvector of the block [bs, be] of T for lam,
 // written (unnormalised L / U first, then z) into column zc of Z (stride lz).
 // Returns false when the vector is not finite.
@@ -538,18 +589,29 @@ __device__ int cold_eig(int d, const ColdSmem &cs, bool values_only, double *hv,
     int g = 1;
     while (2 * g * d <= T && g < 16) g *= 2;
     if (tid < g * d) {
+      // (g NP + 1)-section: thread q of the eigenvalue's group of g takes the NP
+      // interior points q NP + 1 .. q NP + NP of the current bracket
+      constexpr int NP = kColdSturmPts;
       const double lo0 = gl * sc - 0x1p-40, hi0 = gh * sc + 0x1p-40;
-      const float bits = log2f((float)(g + 1));
+      const float bits = log2f((float)(g * NP + 1));
       const int rounds = (int)ceilf(54.0f / bits);
-      const double ig = 1.0 / (g + 1);
+      const double ig = 1.0 / (g * NP + 1);
       const int j = tid / g, q = tid - j * g;
       const int b0 = cs.bs[j], b1 = cs.be[j], jj = j - b0;
       double lo = lo0, hi = hi0;
       const unsigned gm = g == 32 ? 0xffffffffu : (((1u << g) - 1u) << (lane & ~(g - 1)));
       for (int rd = 0; rd < rounds; ++rd) {
-        const double x = fma(hi - lo, (q + 1) * ig, lo);
-        const int c = sturm_count(cs.dg, cs.e2, b0, b1, x);
-        double lc = c <= jj ? x : -CUDART_INF, hc = c > jj ? x : CUDART_INF;
+        double x[NP];
+        int c[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) x[p] = fma(hi - lo, (q * NP + p + 1) * ig, lo);
+        sturm_count_n<NP>(cs.dg, cs.e2, b0, b1, x, c);
+        double lc = -CUDART_INF, hc = CUDART_INF;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {  // x ascending: the last point with count <= jj, the first above
+          if (c[p] <= jj) lc = x[p];
+          if (c[p] > jj && hc == CUDART_INF) hc = x[p];
+        }
         for (int o = g >> 1; o > 0; o >>= 1) {
           lc = fmax(lc, __shfl_xor_sync(gm, lc, o));
           hc = fmin(hc, __shfl_xor_sync(gm, hc, o));
@@ -688,7 +750,7 @@ __device__ int cold_one(const DevProblem &P, const DevState &S, const DevWork &W
         cs.Z[a * cs.lv + b] = xg[e];
       }
     } else {
-      constexpr int NB = 4;  // every load of the batch in flight before the stores (they may alias)
+      constexpr int NB = kColdLoadBatch;  // every load of the batch in flight before the stores (they may alias)
       for (int e0 = tid; e0 < d * d; e0 += NB * T) {
         double xv[NB], xo[NB];
 #pragma unroll

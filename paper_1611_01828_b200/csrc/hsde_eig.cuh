@@ -1209,6 +1209,7 @@ struct ConeArgs {
   int fail_only;     // k_cone_block: only the slots flagged in cfail (HOT: raw X in W.xarg)
   int cold;          // k_cone_split: hand-overs go to the cold path (X kept in W.xarg)
   int cold_pass;     // k_cone_cold after k_cone_split: 0 the predicted cliques (W.ccur), 1 its hand-overs
+  int pf_ahead;      // k_cone_split: resident CTA slots (0 = off); slot b prefetches the inputs of slot b + pf_ahead into L2
 };
 
 // Hot-path load of slot j: builds arg_s and performs the v / w_v update and

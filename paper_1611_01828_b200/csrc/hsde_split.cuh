@@ -270,6 +270,21 @@ __device__ __forceinline__ double cta_min(double v, double *red) {
 // float rounding (no integer division in the element loops)
 __device__ __forceinline__ int qdiv(int e, float inv) { return (int)(((float)e + 0.5f) * inv); }
 
+// 1 / x to ~1 ulp without the division's slow-path branch (a float seed and
+// three Newton steps: the element loops interleave several of these); x outside
+// the float range falls back to the IEEE reciprocal.  The Riccati denominators
+// only need a consistent, accurate value: an ulp in 1 / Delta moves the fixed
+// point like an ulp in diag B.
+__device__ __forceinline__ double fast_rcp(double x) {
+  const float f = __frcp_rn(__double2float_rn(x));
+  if (!(fabsf(f) > 1e-37f && fabsf(f) < 1e37f)) return __drcp_rn(x);
+  double y = (double)f;
+  y = fma(y, fma(-x, y, 1.0), y);
+  y = fma(y, fma(-x, y, 1.0), y);
+  y = fma(y, fma(-x, y, 1.0), y);
+  return y;
+}
+
 // every in-place pass keeps its output blocks in registers (kSplitMaxB per warp)
 __device__ __forceinline__ bool split_fits(int r, int n, int nw) {
   const int br = (r + 15) >> 4, bn = (n + 15) >> 4, bd = (r + n + 15) >> 4, cap = kSplitMaxB * nw;
@@ -358,7 +373,30 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     }
     __syncthreads();
     SPLIT_STAMP(1);
-  
+  }
+  // ---- second wave: the clique that takes a slot of this wave next
+  //      (blockIdx + resident slots) gets its inputs prefetched into L2 now --
+  //      HBM is idle while the first wave computes (its loads all came at once)
+  if (ca.pf_ahead > 0 && (int)blockIdx.x + ca.pf_ahead < ca.count) {
+    const int kp = ca.ids[blockIdx.x + ca.pf_ahead];
+    if (!(W.ccur && W.ccur[kp])) {
+      const int64_t po = P.cl_off[kp], vo = P.n_c + P.n_d + P.m;
+      const int dq = P.cl_size[kp];
+      const int nl = (dq * dq * 8 + 127) >> 7;  // 128-byte lines per d x d array
+      auto pf = [&](const double *base) {
+        for (int ln = tid; ln < nl; ln += T)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char *>(base) + ((int64_t)ln << 7)));
+      };
+      pf(S.u + so + po);
+      pf(S.w + so + po);
+      pf(S.u + vo + po);
+      pf(S.w + vo + po);
+      pf(P.mz + P.n_c + po);
+      pf(P.mz + vo + po);
+      pf(W.vstore + po);
+      for (int e = tid; e < (nl + 1) / 2; e += T)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char *>(P.slot_cov + po) + ((int64_t)e << 7)));
+    }
   }
   // ---- B = Vt X Vt' by column strips of T = Vt X, all from shared memory:
   //      X -> the hand-off buffer (global, L2-resident), Vt -> R1, then per
@@ -628,15 +666,16 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   for (int e = tid; e < n * r; e += T) {
     const int i = qdiv(e, invr), j = e - i * r;
     const double bnp = R1[(r + i) * L + j];
-    R1[(r + i) * L + j] = bnp / (lam[j] - lam[r + i]);
+    R1[(r + i) * L + j] = bnp * fast_rcp(lam[j] - lam[r + i]);
     x2 += bnp * bnp;  // the first increment in residual units (Delta * dX)
   }
   __syncthreads();
   // Yn_0 = -(E_PP + B_PN X_0)
   team_mm1<false, false>(r, r, BPN, XX, n, [&](int i, int j, double v) { Ybuf[0][i * ly + j] = -(v + R1[i * L + j]); });
-  double prev = sqrt(cta_sum(x2, red)), prev2 = prev;
-  const double tolR = kSplitTol * sqrt(nb2);
-  bool ok = prev == 0.0;
+  const double inb2 = nb2 > 0.0 ? 1.0 / nb2 : 0.0;
+  float prev = sqrtf((float)(cta_sum(x2, red) * inb2)), prev2 = prev;  // increments relative to |B|_F
+  const float tolR = (float)kSplitTol;
+  bool ok = prev == 0.0f;
   int it = 0, yb = 0;
   const int mb = (n + 15) >> 4, nbr = (r + 15) >> 4, nx = mb * nbr, ny = nbr * nbr;
   const float invbr = 1.0f / nbr, invbn = 1.0f / mb, invbd = 1.0f / ((d + 15) >> 4);
@@ -674,7 +713,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
         const int bi = qdiv(t, invbr), bj = t - bi * nbr;
         blk16_each(c[s], bi * 16, bj * 16, n, r, [&](int i, int j, double v) {
           const double dl = lam[j] - lam[r + i];
-          const double x = (R1[j * L + r + i] + v) / dl;
+          const double x = (R1[j * L + r + i] + v) * fast_rcp(dl);
           const double dx = (x - R1[(r + i) * L + j]) * dl;  // increment in residual units
           acc += dx * dx;
           R1[(r + i) * L + j] = x;
@@ -685,11 +724,14 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     double *rb = red + 16 * (it & 1);  // alternating halves: no barrier before the next pass writes
     if (lane == 0) rb[w] = acc;
     __syncthreads();
-    const double delta = sqrt(red_total(rb, nw));
+    // the decision runs in float on residuals relative to |B|_F (every thread
+    // the same deterministic arithmetic; an fp64 sqrt and two divisions per pass
+    // sat on the critical path of every warp)
+    const float delta = sqrtf((float)(red_total(rb, nw) * inb2));
     if (newy) yb ^= 1;
     // contraction per pass: over two passes (the lagged quadratic term makes
     // consecutive increments non-monotone), over one for the first pass
-    const double rho = it == 0 ? delta / prev : sqrt(delta / prev2);
+    const float rho = it == 0 ? delta / prev : sqrtf(delta / prev2);
     // Increments are measured in residual units (Delta o dY, the Riccati residual
     // the pass removed), against |B|_F: X then solves the Riccati equation of a
     // matrix within ~kSplitTol |B|_F of B, and P(.) is 1-Lipschitz, so P is
@@ -698,8 +740,8 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     // residual delta rho / (1 - rho) is below the tolerance, or the increment
     // itself is at the rounding level; stalled: no contraction (or NaN) -- the
     // pass budget bounds slow contraction.
-    if (delta <= 0.1 * tolR || (rho < kSplitStall && delta * rho <= tolR * (1.0 - rho))) ok = true;
-    else if (!(rho < kSplitStall)) {
+    if (delta <= 0.1f * tolR || (rho < (float)kSplitStall && delta * rho <= tolR * (1.0f - rho))) ok = true;
+    else if (!(rho < (float)kSplitStall)) {
       if (W.dbg && tid == 0) {  // diagnostics: (refreshed, pass, rho, delta, g, off, r) of up to 4 stalls
         const unsigned long long c = atomicAdd(reinterpret_cast<unsigned long long *>(W.dbg + 23), 1ull);
         if (c < 4) {

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import logging
 import math
+import threading
 import time
 import weakref
 from dataclasses import dataclass
@@ -457,6 +458,11 @@ class _Session:
         self.settings = settings
         self.shards = None
         self.comm = comm
+        # The report's pattern index (solver.py:443-452) depends on the problem only:
+        # it is built on a host thread during the device setup and the iterations
+        # (numpy and the library release the GIL), and joined in _classify.
+        self.index_thread = threading.Thread(target=_pattern_index, args=(self.cp, dp), daemon=True)
+        self.index_thread.start()
         kw = dict(alpha=settings.alpha, tol=settings.tol, infeas_tau_tol=settings.infeas_tau_tol,
                   infeas_kappa_tol=settings.infeas_kappa_tol,
                   check_interval=settings.check_interval, normalize=normalize,
@@ -535,7 +541,8 @@ def _pattern_index(cp: CompressedProblem, dp):
     starts = np.concatenate([[0], np.cumsum(dims)])
     # block, block-local (i, j), and the covered position of the flat id
     # gj * n + gi (= np.searchsorted(cp.covered, gj * n + gi)), in the library
-    out = _lib.pattern_index(cp.covered, n, code, starts)
+    b, i, j, pos_c, hit = _lib.pattern_index(cp.covered, n, code, starts)
+    out = (b, i, j, pos_c, None if bool(hit.all()) else hit)  # hit None: every row is covered
     cp._cache[key] = out
     return out
 
@@ -544,7 +551,10 @@ def _pattern_entries(cp: CompressedProblem, dp, xc: np.ndarray) -> PatternEntrie
     """[block, i, j, value] rows (1-based, block-local) on the aggregate pattern
     plus the diagonal (solver.py:443-452); ``xc`` is a covered-coordinate vector."""
     b, i, j, pos_c, hit = _pattern_index(cp, dp)
-    vals = np.where(hit, xc[pos_c] if cp.N_c else 0.0, 0.0)
+    if hit is None:
+        vals = xc[pos_c]
+    else:
+        vals = np.where(hit, xc[pos_c] if cp.N_c else 0.0, 0.0)
     return PatternEntries(b, i, j, vals)
 
 
@@ -559,6 +569,10 @@ def _problem_stats(cp: CompressedProblem, dp) -> ProblemStats:
 def _classify(sess: _Session, chk: np.ndarray, iterations: int, timing: Timing) -> SolverReport:
     """solver.py:521-605 on the device iterate."""
     st, cp, dp = sess.settings, sess.cp, sess.dp
+    th = getattr(sess, "index_thread", None)
+    if th is not None:
+        th.join()
+        sess.index_thread = None
     stats = _problem_stats(cp, dp)
     sign = float(getattr(dp, "objective_sign", cp.objective_sign))
     tau, kappa = float(chk[3]), float(chk[4])
@@ -577,8 +591,10 @@ def _classify(sess: _Session, chk: np.ndarray, iterations: int, timing: Timing) 
             u = sess.unscaled()
             xt = u[cp.sl_x] / tau
             yt = u[cp.sl_y] / tau
-        obj_p = sign * float(cp.c @ xt)
-        obj_d = sign * float(cp.b @ yt)
+        # (einsum's own loops, not BLAS ddot: OpenBLAS workers keep spinning after a
+        # threaded call and slowed the next solve's staged H2D copies by ~40 ms)
+        obj_p = sign * float(np.einsum("i,i->", cp.c, xt))
+        obj_d = sign * float(np.einsum("i,i->", cp.b, yt))
         if res.max() <= st.tol:
             if hvt is None:
                 hvt = cp.scatter(u[cp.sl_v] / tau)

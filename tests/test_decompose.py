@@ -98,5 +98,9 @@ def test_report_pattern_index_matches_numpy(golden_dir):
         bj = np.searchsorted(starts, gj, side="right") - 1
         want = (bi + 1, gi - starts[bi] + 1, gj - starts[bj] + 1, pos_c, hit)
         got = S._pattern_index(cp, cp)
-        for a, b in zip(got, want):
+        for a, b in zip(got[:4], want[:4]):
             assert np.array_equal(a, b), t
+        if got[4] is None:  # every row covered
+            assert want[4].all(), t
+        else:
+            assert np.array_equal(got[4], want[4]), t

@@ -71,6 +71,48 @@ def test_compress_expand_roundtrip():
     assert np.array_equal(mir.dec.gather(cp.expand_x(x)), cp.gather(x))
 
 
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_library_cover_layout_matches_numpy(cfg):
+    """problem.compress through the library (hsde_cover_*: bit mask + popcount ranks
+    on host threads) equals its numpy restatement on the reference layout, and
+    recovers the generator's covered set; unsorted / duplicated A entries and int64
+    column ids go through the same path."""
+    import scipy.sparse as sp
+
+    cp = make_config(cfg)
+    dp = expand_to_mirror(cp)
+    a, b = compress(dp), compress(dp, _numpy_only=True)
+    assert np.array_equal(a.covered, cp.covered) and np.array_equal(a.covered, b.covered)
+    assert np.array_equal(a.c, b.c) and np.array_equal(a.slot_cov, b.slot_cov)
+    for x, y in ((a.A, b.A), (a.A, cp.A)):
+        assert np.array_equal(x.indptr, y.indptr) and np.array_equal(x.indices, y.indices)
+        assert np.array_equal(x.data, y.data)
+    # a COO input with shuffled, split entries: canonicalised first, same result
+    coo = dp.A.tocoo()
+    perm = np.random.default_rng(0).permutation(coo.nnz)
+    rows = np.concatenate([coo.row[perm], coo.row[perm[:7]]])
+    cols = np.concatenate([coo.col[perm], coo.col[perm[:7]]]).astype(np.int64)
+    vals = np.concatenate([coo.data[perm], np.zeros(7)])
+    vals[:7] *= 0.5
+    vals[-7:] = vals[:7]
+    dp2 = type(dp)(n=dp.n, m=dp.m, c=dp.c, A=sp.coo_matrix((vals, (rows, cols)), shape=dp.A.shape), b=dp.b,
+                   dec=dp.dec, aggregate=None, block_dims=dp.block_dims, objective_sign=dp.objective_sign)
+    c2 = compress(dp2)
+    assert np.array_equal(c2.covered, a.covered) and np.array_equal(c2.A.indices, a.A.indices)
+    assert np.allclose(c2.A.data, a.A.data, rtol=1e-15, atol=0)
+
+
+def test_library_cover_layout_rejects_bad_ids():
+    with pytest.raises(ValueError):
+        _lib.cover_layout(16, np.zeros(16), np.array([3, 16], dtype=np.int64), np.array([1], dtype=np.int32))
+    with pytest.raises(ValueError):
+        _lib.cover_layout(16, np.zeros(16), np.array([3], dtype=np.int64), np.array([-1], dtype=np.int64))
+    cov, cc, pos, sc = _lib.cover_layout(16, np.eye(4).ravel(), np.array([1, 5], dtype=np.int64),
+                                         np.array([15, 2], dtype=np.int64))
+    assert cov.tolist() == [0, 1, 2, 5, 10, 15] and cc.tolist() == [1, 0, 0, 1, 1, 1]
+    assert pos.tolist() == [5, 2] and sc.tolist() == [1, 3]
+
+
 def test_full_layout_compress_keeps_all_coordinates():
     cp = make_config(1)
     mir = expand_to_mirror(cp)

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-timeout 800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 HSDE_TIMING=1 timeout 600 python tools/e2e_profile.py 4 > gpurun_out/e2e_timing.log 2>&1
-timeout 300 python bench.py --no-extras --no-cpu > gpurun_out/bench_quick.json 2>&1
+timeout 300 python tools/setup_profile.py 4 > gpurun_out/setup_profile.log 2>&1
