@@ -127,6 +127,7 @@ struct ShardDev {
   int grid_rhs = 1, grid_xupd = 1;  // light CTAs of k_rhs; k_xupd grid (no partials)
   size_t schur_smem = 0;
   std::vector<int> sizes;         // clique sizes (host copy)
+  std::vector<char> in_block;     // clique runs on a CTA team (block plan)
   int64_t maxcol = 0;
   double nc2_owned = 0;           // sum of c^2 over owned coordinates (original units)
 };
@@ -831,20 +832,35 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
   std::vector<int> wids[3], bids;
   const int wcap[3] = {8, 16, 32};
   int dpb = 2;
-  // few cliques (less than two per SM): CTA teams for every clique of order
-  // >= 8 -- the fast / cold paths cut the projection latency that a warp team
-  // cannot hide (config 0: 20 cliques of order 20)
-  const bool few = p <= 296;
+  // A size class with few cliques (CTA teams stay below two per SM) goes to CTA
+  // teams, largest class first, down to order 8: the fast / cold paths cut the
+  // projection latency that a single warp cannot hide (config 0: 20 cliques of
+  // order 20; config 3: its 16 cliques of order 17-29 took 245 us as warp teams
+  // and bounded the whole iteration)
+  int ncls[4] = {0, 0, 0, 0};  // orders 8 (exactly), 9-16, 17-32, > 32
+  auto cls_of = [](int d) { return d > 32 ? 3 : d > 16 ? 2 : d > 8 ? 1 : d == 8 ? 0 : -1; };
+  for (int k = 0; k < p; ++k)
+    if (cls_of(sizes[k]) >= 0) ++ncls[cls_of(sizes[k])];
+  bool cta_cls[4] = {false, false, false, true};
+  for (int c = 2, n_cta = ncls[3]; c >= 0; --c) {
+    if (ncls[c] == 0) continue;
+    if (n_cta + ncls[c] > 2 * h->n_sm) break;
+    cta_cls[c] = true;
+    n_cta += ncls[c];
+  }
   for (int k = 0; k < p; ++k) {
     const int d = sizes[k];
     const int dp = d + (d & 1);
-    if (d <= 32 && !(few && d >= 8)) {
+    const int c = cls_of(d);
+    if (c < 0 || !cta_cls[c]) {
       wids[dp <= 8 ? 0 : dp <= 16 ? 1 : 2].push_back(k);
     } else {
       bids.push_back(k);
       dpb = std::max(dpb, dp);
     }
   }
+  s.in_block.assign(std::max(p, 1), 0);
+  for (int k : bids) s.in_block[k] = 1;
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->dev);
   if (maxsm <= 0) maxsm = 227 * 1024;
@@ -2511,7 +2527,7 @@ int hsde_stats(hsde_t *h, double *out) {
     const bool cold_ran = s.block_plan.cold_cv && !h->jacobi;
     for (int i = 0; i < s.block_plan.count; ++i) n_fail += cf[i] != 0;
     for (int k = 0; k < s.P.p; ++k) {
-      const bool big = s.sizes[k] > 32;
+      const bool big = s.in_block[k] != 0;  // CTA team (order > 32, or a small class with few cliques)
       // final states: 0 fast path, 16 fast path after Jacobi sweeps (resumed),
       // 33 cold / Jacobi path (no basis), 34..37 after a hand-over (reason + 34)
       const bool resumed = big && split_ran && cs[k] == SPLIT_DONE + 16;
@@ -2542,7 +2558,7 @@ int hsde_stats(hsde_t *h, double *out) {
   }
   int nbig = 0;
   for (auto &s : h->sh)
-    for (int k = 0; k < s.P.p; ++k) nbig += s.sizes[k] > 32;
+    for (int k = 0; k < s.P.p; ++k) nbig += s.in_block[k] != 0;
   out[4] = nbig ? n_done / nbig : 0.0;
   out[5] = nbig ? n_hand / nbig : 0.0;
   out[6] = n_done ? n_fp / n_done : 0.0;

@@ -271,14 +271,14 @@ __device__ __forceinline__ double cta_min(double v, double *red) {
 __device__ __forceinline__ int qdiv(int e, float inv) { return (int)(((float)e + 0.5f) * inv); }
 
 // 1 / x to ~1 ulp without the division's slow-path branch (a float seed and
-// three Newton steps: the element loops interleave several of these); x outside
-// the float range falls back to the IEEE reciprocal.  The Riccati denominators
+// three Newton steps, no branch: the element loops interleave several of
+// these).  The Riccati denominators
 // only need a consistent, accurate value: an ulp in 1 / Delta moves the fixed
 // point like an ulp in diag B.
 __device__ __forceinline__ double fast_rcp(double x) {
-  const float f = __frcp_rn(__double2float_rn(x));
-  if (!(fabsf(f) > 1e-37f && fabsf(f) < 1e37f)) return __drcp_rn(x);
-  double y = (double)f;
+  // (x outside the float range gives inf / NaN: the fixed point then reads as
+  // stalled and the clique goes to the cold path)
+  double y = (double)__frcp_rn(__double2float_rn(x));
   y = fma(y, fma(-x, y, 1.0), y);
   y = fma(y, fma(-x, y, 1.0), y);
   y = fma(y, fma(-x, y, 1.0), y);
@@ -710,14 +710,32 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     for (int s = 0; s < kSplitMaxB; ++s) {
       const int t = w + s * nw;
       if (t < nx) {
+        // the block's eight elements per lane as straight-line code on clamped
+        // indices (independent chains interleave; only the stores are predicated)
         const int bi = qdiv(t, invbr), bj = t - bi * nbr;
-        blk16_each(c[s], bi * 16, bj * 16, n, r, [&](int i, int j, double v) {
-          const double dl = lam[j] - lam[r + i];
-          const double x = (R1[j * L + r + i] + v) * fast_rcp(dl);
-          const double dx = (x - R1[(r + i) * L + j]) * dl;  // increment in residual units
-          acc += dx * dx;
-          R1[(r + i) * L + j] = x;
-        });
+        const int q = lane >> 2, kk = lane & 3;
+#pragma unroll
+        for (int h4 = 0; h4 < 2; ++h4) {  // (four at a time: eight cost spills under the 80-register cap)
+          double xn[4], dxs[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int a = h4, b = u >> 1, e = u & 1;
+            const int i = min(bi * 16 + 8 * a + q, n - 1), j = min(bj * 16 + 8 * b + 2 * kk + e, r - 1);
+            const double dl = lam[j] - lam[r + i];
+            const double x = (R1[j * L + r + i] + c[s][a][b][e]) * fast_rcp(dl);
+            dxs[u] = (x - R1[(r + i) * L + j]) * dl;  // increment in residual units
+            xn[u] = x;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int a = h4, b = u >> 1, e = u & 1;
+            const int i = bi * 16 + 8 * a + q, j = bj * 16 + 8 * b + 2 * kk + e;
+            if (i < n && j < r) {
+              acc = fma(dxs[u], dxs[u], acc);
+              R1[(r + i) * L + j] = xn[u];
+            }
+          }
+        }
       }
     }
     acc = warp_sum(acc);
@@ -727,7 +745,10 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     // the decision runs in float on residuals relative to |B|_F (every thread
     // the same deterministic arithmetic; an fp64 sqrt and two divisions per pass
     // sat on the critical path of every warp)
-    const float delta = sqrtf((float)(red_total(rb, nw) * inb2));
+    double tot = lane < nw ? rb[lane] : 0.0;  // butterfly: the same bits in every lane and warp
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    const float delta = sqrtf((float)(tot * inb2));
     if (newy) yb ^= 1;
     // contraction per pass: over two passes (the lagged quadratic term makes
     // consecutive increments non-monotone), over one for the first pass

@@ -12,6 +12,6 @@ for i in range(12):
     st = h.stats()
     dbg = h.debug_jacobi(0)
     stamps = dbg[48:57]
-    print((i + 1) * 20, round(ms / 20 * 1e3, 1), "us/it", {k: round(v, 3) for k, v in st.items() if k in ("split_done", "split_fp_iters", "split_resumed", "cold_done", "handoff_refresh", "handoff_stall")},
+    print((i + 1) * 20, round(ms / 20 * 1e3, 1), "us/it", {k: round(v, 3) for k, v in st.items()},
           "phases", [int(stamps[j + 1] - stamps[j]) for j in range(8)], flush=True)
 h.close()
