@@ -677,12 +677,24 @@ __device__ void cold_finish(int d, const ColdSmem &cs, double *vst, double *g2, 
       }
       break;
     }
-    team_mm1<false, false>(d, d, Opd{Vs, lv, 1}, Opd{g2, d, 1}, d, [&](int a, int b, double v) {
+    team_mm1<false, false, false, 5>(d, d, Opd{Vs, lv, 1}, Opd{g2, d, 1}, d, [&](int a, int b, double v) {  // G from L2
       vst[(int64_t)b * d + a] = fma(-0.5, v, 1.5 * Vs[(int64_t)a * lv + b]);
     });
-    for (int e = tid; e < d * d; e += blockDim.x) {
-      const int k = e / d, i = e - k * d;
-      Vs[(int64_t)i * lv + k] = vst[(int64_t)k * d + i];
+    {  // V back from the store, eight loads in flight per thread
+      const float invd = 1.0f / d;
+      for (int e0 = tid; e0 < d * d; e0 += 8 * blockDim.x) {
+        double v8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v8[q] = vst[min(e0 + q * (int)blockDim.x, d * d - 1)];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int e = e0 + q * blockDim.x;
+          if (e < d * d) {
+            const int k = qdiv(e, invd), i = e - k * d;
+            Vs[(int64_t)i * lv + k] = v8[q];
+          }
+        }
+      }
     }
     __syncthreads();
     // one step takes a departure of 2^-26 below rounding; a second one covers
@@ -817,7 +829,18 @@ __device__ int cold_one(const DevProblem &P, const DevState &S, const DevWork &W
     cold_finish(
         d, cs, W.vstore + off, g2, xat, [&](int a, int b, double v) { su[a * d + b] = v; }, W.dbg);
     __syncthreads();
-    for (int e = tid; e < d * d; e += T) sw[e] += su[e];  // w_s = (w_s - us_h) + P (solver.py:391-394)
+    for (int e0 = tid; e0 < d * d; e0 += 8 * T) {  // w_s = (w_s - us_h) + P (solver.py:391-394), batched loads
+      double a8[8], b8[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = min(e0 + q * T, d * d - 1);
+        a8[q] = sw[e];
+        b8[q] = su[e];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (e0 + q * T < d * d) sw[e0 + q * T] = a8[q] + b8[q];
+    }
     if (tid == 0) {
       W.vvalid[k] = 1;
       if (W.sweeps) W.sweeps[k] = 0;

@@ -82,7 +82,9 @@ struct Opd {
 // c[a][b][e] = D(i0 + 8a + q, j0 + 8b + 2kk + e)).  Rows >= M and columns >= N
 // read a clamped valid row / column (their results are discarded by the
 // caller); k >= K is zero-filled.  BROW: B's row k is brow[k] (row gather).
-template <bool BROW = false>
+// UNR: k-steps per trip (an operand in global memory wants the loads of several
+// k-steps in flight: L2 latency, not shared-memory latency, paces the chain).
+template <bool BROW = false, int UNR = 2>
 __device__ __forceinline__ void blk16(double (&c)[2][2][2], const Opd &A, const Opd &B, int i0, int j0, int M,
                                       int N, int K, const int *brow = nullptr) {
   const int lane = threadIdx.x & 31, q = lane >> 2, kk = lane & 3;
@@ -99,6 +101,38 @@ __device__ __forceinline__ void blk16(double (&c)[2][2][2], const Opd &A, const 
   // second tile row / column outside the output: skip its products (warp-uniform)
   const bool ha = i0 + 8 < M, hb = j0 + 8 < N;
   int k0 = 0;
+  if (UNR > 2) {
+    // batches of UNR k-steps: every operand load of the batch issued before its products
+    for (; k0 + 4 * UNR <= K4; k0 += 4 * UNR) {
+      double x0[UNR], x1[UNR], y0[UNR], y1[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        x0[u] = a0[u * sa];
+        x1[u] = a1[u * sa];
+        if (BROW) {
+          const int ro = brow[k0 + 4 * u + kk] * B.rs;
+          y0[u] = b0[ro];
+          y1[u] = b1[ro];
+        } else {
+          y0[u] = b0[u * sb];
+          y1[u] = b1[u * sb];
+        }
+      }
+      a0 += UNR * sa;
+      a1 += UNR * sa;
+      if (!BROW) {
+        b0 += UNR * sb;
+        b1 += UNR * sb;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        dmma884(c[0][0][0], c[0][0][1], x0[u], y0[u]);
+        if (hb) dmma884(c[0][1][0], c[0][1][1], x0[u], y1[u]);
+        if (ha) dmma884(c[1][0][0], c[1][0][1], x1[u], y0[u]);
+        if (ha && hb) dmma884(c[1][1][0], c[1][1][1], x1[u], y1[u]);
+      }
+    }
+  }
 #pragma unroll 2
   for (; k0 < K4; k0 += 4) {
     double x0 = *a0, x1 = *a1, y0, y1;
@@ -177,7 +211,7 @@ __device__ __forceinline__ void upper_block(int t, int nb, int &bi, int &bj) {
 // triangles from the upper values (exactly symmetric).  INPLACE: every warp
 // finishes reading before the first emit (the output may overwrite an
 // operand; at most kSplitMaxB blocks per warp).  Ends with a barrier.
-template <bool SYM, bool INPLACE, bool BROW = false, class Emit>
+template <bool SYM, bool INPLACE, bool BROW = false, int UNR = 2, class Emit>
 __device__ void team_mm(int M, int N, const Opd &A1, const Opd &B1, int K1, const Opd &A2, const Opd &B2, int K2,
                         Emit emit, const int *brow = nullptr) {
   const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -216,7 +250,7 @@ __device__ void team_mm(int M, int N, const Opd &A1, const Opd &B1, int K1, cons
       if (t < nblk) {
         int i0, j0;
         place(t, i0, j0);
-        if (K1 > 0) blk16<BROW>(c[s], A1, B1, i0, j0, M, N, K1, brow);
+        if (K1 > 0) blk16<BROW, UNR>(c[s], A1, B1, i0, j0, M, N, K1, brow);
         if (K2 > 0) blk16(c[s], A2, B2, i0, j0, M, N, K2);
       }
     }
@@ -236,7 +270,7 @@ __device__ void team_mm(int M, int N, const Opd &A1, const Opd &B1, int K1, cons
       blk16_zero(c);
       int i0, j0;
       place(t, i0, j0);
-      if (K1 > 0) blk16<BROW>(c, A1, B1, i0, j0, M, N, K1, brow);
+      if (K1 > 0) blk16<BROW, UNR>(c, A1, B1, i0, j0, M, N, K1, brow);
       if (K2 > 0) blk16(c, A2, B2, i0, j0, M, N, K2);
       out(c, i0, j0);
     }
@@ -244,10 +278,10 @@ __device__ void team_mm(int M, int N, const Opd &A1, const Opd &B1, int K1, cons
   __syncthreads();
 }
 
-template <bool SYM, bool INPLACE, bool BROW = false, class Emit>
+template <bool SYM, bool INPLACE, bool BROW = false, int UNR = 2, class Emit>
 __device__ __forceinline__ void team_mm1(int M, int N, const Opd &A, const Opd &B, int K, Emit emit,
                                          const int *brow = nullptr) {
-  team_mm<SYM, INPLACE, BROW>(M, N, A, B, K, A, B, 0, emit, brow);
+  team_mm<SYM, INPLACE, BROW, UNR>(M, N, A, B, K, A, B, 0, emit, brow);
 }
 
 __device__ __forceinline__ double cta_sum(double v, double *red) {
