@@ -287,17 +287,22 @@ int h2d_staged(hsde_handle *h, void *dst, const void *src, size_t bytes) {
 }
 
 template <class T>
-int dupload(hsde_handle *h, T **p, const T *src, size_t n) {
-  RC(dalloc(h, p, n));
-  if (n * sizeof(T) >= kStagedMin) return h2d_staged(h, *p, src, n * sizeof(T));
+int dcopy(hsde_handle *h, T *dst, const T *src, size_t n) {
+  if (n * sizeof(T) >= kStagedMin) return h2d_staged(h, dst, src, n * sizeof(T));
   if (n) {
-    cudaError_t e = cudaMemcpy(*p, src, n * sizeof(T), cudaMemcpyHostToDevice);
+    cudaError_t e = cudaMemcpy(dst, src, n * sizeof(T), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
       h->err = std::string("cudaMemcpy H2D: ") + cudaGetErrorString(e);
       return HSDE_ERR_CUDA;
     }
   }
   return 0;
+}
+
+template <class T>
+int dupload(hsde_handle *h, T **p, const T *src, size_t n) {
+  RC(dalloc(h, p, n));
+  return dcopy(h, *p, src, n);
 }
 
 int grid_for(int64_t n, int cap = 148 * 8) {
@@ -1499,14 +1504,28 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
   int *a_col = nullptr, *at_row_d = nullptr;
   double *a_val = nullptr, *at_val_d = nullptr;
   std::vector<int64_t> rp(m + 1, 0);
+  // (single shard) A goes up on a host thread -- staged pinned copies on their own
+  // stream -- while this thread builds the segments, cover lists and small
+  // uploads, none of which read A; joined before the CSC is built
+  std::thread a_up;
+  struct Joiner {
+    std::thread &t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } a_join{a_up};
+  int a_rc = 0;
   if (!d->owned) {
     rp.assign(d->a_row_ptr, d->a_row_ptr + m + 1);
-    RC(dupload(h, &a_rp, d->a_row_ptr, m + 1));
-    RC(dupload(h, &a_col, d->a_col, nnz));
-    RC(dupload(h, &a_val, d->a_val, nnz));
-    tick("  A upload");
-    RC(check_csr_device(h, a_rp, a_col, m, n_c));
-    RC(build_csc_device(h, m, n_c, nnz, a_rp, a_col, a_val, &at_cp_d, &at_row_d, &at_val_d));
+    RC(dalloc(h, &a_rp, (size_t)m + 1));
+    RC(dalloc(h, &a_col, (size_t)nnz));
+    RC(dalloc(h, &a_val, (size_t)nnz));
+    a_up = std::thread([&a_rc, h, d, a_rp, a_col, a_val, m, nnz] {
+      cudaSetDevice(h->dev);
+      a_rc = dcopy(h, a_rp, d->a_row_ptr, (size_t)m + 1);
+      if (!a_rc) a_rc = dcopy(h, a_col, d->a_col, (size_t)nnz);
+      if (!a_rc) a_rc = dcopy(h, a_val, d->a_val, (size_t)nnz);
+    });
   } else {
     // CSC over all local columns (A' g is needed on every local coordinate)
     int64_t *f_rp = nullptr;
@@ -1541,26 +1560,7 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
     RC(dupload(h, &a_col, col.data(), col.size()));
     RC(dupload(h, &a_val, val.data(), val.size()));
   }
-  {
-    // longest owned column (diagonal-Schur test)
-    unsigned long long *mx = nullptr;
-    CK(pool_malloc(h, (void **)&mx, sizeof(unsigned long long)));
-    CK(cudaMemset(mx, 0, sizeof(unsigned long long)));
-    unsigned char *own_tmp = nullptr;
-    if (d->owned) {
-      CK(pool_malloc(h, (void **)&own_tmp, n_c));
-      CK(cudaMemcpy(own_tmp, owned.data(), n_c, cudaMemcpyHostToDevice));
-    }
-    k_maxcol<<<grid_for(n_c), kBlock, 0, h->st>>>(at_cp_d, n_c, own_tmp, mx);
-    CKL();
-    unsigned long long hm = 0;
-    CK(cudaMemcpyAsync(&hm, mx, sizeof hm, cudaMemcpyDeviceToHost, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    s.maxcol = (int64_t)hm;
-    pool_free(h, mx);
-    pool_free(h, own_tmp);
-  }
-  tick("  A CSR+CSC (device)");
+  tick("  A alloc / sharded CSR+CSC");
   // row segments
   std::vector<int> seg_row, row_seg(m + 1, 0);
   std::vector<int64_t> seg_beg;
@@ -1634,6 +1634,33 @@ int build_shard(hsde_handle *h, ShardDev &s, const hsde_problem_desc *d) {
     P.sep_local = sep_local_d;
     P.sep_pos = sep_pos_d;
   }
+  if (a_up.joinable()) {
+    a_up.join();
+    RC(a_rc);
+    tick("  A upload (joined)");
+    RC(check_csr_device(h, a_rp, a_col, m, n_c));
+    RC(build_csc_device(h, m, n_c, nnz, a_rp, a_col, a_val, &at_cp_d, &at_row_d, &at_val_d));
+  }
+  {
+    // longest owned column (diagonal-Schur test)
+    unsigned long long *mx = nullptr;
+    CK(pool_malloc(h, (void **)&mx, sizeof(unsigned long long)));
+    CK(cudaMemset(mx, 0, sizeof(unsigned long long)));
+    unsigned char *own_tmp = nullptr;
+    if (d->owned) {
+      CK(pool_malloc(h, (void **)&own_tmp, n_c));
+      CK(cudaMemcpy(own_tmp, owned.data(), n_c, cudaMemcpyHostToDevice));
+    }
+    k_maxcol<<<grid_for(n_c), kBlock, 0, h->st>>>(at_cp_d, n_c, own_tmp, mx);
+    CKL();
+    unsigned long long hm = 0;
+    CK(cudaMemcpyAsync(&hm, mx, sizeof hm, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    s.maxcol = (int64_t)hm;
+    pool_free(h, mx);
+    pool_free(h, own_tmp);
+  }
+  tick("  A CSR+CSC (device)");
   P.a_rp = a_rp;
   P.a_col = a_col;
   P.a_val = a_val;
