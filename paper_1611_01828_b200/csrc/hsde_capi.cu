@@ -202,6 +202,34 @@ void retain_pool(int dev) {
   done[dev] = true;
 }
 
+// Pinned host slots for the check results.  cudaMallocHost / cudaFreeHost per
+// handle cost 10-450 ms sporadically (measured: one solve in ~6 paid it in
+// hsde_destroy or hsde_create); handles take 64-double slots from process-wide
+// pinned slabs instead (portable, grown 32 slots at a time, never freed).
+std::mutex g_pin_mu;
+std::vector<double *> g_pin_free;
+
+double *pinned_slot_acquire() {
+  std::lock_guard<std::mutex> lock(g_pin_mu);
+  if (g_pin_free.empty()) {
+    double *slab = nullptr;
+    if (cudaHostAlloc((void **)&slab, 32 * 64 * sizeof(double), cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    for (int i = 0; i < 32; ++i) g_pin_free.push_back(slab + 64 * i);
+  }
+  double *p = g_pin_free.back();
+  g_pin_free.pop_back();
+  return p;
+}
+
+void pinned_slot_release(double *p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lock(g_pin_mu);
+  g_pin_free.push_back(p);
+}
+
 // pool allocation usable from any stream on return
 cudaError_t pool_malloc(hsde_handle *h, void **p, size_t bytes) {
   cudaError_t e = cudaMallocAsync(p, std::max<size_t>(bytes, 1), h->st);
@@ -1993,8 +2021,9 @@ int hsde_create_sharded(const hsde_problem_desc *descs, int32_t nshards, const h
   h->warm = !(s->flags & HSDE_FLAG_COLD_EIG);
   h->split = !(s->flags & HSDE_FLAG_NO_SPLIT);
   h->jacobi = (s->flags & HSDE_FLAG_JACOBI) != 0;
-  if (cudaMallocHost(&h->h_chk, 64 * sizeof(double)) != cudaSuccess) {
-    g_create_error = "cudaMallocHost failed";
+  h->h_chk = pinned_slot_acquire();
+  if (!h->h_chk) {
+    g_create_error = "cudaHostAlloc failed";
     delete h;
     return HSDE_ERR_CUDA;
   }
@@ -2014,14 +2043,18 @@ int hsde_create(const hsde_problem_desc *desc, const hsde_settings *settings, hs
 
 void hsde_destroy(hsde_t *h) {
   if (!h) return;
+  SetupTimer tick;
   cudaSetDevice(h->dev);
   if (h->st) cudaStreamSynchronize(h->st);
+  tick("destroy: sync");
   if (h->g1) cudaGraphExecDestroy(h->g1);
   if (h->gci) cudaGraphExecDestroy(h->gci);
+  tick("destroy: graphs");
   if (h->nccl) ncclCommDestroy(h->nccl);
   for (void *p : h->bufs) pool_free(h, p);
   if (h->st) cudaStreamSynchronize(h->st);
-  if (h->h_chk) cudaFreeHost(h->h_chk);
+  tick("destroy: pool frees");
+  pinned_slot_release(h->h_chk);
   for (int a = 0; a < hsde_handle::kAux; ++a) {
     if (h->aux[a]) cudaStreamDestroy(h->aux[a]);
     if (h->ev_join[a]) cudaEventDestroy(h->ev_join[a]);
@@ -2029,6 +2062,7 @@ void hsde_destroy(hsde_t *h) {
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_xjoin) cudaEventDestroy(h->ev_xjoin);
   if (h->st) cudaStreamDestroy(h->st);
+  tick("destroy: streams");
   delete h;
 }
 

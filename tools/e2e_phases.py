@@ -12,7 +12,7 @@ from paper_1611_01828_b200.synthetic import make_config  # noqa: E402
 
 cp = make_config(int(sys.argv[1]) if len(sys.argv) > 1 else 4)
 H.solve_decomposed(make_config(0), H.SolverSettings())
-for rep in range(5):
+for rep in range(int(sys.argv[2]) if len(sys.argv) > 2 else 5):
     cp._cache.pop("pattern_index", None)
     st = H.SolverSettings()
     t0 = time.perf_counter()
