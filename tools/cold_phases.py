@@ -19,7 +19,7 @@ from paper_1611_01828_b200 import _lib  # noqa: E402
 from paper_1611_01828_b200.synthetic import make_config  # noqa: E402
 
 names = ["load", "tridiag", "bisect", "twisted", "backtr", "newton-schulz", "P"]
-cp = make_config(4)
+cp = make_config(int(sys.argv[1]) if len(sys.argv) > 1 else 4)
 h = _lib.Handle(cp)
 rng = np.random.default_rng(1)
 v = rng.normal(size=h.total)
