@@ -373,27 +373,32 @@ def run_ours(args):
     #     (one event set per iteration, one sync at the end);
     # (b) steady state: the first handle goes on to iteration >= 220, then 20
     #     profiled iterations (every clique on the warm fast path).
-    if comm is None:
-        h2 = _lib.Handle(cp, device=dev)
-    else:
-        h2 = _lib.Handle(cp, shards=[shards[rank]], comm=init_comm(), device=dev)
-    h2.iterate(args.warmup)
-    h2.sync()
-    prof_iters = args.steps
-    prof, launches = h2.profile_iterations(prof_iters)
-    eig_stats = h2.stats()
-    h2.close()
-    gpu_launches_per_iter = (launches - 1) / prof_iters
     peaks = load_peaks()
     half = h.half_passes
-    dominant, roofs = roofline_for(cp, prof, prof_iters, peaks, half)
     done = args.warmup + args.steps
-    if done < 220:
-        h.iterate(220 - done)
-        h.sync()
-    steady_iters = 20
-    prof_s, _ = h.profile_iterations(steady_iters)
-    _, roofs_s = roofline_for(cp, prof_s, steady_iters, peaks, half)
+    roofs_s, prof_s, steady_iters = None, {}, 20
+    if comm is None:
+        h2 = _lib.Handle(cp, device=dev)
+        h2.iterate(args.warmup)
+        h2.sync()
+        prof_iters = args.steps
+        prof, launches = h2.profile_iterations(prof_iters)
+        eig_stats = h2.stats()
+        h2.close()
+        window = f"iterations {args.warmup + 1}..{args.warmup + args.steps} (the window `value` times)"
+        if done < 220:
+            h.iterate(220 - done)
+            h.sync()
+        prof_s, _ = h.profile_iterations(steady_iters)
+        _, roofs_s = roofline_for(cp, prof_s, steady_iters, peaks, half)
+    else:
+        # sharded (one rank per GPU): the same handle goes on, one communicator per process
+        prof_iters = min(args.steps, 20)
+        prof, launches = h.profile_iterations(prof_iters)
+        eig_stats = h.stats()
+        window = f"iterations {done + 1}..{done + prof_iters} (after the timed window, same handle)"
+    gpu_launches_per_iter = (launches - 1) / prof_iters
+    dominant, roofs = roofline_for(cp, prof, prof_iters, peaks, half)
     h.close()
     line = None
     if rank == 0:
@@ -411,8 +416,7 @@ def run_ours(args):
         }
         if roofs:
             line["roofline"] = dict(roofs[dominant], kernel=KERNELS.get(dominant, dominant),
-                                    window=f"iterations {args.warmup + 1}..{args.warmup + args.steps} "
-                                           "(the window `value` times)")
+                                    window=window)
             line["roofline_all"] = roofs
         if roofs_s:
             line["roofline_steady_state"] = {
