@@ -179,10 +179,17 @@ class _Mapper:
         self.cp = cp
         self.n2 = n2
         self.full = cp.N_c == n2
-        if not self.full:
-            mask = np.ones(n2, dtype=bool)
-            mask[cp.covered] = False
-            self.off = np.flatnonzero(mask)
+        self._off = None
+
+    @property
+    def off(self) -> np.ndarray:
+        """Off-pattern flat ids (built on first use: n^2 long scans, 2.6e8 for config 4,
+        that a plain solve never needs)."""
+        if self._off is None:
+            mask = np.ones(self.n2, dtype=bool)
+            mask[self.cp.covered] = False
+            self._off = np.flatnonzero(mask)
+        return self._off
 
     def down(self, full_vec: np.ndarray) -> np.ndarray:
         full_vec = np.asarray(full_vec, dtype=float)
