@@ -260,13 +260,35 @@ class CompressedProblem:
         return out
 
 
-def compress(dp, full: bool = False, _numpy_only: bool = False) -> CompressedProblem:
+def edges_array(agg, n: int):
+    """The aggregate pattern's (i, j) pairs (graphs.py:37: a frozenset of tuples) as a
+    lexicographically sorted (E, 2) int64 array -- the order of ``sorted(agg.edges)``,
+    without a Python-level sort of up to millions of tuples."""
+    if agg is None or getattr(agg, "edges", None) is None:
+        return None
+    ed = agg.edges
+    if isinstance(ed, np.ndarray):
+        e = np.asarray(ed, dtype=np.int64).reshape(-1, 2)
+    else:
+        import itertools
+
+        e = np.fromiter(itertools.chain.from_iterable(ed), dtype=np.int64, count=2 * len(ed)).reshape(-1, 2)
+    if e.shape[0] > 1:
+        code = e[:, 0] * max(int(n), int(e[:, 1].max(initial=0)) + 1) + e[:, 1]
+        if not bool(np.all(code[1:] > code[:-1])):
+            e = e[np.argsort(code, kind="stable")]
+    return e
+
+
+def compress(dp, full: bool = False, _numpy_only: bool = False, with_edges: bool = True) -> CompressedProblem:
     """Build the covered layout from a reference-style DecomposedProblem.
 
     ``dp`` may be the reference's own object or the mirror above.  Covered =
     clique-selected coordinates (D > 0) + A's column support + c's support.
     ``full=True`` keeps all n**2 coordinates (the unit-level API uses it for
     small problems so arbitrary reference-layout vectors run on the device).
+    ``with_edges=False`` skips the aggregate pattern's edge list (the report's
+    pattern index then takes it from ``dp`` itself, off the critical path).
     """
     n, m = int(dp.n), int(dp.m)
     n2 = n * n
@@ -313,11 +335,7 @@ def compress(dp, full: bool = False, _numpy_only: bool = False) -> CompressedPro
     cliques = tuple(np.asarray(c, dtype=np.int64) for c in dp.dec.cliques)
     sizes = np.asarray(dp.dec.sizes, dtype=np.int64)
     offsets = np.asarray(dp.dec.offsets, dtype=np.int64)
-    agg = getattr(dp, "aggregate", None)
-    edges = None
-    if agg is not None and getattr(agg, "edges", None) is not None:
-        e = sorted(agg.edges)
-        edges = np.asarray(e, dtype=np.int64).reshape(-1, 2)
+    edges = edges_array(getattr(dp, "aggregate", None), n) if with_edges else None
     return CompressedProblem(
         n=n, m=m, covered=covered, c=c_cov, A=Ac,
         b=np.asarray(dp.b, dtype=float).copy(), cliques=cliques, sizes=sizes,

@@ -30,7 +30,7 @@ import scipy.sparse as sp
 
 from . import _lib
 from .errors import EigenFailure, FactorizationFailure, TauZero
-from .problem import CompressedProblem, compress
+from .problem import CompressedProblem, compress, edges_array
 from .report import (STATUS_DUAL_INFEASIBLE, STATUS_MAX_ITERS, STATUS_OPTIMAL,
                      STATUS_PRIMAL_INFEASIBLE, PatternEntries, ProblemStats, Residuals, SolverReport,
                      Timing)
@@ -459,7 +459,7 @@ class _Session:
         from .shard import make_shards
 
         self.dp = dp
-        self.cp = dp if isinstance(dp, CompressedProblem) else compress(dp)
+        self.cp = dp if isinstance(dp, CompressedProblem) else compress(dp, with_edges=False)
         self.n2 = self.cp.N_c if isinstance(dp, CompressedProblem) else int(dp.n) ** 2
         self.mapper = _Mapper(self.cp, self.n2)
         self.settings = settings
@@ -532,7 +532,9 @@ def _pattern_index(cp: CompressedProblem, dp):
     if isinstance(dp, CompressedProblem) or getattr(dp, "aggregate", None) is None:
         edges = cp.aggregate_edges if cp.aggregate_edges is not None else np.zeros((0, 2), np.int64)
     else:
-        edges = np.asarray(sorted(dp.aggregate.edges), dtype=np.int64).reshape(-1, 2)
+        edges = edges_array(dp.aggregate, n)
+        if edges is None:
+            edges = np.zeros((0, 2), np.int64)
     diag = np.arange(n, dtype=np.int64)
     edges = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
     ecode = edges[:, 0] * n + edges[:, 1]
