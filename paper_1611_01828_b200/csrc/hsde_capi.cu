@@ -340,6 +340,26 @@ int grid_for(int64_t n, int cap = 148 * 8) {
   return (int)g;
 }
 
+// Kernel launch with (pdl) programmatic stream serialisation: the kernel may be
+// scheduled while the previous kernel of the stream drains; it calls pdl_wait()
+// before touching anything (hsde_kernels.cuh).  Captured into the iteration graphs
+// as programmatic dependency edges.
+template <class... KArgs, class... Args>
+cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, KArgs(std::forward<Args>(args))...);
+}
+
 double *buf_ptr(ShardDev &s, int which) {
   switch (which) {
     case BUF_SEP: return s.W.sepbuf;
@@ -557,18 +577,15 @@ int dev_dot_owned(hsde_handle *h, ShardDev &s, const double *a, const double *b,
 
 // q0 = A t0 of one shard: tile partials + ordered row sums into W.qbuf (half
 // passes), or row-segment partials in W.qseg (+ W.qbuf when sharded)
-int launch_aq(hsde_handle *h, ShardDev &s, cudaStream_t st, int *nl) {
+int launch_aq(hsde_handle *h, ShardDev &s, cudaStream_t st, int *nl, bool pdl = false) {
   const DevProblem &P = s.P;
   if (P.half) {
     // (forming the pair sums while staging each tile instead measured 24 us
     // slower: the gathers sit at the start of every CTA, 4x redundant)
-    k_pair_sum<<<grid_for(P.n_pair), kBlock, 0, st>>>(P, s.W.t, s.W.xq);
-    CKL();
-    k_spmv_half<false><<<P.rt_ntile * P.rt_split, kBlock, sizeof(double) * P.rt_tile, st>>>(P, s.W.xq,
-                                                                                            s.W.rtpart);
-    CKL();
-    k_rowsum_tiles<<<grid_for((int64_t)P.m * 32), kBlock, 0, st>>>(P, s.W.rtpart, s.W.qbuf);
-    CKL();
+    CK(launch_k(pdl, k_pair_sum, grid_for(P.n_pair), kBlock, 0, st, P, s.W.t, s.W.xq));
+    CK(launch_k(pdl, k_spmv_half<false>, P.rt_ntile * P.rt_split, kBlock, sizeof(double) * P.rt_tile, st, P,
+                s.W.xq, s.W.rtpart));
+    CK(launch_k(pdl, k_rowsum_tiles, grid_for((int64_t)P.m * 32), kBlock, 0, st, P, s.W.rtpart, s.W.qbuf));
     *nl += 3;
     return 0;
   }
@@ -587,12 +604,12 @@ int launch_aq(hsde_handle *h, ShardDev &s, cudaStream_t st, int *nl) {
 bool q_in_buf(const hsde_handle *h, const ShardDev &s) { return s.P.half || h->multi(); }
 
 // ua = t0 - P^{-1} A' g (+ block partials of c.ua)
-int launch_ua(hsde_handle *h, ShardDev &s, cudaStream_t st, bool with_dot) {
+int launch_ua(hsde_handle *h, ShardDev &s, cudaStream_t st, bool with_dot, bool pdl = false) {
   const DevProblem &P = s.P;
   if (P.half) {
     const size_t sm = sizeof(double) * (size_t)P.m;
-    if (with_dot) k_ua_half<true><<<s.grid_ua, kBlock, sm, st>>>(P, s.W, s.W.qp);
-    else k_ua_half<false><<<s.grid_ua, kBlock, sm, st>>>(P, s.W, s.W.qp);
+    if (with_dot) CK(launch_k(pdl, k_ua_half<true>, s.grid_ua, kBlock, sm, st, P, s.W, s.W.qp));
+    else CK(launch_k(pdl, k_ua_half<false>, s.grid_ua, kBlock, sm, st, P, s.W, s.W.qp));
   } else {
     if (with_dot) k_ua<true><<<s.grid_ua, kBlock, 0, st>>>(P, s.W, s.W.qp);
     else k_ua<false><<<s.grid_ua, kBlock, 0, st>>>(P, s.W, s.W.qp);
@@ -665,6 +682,13 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
   cudaStream_t st = h->st;
   const int G = (int)h->sh.size();
   const bool exact = (h->set.flags & HSDE_FLAG_EXACT_UY) != 0 && !h->multi();
+  // programmatic dependent launches along the affine chain (one shard, half
+  // passes, no all-reduce or event in between; not under the per-kernel profile)
+  static const int pdl_env = [] {
+    const char *e = std::getenv("HSDE_PDL");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool pdl = pdl_env && !ev && G == 1 && !h->multi() && h->sh[0].P.half && !exact && h->n_sep == 0;
   int nl = 0;
   auto mark = [&](int s) {
     if (ev) cudaEventRecord(ev[s], st);
@@ -691,21 +715,20 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
       CKL();
       ++nl;
     }
-    RC(launch_aq(h, s, st, &nl));
+    RC(launch_aq(h, s, st, &nl, pdl));
   }
   mark(PS_SPMV);
   RC(reduce(h, BUF_Q, h->sh[0].P.m));
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
-    k_schur<<<s.grid_schur, kBlock, s.schur_smem, st>>>(s.P, s.W.qseg, q_in_buf(h, s) ? s.W.qbuf : nullptr,
-                                                        s.W.ry, s.W.qp);
-    CKL();
+    CK(launch_k(pdl, k_schur, s.grid_schur, kBlock, s.schur_smem, st, s.P, s.W.qseg,
+                q_in_buf(h, s) ? s.W.qbuf : nullptr, s.W.ry, s.W.qp));
     ++nl;
   }
   mark(PS_SCHUR);
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
-    RC(launch_ua(h, s, st, true));
+    RC(launch_ua(h, s, st, true, pdl));
     ++nl;
     if (h->multi()) {
       k_sum_parts<<<1, 1024, 0, st>>>(s.W.part, s.grid_ua, s.W.red);
@@ -726,9 +749,8 @@ int launch_iteration(hsde_handle *h, cudaEvent_t *ev = nullptr, int *launches = 
   mark(PS_COMM);
   for (int g = 0; g < G; ++g) {
     ShardDev &s = h->sh[g];
-    k_scalars<<<1, 1024, 0, st>>>(s.P, s.S, s.W, s.grid_ua, exact ? 1 : 0, s.d_tmp3,
-                                  h->multi() ? s.W.red : nullptr);
-    CKL();
+    CK(launch_k(pdl, k_scalars, 1, 1024, 0, st, s.P, s.S, s.W, s.grid_ua, exact ? 1 : 0, s.d_tmp3,
+                h->multi() ? s.W.red : nullptr));
     ++nl;
   }
   mark(PS_SCALARS);

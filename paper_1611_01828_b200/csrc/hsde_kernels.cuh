@@ -151,6 +151,16 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Programmatic dependent launch (the hot chain k_rhs -> ... -> k_scalars of one
+// stream): a kernel launched with programmatic stream serialisation may be
+// scheduled while its predecessor drains; pdl_wait() returns once the
+// predecessor grid has completed and its writes are visible (a no-op for a
+// normal launch), pdl_trigger() lets the successor's launch begin.  Every
+// thread calls pdl_wait() first, on every path, so completion stays transitive
+// along the chain.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Fixed-order block sum; result valid in thread 0.  `sh` holds >= 32 doubles.
 __device__ __forceinline__ double block_sum(double v, double *sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -217,6 +227,7 @@ template <bool FROM_STATE>
 __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWork W,
                                                 const double *rx, const double *rs,
                                                 const double *rv, int nb_heavy) {
+  pdl_wait();
   double atau = 0.0;
   if (FROM_STATE) atau = S.u[P.total - 1] + S.w[P.total - 1];
   if ((int)blockIdx.x >= nb_heavy) {
@@ -244,12 +255,16 @@ __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWor
         rhs_finish<FROM_STATE>(P, S, W, rx, atau, lq[q], sg[q], sv[q]);
       }
     }
+    pdl_trigger();
     return;
   }
   // heavy coordinates: one warp each, lanes stride the slot list
   const int lane = threadIdx.x & 31;
   const int hw = (int)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (hw >= P.n_heavy) return;
+  if (hw >= P.n_heavy) {
+    pdl_trigger();
+    return;
+  }
   const int l = P.heavy[hw];
   double sg = 0.0, sv = 0.0;
   for (int e = P.cov_ptr[l] + lane; e < P.cov_ptr[l + 1]; e += 32)
@@ -257,6 +272,7 @@ __global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWor
   sg = warp_sum(sg);
   sv = warp_sum(sv);
   if (lane == 0) rhs_finish<FROM_STATE>(P, S, W, rx, atau, l, sg, sv);
+  pdl_trigger();
 }
 
 // t of the separator coordinates once their pull-scatter partials are all-reduced
@@ -312,6 +328,7 @@ __global__ void __launch_bounds__(kBlock) k_schur(DevProblem P, const double *__
                                                    const double *__restrict__ ry,
                                                    double *__restrict__ g) {
   extern __shared__ double qs[];
+  pdl_wait();
   for (int i = threadIdx.x; i < P.m; i += blockDim.x) {
     double q = 0.0;
     if (qfull) {
@@ -325,6 +342,7 @@ __global__ void __launch_bounds__(kBlock) k_schur(DevProblem P, const double *__
   if (P.schur_diag) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.m; i += gridDim.x * blockDim.x)
       g[i] = qs[i] * P.sinv[i];
+    pdl_trigger();
     return;
   }
   // kSchurSplit warps per row (contiguous column segments), rows in pairs per
@@ -362,6 +380,7 @@ __global__ void __launch_bounds__(kBlock) k_schur(DevProblem P, const double *__
     }
     __syncthreads();
   }
+  pdl_trigger();
 }
 
 // ua = t0 - P^{-1} (A' g)  (solver.py:232-235, see the header); WITH_DOT: block
@@ -413,10 +432,12 @@ constexpr int kRowTileSplit = 2;  // default P.rt_split: CTAs per tile (row grou
 
 // pair values x_q = t_l + t_mirror (t_l on the diagonal)
 __global__ void k_pair_sum(DevProblem P, const double *__restrict__ t, double *__restrict__ xq) {
+  pdl_wait();
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < P.n_pair; q += gridDim.x * blockDim.x) {
     const int l = P.pair_l[q], mm = P.pair_m[q];
     xq[q] = mm != l ? t[l] + t[mm] : t[l];
   }
+  pdl_trigger();
 }
 
 // q0 partials: part[r * ntile + tile] = sum over the tile's owned pairs of
@@ -426,6 +447,7 @@ template <bool PAIRS>
 __global__ void __launch_bounds__(kBlock) k_spmv_half(DevProblem P, const double *__restrict__ xq,
                                                        double *__restrict__ part) {
   extern __shared__ double xs[];  // [P.rt_tile]
+  pdl_wait();
   const int tile = blockIdx.x / P.rt_split, rr = blockIdx.x - tile * P.rt_split;
   const int q0 = tile * P.rt_tile, wn = min(P.rt_tile, P.n_pair - q0);
   if (PAIRS) {
@@ -459,10 +481,12 @@ __global__ void __launch_bounds__(kBlock) k_spmv_half(DevProblem P, const double
     const int rq = gr * 32 + lane;
     if (rq < P.m) part[(int64_t)P.rt_row[(int64_t)tile * P.m + rq] * P.rt_ntile + tile] = acc;
   }
+  pdl_trigger();
 }
 
 // q0_r = ordered sum of the row's tile partials (one warp per row)
 __global__ void k_rowsum_tiles(DevProblem P, const double *__restrict__ part, double *__restrict__ q) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < P.m; r += warps) {
@@ -471,6 +495,7 @@ __global__ void k_rowsum_tiles(DevProblem P, const double *__restrict__ part, do
     a = warp_sum(a);
     if (lane == 0) q[r] = a;
   }
+  pdl_trigger();
 }
 
 // ua = t0 - P^{-1} A' g over mirror pairs (one warp per SELL slice, lane =
@@ -479,6 +504,7 @@ template <bool WITH_DOT>
 __global__ void __launch_bounds__(kBlock) k_ua_half(DevProblem P, DevWork W, const double *__restrict__ g) {
   extern __shared__ double sg[];
   __shared__ double sh[32];
+  pdl_wait();
   for (int i = threadIdx.x; i < P.m; i += blockDim.x) sg[i] = g[i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -504,6 +530,7 @@ __global__ void __launch_bounds__(kBlock) k_ua_half(DevProblem P, DevWork W, con
     dot = block_sum(dot, sh);
     if (threadIdx.x == 0) W.part[blockIdx.x] = dot;
   }
+  pdl_trigger();
 }
 
 // ---------------------------------------------------------------------------
@@ -516,6 +543,7 @@ __global__ void __launch_bounds__(1024) k_scalars(DevProblem P, DevState S, DevW
                                                   const double *__restrict__ cua_red) {
   __shared__ double sh[32];
   __shared__ double bc[4];
+  pdl_wait();
   const int64_t yo = P.n_c + P.n_d;
   // k_cone_split schedule (hsde_split.cuh): ids and keys loaded first, the
   // partition done at the end (their latency hides behind the sums)
