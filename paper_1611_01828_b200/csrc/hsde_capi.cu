@@ -472,6 +472,17 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
   }();
   ConeArgs ca{pl.ids, pl.count, pl.dpmax, in, out, in_scale, h->warm ? 1 : 0, pl.pscratch, pl.pstride, 0,
               split_refresh, split_vupdate};
+  // cold / warm policy thresholds (hsde_split.cuh, hsde_cold.cuh)
+  static const double pol_f2c = [] {
+    const char *e = std::getenv("HSDE_POL_F2C");
+    return e ? std::atof(e) : 0.1225;
+  }();
+  static const double pol_c2f = [] {
+    const char *e = std::getenv("HSDE_POL_C2F");
+    return e ? std::atof(e) : 0.36;
+  }();
+  ca.pol_f2c = pol_f2c;
+  ca.pol_c2f = pol_c2f;
   if (!block) {
     const int grid = (pl.count + pl.per_block - 1) / pl.per_block;
     const int thr = pl.per_block * 32;

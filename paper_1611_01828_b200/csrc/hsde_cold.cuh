@@ -821,7 +821,7 @@ __device__ int cold_one(const DevProblem &P, const DevState &S, const DevWork &W
     const bool prev = (W.vvalid[k] & ~kVRefresh) > 0;
     // (measured on config 4: off(B) / |X - X_prev|_F ~ 0.3 - 0.5, so |dX| <= 0.6 g
     // predicts off(B) <~ 0.3 g, inside the fast path's 0.45 g)
-    if (tid == 0) W.cnext[k] = (prev && dx2 <= 0.36 * g * g) ? 0 : 1;  // |dX| <= 0.6 g
+    if (tid == 0) W.cnext[k] = (prev && dx2 <= ca.pol_c2f * g * g) ? 0 : 1;  // default |dX| <= 0.6 g
   }
   if (MODE == CONE_HOT) {
     double *su = S.u + so + off, *sw = S.w + so + off;

@@ -1210,6 +1210,8 @@ struct ConeArgs {
   int cold;          // k_cone_split: hand-overs go to the cold path (X kept in W.xarg)
   int cold_pass;     // k_cone_cold after k_cone_split: 0 the predicted cliques (W.ccur), 1 its hand-overs
   int pf_ahead;      // k_cone_split: resident CTA slots (0 = off); slot b prefetches the inputs of slot b + pf_ahead into L2
+  double pol_f2c;    // fast path -> cold next iteration when off(B)^2 > pol_f2c g^2 (default 0.1225: off > 0.35 g)
+  double pol_c2f;    // cold path -> fast next iteration when |X - X_prev|_F^2 <= pol_c2f g^2 (default 0.36: |dX| <= 0.6 g)
 };
 
 // Hot-path load of slot j: builds arg_s and performs the v / w_v update and

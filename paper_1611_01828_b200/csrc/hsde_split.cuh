@@ -1024,7 +1024,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
   if (tid == 0 && W.sweeps) W.sweeps[k] = -it;  // (stats: fixed-point iterations)
   // next iteration: the cold path when this basis was already near the bound
   // (off(B) > 0.35 g: the drift of a kept basis grows), else the fast path
-  if (tid == 0 && W.cnext && !refreshed) W.cnext[k] = o2 > 0.1225 * g * g ? 1 : 0;
+  if (tid == 0 && W.cnext && !refreshed) W.cnext[k] = o2 > ca.pol_f2c * g * g ? 1 : 0;
   // schedule key for the next iteration: passes, plus a refresh risk when off(B)
   // is already near the applicability bound
   if (tid == 0) W.ckey[k] = o2 > kSplitKey2 * kSplitOff2 * g * g ? 1 : 0;
