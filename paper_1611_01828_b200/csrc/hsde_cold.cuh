@@ -129,6 +129,18 @@ __device__ __forceinline__ double warp_allsum(double v) {
 // skipped; rows <= s inside a live chunk are frozen (zero multipliers).  The
 // owner of column s + 1 leaves it in colbuf while updating it, so the next
 // producer reads it from shared memory instead of selecting a register slot.
+// f(a[c]) for a run-time slot c in [LO, HI): a tree of warp-uniform branches
+template <int LO, int HI, int MC, int MR, class F>
+__device__ __forceinline__ void slot_dispatch(double (&a)[MC][MR], int c, F f) {
+  if constexpr (HI - LO == 1) {
+    f(a[LO]);
+  } else {
+    constexpr int MID = (LO + HI) / 2;
+    if (c < MID) slot_dispatch<LO, MID>(a, c, f);
+    else slot_dispatch<MID, HI>(a, c, f);
+  }
+}
+
 template <int MC, int MR>
 __device__ void cold_tridiag(double (&a)[MC][MR], int d, const ColdSmem &cs, double *hv, double *dbg) {
   constexpr int NW = kColdNW;
@@ -228,25 +240,30 @@ __device__ void cold_tridiag(double (&a)[MC][MR], int d, const ColdSmem &cs, dou
     if (stamp) dbg[18] = (double)clock64();
     __syncthreads();
     if (stamp) dbg[19] = (double)clock64();
-    {  // p = tau A v, one thread per row
-      const int t = threadIdx.x;
-      if (t > s && t < d) {
-        double p = 0.0;
-#pragma unroll
-        for (int q = 0; q < NW; ++q) p += rb[q * rl + t];
-        cs.pbuf[t] = tau * p;
-      }
-    }
     double dot = 0.0;
 #pragma unroll
     for (int q = 0; q < NW; ++q) dot += db[q];
     const double K = -0.5 * tau * tau * dot;  // w = p + K v (dsytd2)
+    {  // p = tau A v and w = p + K v, one thread per row (0 on the dead rows): the
+       // update reads w_k with one load per column instead of p_k, v_k and an fma
+      const int t = threadIdx.x;
+      if (t < rl) {
+        double wv = 0.0;
+        if (t > s && t < d) {
+          double p = 0.0;
+#pragma unroll
+          for (int q = 0; q < NW; ++q) p += rb[q * rl + t];
+          wv = fma(K, vb[t], tau * p);
+        }
+        cs.pbuf[t] = wv;
+      }
+    }
     __syncthreads();
     double wr[MR];
 #pragma unroll
     for (int r = 0; r < MR; ++r) {
       const int i = 32 * r + lane;
-      wr[r] = (i > s && i < d) ? fma(K, vr[r], cs.pbuf[i]) : 0.0;
+      wr[r] = i < rl ? cs.pbuf[i] : 0.0;
     }
 #pragma unroll
     for (int g = 0; g < MC; g += 4) {
@@ -256,7 +273,7 @@ __device__ void cold_tridiag(double (&a)[MC][MR], int d, const ColdSmem &cs, dou
         for (int u = 0; u < 4; ++u) {
           const int k = w + NW * (g + u);
           v4[u] = g + u < MC ? vb[k] : 0.0;
-          w4[u] = (g + u < MC && k > s && k < d) ? fma(K, v4[u], cs.pbuf[k]) : 0.0;
+          w4[u] = (g + u < MC && k < d) ? cs.pbuf[k] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -265,15 +282,16 @@ __device__ void cold_tridiag(double (&a)[MC][MR], int d, const ColdSmem &cs, dou
             if (g + u < MC) a[g + u][r] = fma(-vr[r], w4[u], fma(-wr[r], v4[u], a[g + u][r]));
       }
     }
-    // the owner of column s + 1 (slot (s + 1) / NW) hands it to the next producer
+    // the owner of column s + 1 (slot (s + 1) / NW) hands it to the next producer;
+    // the slot is found by a uniform branch tree (the register file cannot be
+    // indexed: a predicated chain over all MC slots cost ~4 MC instructions on the
+    // warp that is the next step's critical path)
     if (w == ((s + 1) & (NW - 1))) {
-      const int c1 = (s + 1) / NW;
+      slot_dispatch<0, MC>(a, (s + 1) / NW, [&](const double (&col)[MR]) {
 #pragma unroll
-      for (int c = 0; c < MC; ++c)
-        if (c == c1)
-#pragma unroll
-          for (int r = 0; r < MR; ++r)
-            if (32 * r + lane < rl) colbuf[32 * r + lane] = a[c][r];
+        for (int r = 0; r < MR; ++r)
+          if (32 * r + lane < rl) colbuf[32 * r + lane] = col[r];
+      });
     }
     __syncwarp();
     if (stamp) dbg[20] = (double)clock64();
