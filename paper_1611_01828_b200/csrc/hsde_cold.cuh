@@ -352,34 +352,39 @@ __device__ __forceinline__ int sturm_count(const double *da, const double *e2, i
 }
 
 // NP Sturm counts of the same block at once (independent recurrences
-// interleaved: the bisection rounds are latency chains of one DFMA per step,
-// so NP points per thread cost about one)
+// interleaved).  pk[k] = (a_k, e_{k-1}^2) packed: one 16-byte shared-memory load
+// per step; the signs of p_k go through a funnel-shift register and the changes
+// are counted once per eight steps (the step is bound by issued instructions:
+// 2 loads + 3 fp64 + 2 integer before, 1 + 3 + 1 now).
 template <int NP>
-__device__ __forceinline__ void sturm_count_n(const double *da, const double *e2, int bs, int be,
-                                              const double (&x)[NP], int (&c)[NP]) {
+__device__ __forceinline__ void sturm_count_n(const double2 *pk, int bs, int be, const double (&x)[NP],
+                                              int (&c)[NP]) {
   double pp[NP], pc[NP];
-  const double a0 = da[bs];
+  unsigned sh[NP];
+  const double a0 = pk[bs].x;
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
     pp[p] = 1.0;
     pc[p] = a0 - x[p];
-    c[p] = sgn_bit(pc[p]);
+    sh[p] = (unsigned)sgn_bit(pc[p]);
+    c[p] = (int)sh[p];
   }
   int k = bs + 1;
   for (; k + 7 <= be; k += 8) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const double ak = da[k + u], ek = e2[k + u - 1];
+      const double2 v = pk[k + u];
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
-        const double pn = fma(ak - x[p], pc[p], -ek * pp[p]);
-        c[p] += sgn_bit(pn) ^ sgn_bit(pc[p]);
+        const double pn = fma(v.x - x[p], pc[p], -v.y * pp[p]);
+        sh[p] = __funnelshift_l((unsigned)__double2hiint(pn), sh[p], 1);  // sign bit shifted in
         pp[p] = pc[p];
         pc[p] = pn;
       }
     }
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
+      c[p] += __popc((sh[p] ^ (sh[p] >> 1)) & 0xffu);  // the eight sign changes of this trip
       const int ex = (__double2hiint(pc[p]) >> 20) & 0x7ff;  // biased exponent (integer pipe)
       if (ex > 1023 + 300 || (ex < 1023 - 300 && ex > 0)) {
         const double f = ex > 1023 ? 0x1p-300 : 0x1p300;
@@ -389,10 +394,10 @@ __device__ __forceinline__ void sturm_count_n(const double *da, const double *e2
     }
   }
   for (; k <= be; ++k) {
-    const double ak = da[k], ek = e2[k - 1];
+    const double2 v = pk[k];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      const double pn = fma(ak - x[p], pc[p], -ek * pp[p]);
+      const double pn = fma(v.x - x[p], pc[p], -v.y * pp[p]);
       c[p] += sgn_bit(pn) ^ sgn_bit(pc[p]);
       pp[p] = pc[p];
       pc[p] = pn;
@@ -594,6 +599,9 @@ __device__ int cold_eig(int d, const ColdSmem &cs, bool values_only, double *hv,
   }
   if (tid == 0) *cs.flag = 0;
   __syncthreads();
+  // (a_k, e_{k-1}^2) packed for the Sturm recurrence, in the (dead) tridiagonalisation buffers
+  double2 *pk = reinterpret_cast<double2 *>(cs.vbuf);
+  for (int i = tid; i < d; i += T) pk[i] = make_double2(cs.dg[i], i > 0 ? cs.e2[i - 1] : 0.0);
   // ---- unreduced blocks; bisection, g threads per eigenvalue (multisection)
   for (int j = tid; j < d; j += T) {
     int b0 = j, b1 = j;
@@ -623,7 +631,7 @@ __device__ int cold_eig(int d, const ColdSmem &cs, bool values_only, double *hv,
         int c[NP];
 #pragma unroll
         for (int p = 0; p < NP; ++p) x[p] = fma(hi - lo, (q * NP + p + 1) * ig, lo);
-        sturm_count_n<NP>(cs.dg, cs.e2, b0, b1, x, c);
+        sturm_count_n<NP>(pk, b0, b1, x, c);
         double lc = -CUDART_INF, hc = CUDART_INF;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {  // x ascending: the last point with count <= jj, the first above
