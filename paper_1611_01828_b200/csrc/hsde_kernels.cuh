@@ -443,8 +443,10 @@ __global__ void k_pair_sum(DevProblem P, const double *__restrict__ t, double *_
 // q0 partials: part[r * ntile + tile] = sum over the tile's owned pairs of
 // A_r,pair x_pair; the tile's pair values are staged in shared memory.
 // PAIRS: x_pair = t_l + t_mirror formed while staging (no separate pair-sum pass)
+// (8 CTAs per SM: 32 registers; three more cost a quarter of the occupancy and
+// 19 us of this HBM-bound pass)
 template <bool PAIRS>
-__global__ void __launch_bounds__(kBlock) k_spmv_half(DevProblem P, const double *__restrict__ xq,
+__global__ void __launch_bounds__(kBlock, 8) k_spmv_half(DevProblem P, const double *__restrict__ xq,
                                                        double *__restrict__ part) {
   extern __shared__ double xs[];  // [P.rt_tile]
   pdl_wait();
