@@ -224,7 +224,7 @@ __device__ __forceinline__ void rhs_finish(const DevProblem &P, const DevState &
 // threads take two coordinates per step with their dependent loads (cover
 // range -> slot -> slot values) interleaved.
 template <bool FROM_STATE>
-__global__ void __launch_bounds__(kBlock, 8) k_rhs(DevProblem P, DevState S, DevWork W,
+__global__ void __launch_bounds__(kBlock) k_rhs(DevProblem P, DevState S, DevWork W,
                                                 const double *rx, const double *rs,
                                                 const double *rv, int nb_heavy) {
   pdl_wait();
