@@ -1,0 +1,700 @@
+# DESIGN — B200-native HSDE-ADMM hot path for chordally decomposed SDPs
+
+This repository rebuilds one hot path of the reference package `chordalsdp`
+(arXiv:1611.01828, pure Python, `/root/reference/pkg/src/chordalsdp`) for the B200:
+**one iteration of the over-relaxed homogeneous self-dual embedding (HSDE) ADMM on a
+chordally decomposed SDP**, plus the residual / certificate checks around it. Hand-written
+sm_100a CUDA in `paper_1611_01828_b200/csrc` does the work. It sits behind a C ABI
+(`include/hsde.h`, `libhsde.so`), under a Python shim that keeps the reference's
+`solve_decomposed` API.
+
+## 0. Scope: SURVEY.md §8 rows and their status
+
+| §8 row | What | Status |
+|---|---|---|
+| (a) a1 `iterate` (solver.py:375-395) | one ADMM sweep | **done**: CUDA-graph-replayed kernel sequence, §3 |
+| (a) a2/a3 `affine_project` / `_solve_inner_parts` (:203-245, :296-318) | block-eliminated affine solve | **done**: `k_rhs`, `k_spmv_seg`, `k_schur`, `k_ua`, `k_scalars` |
+| (a) a4/a5 `project_cone` / `project_psd_batch` (:321-355, symmat.py:153-165) | batched clique PSD projections | **done**: `k_cone_cold` (cold path, d ≤ 96: Householder tridiagonalisation, bisection, twisted factorisations, compact-WY back transformation and V max(Λ,0) Vᵀ on fp64 DMMA), `k_cone_split` (warm hot path, 8 ≤ d ≤ 96: invariant-subspace projection on DMMA blocks), `k_cone_warp` / `k_cone_wcold` (warp teams, d ≤ 32), `k_cone_block` (Jacobi path: d > 96 and every failure of the other paths) |
+| (a) a6 gather / scatter (graphs.py:245-252) | selector maps | **done**: atomic-free pull-scatter fused into `k_rhs` / `k_pull`; gather fused into the cone load |
+| (a) a7 `setup_cache` (:248-283) | Schur factor, ζ, M⁻¹ζ | **done on device**: dense chunks + cuBLAS DGEMM, cuSOLVER Cholesky, explicit S⁻¹, device inner solve for M⁻¹ζ |
+| (a) a8 `residuals` (:398-429) | pres / dres / gap | **done on device** (`hsde_check`, one host sync per check) |
+| (a) a9 `_try_certificates` (:455-505) | infeasibility certificates | **done on device** (`hsde_certificate`; min clique eigenvalue by the Jacobi kernel) |
+| (a) a10 loop, normalisation, merit tracker (:634-772) | driver | **done** (`solver.py` shim; merit on device) |
+| (a) a11 `_classify` / `recover` (:521-617) | report | **done** (host Python, as in the reference); solution / certificate entry lists and `recover` are compared with the reference's own reports (`test_report_entries_match_reference`, `test_recover_matches_solve_report`) |
+| (b) boundary | C ABI + reference-named Python API | **done**: §2, `INTEGRATION.md` |
+| (c) oracle | CPU restatement pinned to the live reference | **done**: §1 |
+| (d) measurement | bench.py contract, roofline, CPU baseline | **done**: §6, `profiles/` |
+| (e) multi-GPU | clique sharding + NCCL all-reduce | **implemented**. Validated on CPU (gloo, world size 2), on one GPU in emulation, and on the NCCL path with a 1-rank communicator. Not yet run on more than one GPU (§5). |
+| (f) next | GPU setup / decomposition / report extraction / SDPA | f1 done (setup on the device, §4); f2 done (`decompose`: C++ chordal extension + maximal cliques with the reference's tie-breaking, compressed layout built directly; identical to the reference on random patterns, config 3's 3,493 cliques and multi-block SDPs; 0.17 s vs 0.82 s for config 3's graph, 0.3 s for config 4's); f3 done (vectorised, lazily materialised report rows; certificate eigenvalues on the device); f4 done (`parse_sdpa`: C++ reader `hsde_sdpa_*` with the reference's token rules, error lines and messages, flat entry arrays fed straight into `decompose`; identical to the reference parser on 44 generated texts, 28 of them malformed) |
+
+## 1. Oracle and parity
+
+* `oracle/hsde_oracle.py` is a numpy/scipy restatement of the reference hot path in the
+  compressed layout. Every function cites the reference `file:line` it follows. It is
+  test infrastructure only. Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s CPU
+  baseline import it.
+* **Pinned** against the live reference, which can be imported in the build container:
+  * `tests/golden/make_goldens.py` runs `chordalsdp` itself and commits fixtures:
+    * the reference's golden first iteration (test_solver_oracles.py:349-373);
+    * 40 random toy problems built with the reference's own test builders
+      (helpers.py:245-297), with reference outputs of `affine_project`, `solve_inner`,
+      `project_cone`, `iterate` and a full solve;
+    * for configs 0-4: the reference iterate at a fixed count (500; config 4 at 40), the
+      check log, and the default to-tolerance report with its solution / certificate
+      entry lists; configs 2 and 3 keep the **full** states (0.5 M and 0.34 M doubles),
+      not samples;
+    * `cfg4_long_reference.npz`: the reference's config-4 iterate at iterations 100 and
+      200 (sampled entries + segment norms; 15-20 s per reference iteration);
+    * every fixture records a hash of the generator output, checked by
+      `test_oracle_pins.py`, so a changed generator cannot silently pair with old goldens.
+  * `tests/test_oracle_pins.py` checks the oracle against these fixtures (CPU, `-m "not gpu"`):
+    1e-14 on the golden iteration, 1e-12 on the operators, 1e-8 on the 500-iteration
+    iterates (measured: 2.6e-12 for config 0).
+* The reference is pure Python, so there is nothing to compile into `oracle/_ref`. Its
+  third-party kernels (numpy 2.3.5, scipy 1.18.1 with OpenBLAS 0.3.30: `dsyevd`,
+  `dpotrf/dpotrs`, `csr_matvec`) are covered by the same fixtures.
+* **GPU parity** (`tests/test_gpu_parity.py`, `tests/test_gpu_shard.py`, `-m gpu`) goes
+  through the C ABI:
+  * the golden first iteration at atol 1e-14;
+  * `affine_project` / `solve_inner` against the dense (I+Q)⁻¹ oracle at 1e-10 and against
+    the reference outputs at 1e-11;
+  * `project_cone` at 1e-12; `iterate` from random starts at 1e-10, with the Moreau
+    invariants;
+  * configs 0/1/2 after 500 iterations within 1e-8 relative of the reference;
+  * the to-tolerance status, iteration count ±2 and objectives within 1e-6 of the reference;
+    config 1 gives `DualInfeasible`, ray "dual", b·y = 1, y within 1e-6;
+  * the error types `FactorizationFailure`, `TauZero` and `EigenFailure`;
+  * bitwise run-to-run reproducibility;
+  * warm vs cold eigensolves, and sharded vs single-shard runs (configs 0-3, and
+    config 4 at G = 2/4/8 in emulation: 1e-10 against the single path, and the
+    reference's to-tolerance report);
+  * config 4 at iterations 100 and 200 against the reference (`test_config4_long_pin`);
+  * the report's `x_entries` / `z_entries` / certificate entry lists against the
+    reference's reports, and `recover` against the solve's own report;
+  * the hot path with cliques of order 80 / 97 / 111 (fast path, cold path and Jacobi
+    path boundaries), the cold path against the Jacobi-only path on config 4, and the
+    cold eigensolvers on adversarial spectra (repeated, clustered to 1e-9, zero, rank
+    one, graded over 12 decades) at 1e-12 of `numpy.linalg.eigh`.
+* Config 4 against the reference (15–17 s per iteration on CPU): the fixture holds the
+  reference's 40-iteration to-tolerance run.
+  * Reference: Optimal, 40 iterations, p −117.89370201, d −144.33222312.
+  * B200: Optimal, 40 iterations, p −117.8937022, d −144.3323644.
+  * The dual objective differs by 9.8e-7 relative, just inside the 1e-6 bar. The CPU
+    oracle shows the same deviation from the reference (it is the problem's
+    conditioning at a 1e-4 stop: the iterate itself matches to 1e-8), so the margin is
+    a property of the workload, not of the kernels; the iterates at 40 / 100 / 200
+    iterations are pinned separately.
+* Config 3 is solved in 780 iterations, the same count as the reference (SURVEY §6);
+  its full-state fixture is `cfg3_reference.npz`.
+
+## 2. Boundary
+
+* The **Python API** keeps the reference's names and signatures:
+  * `SolverSettings` (solver.py:68-99, same defaults: α=1.6, normalize, check every 20).
+  * `solve_decomposed(dp, settings, iteration_callback, setup_elapsed)` (:690-772).
+  * `setup_cache`, `solve_inner`, `affine_project`, `project_cone`, `iterate`, `residuals`,
+    `recover`, `build_hsde`, `initial_state`, `HsdeState`, `VariableLayout`,
+    `IterationInfo`.
+  * `FactorizationFailure`, `TauZero`, `EigenFailure`.
+  * `SolverReport` / `Residuals` / `Timing` / `ProblemStats` with identical JSON (sdpa.py:237-319).
+  * `dp` is the reference's own `DecomposedProblem` (duck-typed) or
+    `problem.CompressedProblem`.
+* The **C ABI** is in `include/hsde.h`. Each entry point cites the reference function it
+  replaces. The reference has no FFI, so the ctypes stub a maintainer would add is in
+  `INTEGRATION.md`.
+* There is **no CPU fallback**. Without `libhsde.so` or a GPU, every product entry point
+  raises. The only host arithmetic on the solve path is report assembly from the final
+  iterate (a11), which the reference also does in Python.
+* The compressed layout is exact, not an approximation (SURVEY §0.6). x is stored only on
+  *covered* coordinates: those selected by a clique, or in the support of A or c.
+  * From the zero start, the other coordinates stay exactly 0.
+  * Covered coordinates keep the reference's flat order, so CSR/CSC accumulate in the
+    reference order.
+  * The unit-level API keeps all n² coordinates on the device when n² ≤ 4M. It therefore
+    accepts arbitrary reference-layout vectors.
+
+## 3. Kernels, data layout, rooflines
+
+**Layout in HBM (per handle):**
+* State: u, w as `[x N_c | s n_d | y m | v n_d | τ]` in fp64.
+* A as given (CSR) and its CSC (built on the device by a stable radix sort), both fp64
+  values / int32 indices. The hot passes do not read them: they stream the **half-pass
+  layouts** below. The CSR/CSC serve the setup, the checks and the full-column fallback.
+* **Half-pass layouts** (`hsde_setup_half.cuh`, built on the device). The covered
+  coordinates come in mirror pairs {(i,j), (j,i)}; an SDP's constraint matrices are
+  symmetric, so column ℓ of A equals column mirror(ℓ) exactly. This is checked at setup;
+  any mismatch, or a pair split across shards, keeps the full-column passes. One
+  column per pair (ℓ ≤ mirror ℓ, ascending) is stored twice:
+  * **SELL-32** for Aᵀg: slices of 32 pairs; element k of lane j at `beg + 32k + j`;
+    16-bit row index + fp64 value; zero padding to the slice's longest column
+    (×1.48 on config 4).
+  * **row-SELL tiles** for A t: tiles of 4096 pairs × groups of 32 rows; element k of
+    row 32g+j at `beg + 32k + j`; 16-bit column-within-tile + fp64 value; ascending
+    column inside a row (×1.26 padding). Only the owned pairs' entries.
+* Cover lists (covered coordinate → slots, ascending slot = bincount order) and
+  slot → covered, both int32.
+* P⁻¹, c, b and M⁻¹ζ; S⁻¹ dense m×m (diagonal when S is diagonal: config 3).
+* The per-clique eigenvector store (warm start, n_d doubles).
+
+**Headline config 4:** 19.2M pair nonzeros → 0.28 GB (SELL-32) + 0.24 GB (row-SELL)
+per iteration, plus 15 MB per N_c-vector and 20 MB per n_d-vector. This exceeds the
+126 MB L2, so consecutive timed iterations stream from HBM.
+
+**The affine step in two passes over A.** With S = I + A P⁻¹Aᵀ, the reference's block
+elimination (t = P⁻¹r, q' = S⁻¹At, ua = t − P⁻¹Aᵀq', uy = ρ_y − A·ua; solver.py:231-241)
+is evaluated as
+
+    t0 = P⁻¹(r − Aᵀρ_y),   g = S⁻¹(A t0 − ρ_y),   ua = t0 − P⁻¹Aᵀg,   uy = −g
+
+which is algebraically identical (q' = g + ρ_y and A·ua = q' because S q' = A t) and
+reads A twice per iteration instead of three times. `HSDE_FLAG_EXACT_UY` keeps an
+explicit uy = ρ_y − A·ua pass; both agree to 1e-10 after 200 iterations (test).
+
+**One iteration = one CUDA graph replay** (`launch_iteration`):
+
+| kernel | reference | work | bound | algorithmic bytes / flops per launch |
+|---|---|---|---|---|
+| `k_rhs` | solver.py:222-231, 300-301 | per covered ℓ: pull-scatter of its slots (warp per coordinate with >32 slots), t0 = P⁻¹r0 | HBM | 44·N_c + 36·n_d |
+| `k_pair_sum` + `k_spmv_half` + `k_rowsum_tiles` | :232 `A @ t` | x_pair = t_ℓ + t_mirror; row-SELL tiles with the tile's x staged in smem (lane = row), ordered tile partials, row sums | HBM | 10·nnz_pairs + 8·N_c + 24·n_pairs |
+| `k_schur` | :232 `cho_solve` | g = S⁻¹(q0 − ρ_y) (four warps per row, fixed-order partials; S⁻¹ read with cached loads so it stays in L2) | L2 | 8·m² |
+| `k_ua_half` | :232-235 | SELL-32 Aᵀg with g staged in smem (lane = pair), ua for both members, block partials of c·ua | HBM | 10·nnz_pairs + 8·n_pairs + 32·N_c |
+| `k_scalars` | :315-317, 388-394 | one CTA: ζ·u, shift, τ/κ, y update, next ρ_y | latency | — |
+| `k_cone_split` | symmat.py:153-165, solver.py:388-394 | CTA (384 threads) per clique with a kept basis (8≤d≤96, warm): slot update, B = VᵀXV, Riccati invariant-subspace projection on DMMA 16×16 blocks, V rotated onto the new subspaces, s/z/v update; cliques it cannot finish are handed to `k_cone_cold` | tensor (fp64 DMMA) | 11·Σd³ (SURVEY §8d) |
+| `k_cone_cold` | same | CTA (128 threads, 3 per SM) per clique without a usable basis (d≤96): slot update, full eigendecomposition (Householder tridiagonalisation in registers, bisection, twisted factorisations, compact-WY back transformation, Newton-Schulz) and P = V max(Λ,0) Vᵀ on DMMA; runs **concurrently** with `k_cone_split` on disjoint cliques, and a second time on the fast path's hand-overs | fp64 (latency) / tensor | 11·Σd³ |
+| `k_cone_block` | same | CTA per clique: the Jacobi path (d > 96, `HSDE_FLAG_JACOBI`, failures of the cold path: eigenvalue pairs closer than 2⁻⁴⁰‖T‖) | fp64 | 11·Σd³ |
+| `k_cone_warp` | same | warp per clique (d≤32), three size classes (dp ≤ 8/16/32) launched as parallel graph branches; a class with few cliques (CTA teams stay below two per SM) runs on CTA teams instead; `k_cone_wcold` is the warp cold path of `project_cone` / certificate eigenvalues | fp64/latency | 11·Σd³ |
+| `k_xupd` | :388-394 | x / w_x update | HBM | 48·N_c |
+
+All reductions are fixed-order (block partials, then an ordered sum), so runs are
+bitwise reproducible (test).
+
+The affine chain `k_rhs → k_pair_sum → k_spmv_half → k_rowsum_tiles → k_schur →
+k_ua_half → k_scalars` is launched with **programmatic dependent launch** (single shard):
+each kernel calls `griddepcontrol.wait` before touching memory and
+`griddepcontrol.launch_dependents` when its CTA is done, so the next kernel's launch
+overlaps the predecessor's tail; the edges are captured into the iteration graphs.
+Worth 1–4% on the launch-bound small configs (config 1: 43.5 → 41.5 µs per iteration),
+nothing measurable on config 4; `HSDE_PDL=0` turns it off.
+
+**PSD projection, hot path for CTA-sized cliques: `k_cone_split`** (`hsde_split.cuh`)
+
+The eigendecomposition is not what the projection needs: P = X₊ depends only on the
+positive invariant subspace of X. With the previous iteration's basis V (rows of the
+per-clique store), B = VᵀXV is nearly diagonal. Sorted by the sign of its diagonal into
+the classes P (r entries) and N (n = d − r), the positive invariant subspace of B is
+span Q, Q = [I; Y], with Y (n×r) the solution near 0 of the Riccati equation
+
+    Y L_P − L_N Y = B_NP + E_NN Y − Y (E_PP + B_PN Y)
+
+(L = diagonal, E = within-class off-diagonal). Every denominator λ_j − λ_i (j ∈ P,
+i ∈ N) is ≥ 2g, g = min|diag B|, so the fixed point contracts at about off(B)/2g however
+close the eigenvalues inside a class are. Then B Q = Q R with R = L_P + E_PP + B_PN Y,
+the orthogonal projector onto span Q is Q G Qᵀ with G = (I + YᵀY)⁻¹, and
+
+    P(B) = B Q G Qᵀ = Q (R G) Qᵀ,     P(X) = Utᵀ K Ut,   Ut = V_Pᵀ + Yᵀ V_Nᵀ,  K = R G.
+
+No truncation: the only errors are the fixed point's (stopped when the estimated error is
+≤ 2.5e-16) and rounding. V is then rotated onto the two new invariant subspaces,
+V' = [S_P Ut; S_N Wt] with Wt = V_Nᵀ − Y V_Pᵀ and the polar factors S = (I + YᵀY)^−½,
+(I + YYᵀ)^−½ (binomial series, Horner), so the next B has only this iteration's
+cross-class coupling.
+* **Applicability**: off(B)² ≤ 0.2 g² (off(B) < 0.45 g: then |E|₂ < g and the class sizes
+  are the inertia, Weyl), r ≤ n, and the in-place passes fit the warps' registers
+  (d ≤ 96: B's 21 upper 16×16 blocks on 12 warps × 2 register blocks, `static_assert`).
+  * off(B) above the bound: far above it (> 0.6 g) the clique is handed to the cold path
+    (X stays in the hand-off buffer); close to it the same CTA runs warm Jacobi sweeps on
+    B (the `hsde_eig.cuh` sweeps, on a scratch carved from the same shared memory — B is
+    in registers, X and V in global memory) until the class-split point, stores the
+    rotated V and continues the split with the rotated B.
+  * r > n: the kernel projects −B instead (its positive class is B's non-positive one)
+    and emits X₊ = X + (−X)₊, with X re-read from the hand-off buffer.
+  * the fixed point stalls (no contraction over two passes), or the passes do not fit
+    the registers: the clique is handed to the cold pass that follows; cliques without a
+    basis (first iteration) are on the cold path from the start.
+  * **Schedule**: each clique leaves a key for the next iteration (1 when off(B) is
+    already above half the bound or the Jacobi path ran); `k_scalars` (one CTA, already
+    on the critical path) partitions the plan so these start in the first wave.
+  * The fixed point stops on the **residual**: each pass's increment is measured as
+    Δ∘δY (the part of the Riccati residual it removed), and the iteration stops when the
+    estimated remaining residual is ≤ 1e-15·|B|_F. Y then solves the Riccati equation of
+    a matrix within that distance of B, and X ↦ X₊ is 1-Lipschitz, so P is accurate to
+    that level even when Y itself is ill-conditioned (g ≪ |B|, where |δY| cannot get
+    below ~ε|B|/g; the earlier |δY| ≤ 1e-15 test declared those cliques stalled and sent
+    them to Jacobi). The contraction is estimated over two passes (the lagged quadratic
+    term makes consecutive increments non-monotone).
+* **Passes** (one CTA of 384 threads, 2 CTAs/SM, 99–111 KB smem): batched hot-slot loads
+  (every load of 4 slots in flight before the stores) → X in smem; X to the hand-off
+  buffer, Vᵀ into smem, then B = VᵀXV by 32-column strips of T = VᵀX (the next strip of X
+  fetched while the tensor cores work on the current one; B's upper 16×16 blocks stay in
+  registers); sort B by class into smem; the Riccati passes — one product pass each, with
+  the quadratic term lagged (refreshed every other pass; it moves by ~|Y|·off/2g per pass,
+  far below the linear contraction); one pass for R, YᵀY, YYᵀ; K = R G by the series
+  K ← R − K YᵀY; the polar series; Ut and Wt in one pass; V' in one pass; T = K Ut;
+  P = Utᵀ T (symmetric: upper blocks, mirrored).
+* **DMMA blocks**: every product is `mma.sync.m8n8k4.f64` with a warp owning 16×16
+  output blocks (2×2 tiles: four independent accumulator chains, one operand load per
+  DMMA; tiles outside the output are skipped). Leading dimensions ≡ 4 (mod 16) doubles
+  make fragment loads of either orientation conflict-free (two wavefronts per warp).
+  In-place passes keep their output blocks in registers until every warp has read the
+  operand. Measured on this B200 (`tools/dmma_bench.cu`): a DMMA has 26 cycles of latency
+  and each SM sub-partition issues one every 16 cycles (36.6 TFLOP/s over 148 SMs), so
+  one warp per sub-partition with four chains saturates the pipe; the kernel is bound by
+  its dependent phases (barriers), not by DMMA issue.
+* **Measured** (config 4, iterations 220+, `tools/riccati_stamps.py`, round 2): 5
+  fixed-point passes per clique; per clique (clock64 stamps of the first CTA) load 64k
+  cycles (the first wave loads 175 MB from HBM at once), B 61k, sort 17k, Riccati 96k,
+  series 35k, Ut/Wt/V' 38k, K·Ut 5k, P 19k: 335k cycles = 0.17 ms per clique, and the
+  400 cliques take **two waves** on 296 resident CTAs (2 per SM: 99–111 KB of shared
+  memory and 384 threads × 80 registers each), so the launch is 0.33 ms (graph) /
+  0.36 ms (eager profile with the empty follow-up launches): 6.3–6.8 TFLOP/s
+  algorithmic = 18–19% of the fp64 DGEMM peak.
+  * One Riccati pass is ~14k cycles: the X products 6.0k (at the DMMA issue limit while
+    both CTAs of an SM are in the same phase: 18 warps × 80 DMMAs × 16 cycles over four
+    sub-partitions), the element update 4.9k, the convergence decision ~2k.
+  * ncu (`profiles/r02/ncu_full_counters.txt`): DMMA sub-pipe 26% active, XU pipe
+    (conversions of the index arithmetic) 32%, LSU 32%, issue slots 30%; nothing is
+    saturated: the kernel is a chain of ~60 barrier-separated phases per clique.
+  * Round-2 changes that moved it: the Riccati update as straight-line code on clamped
+    indices (independent chains interleave; only the stores are predicated), a
+    branch-free reciprocal (float seed + three Newton steps) instead of the division, a
+    butterfly total and a float convergence decision: steady launch 0.368 → 0.353 ms.
+    Making every branch around the DMMAs provably warp-uniform (warp index and the
+    CTA-uniform control values through shuffle broadcasts) removes the `WARPSYNC.ALL`
+    nvcc puts in front of each `mma.sync` (2 of the 3 issued instructions per DMMA are
+    `WARPSYNC.ALL` and `NOP`): measured, no change in either cone kernel, not kept.
+    An L2 prefetch of the second wave's inputs by the first wave (after its own load,
+    when HBM is idle) is worth ~1% but raises the launch's DRAM traffic by 18% (lines
+    evicted before use): kept behind `HSDE_SPLIT_PREFETCH=1`, off by default.
+  * What bounds it now: (i) wave quantisation — 400 cliques on 296 slots cost two full
+    waves, a third CTA per SM needs ≤ 75 KB of shared memory and the Riccati / tail
+    phases need R1 (54 KB) plus 43 KB of Y / Ut / S_N; (ii) the 80-register cap of
+    384 × 2 threads per SM (828 B of spill stores); (iii) phase latency. The ≥ 40% bar
+    needs the launch at 0.16 ms, which is the DMMA issue floor for the flops this scheme
+    executes (~1.6× the algorithmic 11 d³); it is not reachable by tuning this kernel.
+* Iterations 90–140 of config 4 are slower (0.66–0.80 ms) because 1–2% of the cliques
+  need a Jacobi refresh (off(B) slightly above g/3 on cliques whose argument is tiny,
+  ~1e-4): one sweep of one clique costs ~0.1 ms on its CTA. The first-wave schedule and
+  the in-place refresh cut that from 0.73–0.89 ms.
+  Measured and not kept: looser thresholds (g/2: more passes everywhere and later
+  hand-overs, since Jacobi resets the within-class drift); a serial 4-launch chain
+  (fast path / Jacobi to the split point / fast path / Jacobi); leaving V fixed between
+  Jacobi refreshes (more passes, periodic bursts of 10–35% hand-overs); 256-thread CTAs
+  with 128 registers (fewer warps: slower); an L2 prefetch of the first wave's inputs
+  (TMA bulk prefetch on a graph branch during `k_ua_half`: +10 µs, it competes with the
+  A stream); the Jacobi fallback as a real call (more spills).
+
+**PSD projection, cold path for CTA-sized cliques: `k_cone_cold`** (`hsde_cold.cuh`)
+
+north_star's large-clique design: a full eigendecomposition X = V Λ Vᵀ per clique, used
+whenever the kept basis is too far from diagonalising the new argument (the first ~17
+iterations of config 4, where X moves by O(10%) per iteration, and every clique whose
+spectrum comes within reach of zero).
+* One CTA of four warps per clique, ~71 KB of shared memory and 168 registers per
+  thread: three CTAs per SM, so the 400 cliques of config 4 run in one wave.
+* **Tridiagonalisation** in LAPACK `dsytd2` order with the matrix in the CTA's
+  *registers* (column k in warp k mod 4, row i in lane i mod 32; produced columns are
+  shifted out, dead blocks skipped). Per step: the owner of column s forms the
+  reflector while the others finish the previous update (named barrier), partial
+  p = τAv sums meet in shared memory (two CTA barriers), rank-2 update in registers.
+* **Eigenvalues** by bisection on each unreduced block (Sturm counts by the three-term
+  determinant recurrence with exact power-of-two rescaling; (a_k, e²_{k−1}) packed so a
+  step is one 16-byte shared-memory load, three fp64 operations and one funnel shift).
+* **Eigenvectors** of T by twisted factorisations (one thread per eigenvalue), written
+  into the sorted column of Z; a pair closer than 2⁻⁴⁰‖T‖ inside one unreduced block is
+  not separable this way: the clique goes to the Jacobi path (flag, follow-up launch).
+* **Back transformation** V = H₀…H_{d−3} Z in compact-WY blocks of 8 reflectors, three
+  DMMA GEMMs per block; **Newton–Schulz** V ← V(3I − VᵀV)/2 on DMMA while
+  max|VᵀV − I| > 2⁻⁴⁶ (twisted vectors of close eigenvalues are orthogonal only to
+  ~ε‖T‖/gap, and the kept basis feeds the warm path for hundreds of iterations); the
+  Gram operand of its second product comes from L2 with five k-steps of loads in
+  flight; **P** = V_P Λ_P V_Pᵀ (or X + V_N|Λ_N|V_Nᵀ when the negative class is smaller).
+* Measured per clique on config 4 (clock64 stamps, `tools/cold_phases.py`,
+  `profiles/r02/cold_phases.txt`): slot load 140k cycles (HBM-bound: all 400 CTAs load
+  245 MB at once), tridiagonalisation 277k, bisection 156k, twisted vectors 80k, back
+  transformation 141k, Newton–Schulz 74k, P 33k: 0.90 M cycles, 0.54 ms for the launch
+  (1.00 M cycles when first built).
+  ncu (`profiles/r02/ncu_cold_*`): 225 M warp instructions per launch, one issued every
+  ~8 cycles per warp with three warps per scheduler (issue slots 33% busy): the kernel
+  is bound by dependent instruction latency times instruction count, not by a pipe —
+  and by registers: 400 cliques fill the SMs with only 2.7 CTAs × 4 warps each, more
+  warps per clique would need the matrix in fewer than 120 registers per thread.
+  What moved it this round, all by cutting instructions or exposed latency: w = p + Kv
+  formed once per row in the tridiagonalisation (the rank-2 update reads one value per
+  column), a uniform branch tree instead of a predicated chain for the column
+  hand-off, (a_k, e²_{k−1}) packed into one 16-byte load per Sturm step with the signs
+  counted through a funnel-shift register (ten issued instructions per step → ~8.5),
+  the Gram operand of Newton–Schulz prefetched five k-steps deep from L2, batched
+  copy-back and w_s update loops.
+  Tried and measured, not kept: three bracket points per thread and round
+  (quad-section: 1.5× the fp64 operations, same time), eight slots per thread in flight in the load (same time:
+  memory-system bound), gathering M⁻¹ζ's slot parts from its x part instead of
+  streaming them (the dependent gather made the load 18% slower), the two qd
+  recurrences of the twisted factorisation as one loop with the progressive pivots
+  parked in global scratch (two chains interleave, but the extra stores and loads
+  made the phase 15% slower).
+
+**Cold / warm policy.** Every clique carries a prediction for the next iteration
+(`W.cnext`): the cold path leaves "fast" when ‖X − X_prev‖_F ≤ 0.6 g (g = min|λ|; off(B)
+measured at 0.3–0.5 of that step on config 4), the fast path leaves "cold" when its
+off(B) exceeded 0.35 g. `k_scalars` partitions the cliques; `k_cone_split` and
+`k_cone_cold` then run as parallel graph branches on disjoint cliques, followed by a
+(normally empty) cold pass over the fast path's hand-overs and the Jacobi fallback.
+On config 4 iterations 1–16 and 18–19 run cold (0.80 ms per iteration), 17 and 20+
+on the fast path (0.62 ms falling to 0.58 ms as the fixed point needs 9 → 5 passes).
+The two thresholds are at their measured optimum (`HSDE_POL_F2C` / `HSDE_POL_C2F`,
+`profiles/r02/policy_sweep.txt`): switching to the fast path earlier (iteration 14–16)
+costs 12+ fixed-point passes and hand-over bursts, and is 1–6% slower over iterations
+1–40 than the cold path it would replace.
+
+**PSD projection: cyclic Jacobi in shared memory** (`hsde_eig.cuh`; cold starts,
+hand-overs, warp-sized cliques, `project_cone`)
+* One round of the round-robin tournament rotates dp/2 disjoint pairs. Parameters are
+  computed one thread per pair, with the pair's players, into double-buffered tables.
+  The previous round's eigenvector rows are updated concurrently (16-byte chunks,
+  consecutive threads on consecutive pairs). Then every 2×2 block (A ← JᵀAJ) transforms
+  independently. Two team barriers per round.
+* **Bank-conflict-free layout**: only the upper triangle is maintained during the sweeps
+  (entry {i,j} at min·lda + max; the lower triangle is restored on exit). lda ≡ 1 (mod 16)
+  puts entry (i,j) in bank (i+j) mod 16 for either orientation, so a row pair's blocks over
+  consecutive column pairs (consecutive players) hit distinct banks. ldv ≡ 2 (mod 16)
+  puts the rows of consecutive players in consecutive 16-byte bank groups. Against the
+  first version this cut shared-memory wavefronts by 35% and the kernel time by 25%.
+* **Warm start** (CTA and warp teams): the previous iteration's eigenvectors V give
+  B = V X Vᵀ via two register-tiled smem GEMMs (two tiles per thread for warps). Jacobi
+  then starts from V: 1–3 sweeps instead of 8. V is refreshed by a cold solve every 64
+  iterations.
+* **Perturbative exits**: the projection's Daleckii–Krein expansion around the diagonal
+  D of B = D + E has error O(off^(k+1)/g^k) at order k, g = min|λ_i| (no eigenvalue can
+  change sign while off ≤ g/1000). The sweeps stop at the first order whose bound is
+  below 1e-15·‖A‖_F (about the rounding floor n·ε of the reconstruction itself):
+  * order 1: M = diag λ₊ + L(E) with the divided differences of max(·,0);
+  * order 2 (CTA teams): + the second-order term, on class-sorted blocks (P = λ>0, N):
+    M_PP −= G|Λ_N|Gᵀ, M_NN = Gᵀ Λ_P G, M_PN += (−λ_j E_PP G + λ_i G E_NN)/(λ_i − λ_j) with
+    G_ij = E_ij/(λ_i − λ_j) — four rectangular tensor-core GEMMs; every denominator ≥ 2g.
+    `tests/test_host.py::test_second_order_projection_formula` checks the formula in numpy
+    (error ∝ off³); `test_project_cone_nearly_diagonal` runs the device path.
+  Otherwise: skip threshold 2⁻⁶⁰‖A‖_F; stop at off ≤ 2⁻⁵⁶‖A‖_F or after a sweep with
+  no rotation. P = V M Vᵀ.
+* **Tensor-core GEMMs** (CTA teams): the warm start B = V X Vᵀ, the rebuilds and the
+  second-order terms run as `mma.sync.m8n8k4.f64` (DMMA) tile GEMMs, one 8×8 output tile
+  per warp at a time, through a per-CTA d×d scratch in global memory (L2-resident) so no
+  GEMM overwrites its operand.
+* ncu (`profiles/r01/ncu_full_summary.txt`): issue- and shared-memory-bound (issue slots
+  ~49%, L1/shared pipe ~76%), 2 CTAs/SM (110 KB each).
+* Tried and measured, not kept: 1024-thread CTA teams when a shard has ≤ 148 cliques
+  (3–4% slower: the rounds are latency-bound, not throughput-bound); second-order exits
+  for warp teams (the extra code costs registers and occupancy: configs 2/3 8–15%
+  slower); a one-sided (Hestenes) variant (more smem traffic); an
+  Ogita–Aishima eigenbasis refinement stage (slower); a block-Jacobi variant with 8×8
+  sub-sweeps and fp64 DMMA (m8n8k4) block updates (correct, 1.1–1.2× slower on config 4:
+  the per-pair sub-sweeps are latency chains that 2 CTAs/SM cannot hide; kept on the
+  `bjacobi-experiment` branch).
+
+## 4. Setup on the device (a7)
+
+* The cover lists (slots of each covered coordinate, ascending: a stable device radix
+  sort of the slot → coordinate map), P⁻¹ and the heavy-coordinate list are built on the
+  device (18 → 5 ms for config 4's 2.56M slots).
+
+* A goes to the device once; the CSC comes from a stable `cub` radix sort on the device
+  (integer counts, deterministic), and the CSR is validated there.
+* P⁻¹ = 1/(1+D/2) uses the global cover counts.
+* S = I + A P⁻¹Aᵀ by a **sparse row-wise kernel** (`k_schur_rows`): warp (row i, part)
+  walks row i's columns and adds (a_il a_jl) p_l into a shared-memory row, parts summed in
+  order — deterministic, bitwise symmetric, Σ_l nnz(col l)² work (5 ms for config 4,
+  against 110 ms for the dense DGEMM it replaced, which stays as the fallback for m too
+  large for a shared-memory row). cuSOLVER `dpotrf`; S⁻¹ from `dpotrs` on I, symmetrised.
+* Failures are reported as `FactorizationFailure`: a non-finite S, a non-positive pivot,
+  or ζs ≤ 0.
+* M⁻¹ζ uses the same device inner solve.
+* Device memory comes from the stream-ordered pool with retained blocks, so a second
+  solve in a process maps no new pages.
+* Config 4 handle creation: ~0.05 s in a warm process (round 2; A upload 13–20 ms
+  on a host thread while the cover lists and small uploads are built, Schur 7 ms,
+  half-pass layouts 4 ms, graphs 3 ms); the reference's setup takes 41 s.
+  `HSDE_TIMING=1` prints the phases.
+* **Reference-layout input** (`problem.compress`, what a `chordalsdp` caller pays before
+  the device sees anything): the reference's `DecomposedProblem` holds a dense c over
+  n² and A over n² columns (2 GB and 2.6e8 columns for config 4). The covered layout is
+  built in the library (`hsde_cover_build` / `hsde_cover_fill`, `csrc/hsde_cover.cpp`,
+  include/hsde.h): a bit mask over n² filled by the host's threads (support of c, the
+  cliques' gather index, A's column ids with atomic ORs), a popcount prefix per 64-bit
+  word, then covered ids, c on them and the rank of every column id / gather index.
+  3.1 s with numpy sorts and masks → 0.27 s (16 threads; ~0.08 s on the GPU box); the
+  numpy restatement stays as the checker
+  (`tests/test_host.py::test_library_cover_layout_matches_numpy`). The off-pattern id
+  list of the layout mapper (an n²-long scan, 2.6e8 for config 4) is built only when a
+  unit-level call needs it, not by a solve. With both, `solve_decomposed` on the
+  reference's own layout costs 0.17 s for config 4 (round-2 start: 2.27 s).
+
+## 5. Multi-GPU (SURVEY §8e)
+
+Cliques are cut in reference order into contiguous ranges balancing Σ(d³ + 8d²)
+(`shard.py`).
+* Every covered coordinate has one **owner**: the rank of its first covering clique.
+  Only the owner adds it into A t, c·ua and the norms.
+* Coordinates touched by several ranks are **separators** (the arrow head; band
+  overlaps). They are replicated on every rank that touches them.
+* The m×m Schur solve, τ/κ and y are replicated.
+* Per iteration there are exactly three all-reduces, captured in the iteration's CUDA
+  graph as `ncclAllReduce`:
+  1. separator pull-scatter partials (|S| doubles; 1600 for config 4);
+  2. the partial A t (m doubles);
+  3. c·ua (1 double).
+* Setup all-reduces |c|², the m×m Schur partial, and ζ·M⁻¹ζ. The checks all-reduce their
+  partial norms.
+* One process per GPU. The NCCL unique id comes from rank 0 via `torch.distributed`
+  (`multigpu.init_comm`).
+
+Validation on this pool's single GPU:
+1. `oracle/sharded_oracle.py` restates the sharded algorithm with explicit reduction
+   points. `tests/test_shard.py` checks it against the single oracle at 1e-10: in process
+   with 2–4 shards, and across **two processes with gloo**.
+2. The same library runs **G shards emulated on one GPU**: same kernels, reductions by a
+   device sum in rank order. `tests/test_gpu_shard.py` matches the single path to 1e-10
+   for configs 0–3, d=40 cliques and **config 4 at G = 2/4/8**, and reproduces the
+   reference to-tolerance results (config 4 included).
+3. The NCCL code path runs on a **1-rank communicator**: the graph captures
+   `ncclAllReduce`. Iterates are bit-identical to single-GPU (1e-12 bar).
+
+Multi-rank NCCL (N>1) has not run here (gpurun gives one GPU). `bench.py --gpus N` under
+torchrun uses it and reports `"scaling": "strong"`, because the problem is fixed and split;
+for N>1 it sets `NCCL_DEBUG=INFO` / `NCCL_DEBUG_SUBSYS=INIT` so the run's stderr shows the
+communicator's N ranks and transports.
+
+**Emulated per-shard times** (`tools/shard_profile.py`, `profiles/r02/shard_profile.txt`;
+config 4 in steady state, the eager profile's phase sums divided by G, no NCCL latency):
+
+| G | cliques per shard | cone launch | A passes + `k_rhs` + `k_xupd` | one rank's iteration | vs G=1 |
+|---|---|---|---|---|---|
+| 1 | 400 | 349 µs | 199 µs | 576 µs | 1.0× |
+| 2 | 200 | 202 µs | 151 µs | 381 µs | 1.5× |
+| 4 | 100 | 156 µs | 102 µs | 280 µs | 2.1× |
+| 8 | 50 | 150 µs | 78 µs | 248 µs | 2.3× |
+
+The half passes stay on in every shard at every G (the shard cut keeps mirror pairs
+together on this pattern). The streaming kernels scale (their per-shard bytes fall as
+1/G, down to the launch floor), the replicated Schur solve and `k_scalars` do not, and
+the cone launch flattens at one clique's latency from G = 4 on: a real 8-GPU run of
+config 4 is therefore expected at ~2× one GPU, before the three all-reduces (~10 µs
+each over NVLink) — the multi-CTA-per-clique mode below is what G ≥ 4 needs.
+
+Known limits of the sharded path (not built this round): (i) a shard of config 4 at G=8
+holds 50 cliques, i.e. 50 CTAs of `k_cone_split` / `k_cone_cold` on 148 SMs — the
+cone launch then costs one clique latency (0.17 ms warm, 0.5 ms cold) whatever G is, so
+the cone part scales only to G≈2–3 without a multi-CTA (cluster) mode per clique;
+(ii) a mirror pair split across shards keeps the full-column A passes on those shards.
+
+## 6. Measurement (`bench.py`)
+
+* **Workload**: BASELINE config 4, the largest configuration, whose working set exceeds L2.
+  A "step" is one ADMM iteration.
+* **value** = iterations/s: K iterations as CUDA-graph replays, CUDA events on the
+  library's stream, max over ranks.
+* **e2e** = iterations / wall time of `solve_decomposed` on host data with default
+  settings (H2D, device setup, solve to 1e-4, report D2H), the median of three complete
+  solves. `e2e_reference_layout` is the same call on the reference's own input layout
+  (dense c over n², A over n² columns): `compress` runs inside the timed call.
+  `to_tol_iterations_per_s` is the rate of that solve's loop alone (iterations 1..40).
+* **roofline**: the dominant kernel's algorithmic flops (11·Σd³) or bytes (table above)
+  per launch, divided by its CUDA-event time. It is profiled **in the window `value`
+  times** (a second handle replays the warm-up, then iterations W+1..W+K run eagerly,
+  one event set per iteration and one synchronisation at the end, so the intervals hold
+  kernel time and not launch latency); `roofline_steady_state` repeats it at iterations
+  220+ where every clique is on the warm fast path. In the driver's window
+  (`--steps 20 --warmup 5`) 14 of the 20 iterations run the cold path, and the slot
+  `k_cone_cta` is the sum of the CTA cone launches of an iteration.
+  * The fp64 peak is measured: `profiles/fp64_peaks.json`, cuBLAS DGEMM 35.5 TF/s, DFMA
+    34.2 TF/s.
+  * The HBM peak is from `MEASURED_PEAKS.json` (6449 GB/s).
+  * Per-launch DRAM traffic comes from ncu (`profiles/ncu_traffic.json`).
+  * `roofline.bound` is `"tensor"` (with `"precision": "fp64"`) for the cone kernel: its
+    products run on the fp64 tensor cores (DMMA; fp64 has no tcgen05 path, SURVEY §0.9),
+    and the peak is the measured DGEMM rate. `roofline_all` lists every kernel. The slot
+    `k_cone_cta` times the CTA cone launch (`k_cone_split` on the hot path).
+* **cpu_baseline** and `--impl reference`:
+  * The reference is pure Python and cannot travel to the GPU box, and the driver's
+    `pip install … --target baseline/_ref` path does not apply to this tier.
+  * The reference arm is therefore the oracle port, timed on the box's host cores with
+    all BLAS threads: one step = one ADMM iteration; W warm-up iterations (≤ 30 s), then K
+    timed iterations (≤ 150 s, `HSDE_REF_BUDGET_S`), so the run ends within ~3 minutes; the
+    line reports the iterations actually timed. Both arms print the identical `config`
+    object. `cpu_baseline` in our own line is timed twice, as BASELINE.md §3 asks: BLAS
+    on all host threads and limited to one thread (threadpoolctl), with the `lscpu`
+    model and core counts (on this pool's 16-core hosts both give ~1.2 iterations/s:
+    the port is bound by its Python-level loop over 400 cliques and the sparse
+    products, not by BLAS threads).
+  * The port works in the compressed layout, so it is about 12× faster than the reference
+    itself on config 4: 1.2 vs 0.066 iterations/s. This baseline is conservative.
+* Other configs (0–3) are reported under `other_configs` (iterations/s and
+  time-to-tolerance).
+* Synthetic data: seeded generators reproduce SURVEY §8(d)'s RNG order. The sizes match
+  the survey table exactly, and config 0's iteration-500 check values match the
+  reference to 8 digits. No public dataset is involved.
+
+## 7. Results (1×B200)
+
+### 7.1 Round 2 (profiles/r02; every number below is from `bench.py` at HEAD on the B200)
+
+Headline workload, config 4 (400 cliques of order 80, m = 1000, 38.4 M nonzeros):
+
+| | round 2 | round 1 (driver) |
+|---|---|---|
+| `value`: iterations/s, driver command `--steps 20 --warmup 5` (iterations 6–25) | **@VALUE@** (@MS@ ms per iteration) | 881 |
+| to-tolerance loop (`to_tol_iterations_per_s`): 40 iterations to 1e-4 | **@TOTOL@ it/s**, @LOOPMS@ ms (reference loop: 606.7 s) | 41.4 ms |
+| steady state, iterations 220+ (`--steps 200 --warmup 220`) | ~1,640–1,700 it/s (0.59–0.61 ms) | 1,728 (r1 builder figure) |
+| `e2e`: `solve_decomposed` on host data, H2D + setup + solve + report, median of 3 | **@E2E@ it/s**, @E2EWALL@ s wall | 249 it/s |
+| `e2e_reference_layout`: the same call on the reference's input (dense c over n², A over n² columns; `compress` inside) | @E2EREF@ it/s, @E2EREFWALL@ s (round-2 start: 17.6 it/s, 2.27 s) | not measured |
+| CPU oracle port (`--impl reference`; 16 host cores) | @REF@ it/s (1 BLAS thread: @REF1@) | 1.17 |
+
+* The round-1 "1,728 it/s" was a steady-state figure (iterations 20–220); the driver's
+  command times iterations 6–25, where round 1 ran Jacobi refreshes at 1.3–2 ms per
+  iteration (881 it/s). Round 2's cold path and the cold/warm policy bring that window to
+  0.8 ms (cold iterations 1–16, 18–19) and 0.6 ms (fast path). The steady state is
+  slightly slower than in round 1 (two extra, normally empty, launches per iteration for
+  the cold pass and the Jacobi fallback, and the policy bookkeeping).
+* e2e wall of 89 ms (median of 40 solves in one process, `tools/e2e_phases.py`): device
+  setup 47 ms (A upload 13–20 ms, Schur 7 ms, half-pass layouts 4 ms, ...), loop
+  27.6 ms, report 11 ms, destroy 3 ms. What moved it from 0.15–0.18 s: the report's dot
+  products without BLAS threads (spinning OpenBLAS workers slowed the *next* solve's
+  staged H2D copies by ~40 ms), the report's pattern index on a host thread during the
+  setup and the loop, A uploaded on a host thread during the rest of the setup, pinned
+  check-result slots from a process-wide slab (`cudaMallocHost` / `cudaFreeHost` per
+  handle cost 10–450 ms in one solve out of ~6), and the faster early iterations.
+
+Per-kernel time per iteration (CUDA events, eager, one event set per iteration and one
+sync at the end) in the driver's window and in steady state, with ncu DRAM traffic per
+launch (`profiles/r02/ncu_full_counters.txt`, iteration ~200):
+
+| kernel | window 6–25 | steady (220+) | DRAM traffic | achieved (steady) |
+|---|---|---|---|---|
+@KTABLE@
+
+* The event-bracketed times of the short streaming kernels carry ~5–9 µs of event
+  overhead each; ncu's own durations (cold caches, `profiles/r02/launches_summary.txt`)
+  are `k_rhs` 37 µs (4.7 TB/s, 72%), `k_ua_half` 64 µs (4.1 TB/s, 63%),
+  `k_spmv_half` 46 + `k_pair_sum` 9 + `k_rowsum_tiles` 6 µs (3.8 TB/s, 58%), `k_xupd`
+  13 µs. ncu DRAM bytes equal the algorithmic bytes within 2% on all of them (no
+  re-reads); they were not changed this round.
+
+Smaller configs (graph replay; to-tolerance through `solve_decomposed`;
+`profiles/r02/small_profile_r02.txt`, launch lists `profiles/r02/launches_cfg*_r02.csv`):
+
+| config | round 2 | round 1 | time to 1e-4 | what bounds it |
+|---|---|---|---|---|
+| 0 | @C0@ it/s | 6.8k | 80 iterations, @C0W@ s wall | 20 cliques of order 20 on CTA teams: all on the cold path every iteration (their spectra touch zero, so the fast path never applies): ~70 µs of latency-bound eigensolve + 8 launches |
+| 1 | @C1@ it/s | 15k | `DualInfeasible` at 60 iterations | 10 cliques of order 16, cold path ~30 µs + 8 launches |
+| 2 | @C2@ it/s | 8.5k | 80 iterations, @C2W@ s wall | 1,990 warp-team cliques of order 11 (`k_cone_warp` 67 µs: warm Jacobi, one wave) |
+| 3 | @C3@ it/s | 3.4k | 780 iterations, @C3W@ s wall (reference: 1,188 s) | its 16 cliques of order 17–29 now run on CTA teams (they took 245 µs as warp teams and bounded the iteration: 277 → 203 µs); then the 391 warp cliques of order 9–16 (95 µs) |
+
+The verdict's small-config targets (30k / 40k / 10k it/s) are not met: with 9–11
+dependent launches per iteration (~2.5 µs each in a graph) and a latency-bound
+eigensolve of 30–130 µs, they need a persistent single-kernel iteration and a leaner
+small-clique eigensolver, which this round did not build.
+
+### 7.2 Round 1 (history, profiles/r01)
+
+| | config 4 |
+|---|---|
+| iterations/s (device-resident, iterations 20–220) | **1,728** (0.58 ms per iteration; 1,680–1,728 over the last runs) |
+| time to 1e-4 | 40 iterations, 0.041 s loop (reference loop: 606.7 s) |
+| e2e `solve_decomposed` (H2D + setup + solve + report; median of 3 solves) | 0.15–0.18 s wall, **249** iterations/s (median; 230–256 over the last runs) |
+| CPU oracle port, 16 threads (the reference arm) | 0.98–1.21 iterations/s (1.18 in the last `--impl reference` run) |
+
+Per-kernel time per iteration (CUDA events, eager, iterations ~220) and ncu DRAM
+traffic per launch (`profiles/r01/ncu_full_summary.txt`, iteration 200):
+
+| kernel | time per iteration | DRAM traffic | achieved |
+|---|---|---|---|
+| cone (`k_cone_split`) | 0.33 ms | 290 MB | 6.9 TFLOP/s algorithmic (19.5% of the fp64 DGEMM peak) |
+| A t (`k_pair_sum`, `k_spmv_half`, `k_rowsum_tiles`) | 0.066 ms | 23 + 214 + 4 MB | 3.5 TB/s algorithmic (54%) |
+| Aᵀg (`k_ua_half`) | 0.068 ms | 258 MB | 3.9 TB/s algorithmic (59%) |
+| `k_rhs` | 0.049 ms | 174 MB | 3.6 TB/s (55%) |
+| `k_xupd` | 0.021 ms | 62 MB | 4.5 TB/s (69%) |
+| `k_schur` | 0.010 ms | 8 MB | L2 |
+
+Round-1 progression on config 4 (same box type): 463 → 981 → 1,352 → 1,699 → 1,728 iterations/s (the last step: `k_ua_half` on a 148×16 grid, run-time Row-SELL tile size with 2 CTAs per tile),
+e2e 11.5 → 216 iterations/s.
+
+**e2e** (`solve_decomposed` on host data, 40 iterations to 1e-4, the median of three
+complete solves with the report caches cleared; the reference arm is the CPU port at 1.2
+iterations/s): ~0.18 s = device setup 0.06–0.08 s + loop 0.043 s (iterations 1–17 run
+Jacobi refreshes: 1.3–2 ms each) + report ~0.05 s. Host-side work moved off the critical
+path this round:
+* large host→device copies go through two pinned 32 MB staging buffers filled by up to 16
+  host threads while the DMA engine drains the other (A, 0.46 GB: 43 → ~5–19 ms;
+  pageable `cudaMemcpy` runs at ~11 GB/s on this host);
+* ζ is zeroed on the device instead of uploading a 56 MB mostly-zero vector; |c| is
+  summed on the host; the cover lists are built on the device (§4);
+* the report takes x, y and H'vt straight from the device (`hsde_report_vectors`: no
+  full-state copy, no host `bincount`; the device sums each coordinate's slots in the
+  reference's order, bit-identical to the host path — GPU test), and its pattern index
+  (blocks, local indices, covered positions: solver.py:443-452) is built by the library
+  in one O(N) pass (`hsde_pattern_index`: the row never decreases in code order, so a
+  per-column pointer into the covered list only moves forward; instead of `np.unique` +
+  `np.searchsorted`, 0.45 s → 0.02 s on the build host; tests/test_decompose.py checks it
+  against the numpy restatement);
+* one cuSOLVER handle per device for the process (creating one per solve cost 20–490 ms).
+
+What remains of the e2e: the A upload (19–60 ms, host-memory bound and variable), the
+first ~17 iterations (1.3–2 ms each: the basis is young, most cliques need a Jacobi
+refresh), the rest of the setup (~35 ms). The steps: two A passes instead of three; bank-conflict-free
+Jacobi; perturbative (first / second order) exits; symmetric half passes in SELL-C-σ
+layouts; tensor-core GEMMs in the cone kernel; device CSC, sparse Schur and lazy report
+rows for setup and report (3.5 s → 0.34 s wall); the class-split exit; then the
+`k_cone_split` fast path (invariant-subspace projection on DMMA blocks, §3).
+
+Smaller configs (graph replay; to-tolerance through `solve_decomposed`):
+
+| config | iterations/s | time to 1e-4 |
+|---|---|---|
+| 0 | 7.0k | 80 iterations, 0.014 s |
+| 1 | 16.0k | `DualInfeasible` at 60 iterations |
+| 2 | 9.2k | 80 iterations, 0.011 s |
+| 3 | 3.4k | 780 iterations, 0.23 s (reference: 1,188 s) |
+
+## 8. Out of scope, and next
+
+Out of scope (SURVEY §2, by the tier contract): the CLI, the HTTP service and the JSON
+front ends.  (SDPA parsing, chordal extension and clique enumeration were widened into
+as §8(f) rows f2/f4; config 3's bench cliques still come from the committed reference
+fixture, which our C++ decomposition reproduces exactly.)
+
+Status against the round-1 verdict's list:
+
+| item | status |
+|---|---|
+| parity gaps (config-4 shards, full states, ≥200-iteration pin, report entries, `recover`, dual-objective margin) | **closed**: §1; 65 GPU tests, 49 CPU tests |
+| fast cold path for CTA cliques | **built** (`k_cone_cold`, §3): config-4 cone launch 0.54 ms cold / 0.33–0.39 ms warm at every iteration (round 1: 1.3–2 ms for iterations 1–17); driver-window bench 881 → ~1,400 it/s, to-tolerance loop 41 → 27.6 ms. The bars "≤ 0.45 ms at every iteration ≥ 2" and "≥ 1,500 it/s" are **not** met: the cold eigensolve is bound by dependent-instruction latency (three CTAs of four warps per SM, one instruction per ~8 cycles per warp) |
+| `k_cone_split` ≥ 40% of fp64 | **not met**: 18–19% steady (0.33 ms), §3 explains what bounds it (two waves on 296 slots, 80-register cap, ~60 barrier-separated phases per clique) |
+| small-config latency path | **partial**: per-class CTA teams, adaptive SpMV tiles; configs 0–3 at 8.7k / 22–24k / 10.4k / 4.9k it/s (§7) |
+| streaming kernels ≥ 65% of HBM | **unchanged** (ncu durations: 58–72%; event-bracketed 53–68%) |
+| multi-GPU readiness | config-4 emulated shards tested at G = 2/4/8; NCCL init lines in `bench.py`; the multi-CTA-per-clique mode and pair ownership across shards are **not** built (§5) |
+| bench hygiene | identical `config` in both arms, two CPU-baseline timings + `lscpu`, `to_tol_iterations_per_s`, `e2e_reference_layout`, roofline profiled in the timed window + steady state, driver-measured numbers in README / §7 |
+
+Next, in order:
+1. Cone kernels. (a) `k_cone_split`: fit three CTAs per SM (≤ 75 KB: stream the X strip
+   and Ut through L2 instead of shared memory, single-buffer Yn) or pair two CTAs per
+   clique in a cluster, so 400 cliques take one wave; fold the within-class rotation
+   (below) into the basis update to cut the fixed-point passes from 5–9 to ~4.
+   (b) `k_cone_cold`: run the DMMA phases (back transformation, Newton–Schulz, P: 25% of
+   the clique) with 8–12 warps in a second kernel; a superlinear finisher for the
+   bisection (it is at its instruction floor: ten issued instructions per Sturm step).
+   The within-class rotation, simulated in numpy on config 4 (40 sampled cliques,
+   iterations 20–60): W_ij = C_ij/(c_jj − c_ii) on well-separated pairs, C the
+   class-compressed operator, cut the passes from 7.4 to 4.0 and kept off(B)/g at 0.02
+   instead of 0.21. The exact-orthogonal form: Ũ = (I + Wᵀ)U with W antisymmetric, so
+   ŨŨᵀ = I + Ỹ where Ỹ = Y_P + WᵀW + WᵀY_P + Y_P W + WᵀY_P W has no O(W) term and the
+   existing polar series applies (≈ +6 small product passes per clique).
+2. A persistent single-kernel iteration for the small configs (grid sync instead of 9–11
+   launches) and a register-resident small-clique eigensolver.
+3. Streaming kernels, from 58–72% towards 80% of HBM. Launch geometry is not the lever
+   (`profiles/r01/grid_sweep_r01.txt`: ±0.5%). The remaining gap is the indirection:
+   `k_rhs` follows a dependent chain (cover range → slot → four state values); the mirror
+   members of `k_ua_half` are strided gathers. Candidates: `k_ua_half` writing Aᵀg per
+   pair only (a pure SELL stream) with ua formed in a coalesced pass fused with c·ua;
+   the pair sums folded into the producer.
+4. Multi-rank NCCL runs at 2/4/8 GPUs once the pool allows, with a multi-CTA mode per
+   clique for G ≥ 4 on config 4.
+5. Host setup: `decompose`'s covered-set union (`np.unique` over Σ|C_k|² slots) can use
+   the same bit-mask cover (`hsde_cover_*`) that `compress` now uses.
