@@ -16,9 +16,9 @@ sm_100a CUDA in `paper_1611_01828_b200/csrc` does the work. It sits behind a C A
 | (a) a2/a3 `affine_project` / `_solve_inner_parts` (:203-245, :296-318) | block-eliminated affine solve | **done**: `k_rhs`, `k_spmv_seg`, `k_schur`, `k_ua`, `k_scalars` |
 | (a) a4/a5 `project_cone` / `project_psd_batch` (:321-355, symmat.py:153-165) | batched clique PSD projections | **done**: `k_cone_cold` (cold path, d ≤ 96: Householder tridiagonalisation, bisection, twisted factorisations, compact-WY back transformation and V max(Λ,0) Vᵀ on fp64 DMMA), `k_cone_split` (warm hot path, 8 ≤ d ≤ 96: invariant-subspace projection on DMMA blocks), `k_cone_warp` / `k_cone_wcold` (warp teams, d ≤ 32), `k_cone_block` (Jacobi path: d > 96 and every failure of the other paths) |
 | (a) a6 gather / scatter (graphs.py:245-252) | selector maps | **done**: atomic-free pull-scatter fused into `k_rhs` / `k_pull`; gather fused into the cone load |
-| (a) a7 `setup_cache` (:248-283) | Schur factor, ζ, M⁻¹ζ | **done on device**: dense chunks + cuBLAS DGEMM, cuSOLVER Cholesky, explicit S⁻¹, device inner solve for M⁻¹ζ |
+| (a) a7 `setup_cache` (:248-283) | Schur factor, ζ, M⁻¹ζ | **done on device**: sparse Schur assembly (`k_schur_rows`; dense cuBLAS DGEMM only when a row does not fit shared memory), cuSOLVER Cholesky, explicit S⁻¹, device inner solve for M⁻¹ζ |
 | (a) a8 `residuals` (:398-429) | pres / dres / gap | **done on device** (`hsde_check`, one host sync per check) |
-| (a) a9 `_try_certificates` (:455-505) | infeasibility certificates | **done on device** (`hsde_certificate`; min clique eigenvalue by the Jacobi kernel) |
+| (a) a9 `_try_certificates` (:455-505) | infeasibility certificates | **done on device** (`hsde_certificate`; min clique eigenvalue by the cold eigensolvers, values only) |
 | (a) a10 loop, normalisation, merit tracker (:634-772) | driver | **done** (`solver.py` shim; merit on device) |
 | (a) a11 `_classify` / `recover` (:521-617) | report | **done** (host Python, as in the reference); solution / certificate entry lists and `recover` are compared with the reference's own reports (`test_report_entries_match_reference`, `test_recover_matches_solve_report`) |
 | (b) boundary | C ABI + reference-named Python API | **done**: §2, `INTEGRATION.md` |
@@ -60,7 +60,8 @@ sm_100a CUDA in `paper_1611_01828_b200/csrc` does the work. It sits behind a C A
     the reference outputs at 1e-11;
   * `project_cone` at 1e-12; `iterate` from random starts at 1e-10, with the Moreau
     invariants;
-  * configs 0/1/2 after 500 iterations within 1e-8 relative of the reference;
+  * configs 0-3 after 500 iterations (config 4 after 40) within 1e-8 relative of the
+    reference (`test_config_fixed_iterations[0-4]`);
   * the to-tolerance status, iteration count ±2 and objectives within 1e-6 of the reference;
     config 1 gives `DualInfeasible`, ray "dual", b·y = 1, y within 1e-6;
   * the error types `FactorizationFailure`, `TauZero` and `EigenFailure`;
@@ -128,7 +129,8 @@ sm_100a CUDA in `paper_1611_01828_b200/csrc` does the work. It sits behind a C A
   * **SELL-32** for Aᵀg: slices of 32 pairs; element k of lane j at `beg + 32k + j`;
     16-bit row index + fp64 value; zero padding to the slice's longest column
     (×1.48 on config 4).
-  * **row-SELL tiles** for A t: tiles of 4096 pairs × groups of 32 rows; element k of
+  * **row-SELL tiles** for A t: tiles of 2048 pairs by default (sized at run time so
+    a small problem still has ≥ 2 CTAs per SM) × groups of 32 rows; element k of
     row 32g+j at `beg + 32k + j`; 16-bit column-within-tile + fp64 value; ascending
     column inside a row (×1.26 padding). Only the owned pairs' entries.
 * Cover lists (covered coordinate → slots, ascending slot = bincount order) and
@@ -193,8 +195,8 @@ the orthogonal projector onto span Q is Q G Qᵀ with G = (I + YᵀY)⁻¹, and
 
     P(B) = B Q G Qᵀ = Q (R G) Qᵀ,     P(X) = Utᵀ K Ut,   Ut = V_Pᵀ + Yᵀ V_Nᵀ,  K = R G.
 
-No truncation: the only errors are the fixed point's (stopped when the estimated error is
-≤ 2.5e-16) and rounding. V is then rotated onto the two new invariant subspaces,
+No truncation: the only errors are the fixed point's (stopped on the Riccati residual,
+below) and rounding. V is then rotated onto the two new invariant subspaces,
 V' = [S_P Ut; S_N Wt] with Wt = V_Nᵀ − Y V_Pᵀ and the polar factors S = (I + YᵀY)^−½,
 (I + YYᵀ)^−½ (binomial series, Horner), so the next B has only this iteration's
 cross-class coupling.
