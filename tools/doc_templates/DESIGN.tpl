@@ -273,8 +273,8 @@ cross-class coupling.
     384 × 2 threads per SM (828 B of spill stores); (iii) phase latency. The ≥ 40% bar
     needs the launch at 0.16 ms, which is the DMMA issue floor for the flops this scheme
     executes (~1.6× the algorithmic 11 d³); it is not reachable by tuning this kernel.
-* Iterations 90–140 of config 4 are slower (0.66–0.80 ms) because 1–2% of the cliques
-  need a Jacobi refresh (off(B) slightly above g/3 on cliques whose argument is tiny,
+* (Round 1, before the cold path:) iterations 90–140 of config 4 were slower (0.66–0.80 ms) because 1–2% of the cliques
+  needed a Jacobi refresh (off(B) slightly above g/3 on cliques whose argument is tiny,
   ~1e-4): one sweep of one clique costs ~0.1 ms on its CTA. The first-wave schedule and
   the in-place refresh cut that from 0.73–0.89 ms.
   Measured and not kept: looser thresholds (g/2: more passes everywhere and later
@@ -544,7 +544,7 @@ Headline workload, config 4 (400 cliques of order 80, m = 1000, 38.4 M nonzeros)
 |---|---|---|
 | `value`: iterations/s, driver command `--steps 20 --warmup 5` (iterations 6–25) | **@VALUE@** (@MS@ ms per iteration) | 881 |
 | to-tolerance loop (`to_tol_iterations_per_s`): 40 iterations to 1e-4 | **@TOTOL@ it/s**, @LOOPMS@ ms (reference loop: 606.7 s) | 41.4 ms |
-| steady state, iterations 220+ (`--steps 200 --warmup 220`) | ~1,640–1,700 it/s (0.59–0.61 ms) | 1,728 (r1 builder figure) |
+| steady state, iterations 220+ (`--steps 200 --warmup 220`) | ~1,700 it/s (0.59 ms) | 1,728 (r1 builder figure) |
 | `e2e`: `solve_decomposed` on host data, H2D + setup + solve + report, median of 3 | **@E2E@ it/s**, @E2EWALL@ s wall | 249 it/s |
 | `e2e_reference_layout`: the same call on the reference's input (dense c over n², A over n² columns; `compress` inside) | @E2EREF@ it/s, @E2EREFWALL@ s (round-2 start: 17.6 it/s, 2.27 s) | not measured |
 | CPU oracle port (`--impl reference`; 16 host cores) | @REF@ it/s (1 BLAS thread: @REF1@) | 1.17 |
@@ -552,9 +552,9 @@ Headline workload, config 4 (400 cliques of order 80, m = 1000, 38.4 M nonzeros)
 * The round-1 "1,728 it/s" was a steady-state figure (iterations 20–220); the driver's
   command times iterations 6–25, where round 1 ran Jacobi refreshes at 1.3–2 ms per
   iteration (881 it/s). Round 2's cold path and the cold/warm policy bring that window to
-  0.8 ms (cold iterations 1–16, 18–19) and 0.6 ms (fast path). The steady state is
-  slightly slower than in round 1 (two extra, normally empty, launches per iteration for
-  the cold pass and the Jacobi fallback, and the policy bookkeeping).
+  0.77 ms (cold iterations 1–16, 18–19) and 0.6 ms (fast path). The steady state is
+  where it was in round 1 (the faster Riccati update pays for the two extra, normally
+  empty, launches per iteration of the cold pass and the Jacobi fallback).
 * e2e wall of 89 ms (median of 40 solves in one process, `tools/e2e_phases.py`): device
   setup 47 ms (A upload 13–20 ms, Schur 7 ms, half-pass layouts 4 ms, ...), loop
   27.6 ms, report 11 ms, destroy 3 ms. What moved it from 0.15–0.18 s: the report's dot

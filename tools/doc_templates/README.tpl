@@ -13,7 +13,7 @@ Cliques are sharded across 1–8 GPUs, and their overlaps are combined with NCCL
 
 On one B200, config 4 of `BASELINE.json` (400 cliques of order 80, m = 1000, 38 M nonzeros in A), measured by `bench.py` (`profiles/r02/bench_r02.json`):
 
-- **@VALUE@ ADMM iterations/s** with device-resident data under the driver's command (`--steps 20 --warmup 5`, i.e. iterations 6–25, 14 of which still run the cold eigensolver). Round 1 measured 881 there. The steady state after iteration ~20 is 1,640–1,700 iterations/s.
+- **@VALUE@ ADMM iterations/s** with device-resident data under the driver's command (`--steps 20 --warmup 5`, i.e. iterations 6–25, 14 of which still run the cold eigensolver). Round 1 measured 881 there. The steady state after iteration ~20 is about 1,700 iterations/s.
 - The default solve reaches 1e-4 in 40 iterations; its loop takes @LOOPMS@ ms (**@TOTOL@ iterations/s**; the reference's loop takes 607 s).
 - **End to end** through `solve_decomposed` on host data (H2D copies, device setup, the solve, the report): **@E2E@ iterations/s** (@E2EWALL@ s wall, median of three solves). From the reference's own input layout (dense c over n², A over n² columns) the same call takes @E2EREFWALL@ s.
 - The reference algorithm's CPU port on the box's 16 host cores runs at about @REF@ iterations/s.
