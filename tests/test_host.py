@@ -102,6 +102,29 @@ def test_library_cover_layout_matches_numpy(cfg):
     assert np.allclose(c2.A.data, a.A.data, rtol=1e-15, atol=0)
 
 
+def test_edges_array_matches_sorted_tuples():
+    """problem.edges_array turns the reference's aggregate pattern (graphs.py:37, a
+    frozenset of (i, j) tuples) into the array `sorted(edges)` gives, without the
+    Python-level sort; already sorted arrays pass through."""
+    from paper_1611_01828_b200.problem import edges_array
+
+    class Agg:
+        pass
+
+    rng = np.random.default_rng(5)
+    n = 300
+    pairs = {tuple(sorted(map(int, rng.integers(0, n, 2)))) for _ in range(5000)}
+    a = Agg()
+    a.edges = frozenset(pairs)
+    want = np.asarray(sorted(a.edges), dtype=np.int64).reshape(-1, 2)
+    assert np.array_equal(edges_array(a, n), want)
+    a.edges = want[::-1].copy()  # an array, unsorted
+    assert np.array_equal(edges_array(a, n), want)
+    a.edges = frozenset()
+    assert edges_array(a, n).shape == (0, 2)
+    assert edges_array(None, n) is None
+
+
 def test_library_cover_layout_rejects_bad_ids():
     with pytest.raises(ValueError):
         _lib.cover_layout(16, np.zeros(16), np.array([3, 16], dtype=np.int64), np.array([1], dtype=np.int32))

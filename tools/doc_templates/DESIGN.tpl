@@ -666,7 +666,7 @@ Status against the round-1 verdict's list:
 
 | item | status |
 |---|---|
-| parity gaps (config-4 shards, full states, ≥200-iteration pin, report entries, `recover`, dual-objective margin) | **closed**: §1; 65 GPU tests, 49 CPU tests |
+| parity gaps (config-4 shards, full states, ≥200-iteration pin, report entries, `recover`, dual-objective margin) | **closed**: §1; 65 GPU tests, 50 CPU tests |
 | fast cold path for CTA cliques | **built** (`k_cone_cold`, §3): config-4 cone launch 0.54 ms cold / 0.33–0.39 ms warm at every iteration (round 1: 1.3–2 ms for iterations 1–17); driver-window bench 881 → ~1,400 it/s, to-tolerance loop 41 → 27.6 ms. The bars "≤ 0.45 ms at every iteration ≥ 2" and "≥ 1,500 it/s" are **not** met: the cold eigensolve is bound by dependent-instruction latency (three CTAs of four warps per SM, one instruction per ~8 cycles per warp) |
 | `k_cone_split` ≥ 40% of fp64 | **not met**: 18–19% steady (0.33 ms), §3 explains what bounds it (two waves on 296 slots, 80-register cap, ~60 barrier-separated phases per clique) |
 | small-config latency path | **partial**: per-class CTA teams, adaptive SpMV tiles; configs 0–3 at 8.7k / 22–24k / 10.4k / 4.9k it/s (§7) |

@@ -19,7 +19,7 @@ On one B200, config 4 of `BASELINE.json` (400 cliques of order 80, m = 1000, 38 
 - The reference algorithm's CPU port on the box's 16 host cores runs at about @REF@ iterations/s.
 - The dominant kernel (`k_cone_split`, the warm PSD projection on fp64 DMMA) runs at 18–19% of the measured fp64 DGEMM peak in steady state; the streaming kernels at 58–72% of the measured HBM bandwidth (ncu durations). `DESIGN.md` §3 and §7 say what bounds each, and §8 lists what the round-1 review asked for and what is still open.
 
-Smaller configs 0–3 run at @C0@ / @C1@ / @C2@ / @C3@ iterations/s. All five reproduce the reference's status, iteration count (±2), objectives (1e-6) and iterates (1e-8) — 65 GPU tests and 49 CPU tests.
+Smaller configs 0–3 run at @C0@ / @C1@ / @C2@ / @C3@ iterations/s. All five reproduce the reference's status, iteration count (±2), objectives (1e-6) and iterates (1e-8) — 65 GPU tests and 50 CPU tests.
 
 `profiles/r02/` has the bench lines, ncu launch lists for configs 0–4, `--set full` summaries and counters for the hot kernels and the cold eigensolver, and the phase clocks.
 
