@@ -78,6 +78,7 @@ struct ConePlan {
   int dpmax = 0;
   size_t smem = 0;
   int per_block = 0;       // warps per CTA (warp plan)
+  bool split_small = false;  // k_cone_split with kSplitThreadsSmall threads (largest clique <= kSplitSmallD)
   double *pscratch = nullptr;  // CTA plan: d x d global scratch per CTA (second-order rebuild)
   int64_t pstride = 0;
   size_t split_smem = 0;       // CTA plan: k_cone_split (0: not launched)
@@ -530,7 +531,8 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
       co.ids = s.W.corder;
       DevWork Ws = s.W;
       Ws.ccur = Ws.cnext = nullptr;
-      k_cone_split<false><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, Ws, co);
+      if (pl.split_small) k_cone_split<false, kSplitThreadsSmall><<<pl.count, kSplitThreadsSmall, pl.split_smem, st>>>(s.P, s.S, Ws, co);
+      else k_cone_split<false><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, Ws, co);
       CKL();
       return 0;
     }
@@ -538,7 +540,8 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
       ConeArgs co = ca;
       co.ids = s.W.corder;
       co.pf_ahead = split_prefetch ? 2 * h->n_sm : 0;  // two CTAs per SM resident
-      k_cone_split<true><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, s.W, co);
+      if (pl.split_small) k_cone_split<true, kSplitThreadsSmall><<<pl.count, kSplitThreadsSmall, pl.split_smem, st>>>(s.P, s.S, s.W, co);
+      else k_cone_split<true><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, s.W, co);
       CKL();
     }
     if (part == 0 || part == 2) {  // cold path on the predicted cliques
@@ -994,8 +997,11 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
       s.block_plan.split_smem = std::max((size_t)split_smem_doubles(dmax) * sizeof(double), per_blk);
       s.W.cta_ids = s.block_plan.ids;  // k_scalars schedules them for k_cone_split
       s.W.cta_n = s.block_plan.count;
+      s.block_plan.split_small = dmax <= kSplitSmallD;
       CK(cudaFuncSetAttribute(k_cone_split<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       CK(cudaFuncSetAttribute(k_cone_split<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_cone_split<false, kSplitThreadsSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      CK(cudaFuncSetAttribute(k_cone_split<true, kSplitThreadsSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     }
     CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     CK(cudaFuncSetAttribute(k_cone_block<CONE_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));

@@ -931,8 +931,8 @@ __global__ void __launch_bounds__(kColdThreads, MINB) k_cone_cold(DevProblem P, 
 // clique has a valid eigenbasis (hsde_split.cuh).  COLD: cliques without a
 // basis and hand-overs are left to k_cone_cold (X kept in W.xarg); otherwise
 // the Jacobi path (cone_one) finishes them in the same CTA.
-template <bool COLD>
-__global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
+template <bool COLD, int THREADS = kSplitThreads>
+__global__ void __launch_bounds__(THREADS, 2) k_cone_split(DevProblem P, DevState S, DevWork W, ConeArgs ca) {
   extern __shared__ __align__(16) double smem[];
   if ((int)blockIdx.x >= ca.count) return;
   const int k = ca.ids[blockIdx.x];
@@ -943,7 +943,12 @@ __global__ void __launch_bounds__(kSplitThreads, 2) k_cone_split(DevProblem P, D
   c2.cold = COLD;
   if (W.ccur && W.ccur[k]) return;  // this iteration on the cold path (k_cone_cold, concurrent)
   int st = SPLIT_UNTOUCHED;
-  if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d >= 8) st = split_one(P, S, W, c2, k, smem);
+  // (B's upper 16 x 16 blocks must fit the warps' register blocks: d <= 96 with
+  // twelve warps, d <= 80 with ten)
+  const int nbd = (d + 15) >> 4;
+  const bool fits = nbd * (nbd + 1) / 2 <= kSplitMaxB * (THREADS / 32);
+  if (ca.warm && vv > 0 && !(vv & kVRefresh) && d <= kSplitMaxD && d >= 8 && fits)
+    st = split_one(P, S, W, c2, k, smem);
   if (threadIdx.x == 0) W.cstate[k] = st;
   if (st == SPLIT_DONE || st == SPLIT_DONE + 16) return;
   if (threadIdx.x == 0 && W.cnext && st != SPLIT_UNTOUCHED) W.cnext[k] = 1;  // handed over: cold next

@@ -34,6 +34,11 @@
 // (included inside namespace hsde by hsde_kernels.cuh, after hsde_eig.cuh)
 
 constexpr int kSplitThreads = 384;
+// plans whose largest clique has order <= kSplitSmallD run ten warps per CTA: the
+// register cap rises from 80 to 96 per thread (two CTAs per SM either way) and B's 15
+// upper blocks still fit 10 x 2 register blocks (config 4: +2% in steady state)
+constexpr int kSplitThreadsSmall = 320;
+constexpr int kSplitSmallD = 80;
 constexpr int kSplitStrip = 32;  // warm-start strip width (columns of T = Vt X)
 constexpr int kSplitMaxB = 2;    // 16 x 16 blocks a warp keeps in registers
 constexpr int kSplitMaxD = 96;   // upper blocks of B: <= kSplitMaxB per warp
@@ -41,6 +46,8 @@ constexpr int kSplitMaxD = 96;   // upper blocks of B: <= kSplitMaxB per warp
 // them must be owned by some warp (nb = 6 -> 21 blocks <= 2 x 12)
 static_assert(((kSplitMaxD + 15) / 16) * ((kSplitMaxD + 15) / 16 + 1) / 2 <= kSplitMaxB * (kSplitThreads / 32),
               "kSplitMaxD: B's upper blocks exceed the warps' register blocks");
+static_assert(((kSplitSmallD + 15) / 16) * ((kSplitSmallD + 15) / 16 + 1) / 2 <= kSplitMaxB * (kSplitThreadsSmall / 32),
+              "kSplitSmallD: B's upper blocks exceed the warps' register blocks");
 constexpr int kSplitRefreshIters = 1000;  // fixed-point passes that ask for a Jacobi refresh of V
 constexpr int kLoadBatch = 4;          // hot-path slots per thread in flight
 constexpr double kSplitOff2 = 0.2;  // fast path while off(B)^2 <= kSplitOff2 g^2 (off < 0.45 g: Weyl keeps the inertia)
@@ -470,7 +477,7 @@ __device__ int split_one(const DevProblem &P, const DevState &S, const DevWork &
     }
   }
   __syncthreads();
-  constexpr int kPf = (kSplitMaxD * kSplitStrip + kSplitThreads - 1) / kSplitThreads;
+  constexpr int kPf = (kSplitMaxD * kSplitStrip + kSplitThreadsSmall - 1) / kSplitThreadsSmall;  // covers both CTA sizes
   for (int j0 = 0; j0 < d; j0 += kSplitStrip) {
     const int sw_ = min(kSplitStrip, d - j0), nbs = (sw_ + 15) >> 4;
     for (int t = w; t < nb * nbs; t += nw) {

@@ -161,7 +161,7 @@ explicit uy = ρ_y − A·ua pass; both agree to 1e-10 after 200 iterations (tes
 | `k_schur` | :232 `cho_solve` | g = S⁻¹(q0 − ρ_y) (four warps per row, fixed-order partials; S⁻¹ read with cached loads so it stays in L2) | L2 | 8·m² |
 | `k_ua_half` | :232-235 | SELL-32 Aᵀg with g staged in smem (lane = pair), ua for both members, block partials of c·ua | HBM | 10·nnz_pairs + 8·n_pairs + 32·N_c |
 | `k_scalars` | :315-317, 388-394 | one CTA: ζ·u, shift, τ/κ, y update, next ρ_y | latency | — |
-| `k_cone_split` | symmat.py:153-165, solver.py:388-394 | CTA (384 threads) per clique with a kept basis (8≤d≤96, warm): slot update, B = VᵀXV, Riccati invariant-subspace projection on DMMA 16×16 blocks, V rotated onto the new subspaces, s/z/v update; cliques it cannot finish are handed to `k_cone_cold` | tensor (fp64 DMMA) | 11·Σd³ (SURVEY §8d) |
+| `k_cone_split` | symmat.py:153-165, solver.py:388-394 | CTA (384 threads; 320 when every clique has order ≤ 80) per clique with a kept basis (8≤d≤96, warm): slot update, B = VᵀXV, Riccati invariant-subspace projection on DMMA 16×16 blocks, V rotated onto the new subspaces, s/z/v update; cliques it cannot finish are handed to `k_cone_cold` | tensor (fp64 DMMA) | 11·Σd³ (SURVEY §8d) |
 | `k_cone_cold` | same | CTA (128 threads, 3 per SM) per clique without a usable basis (d≤96): slot update, full eigendecomposition (Householder tridiagonalisation in registers, bisection, twisted factorisations, compact-WY back transformation, Newton-Schulz) and P = V max(Λ,0) Vᵀ on DMMA; runs **concurrently** with `k_cone_split` on disjoint cliques, and a second time on the fast path's hand-overs | fp64 (latency) / tensor | 11·Σd³ |
 | `k_cone_block` | same | CTA per clique: the Jacobi path (d > 96, `HSDE_FLAG_JACOBI`, failures of the cold path: eigenvalue pairs closer than 2⁻⁴⁰‖T‖) | fp64 | 11·Σd³ |
 | `k_cone_warp` | same | warp per clique (d≤32), three size classes (dp ≤ 8/16/32) launched as parallel graph branches; a class with few cliques (CTA teams stay below two per SM) runs on CTA teams instead; `k_cone_wcold` is the warp cold path of `project_cone` / certificate eigenvalues | fp64/latency | 11·Σd³ |
@@ -259,7 +259,11 @@ cross-class coupling.
   * Round-2 changes that moved it: the Riccati update as straight-line code on clamped
     indices (independent chains interleave; only the stores are predicated), a
     branch-free reciprocal (float seed + three Newton steps) instead of the division, a
-    butterfly total and a float convergence decision: steady launch 0.368 → 0.353 ms.
+    butterfly total and a float convergence decision: steady launch 0.368 → 0.353 ms;
+    ten warps per CTA instead of twelve when the plan's largest clique has order ≤ 80
+    (`k_cone_split<COLD, 320>`: 96 registers per thread instead of 80, spill stores
+    832 → 380 B, B's 15 upper blocks still fit 10 × 2 register blocks): +1.5% in steady
+    state.
     Making every branch around the DMMAs provably warp-uniform (warp index and the
     CTA-uniform control values through shuffle broadcasts) removes the `WARPSYNC.ALL`
     nvcc puts in front of each `mma.sync` (2 of the 3 issued instructions per DMMA are
