@@ -224,7 +224,7 @@ cross-class coupling.
     below ~ε|B|/g; the earlier |δY| ≤ 1e-15 test declared those cliques stalled and sent
     them to Jacobi). The contraction is estimated over two passes (the lagged quadratic
     term makes consecutive increments non-monotone).
-* **Passes** (one CTA of 384 threads, 2 CTAs/SM, 99–111 KB smem): batched hot-slot loads
+* **Passes** (one CTA of 320 or 384 threads, 2 CTAs/SM, 99–111 KB smem): batched hot-slot loads
   (every load of 4 slots in flight before the stores) → X in smem; X to the hand-off
   buffer, Vᵀ into smem, then B = VᵀXV by 32-column strips of T = VᵀX (the next strip of X
   fetched while the tensor cores work on the current one; B's upper 16×16 blocks stay in
@@ -247,7 +247,7 @@ cross-class coupling.
   cycles (the first wave loads 175 MB from HBM at once), B 61k, sort 17k, Riccati 96k,
   series 35k, Ut/Wt/V' 38k, K·Ut 5k, P 19k: 335k cycles = 0.17 ms per clique, and the
   400 cliques take **two waves** on 296 resident CTAs (2 per SM: 99–111 KB of shared
-  memory and 384 threads × 80 registers each), so the launch is 0.33 ms (graph) /
+  memory and 320 threads × 96 registers each on config 4), so the launch is 0.33 ms (graph) /
   0.36 ms (eager profile with the empty follow-up launches): 6.3–6.8 TFLOP/s
   algorithmic = 18–19% of the fp64 DGEMM peak.
   * One Riccati pass is ~14k cycles: the X products 6.0k (at the DMMA issue limit while
@@ -273,8 +273,9 @@ cross-class coupling.
     evicted before use): kept behind `HSDE_SPLIT_PREFETCH=1`, off by default.
   * What bounds it now: (i) wave quantisation — 400 cliques on 296 slots cost two full
     waves, a third CTA per SM needs ≤ 75 KB of shared memory and the Riccati / tail
-    phases need R1 (54 KB) plus 43 KB of Y / Ut / S_N; (ii) the 80-register cap of
-    384 × 2 threads per SM (828 B of spill stores); (iii) phase latency. The ≥ 40% bar
+    phases need R1 (54 KB) plus 43 KB of Y / Ut / S_N; (ii) the register cap of two
+    CTAs per SM (96 per thread with ten warps: 380 B of spill stores remain); (iii)
+    phase latency. The ≥ 40% bar
     needs the launch at 0.16 ms, which is the DMMA issue floor for the flops this scheme
     executes (~1.6× the algorithmic 11 d³); it is not reachable by tuning this kernel.
 * (Round 1, before the cold path:) iterations 90–140 of config 4 were slower (0.66–0.80 ms) because 1–2% of the cliques
