@@ -531,8 +531,7 @@ int launch_cone(hsde_handle *h, ShardDev &s, int mode, const ConePlan &pl, bool 
       co.ids = s.W.corder;
       DevWork Ws = s.W;
       Ws.ccur = Ws.cnext = nullptr;
-      if (pl.split_small) k_cone_split<false, kSplitThreadsSmall><<<pl.count, kSplitThreadsSmall, pl.split_smem, st>>>(s.P, s.S, Ws, co);
-      else k_cone_split<false><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, Ws, co);
+      k_cone_split<false><<<pl.count, kSplitThreads, pl.split_smem, st>>>(s.P, s.S, Ws, co);
       CKL();
       return 0;
     }
@@ -1000,7 +999,6 @@ int setup_cone_plans(hsde_handle *h, ShardDev &s, const int32_t *sizes, int p) {
       s.block_plan.split_small = dmax <= kSplitSmallD;
       CK(cudaFuncSetAttribute(k_cone_split<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       CK(cudaFuncSetAttribute(k_cone_split<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-      CK(cudaFuncSetAttribute(k_cone_split<false, kSplitThreadsSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       CK(cudaFuncSetAttribute(k_cone_split<true, kSplitThreadsSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     }
     CK(cudaFuncSetAttribute(k_cone_block<CONE_HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
