@@ -192,6 +192,15 @@ __device__ __forceinline__ void blk16_zero(double (&c)[2][2][2]) {
 template <class F>
 __device__ __forceinline__ void blk16_each(const double (&c)[2][2][2], int i0, int j0, int M, int N, F f) {
   const int lane = threadIdx.x & 31, q = lane >> 2, kk = lane & 3;
+  if (i0 + 16 <= M && j0 + 16 <= N) {  // interior block (warp-uniform): no per-element bounds tests
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) f(i0 + 8 * a + q, j0 + 8 * b + 2 * kk + e, c[a][b][e]);
+    return;
+  }
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll

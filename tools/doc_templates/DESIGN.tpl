@@ -317,8 +317,8 @@ spectrum comes within reach of zero).
   flight; **P** = V_P Λ_P V_Pᵀ (or X + V_N|Λ_N|V_Nᵀ when the negative class is smaller).
 * Measured per clique on config 4 (clock64 stamps, `tools/cold_phases.py`,
   `profiles/r02/cold_phases.txt`): slot load 140k cycles (HBM-bound: all 400 CTAs load
-  245 MB at once), tridiagonalisation 277k, bisection 156k, twisted vectors 80k, back
-  transformation 141k, Newton–Schulz 74k, P 33k: 0.90 M cycles, 0.54 ms for the launch
+  245 MB at once), tridiagonalisation 280k, bisection 156k, twisted vectors 79k, back
+  transformation 131k, Newton–Schulz 76k, P 34k: 0.90 M cycles, 0.54 ms for the launch
   (1.00 M cycles when first built).
   ncu (`profiles/r02/ncu_cold_*`): 225 M warp instructions per launch, one issued every
   ~8 cycles per warp with three warps per scheduler (issue slots 33% busy): the kernel
@@ -331,7 +331,8 @@ spectrum comes within reach of zero).
   hand-off, (a_k, e²_{k−1}) packed into one 16-byte load per Sturm step with the signs
   counted through a funnel-shift register (ten issued instructions per step → ~8.5),
   the Gram operand of Newton–Schulz prefetched five k-steps deep from L2, batched
-  copy-back and w_s update loops.
+  copy-back and w_s update loops, no per-element bounds tests in the epilogue of
+  interior 16×16 blocks (back transformation 141k → 131k).
   Tried and measured, not kept: three bracket points per thread and round
   (quad-section: 1.5× the fp64 operations, same time), eight slots per thread in flight in the load (same time:
   memory-system bound), gathering M⁻¹ζ's slot parts from its x part instead of
