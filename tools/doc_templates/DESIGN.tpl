@@ -268,6 +268,10 @@ cross-class coupling.
     CTA-uniform control values through shuffle broadcasts) removes the `WARPSYNC.ALL`
     nvcc puts in front of each `mma.sync` (2 of the 3 issued instructions per DMMA are
     `WARPSYNC.ALL` and `NOP`): measured, no change in either cone kernel, not kept.
+    A separate k-loop without the tile tests for blocks that lie fully inside the output
+    (loop unswitching by hand): 3% slower in steady state (code size), not kept; the
+    same idea in the block epilogue (no per-element bounds tests on interior blocks) is
+    kept (+1%).
     An L2 prefetch of the second wave's inputs by the first wave (after its own load,
     when HBM is idle) is worth ~1% but raises the launch's DRAM traffic by 18% (lines
     evicted before use): kept behind `HSDE_SPLIT_PREFETCH=1`, off by default.
